@@ -1,0 +1,137 @@
+/*
+ * mrep.h -- C ABI of libmrep.so, the B200 (sm_100a) M-rep B-spline point
+ * projection / inversion library.
+ *
+ * Plain pointers, sizes and an opaque CUDA stream (`void* stream`, a
+ * cudaStream_t; NULL = legacy default stream).  No torch types.  Every entry
+ * returns an int status (MREP_OK = 0) unless stated otherwise; on a CUDA
+ * failure the message is available from mrep_last_error().
+ *
+ * Pointer convention: `_dev` arguments are device pointers, `_host` arguments
+ * host pointers (pinned or pageable).  Arrays are C-contiguous float64 unless
+ * stated; a point array of n points in dimension d is [n][d] (d = 2 or 3).
+ *
+ * Each entry cites the reference interface it replaces
+ * (/root/reference/pkg/src/splinemat/<file>:<line>).
+ */
+#ifndef MREP_H
+#define MREP_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MREP_API __attribute__((visibility("default")))
+#else
+#define MREP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MREP_OK 0
+#define MREP_ERR_ARG 1
+#define MREP_ERR_CUDA 2
+#define MREP_ERR_DEPTH 3   /* DepthExceeded (reduce_approx.py:265-268) */
+#define MREP_ERR_NODEV 4
+
+/* mrep_project flags */
+#define MREP_SCREEN 1u   /* BVH-culled exact solve (t/foot/dist/seg identical; cand = candidates examined) */
+#define MREP_STATS 2u    /* brute-force mode with per-query stats + soundness (forces !MREP_SCREEN) */
+
+/* Work counters written (accumulated) by mrep_project when `counters_dev` != NULL. */
+#define MREP_CNT_PAIRS 0      /* (query, cubic) pairs solved: E, quartic, rebase, pieces */
+#define MREP_CNT_SURVIVORS 1  /* pieces that survived elimination and were clipped */
+#define MREP_CNT_CLIP_ITERS 2 /* Bezier-clipping iterations over all survivors */
+#define MREP_CNT_SEAMS 3      /* seam-distance evaluations */
+#define MREP_CNT_BOXES 4      /* BVH box lower-bound tests */
+#define MREP_CNT_PASS2 5      /* queries that needed the exact tie-band second pass */
+#define MREP_NUM_COUNTERS 8
+
+MREP_API const char* mrep_last_error(void);
+MREP_API int mrep_version(void);
+MREP_API int mrep_device_count(void);
+
+/* ---------------------------------------------------------------------
+ * Segment table: the device-resident form of a PreparedCurve
+ * (project.py:110-121, 220-242).  Packed 256-B records per cubic (power
+ * coefficients, control points, interval, end seam) plus an 8-ary AABB
+ * hierarchy over the cubics for screening.
+ * ------------------------------------------------------------------- */
+MREP_API int64_t mrep_table_bytes(int64_t S);
+MREP_API int mrep_table_pack(const double* seg_pts_dev, /* [S][4][d] */
+                    const double* seg_ta_dev, const double* seg_tb_dev, /* [S] */
+                    const double* seam_t_dev,                           /* [S+1] */
+                    const double* seam_pt_dev,                          /* [S+1][d] */
+                    int64_t S, int d, void* table_dev, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Projection of n queries onto one prepared curve.  Replaces
+ * _kernels._project_block (_kernels.py:369-502) as driven by
+ * project_prepared (project.py:245-289).  Outputs are caller-allocated
+ * device arrays; out_seg (int32, winning cubic: seam s -> max(s-1,0)),
+ * out_stats ([n][6] int64) and out_sound may be NULL.  out_stats/out_sound
+ * are written only with MREP_STATS.
+ * ------------------------------------------------------------------- */
+MREP_API int mrep_project(const void* table_dev, int64_t S, int d, const double* queries_dev, int64_t n,
+                 double clip_tol, int max_iter, int soundness_samples, unsigned flags,
+                 double* out_t_dev, double* out_foot_dev, double* out_dist_dev,
+                 int64_t* out_cand_dev, int32_t* out_seg_dev, int64_t* out_stats_dev,
+                 double* out_sound_dev, uint64_t* counters_dev, void* stream);
+
+/* Same, HOST buffers in and out (the end-to-end call): chunked H2D / kernel /
+ * D2H pipeline on two internal streams; synchronous on return.
+ * out_seg_host may be NULL. */
+MREP_API int mrep_project_host(const void* table_dev, int64_t S, int d, const double* queries_host,
+                      int64_t n, double clip_tol, int max_iter, unsigned flags,
+                      double* out_t_host, double* out_foot_host, double* out_dist_host,
+                      int64_t* out_cand_host, int32_t* out_seg_host);
+
+/* Exact drop-in for _kernels._project_block (_kernels.py:369-371): the raw
+ * prepared arrays, all DEVICE pointers, brute force with stats. */
+MREP_API int mrep_project_block(const double* seg_pts, const double* seg_ta, const double* seg_tb,
+                       const double* seam_t, const double* seam_pt, int64_t S, int d,
+                       const double* queries, int64_t n, double clip_tol, int max_iter,
+                       int soundness_samples, double* out_t, double* out_foot, double* out_dist,
+                       int64_t* out_cand, int64_t* out_stats, double* out_sound, void* stream);
+
+/* Knot span of each parameter: searchsorted(knots, t, 'right') - 1 clipped
+ * to [p, m - p - 2] (the span convention of core.py:108-112). */
+MREP_API int mrep_knot_span(const double* knots_dev, int64_t m, int p, const double* t_dev, int64_t n,
+                   int32_t* span_dev, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Per-operation batch kernels (the public single-pair ops of project.py
+ * and distance.py, batched; same device routines the projection uses).
+ * ------------------------------------------------------------------- */
+/* _kernels._quartic_roots_01 (_kernels.py:91-176) / distance.solve_quartic */
+MREP_API int mrep_quartic_roots(const double* coeffs_dev /*[n][5]*/, int64_t n, double* roots_dev /*[n][4]*/,
+                       int64_t* counts_dev, void* stream);
+/* _kernels._newton_quartic_block (_kernels.py:515-566), bench baseline */
+MREP_API int mrep_newton_quartic_roots(const double* coeffs_dev, int64_t n, double* roots_dev,
+                              int64_t* counts_dev, void* stream);
+/* _kernels._distance_poly (_kernels.py:179-199) / distance.distance_polys */
+MREP_API int mrep_distance_poly(const double* P_dev /*[n][4][d]*/, const double* q_dev /*[n][d]*/,
+                       int64_t n, int d, double* e_dev /*[n][6]*/, void* stream);
+/* _kernels._restrict_ordinates (_kernels.py:202-226) / project.clip */
+MREP_API int mrep_restrict_ordinates(const double* b_dev /*[n][6]*/, const double* lo_dev,
+                            const double* hi_dev, int64_t n, double* out_dev, void* stream);
+/* _kernels._eval_ordinates (_kernels.py:229-236) / NonParametricBezier.__call__ */
+MREP_API int mrep_eval_ordinates(const double* b_dev, const double* u_dev, int64_t n, double* out_dev,
+                        void* stream);
+/* _kernels._hull_cross (_kernels.py:239-303) / project.hull_x_intersections */
+MREP_API int mrep_hull_cross(const double* b_dev, int64_t n, int32_t* found_dev, double* z_dev /*[n][2]*/,
+                    void* stream);
+/* _kernels._clip_root (_kernels.py:306-341) / project.clip_root; widths [n][max_iter] */
+MREP_API int mrep_clip_root(const double* b_dev, int64_t n, double tol, int max_iter, double* root_dev,
+                   int32_t* ok_dev, int32_t* used_dev, double* widths_dev, void* stream);
+/* _kernels._decasteljau_point (_kernels.py:344-357) */
+MREP_API int mrep_cubic_points(const double* P_dev /*[n][4][d]*/, const double* u_dev, int64_t n, int d,
+                      double* out_dev /*[n][d]*/, void* stream);
+/* project.rebase_batch (project.py:134-137): b = T5 e */
+MREP_API int mrep_rebase(const double* e_dev /*[n][6]*/, int64_t n, double* b_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MREP_H */

@@ -1,0 +1,201 @@
+"""Batched device operations over libmrep (numpy in, numpy out).
+
+Each function moves its inputs to the GPU, runs one libmrep kernel and
+returns host arrays.  They back the public single-pair ops of the reference
+(project.py:124-209, distance.py:34-94) and the parity tests; the batch
+projection itself keeps its data on the device (see project.py).
+"""
+
+import numpy as np
+
+from . import _lib as L
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def quartic_roots(coeffs):
+    """_kernels._quartic_block: (n,5) -> roots (n,4) (NaN-padded), counts (n,)."""
+    torch = L._torch()
+    c = L.to_dev(_f64(coeffs).reshape(-1, 5))
+    n = c.shape[0]
+    roots = torch.full((n, 4), float("nan"), dtype=torch.float64, device=c.device)
+    counts = L.empty((n,), torch.int64)
+    L.check(L.lib().mrep_quartic_roots(L.ptr(c), n, L.ptr(roots), L.ptr(counts), L.stream_ptr()))
+    return L.to_host(roots), L.to_host(counts)
+
+
+def newton_quartic_roots(coeffs):
+    """_kernels._newton_quartic_block (the bench's multistart-Newton baseline)."""
+    torch = L._torch()
+    c = L.to_dev(_f64(coeffs).reshape(-1, 5))
+    n = c.shape[0]
+    roots = torch.full((n, 4), float("nan"), dtype=torch.float64, device=c.device)
+    counts = L.empty((n,), torch.int64)
+    L.check(L.lib().mrep_newton_quartic_roots(L.ptr(c), n, L.ptr(roots), L.ptr(counts),
+                                              L.stream_ptr()))
+    return L.to_host(roots), L.to_host(counts)
+
+
+def distance_poly(P, q):
+    """_kernels._distance_poly batched: P (n,4,d), q (n,d) -> e (n,6)."""
+    P = _f64(P)
+    q = _f64(q)
+    if P.ndim == 2:
+        P = P[None]
+        q = q[None]
+    n, _, d = P.shape
+    Pd, qd = L.to_dev(P), L.to_dev(q)
+    e = L.empty((n, 6))
+    L.check(L.lib().mrep_distance_poly(L.ptr(Pd), L.ptr(qd), n, d, L.ptr(e), L.stream_ptr()))
+    return L.to_host(e)
+
+
+def restrict_ordinates(b, lo, hi):
+    b = _f64(b).reshape(-1, 6)
+    n = b.shape[0]
+    lo = np.broadcast_to(_f64(lo), (n,)).copy()
+    hi = np.broadcast_to(_f64(hi), (n,)).copy()
+    bd, lod, hid = L.to_dev(b), L.to_dev(lo), L.to_dev(hi)
+    out = L.empty((n, 6))
+    L.check(L.lib().mrep_restrict_ordinates(L.ptr(bd), L.ptr(lod), L.ptr(hid), n, L.ptr(out),
+                                            L.stream_ptr()))
+    return L.to_host(out)
+
+
+def eval_ordinates(b, u):
+    b = _f64(b).reshape(-1, 6)
+    n = b.shape[0]
+    u = np.broadcast_to(_f64(u), (n,)).copy()
+    bd, ud = L.to_dev(b), L.to_dev(u)
+    out = L.empty((n,))
+    L.check(L.lib().mrep_eval_ordinates(L.ptr(bd), L.ptr(ud), n, L.ptr(out), L.stream_ptr()))
+    return L.to_host(out)
+
+
+def hull_cross(b):
+    torch = L._torch()
+    b = _f64(b).reshape(-1, 6)
+    n = b.shape[0]
+    bd = L.to_dev(b)
+    found = L.empty((n,), torch.int32)
+    z = L.empty((n, 2))
+    L.check(L.lib().mrep_hull_cross(L.ptr(bd), n, L.ptr(found), L.ptr(z), L.stream_ptr()))
+    return L.to_host(found).astype(bool), L.to_host(z)
+
+
+def clip_root(b, tol, max_iter):
+    torch = L._torch()
+    b = _f64(b).reshape(-1, 6)
+    n = b.shape[0]
+    bd = L.to_dev(b)
+    root = L.empty((n,))
+    ok = L.empty((n,), torch.int32)
+    used = L.empty((n,), torch.int32)
+    widths = L.empty((n, max(int(max_iter), 1)))
+    L.check(L.lib().mrep_clip_root(L.ptr(bd), n, float(tol), int(max_iter), L.ptr(root),
+                                   L.ptr(ok), L.ptr(used), L.ptr(widths), L.stream_ptr()))
+    return (L.to_host(root), L.to_host(ok).astype(bool), L.to_host(used),
+            L.to_host(widths)[:, : int(max_iter)])
+
+
+def cubic_points(P, u):
+    P = _f64(P)
+    if P.ndim == 2:
+        P = P[None]
+    n, _, d = P.shape
+    u = np.broadcast_to(_f64(u), (n,)).copy()
+    Pd, ud = L.to_dev(P), L.to_dev(u)
+    out = L.empty((n, d))
+    L.check(L.lib().mrep_cubic_points(L.ptr(Pd), L.ptr(ud), n, d, L.ptr(out), L.stream_ptr()))
+    return L.to_host(out)
+
+
+def rebase(e):
+    e = _f64(e).reshape(-1, 6)
+    n = e.shape[0]
+    ed = L.to_dev(e)
+    out = L.empty((n, 6))
+    L.check(L.lib().mrep_rebase(L.ptr(ed), n, L.ptr(out), L.stream_ptr()))
+    return L.to_host(out)
+
+
+def project_block(seg_pts, seg_ta, seg_tb, seam_t, seam_pt, queries, clip_tol=1e-6,
+                  max_iter=8, soundness_samples=0):
+    """Drop-in for _kernels._project_block on host arrays (brute force + stats)."""
+    torch = L._torch()
+    sp, ta, tb = L.to_dev(_f64(seg_pts)), L.to_dev(_f64(seg_ta)), L.to_dev(_f64(seg_tb))
+    st, spt = L.to_dev(_f64(seam_t)), L.to_dev(_f64(seam_pt))
+    q = L.to_dev(_f64(np.atleast_2d(queries)))
+    S, _, d = sp.shape
+    n = q.shape[0]
+    out_t, out_foot, out_dist = L.empty((n,)), L.empty((n, d)), L.empty((n,))
+    out_cand = L.empty((n,), torch.int64)
+    out_stats = torch.zeros((n, 6), dtype=torch.int64, device=q.device)
+    out_sound = L.empty((n,))
+    L.check(L.lib().mrep_project_block(
+        L.ptr(sp), L.ptr(ta), L.ptr(tb), L.ptr(st), L.ptr(spt), S, d, L.ptr(q), n,
+        float(clip_tol), int(max_iter), int(soundness_samples), L.ptr(out_t), L.ptr(out_foot),
+        L.ptr(out_dist), L.ptr(out_cand), L.ptr(out_stats), L.ptr(out_sound), L.stream_ptr()))
+    return (L.to_host(out_t), L.to_host(out_foot), L.to_host(out_dist), L.to_host(out_cand),
+            L.to_host(out_stats), L.to_host(out_sound))
+
+
+class DeviceTable:
+    """Device-resident segment table of one prepared curve (+ its AABB tree).
+
+    Built once from the packed arrays of a PreparedCurve (project.py:225-238)
+    by ``mrep_table_pack``; reused by every projection batch.
+    """
+
+    def __init__(self, seg_pts, seg_ta, seg_tb, seam_t, seam_pt):
+        torch = L._torch()
+        sp = seg_pts if isinstance(seg_pts, torch.Tensor) else L.to_dev(_f64(seg_pts))
+        self.S, _, self.d = sp.shape
+        args = [x if isinstance(x, torch.Tensor) else L.to_dev(_f64(x))
+                for x in (seg_ta, seg_tb, seam_t, seam_pt)]
+        nbytes = L.lib().mrep_table_bytes(self.S)
+        if nbytes <= 0:
+            raise ValueError("segment table needs at least one cubic")
+        self.buf = torch.empty((nbytes // 8,), dtype=torch.float64, device=sp.device)
+        L.check(L.lib().mrep_table_pack(L.ptr(sp), *[L.ptr(a) for a in args], self.S, self.d,
+                                        L.ptr(self.buf), L.stream_ptr()))
+
+    def project(self, queries, clip_tol=1e-6, max_iter=8, soundness_samples=0, screen=True,
+                stats=False, counters=None):
+        """Project device queries (n, d); returns device tensors
+        (t, foot, dist, cand, seg, stats|None, sound|None)."""
+        torch = L._torch()
+        q = queries if isinstance(queries, torch.Tensor) else L.to_dev(_f64(queries))
+        q = q.contiguous()
+        n = q.shape[0]
+        dev = q.device
+        t = torch.empty((n,), dtype=torch.float64, device=dev)
+        foot = torch.empty((n, self.d), dtype=torch.float64, device=dev)
+        dist = torch.empty((n,), dtype=torch.float64, device=dev)
+        cand = torch.empty((n,), dtype=torch.int64, device=dev)
+        seg = torch.empty((n,), dtype=torch.int32, device=dev)
+        st = torch.zeros((n, 6), dtype=torch.int64, device=dev) if stats else None
+        sound = torch.empty((n,), dtype=torch.float64, device=dev) if stats else None
+        flags = (L.MREP_STATS if stats else 0) | (L.MREP_SCREEN if (screen and not stats) else 0)
+        L.check(L.lib().mrep_project(
+            L.ptr(self.buf), self.S, self.d, L.ptr(q), n, float(clip_tol), int(max_iter),
+            int(soundness_samples), flags, L.ptr(t), L.ptr(foot), L.ptr(dist), L.ptr(cand),
+            L.ptr(seg), L.ptr(st), L.ptr(sound), L.ptr(counters), L.stream_ptr()))
+        return t, foot, dist, cand, seg, st, sound
+
+    def project_host(self, queries, out=None, clip_tol=1e-6, max_iter=8, screen=True):
+        """End-to-end call on HOST arrays through mrep_project_host."""
+        q = np.ascontiguousarray(queries, dtype=np.float64)
+        n = q.shape[0]
+        if out is None:
+            out = (np.empty(n), np.empty((n, self.d)), np.empty(n),
+                   np.empty(n, dtype=np.int64), np.empty(n, dtype=np.int32))
+        t, foot, dist, cand, seg = out
+        import ctypes
+        p = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+        L.check(L.lib().mrep_project_host(
+            L.ptr(self.buf), self.S, self.d, p(q), n, float(clip_tol), int(max_iter),
+            L.MREP_SCREEN if screen else 0, p(t), p(foot), p(dist), p(cand), p(seg)))
+        return out

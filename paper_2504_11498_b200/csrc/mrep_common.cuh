@@ -1,0 +1,111 @@
+// mrep_common.cuh -- error plumbing and device table layout shared by the
+// libmrep translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/mrep.h"
+
+namespace mrep {
+
+void set_error(const std::string& msg);
+
+#define MREP_CUDA_CHECK(expr)                                                        \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess) {                                                         \
+      ::mrep::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));         \
+      return MREP_ERR_CUDA;                                                          \
+    }                                                                                \
+  } while (0)
+
+#define MREP_LAUNCH_CHECK()                                                          \
+  do {                                                                               \
+    cudaError_t _e = cudaGetLastError();                                             \
+    if (_e != cudaSuccess) {                                                         \
+      ::mrep::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e));    \
+      return MREP_ERR_CUDA;                                                          \
+    }                                                                                \
+  } while (0)
+
+// ---------------------------------------------------------------- table
+// One 256-B record per cubic (32 doubles):
+//   [0..11]  w[k][dim], k = 0..3 power coefficients (B3 P), dim-major inside k
+//   [12..23] P[j][dim], control points
+//   [24] ta  [25] tb  [26] seam_t[s+1]  [27..29] seam_pt[s+1]  [30..31] pad
+// Header (64 doubles) before the records: [0] seam_t[0], [1..3] seam_pt[0],
+// [4] coordinate scale (max |coord| of the control points).
+// AABB hierarchy after the records: 8-ary over contiguous cubic ranges,
+// level 0 = one box per cubic, top level = 1 box; 6 doubles per box
+// (lo xyz, hi xyz).
+constexpr int REC = 32;
+constexpr int HDR = 64;
+constexpr int FANOUT = 8;
+constexpr int MAX_LEVELS = 12;
+
+struct TableLayout {
+  int64_t S;
+  int top;  // index of the root level (>= 1)
+  int64_t lvl_off[MAX_LEVELS];  // in boxes, from the start of the box area
+  int64_t lvl_cnt[MAX_LEVELS];
+  int64_t total_boxes;
+  int64_t rec_off;  // in doubles from table start
+  int64_t box_off;  // in doubles from table start
+  int64_t total_doubles;
+};
+
+inline TableLayout table_layout(int64_t S) {
+  TableLayout L{};
+  L.S = S;
+  int64_t cnt = S, off = 0;
+  int lv = 0;
+  for (;;) {
+    L.lvl_off[lv] = off;
+    L.lvl_cnt[lv] = cnt;
+    off += cnt;
+    if (lv >= 1 && cnt <= 1) break;
+    cnt = (cnt + FANOUT - 1) / FANOUT;
+    ++lv;
+  }
+  L.top = lv;
+  L.total_boxes = off;
+  L.rec_off = HDR;
+  L.box_off = HDR + S * REC;
+  L.total_doubles = L.box_off + off * 6;
+  return L;
+}
+
+struct TableView {
+  const double* hdr;
+  const double* rec;
+  const double* box;
+  int64_t S;
+  int top;
+  int64_t lvl_off[MAX_LEVELS];
+  int64_t lvl_cnt[MAX_LEVELS];
+};
+
+inline TableView table_view(const void* table, int64_t S) {
+  TableLayout L = table_layout(S);
+  TableView v{};
+  const double* base = static_cast<const double*>(table);
+  v.hdr = base;
+  v.rec = base + L.rec_off;
+  v.box = base + L.box_off;
+  v.S = S;
+  v.top = L.top;
+  for (int i = 0; i < MAX_LEVELS; ++i) {
+    v.lvl_off[i] = L.lvl_off[i];
+    v.lvl_cnt[i] = L.lvl_cnt[i];
+  }
+  return v;
+}
+
+inline unsigned grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+}  // namespace mrep

@@ -1,0 +1,152 @@
+// mrep_host.cu -- end-to-end projection from HOST buffers.
+//
+// The reference's project_prepared (project.py:245-289) takes numpy arrays in
+// host memory and returns numpy arrays; this entry point keeps that contract
+// at the C ABI: queries in host memory, results written to host memory,
+// synchronous on return.  The batch is cut into chunks that flow through a
+// two-slot pipeline (H2D of chunk i+1 and D2H of chunk i-1 overlap the
+// kernel of chunk i on separate copy engines).  Pinned caller buffers are
+// copied directly; pageable ones are staged through cached pinned buffers.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "mrep_common.cuh"
+
+namespace mrep {
+
+namespace {
+
+constexpr int64_t CHUNK = 1 << 18;  // queries per pipeline slot
+
+struct Slot {
+  cudaStream_t st = nullptr;
+  cudaEvent_t done = nullptr;
+  double *dq = nullptr, *dt = nullptr, *dfoot = nullptr, *ddist = nullptr;
+  int64_t* dcand = nullptr;
+  int32_t* dseg = nullptr;
+  double *hq = nullptr, *ht = nullptr, *hfoot = nullptr, *hdist = nullptr;
+  int64_t* hcand = nullptr;
+  int32_t* hseg = nullptr;
+  int64_t lo = 0, cnt = 0;  // chunk in flight (for staged write-back)
+  bool busy = false;
+};
+
+struct HostCtx {
+  std::mutex mu;
+  int device = -1;
+  Slot slot[2];
+  bool ready = false;
+};
+
+HostCtx g_ctx;
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+int ensure_ctx() {
+  int dev = 0;
+  MREP_CUDA_CHECK(cudaGetDevice(&dev));
+  if (g_ctx.ready && g_ctx.device == dev) return MREP_OK;
+  for (auto& s : g_ctx.slot) {
+    MREP_CUDA_CHECK(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+    MREP_CUDA_CHECK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+    MREP_CUDA_CHECK(cudaMalloc(&s.dq, CHUNK * 3 * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMalloc(&s.dt, CHUNK * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMalloc(&s.dfoot, CHUNK * 3 * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMalloc(&s.ddist, CHUNK * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMalloc(&s.dcand, CHUNK * sizeof(int64_t)));
+    MREP_CUDA_CHECK(cudaMalloc(&s.dseg, CHUNK * sizeof(int32_t)));
+    MREP_CUDA_CHECK(cudaMallocHost(&s.hq, CHUNK * 3 * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMallocHost(&s.ht, CHUNK * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMallocHost(&s.hfoot, CHUNK * 3 * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMallocHost(&s.hdist, CHUNK * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMallocHost(&s.hcand, CHUNK * sizeof(int64_t)));
+    MREP_CUDA_CHECK(cudaMallocHost(&s.hseg, CHUNK * sizeof(int32_t)));
+  }
+  g_ctx.device = dev;
+  g_ctx.ready = true;
+  return MREP_OK;
+}
+
+}  // namespace
+}  // namespace mrep
+
+using namespace mrep;
+
+extern "C" int mrep_project_host(const void* table, int64_t S, int d, const double* queries,
+                                 int64_t n, double clip_tol, int max_iter, unsigned flags,
+                                 double* out_t, double* out_foot, double* out_dist,
+                                 int64_t* out_cand, int32_t* out_seg) {
+  if (n < 0 || (d != 2 && d != 3) || S < 1 || !table) {
+    set_error("mrep_project_host: bad arguments");
+    return MREP_ERR_ARG;
+  }
+  if (n == 0) return MREP_OK;
+  std::lock_guard<std::mutex> lock(g_ctx.mu);
+  int rc = ensure_ctx();
+  if (rc != MREP_OK) return rc;
+  flags &= ~MREP_STATS;
+  const bool pin_in = is_pinned(queries);
+  const bool pin_out = is_pinned(out_t) && is_pinned(out_foot) && is_pinned(out_dist) &&
+                       is_pinned(out_cand) && (!out_seg || is_pinned(out_seg));
+
+  auto write_back = [&](Slot& s) -> int {
+    if (!s.busy) return MREP_OK;
+    MREP_CUDA_CHECK(cudaEventSynchronize(s.done));
+    if (!pin_out) {
+      std::memcpy(out_t + s.lo, s.ht, s.cnt * sizeof(double));
+      std::memcpy(out_foot + s.lo * d, s.hfoot, s.cnt * d * sizeof(double));
+      std::memcpy(out_dist + s.lo, s.hdist, s.cnt * sizeof(double));
+      std::memcpy(out_cand + s.lo, s.hcand, s.cnt * sizeof(int64_t));
+      if (out_seg) std::memcpy(out_seg + s.lo, s.hseg, s.cnt * sizeof(int32_t));
+    }
+    s.busy = false;
+    return MREP_OK;
+  };
+
+  int64_t nchunks = (n + CHUNK - 1) / CHUNK;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    Slot& s = g_ctx.slot[c & 1];
+    if ((rc = write_back(s)) != MREP_OK) return rc;
+    s.lo = c * CHUNK;
+    s.cnt = (s.lo + CHUNK <= n) ? CHUNK : n - s.lo;
+    const double* src = queries + s.lo * d;
+    if (!pin_in) {
+      std::memcpy(s.hq, src, s.cnt * d * sizeof(double));
+      src = s.hq;
+    }
+    MREP_CUDA_CHECK(
+        cudaMemcpyAsync(s.dq, src, s.cnt * d * sizeof(double), cudaMemcpyHostToDevice, s.st));
+    rc = mrep_project(table, S, d, s.dq, s.cnt, clip_tol, max_iter, 0, flags, s.dt, s.dfoot,
+                      s.ddist, s.dcand, s.dseg, nullptr, nullptr, nullptr, s.st);
+    if (rc != MREP_OK) return rc;
+    double* ht = pin_out ? out_t + s.lo : s.ht;
+    double* hf = pin_out ? out_foot + s.lo * d : s.hfoot;
+    double* hd = pin_out ? out_dist + s.lo : s.hdist;
+    int64_t* hc = pin_out ? out_cand + s.lo : s.hcand;
+    int32_t* hs = pin_out ? (out_seg ? out_seg + s.lo : nullptr) : s.hseg;
+    MREP_CUDA_CHECK(cudaMemcpyAsync(ht, s.dt, s.cnt * sizeof(double), cudaMemcpyDeviceToHost, s.st));
+    MREP_CUDA_CHECK(
+        cudaMemcpyAsync(hf, s.dfoot, s.cnt * d * sizeof(double), cudaMemcpyDeviceToHost, s.st));
+    MREP_CUDA_CHECK(
+        cudaMemcpyAsync(hd, s.ddist, s.cnt * sizeof(double), cudaMemcpyDeviceToHost, s.st));
+    MREP_CUDA_CHECK(
+        cudaMemcpyAsync(hc, s.dcand, s.cnt * sizeof(int64_t), cudaMemcpyDeviceToHost, s.st));
+    if (hs)
+      MREP_CUDA_CHECK(
+          cudaMemcpyAsync(hs, s.dseg, s.cnt * sizeof(int32_t), cudaMemcpyDeviceToHost, s.st));
+    MREP_CUDA_CHECK(cudaEventRecord(s.done, s.st));
+    s.busy = true;
+  }
+  for (auto& s : g_ctx.slot)
+    if ((rc = write_back(s)) != MREP_OK) return rc;
+  return MREP_OK;
+}

@@ -1,0 +1,976 @@
+// mrep_project.cu -- batch point projection onto one prepared curve (sm_100a).
+//
+// Replaces the reference's fused per-query loop _kernels._project_block
+// (/root/reference/pkg/src/splinemat/_kernels.py:369-502) as driven by
+// project_prepared (project.py:245-289).
+//
+// Mapping: one query per thread; the per-(query, cubic) solve is the
+// register-resident routine chain of mrep_math.cuh on the FP64 pipe.
+// Two modes share the candidate generator:
+//   dense  (reference semantics): every seam and every cubic, with the six
+//          per-query stats columns and the soundness minimum;
+//   screen (MREP_SCREEN): an 8-ary AABB hierarchy over the cubics prunes
+//          every cubic whose box lower bound exceeds the running best
+//          candidate distance + the 1e-12 tie band (+ a rounding margin), so
+//          the winner -- and t, foot, dist, segment -- is the one dense mode
+//          finds; only the candidate count differs (documented in DESIGN.md).
+// Reduction: the reference's two-pass "min distance, then min t inside
+// dmin + 1e-12" (_kernels.py:480-490) is made streaming and order-free with a
+// 4-slot tie-band buffer keyed by each candidate's position in the
+// reference's candidate order; if more than 4 candidates share the band, the
+// query is re-run in an exact second pass with the final dmin.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <mutex>
+#include <string>
+
+#include "mrep_common.cuh"
+#include "mrep_math.cuh"
+
+namespace mrep {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+constexpr uint64_t SURV_BIT = 1ull << 62;
+constexpr int BAND_K = 4;
+constexpr int LIST_CAP = 32;
+constexpr int BLOCK = 128;
+
+struct ProjParams {
+  TableView tab;
+  const double* q;
+  int64_t n;
+  double clip_tol;
+  int max_iter;
+  int soundness;
+  double* out_t;
+  double* out_foot;
+  double* out_dist;
+  int64_t* out_cand;
+  int32_t* out_seg;
+  int64_t* out_stats;
+  double* out_sound;
+  uint64_t* counters;
+  unsigned long long* pass2_count;
+  int64_t* pass2_list;
+};
+
+// ------------------------------------------------------------ tie band
+struct Band {
+  double dmin, lim;
+  double t[BAND_K], d[BAND_K], v[BAND_K];
+  uint64_t ord[BAND_K];
+  unsigned valid;
+  bool overflow;
+  bool pass2;  // second pass: dmin/lim fixed, keep the single (t, ord) minimum
+};
+
+__device__ __forceinline__ void band_init(Band& B, bool pass2, double dmin2) {
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  B.valid = 0;
+  B.overflow = false;
+  B.pass2 = pass2;
+  B.dmin = pass2 ? dmin2 : INF;
+  B.lim = pass2 ? dmin2 + 1e-12 : INF;
+#pragma unroll
+  for (int j = 0; j < BAND_K; ++j) {
+    B.t[j] = INF;
+    B.d[j] = INF;
+    B.v[j] = 0.0;
+    B.ord[j] = ~0ull;
+  }
+}
+
+// Offer one candidate (t, d) with foot recipe v and reference order key ord.
+__device__ __forceinline__ void band_offer(Band& B, double t, double d, double v, uint64_t ord) {
+  if (!(d <= B.lim)) return;
+  if (B.pass2) {
+    if (t < B.t[0] || (t == B.t[0] && ord < B.ord[0])) {
+      B.t[0] = t;
+      B.d[0] = d;
+      B.v[0] = v;
+      B.ord[0] = ord;
+      B.valid = 1;
+    }
+    return;
+  }
+  if (d < B.dmin) {
+    B.dmin = d;
+    B.lim = d + 1e-12;
+#pragma unroll
+    for (int j = 0; j < BAND_K; ++j)
+      if (((B.valid >> j) & 1u) && B.d[j] > B.lim) B.valid &= ~(1u << j);
+  }
+#pragma unroll
+  for (int j = 0; j < BAND_K; ++j)
+    if (((B.valid >> j) & 1u) && B.ord[j] == ord) return;  // same candidate re-offered
+  bool placed = false;
+#pragma unroll
+  for (int j = 0; j < BAND_K; ++j) {
+    if (!placed && !((B.valid >> j) & 1u)) {
+      B.t[j] = t;
+      B.d[j] = d;
+      B.v[j] = v;
+      B.ord[j] = ord;
+      B.valid |= 1u << j;
+      placed = true;
+    }
+  }
+  if (!placed) B.overflow = true;
+}
+
+struct Pick {
+  double t, d, v;
+  uint64_t ord;
+  bool ok;
+};
+
+// min t inside the band, ties by reference order (_kernels.py:485-490);
+// select-based so the band never leaves registers
+__device__ __forceinline__ Pick band_pick(const Band& B) {
+  Pick p{0.0, 0.0, 0.0, 0ull, false};
+#pragma unroll
+  for (int j = 0; j < BAND_K; ++j) {
+    bool take = ((B.valid >> j) & 1u) &&
+                (!p.ok || B.t[j] < p.t || (B.t[j] == p.t && B.ord[j] < p.ord));
+    p.t = take ? B.t[j] : p.t;
+    p.d = take ? B.d[j] : p.d;
+    p.v = take ? B.v[j] : p.v;
+    p.ord = take ? B.ord[j] : p.ord;
+    p.ok = p.ok || take;
+  }
+  return p;
+}
+
+struct QStats {
+  int64_t pieces, c3l, c3g, cfl, cfg, noroot;
+  double sound;
+  uint64_t pairs, surv, clip_it, seams, boxes, offers;
+};
+
+// ------------------------------------------------------------ records
+template <int D>
+__device__ __forceinline__ void seam_point(const TableView& T, int64_t s, double (&pt)[D],
+                                           double& st) {
+  if (s == 0) {
+    st = T.hdr[0];
+#pragma unroll
+    for (int k = 0; k < D; ++k) pt[k] = T.hdr[1 + k];
+  } else {
+    const double* r = T.rec + (s - 1) * REC;
+    st = r[26];
+#pragma unroll
+    for (int k = 0; k < D; ++k) pt[k] = r[27 + k];
+  }
+}
+
+// _kernels.py:404-413 for one seam
+template <int D>
+__device__ __forceinline__ void offer_seam(const TableView& T, int64_t s, const double (&q)[D],
+                                           Band& B, QStats& st) {
+  double pt[D], stt;
+  seam_point<D>(T, s, pt, stt);
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    double diff = q[k] - pt[k];
+    acc += diff * diff;
+  }
+  st.seams++;
+  st.offers++;
+  band_offer(B, stt, sqrt(acc), -1.0, (uint64_t)s);
+}
+
+// _kernels.py:421-479 for one cubic s: E, E' roots, monotone pieces,
+// elimination, clipping, foot points; survivors are offered to the band.
+template <int D, bool STATS>
+__device__ __forceinline__ void solve_segment(const TableView& T, int64_t s, const double (&q)[D],
+                                              double clip_tol, int max_iter, int soundness,
+                                              Band& B, QStats& st) {
+  const double* r = T.rec + s * REC;
+  double w[4][D];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int dim = 0; dim < D; ++dim) w[k][dim] = __ldg(r + k * 3 + dim);
+  double e[6];
+  distance_poly_w<D>(w, q, e);
+  double ep[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) ep[k] = (double)(k + 1) * e[k + 1];
+  Roots4 rt = quartic_roots_01(ep);
+  // interior split points (1e-10 < r < 1 - 1e-10), compacted in order
+  double b1 = 1.0, b2 = 1.0, b3 = 1.0, b4 = 1.0;
+  int nin = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double x = rt.r[i];
+    if (i < rt.count && 1e-10 < x && x < 1.0 - 1e-10) {
+      b1 = (nin == 0) ? x : b1;
+      b2 = (nin == 1) ? x : b2;
+      b3 = (nin == 2) ? x : b3;
+      b4 = (nin == 3) ? x : b4;
+      ++nin;
+    }
+  }
+  double bseg[6];
+  rebase5(e, bseg);
+  st.pairs++;
+  double lo = 0.0;
+  for (int k = 0; k <= nin; ++k) {
+    double hi = (k == nin) ? 1.0 : (k == 0 ? b1 : (k == 1 ? b2 : (k == 2 ? b3 : b4)));
+    double bp[6];
+    restrict_ordinates(bseg, lo, hi, bp);
+    if (!(bp[0] < 0.0 && bp[0] * bp[5] <= 0.0)) {
+      if (STATS && soundness > 0) {
+        for (int si = 0; si < soundness; ++si) {
+          double v = lo + (hi - lo) * (double)si / ((double)soundness - 1.0);
+          double acc = 0.0;
+#pragma unroll
+          for (int dim = 0; dim < D; ++dim) {
+            double f = decasteljau1(__ldg(r + 12 + dim), __ldg(r + 15 + dim), __ldg(r + 18 + dim),
+                                    __ldg(r + 21 + dim), v);
+            double diff = q[dim] - f;
+            acc += diff * diff;
+          }
+          if (acc < st.sound) st.sound = acc;
+        }
+      }
+      lo = hi;
+      continue;
+    }
+    if (STATS) st.pieces++;
+    ClipOut co = clip_root(bp, clip_tol, max_iter);
+    st.surv++;
+    st.clip_it += (uint64_t)co.used;
+    if (!co.ok) {
+      if (STATS) st.noroot++;
+      lo = hi;
+      continue;
+    }
+    double ta = __ldg(r + 24), tb = __ldg(r + 25);
+    if (STATS) {
+      double gscale = (hi - lo) * (tb - ta);
+      if (co.w3 <= clip_tol) st.c3l++;
+      if (co.w3 * gscale <= clip_tol) st.c3g++;
+      if (co.wf <= clip_tol) st.cfl++;
+      if (co.wf * gscale <= clip_tol) st.cfg++;
+    }
+    double v = lo + co.root * (hi - lo);
+    double acc = 0.0;
+#pragma unroll
+    for (int dim = 0; dim < D; ++dim) {
+      double f = decasteljau1(__ldg(r + 12 + dim), __ldg(r + 15 + dim), __ldg(r + 18 + dim),
+                              __ldg(r + 21 + dim), v);
+      double diff = q[dim] - f;
+      acc += diff * diff;
+    }
+    st.offers++;
+    band_offer(B, ta + v * (tb - ta), sqrt(acc), v, SURV_BIT | ((uint64_t)s << 3) | (uint64_t)k);
+    lo = hi;
+  }
+}
+
+// ------------------------------------------------------------ screening
+template <int D>
+__device__ __forceinline__ double box_lb2(const TableView& T, int64_t box, const double (&q)[D]) {
+  const double* b = T.box + box * 6;
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    double g = fmax(0.0, fmax(__ldg(b + k) - q[k], q[k] - __ldg(b + 3 + k)));
+    acc += g * g;
+  }
+  return acc;
+}
+
+// Cut-off radius: a box whose lower bound exceeds it cannot hold a candidate
+// inside dmin + 1e-12 (margins cover rounding of the box bound and of the
+// foot-point evaluation; they only ever keep extra work).
+__device__ __forceinline__ double cut2(double dmin, double scale) {
+  double c = dmin * (1.0 + 1e-7) + 1e-11 + 1e-13 * scale;
+  return c * c;
+}
+
+template <int D>
+__device__ __forceinline__ uint32_t child_mask(const TableView& T, int level, int64_t idx,
+                                               const double (&q)[D], double c2, QStats& st) {
+  // children of node idx at `level` live at level-1, indices idx*8 + c
+  uint32_t m = 0;
+  int64_t first = idx * FANOUT;
+  int64_t cnt = T.lvl_cnt[level - 1];
+  int64_t off = T.lvl_off[level - 1];
+#pragma unroll
+  for (int c = 0; c < FANOUT; ++c) {
+    int64_t ch = first + c;
+    if (ch < cnt) {
+      st.boxes++;
+      if (box_lb2<D>(T, off + ch, q) <= c2) m |= 1u << c;
+    }
+  }
+  return m;
+}
+
+template <int D, bool STATS>
+__device__ void gen_screened(const TableView& T, const double (&q)[D], double scale,
+                             double clip_tol, int max_iter, Band& B, QStats& st) {
+  // 1) greedy descent to a nearby cubic: its seams give the first upper bound
+  {
+    int level = T.top;
+    int64_t idx = 0;
+    while (level > 0) {
+      int64_t first = idx * FANOUT, cnt = T.lvl_cnt[level - 1], off = T.lvl_off[level - 1];
+      double best = 0.0;
+      int64_t bi = first;
+      for (int c = 0; c < FANOUT; ++c) {
+        int64_t ch = first + c;
+        if (ch < cnt) {
+          st.boxes++;
+          double lb = box_lb2<D>(T, off + ch, q);
+          if (c == 0 || lb < best) {
+            best = lb;
+            bi = ch;
+          }
+        }
+      }
+      idx = bi;
+      --level;
+    }
+    offer_seam<D>(T, idx, q, B, st);
+    offer_seam<D>(T, idx + 1, q, B, st);
+  }
+  // 2) depth-first traversal with 8-bit child masks per level; surviving
+  //    leaf cubics are queued and solved in batches of LIST_CAP (one call
+  //    site for the solve keeps the instruction footprint small)
+  int64_t list[LIST_CAP];
+  uint64_t masks = 0;
+  int level = T.top;
+  int64_t idx = 0;
+  masks = (uint64_t)child_mask<D>(T, level, 0, q, cut2(B.dmin, scale), st) << (8 * level);
+  bool done = false;
+  while (!done) {
+    int nlist = 0;
+    while (nlist < LIST_CAP) {
+      uint32_t mk = (uint32_t)(masks >> (8 * level)) & 0xffu;
+      if (mk == 0) {
+        if (level == T.top) {
+          done = true;
+          break;
+        }
+        ++level;
+        idx /= FANOUT;
+        continue;
+      }
+      int c = __ffs(mk) - 1;
+      masks &= ~(1ull << (8 * level + c));
+      int64_t ch = idx * FANOUT + c;
+      double c2 = cut2(B.dmin, scale);
+      st.boxes++;
+      if (level - 1 == 0) {
+        // leaf cubic: re-test with the current bound, queue it, offer its seams
+        if (box_lb2<D>(T, T.lvl_off[0] + ch, q) <= c2) {
+          offer_seam<D>(T, ch, q, B, st);
+          offer_seam<D>(T, ch + 1, q, B, st);
+          list[nlist++] = ch;
+        }
+      } else if (box_lb2<D>(T, T.lvl_off[level - 1] + ch, q) <= c2) {
+        --level;
+        idx = ch;
+        masks |= (uint64_t)child_mask<D>(T, level, idx, q, c2, st) << (8 * level);
+      }
+    }
+    // 3) exact solve of the queued cubics that still pass the current bound
+    for (int i = 0; i < nlist; ++i) {
+      st.boxes++;
+      if (box_lb2<D>(T, T.lvl_off[0] + list[i], q) <= cut2(B.dmin, scale))
+        solve_segment<D, STATS>(T, list[i], q, clip_tol, max_iter, 0, B, st);
+    }
+  }
+}
+
+template <int D, bool STATS>
+__device__ void gen_dense(const TableView& T, const double (&q)[D], double clip_tol, int max_iter,
+                          int soundness, Band& B, QStats& st) {
+  for (int64_t s = 0; s <= T.S; ++s) offer_seam<D>(T, s, q, B, st);
+  for (int64_t s = 0; s < T.S; ++s)
+    solve_segment<D, STATS>(T, s, q, clip_tol, max_iter, soundness, B, st);
+}
+
+__device__ __forceinline__ void warp_count(uint64_t* counters, int slot, uint64_t v) {
+  if (!counters) return;
+  unsigned lo = (unsigned)(v & 0xffffffffu), hi = (unsigned)(v >> 32);
+  unsigned mask = __activemask();
+  unsigned slo = __reduce_add_sync(mask, lo);
+  unsigned shi = __reduce_add_sync(mask, hi);
+  int leader = __ffs(mask) - 1;
+  if ((threadIdx.x & 31) == leader)
+    atomicAdd((unsigned long long*)&counters[slot], (unsigned long long)slo +
+                                                        ((unsigned long long)shi << 32));
+}
+
+template <int D>
+__device__ __forceinline__ void write_winner(const ProjParams& p, int64_t qi, const Pick& w) {
+  const TableView& T = p.tab;
+  const double NaN = __longlong_as_double(0x7ff8000000000000LL);
+  if (!w.ok) {
+    p.out_t[qi] = NaN;
+    p.out_dist[qi] = NaN;
+#pragma unroll
+    for (int k = 0; k < D; ++k) p.out_foot[qi * D + k] = NaN;
+    if (p.out_seg) p.out_seg[qi] = -1;
+    return;
+  }
+  uint64_t ord = w.ord;
+  double foot[D];
+  int32_t seg;
+  if (ord & SURV_BIT) {
+    int64_t s = (int64_t)((ord & ~SURV_BIT) >> 3);
+    const double* r = T.rec + s * REC;
+    double v = w.v;
+#pragma unroll
+    for (int dim = 0; dim < D; ++dim)
+      foot[dim] = decasteljau1(r[12 + dim], r[15 + dim], r[18 + dim], r[21 + dim], v);
+    seg = (int32_t)s;
+  } else {
+    int64_t s = (int64_t)ord;
+    double stt;
+    seam_point<D>(T, s, foot, stt);
+    seg = (int32_t)(s > 0 ? s - 1 : 0);
+  }
+  p.out_t[qi] = w.t;
+  p.out_dist[qi] = w.d;
+#pragma unroll
+  for (int k = 0; k < D; ++k) p.out_foot[qi * D + k] = foot[k];
+  if (p.out_seg) p.out_seg[qi] = seg;
+}
+
+template <int D, bool SCREEN, bool STATS>
+__global__ void __launch_bounds__(BLOCK) project_kernel(ProjParams p) {
+  int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool active = qi < p.n;
+  QStats st{};
+  st.sound = __longlong_as_double(0x7ff0000000000000LL);
+  if (active) {
+    double q[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) q[k] = p.q[qi * D + k];
+    Band B;
+    band_init(B, false, 0.0);
+    if (SCREEN) {
+      double scale = p.tab.hdr[4];
+#pragma unroll
+      for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
+      gen_screened<D, STATS>(p.tab, q, scale, p.clip_tol, p.max_iter, B, st);
+    } else {
+      gen_dense<D, STATS>(p.tab, q, p.clip_tol, p.max_iter, p.soundness, B, st);
+    }
+    if (B.overflow) {
+      // more than BAND_K candidates inside the tie band: exact second pass
+      p.out_dist[qi] = B.dmin;
+      unsigned long long slot = atomicAdd(p.pass2_count, 1ull);
+      p.pass2_list[slot] = qi;
+      if (p.out_seg) p.out_seg[qi] = -2;
+    } else {
+      write_winner<D>(p, qi, band_pick(B));
+    }
+    if (p.out_cand) p.out_cand[qi] = (int64_t)(SCREEN ? st.offers : (uint64_t)(p.tab.S + 1) + st.offers - st.seams);
+    if (STATS) {
+      if (p.out_stats) {
+        int64_t* o = p.out_stats + qi * 6;
+        o[0] = st.pieces;
+        o[1] = st.c3l;
+        o[2] = st.c3g;
+        o[3] = st.cfl;
+        o[4] = st.cfg;
+        o[5] = st.noroot;
+      }
+      if (p.out_sound) p.out_sound[qi] = st.sound;
+    }
+  }
+  warp_count(p.counters, MREP_CNT_PAIRS, st.pairs);
+  warp_count(p.counters, MREP_CNT_SURVIVORS, st.surv);
+  warp_count(p.counters, MREP_CNT_CLIP_ITERS, st.clip_it);
+  warp_count(p.counters, MREP_CNT_SEAMS, st.seams);
+  warp_count(p.counters, MREP_CNT_BOXES, st.boxes);
+}
+
+template <int D, bool SCREEN>
+__global__ void __launch_bounds__(BLOCK) project_pass2_kernel(ProjParams p) {
+  unsigned long long total = *p.pass2_count;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    int64_t qi = p.pass2_list[i];
+    double q[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) q[k] = p.q[qi * D + k];
+    Band B;
+    band_init(B, true, p.out_dist[qi]);
+    QStats st{};
+    st.sound = 0.0;
+    if (SCREEN) {
+      double scale = p.tab.hdr[4];
+#pragma unroll
+      for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
+      gen_screened<D, false>(p.tab, q, scale, p.clip_tol, p.max_iter, B, st);
+    } else {
+      gen_dense<D, false>(p.tab, q, p.clip_tol, p.max_iter, 0, B, st);
+    }
+    write_winner<D>(p, qi, Pick{B.t[0], B.d[0], B.v[0], B.ord[0], B.valid != 0});
+  }
+  if (p.counters && blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd((unsigned long long*)&p.counters[MREP_CNT_PASS2], total);
+}
+
+// ------------------------------------------------------------ table build
+__global__ void pack_records_kernel(const double* seg_pts, const double* seg_ta,
+                                    const double* seg_tb, const double* seam_t,
+                                    const double* seam_pt, int64_t S, int d, double* hdr,
+                                    double* rec, double* box0) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s == 0) {
+    hdr[0] = seam_t[0];
+    for (int k = 0; k < 3; ++k) hdr[1 + k] = k < d ? seam_pt[k] : 0.0;
+  }
+  if (s >= S) return;
+  double* r = rec + s * REC;
+  double P[4][3];
+  for (int j = 0; j < 4; ++j)
+    for (int k = 0; k < 3; ++k) P[j][k] = k < d ? seg_pts[(s * 4 + j) * d + k] : 0.0;
+  double amax = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    double w0, w1, w2, w3;
+    cubic_power_coeffs(P[0][k], P[1][k], P[2][k], P[3][k], w0, w1, w2, w3);
+    r[0 * 3 + k] = w0;
+    r[1 * 3 + k] = w1;
+    r[2 * 3 + k] = w2;
+    r[3 * 3 + k] = w3;
+    double lo = P[0][k], hi = P[0][k];
+    for (int j = 0; j < 4; ++j) {
+      r[12 + j * 3 + k] = P[j][k];
+      lo = fmin(lo, P[j][k]);
+      hi = fmax(hi, P[j][k]);
+      amax = fmax(amax, fabs(P[j][k]));
+    }
+    box0[s * 6 + k] = lo;
+    box0[s * 6 + 3 + k] = hi;
+  }
+  r[24] = seg_ta[s];
+  r[25] = seg_tb[s];
+  r[26] = seam_t[s + 1];
+  for (int k = 0; k < 3; ++k) r[27 + k] = k < d ? seam_pt[(s + 1) * d + k] : 0.0;
+  r[30] = 0.0;
+  r[31] = 0.0;
+  // header[4]: max |coordinate| (positive doubles order like their bit patterns)
+  atomicMax((unsigned long long*)&hdr[4], (unsigned long long)__double_as_longlong(amax));
+}
+
+__global__ void reduce_boxes_kernel(const double* child, int64_t nchild, double* parent,
+                                    int64_t nparent) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nparent) return;
+  double lo[3], hi[3];
+  for (int k = 0; k < 3; ++k) {
+    lo[k] = child[i * FANOUT * 6 + k];
+    hi[k] = child[i * FANOUT * 6 + 3 + k];
+  }
+  for (int c = 1; c < FANOUT; ++c) {
+    int64_t ch = i * FANOUT + c;
+    if (ch >= nchild) break;
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = fmin(lo[k], child[ch * 6 + k]);
+      hi[k] = fmax(hi[k], child[ch * 6 + 3 + k]);
+    }
+  }
+  for (int k = 0; k < 3; ++k) {
+    parent[i * 6 + k] = lo[k];
+    parent[i * 6 + 3 + k] = hi[k];
+  }
+}
+
+__global__ void knot_span_kernel(const double* knots, int64_t m, int p, const double* t, int64_t n,
+                                 int32_t* span) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double x = t[i];
+  // searchsorted(knots, x, 'right'): first index with knots[idx] > x
+  int64_t lo = 0, hi = m;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (knots[mid] <= x) lo = mid + 1;
+    else hi = mid;
+  }
+  int64_t s = lo - 1;
+  int64_t last = m - p - 2;
+  if (s < p) s = p;
+  if (s > last) s = last;
+  span[i] = (int32_t)s;
+}
+
+// ------------------------------------------------------------ per-op kernels
+__global__ void quartic_kernel(const double* c, int64_t n, double* roots, int64_t* counts) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double cc[5];
+  for (int k = 0; k < 5; ++k) cc[k] = c[i * 5 + k];
+  Roots4 r = quartic_roots_01(cc);
+  counts[i] = r.count;
+  for (int k = 0; k < 4; ++k)
+    if (k < r.count) roots[i * 4 + k] = r.r[k];
+}
+
+// _kernels.py:515-566
+__global__ void newton_quartic_kernel(const double* cp, int64_t n, double* roots, int64_t* counts) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double c[5];
+  for (int k = 0; k < 5; ++k) c[k] = cp[i * 5 + k];
+  double scale = 0.0;
+  for (int j = 0; j < 5; ++j)
+    if (fabs(c[j]) > scale) scale = fabs(c[j]);
+  double found[8];
+  int nf = 0;
+  for (int s = 0; s < 8; ++s) {
+    double x = (double)s / 7.0;
+    bool conv = false;
+    for (int it = 0; it < 40; ++it) {
+      double f = c[0] + x * (c[1] + x * (c[2] + x * (c[3] + x * c[4])));
+      double df = c[1] + x * (2.0 * c[2] + x * (3.0 * c[3] + x * 4.0 * c[4]));
+      if (df == 0.0) break;
+      double step = f / df;
+      x -= step;
+      if (fabs(step) < 1e-14) {
+        conv = true;
+        break;
+      }
+    }
+    if (!conv) continue;
+    double f = c[0] + x * (c[1] + x * (c[2] + x * (c[3] + x * c[4])));
+    if (fabs(f) <= 1e-9 * scale && -1e-12 <= x && x <= 1.0 + 1e-12) {
+      if (x < 0.0) x = 0.0;
+      else if (x > 1.0) x = 1.0;
+      bool dup = false;
+      for (int k = 0; k < nf; ++k)
+        if (fabs(found[k] - x) <= 1e-10) dup = true;
+      if (!dup && nf < 8) found[nf++] = x;
+    }
+  }
+  for (int a = 1; a < nf; ++a) {
+    double x = found[a];
+    int b = a - 1;
+    while (b >= 0 && found[b] > x) {
+      found[b + 1] = found[b];
+      --b;
+    }
+    found[b + 1] = x;
+  }
+  int keep = nf < 4 ? nf : 4;
+  counts[i] = keep;
+  for (int k = 0; k < keep; ++k) roots[i * 4 + k] = found[k];
+}
+
+__global__ void distance_poly_kernel(const double* P, const double* q, int64_t n, int d,
+                                     double* e) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double ee[6];
+  if (d == 3) {
+    double w[4][3], qq[3];
+    for (int k = 0; k < 3; ++k) {
+      cubic_power_coeffs(P[(i * 4 + 0) * 3 + k], P[(i * 4 + 1) * 3 + k], P[(i * 4 + 2) * 3 + k],
+                         P[(i * 4 + 3) * 3 + k], w[0][k], w[1][k], w[2][k], w[3][k]);
+      qq[k] = q[i * 3 + k];
+    }
+    distance_poly_w<3>(w, qq, ee);
+  } else {
+    double w[4][2], qq[2];
+    for (int k = 0; k < 2; ++k) {
+      cubic_power_coeffs(P[(i * 4 + 0) * 2 + k], P[(i * 4 + 1) * 2 + k], P[(i * 4 + 2) * 2 + k],
+                         P[(i * 4 + 3) * 2 + k], w[0][k], w[1][k], w[2][k], w[3][k]);
+      qq[k] = q[i * 2 + k];
+    }
+    distance_poly_w<2>(w, qq, ee);
+  }
+  for (int k = 0; k < 6; ++k) e[i * 6 + k] = ee[k];
+}
+
+__global__ void restrict_kernel(const double* b, const double* lo, const double* hi, int64_t n,
+                                double* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double bb[6], o[6];
+  for (int k = 0; k < 6; ++k) bb[k] = b[i * 6 + k];
+  restrict_ordinates(bb, lo[i], hi[i], o);
+  for (int k = 0; k < 6; ++k) out[i * 6 + k] = o[k];
+}
+
+__global__ void eval_ord_kernel(const double* b, const double* u, int64_t n, double* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double bb[6];
+  for (int k = 0; k < 6; ++k) bb[k] = b[i * 6 + k];
+  out[i] = eval_ordinates(bb, u[i]);
+}
+
+__global__ void hull_kernel(const double* b, int64_t n, int32_t* found, double* z) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double bb[6];
+  for (int k = 0; k < 6; ++k) bb[k] = b[i * 6 + k];
+  double z1, z2;
+  found[i] = hull_cross(bb, z1, z2) ? 1 : 0;
+  z[i * 2] = z1;
+  z[i * 2 + 1] = z2;
+}
+
+// full widths array variant of clip_root for the per-op API (_kernels.py:306-341)
+__global__ void clip_kernel(const double* b, int64_t n, double tol, int max_iter, double* root,
+                            int32_t* okp, int32_t* usedp, double* widths) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double cur[6];
+  for (int k = 0; k < 6; ++k) cur[k] = b[i * 6 + k];
+  double* w = widths + i * max_iter;
+  double lo = 0.0, hi = 1.0;
+  int used = 0;
+  for (int it = 0; it < max_iter; ++it) {
+    double z1, z2;
+    if (!hull_cross(cur, z1, z2)) {
+      for (int k = it; k < max_iter; ++k) w[k] = hi - lo;
+      root[i] = 0.5 * (lo + hi);
+      okp[i] = 0;
+      usedp[i] = it;
+      return;
+    }
+    used = it + 1;
+    double nlo = lo + z1 * (hi - lo), nhi = lo + z2 * (hi - lo);
+    if (z2 - z1 < 1e-15) {
+      for (int k = it; k < max_iter; ++k) w[k] = 0.0;
+      root[i] = nlo;
+      okp[i] = 1;
+      usedp[i] = used;
+      return;
+    }
+    restrict_ordinates(cur, z1, z2, cur);
+    lo = nlo;
+    hi = nhi;
+    w[it] = hi - lo;
+    if (hi - lo <= tol) {
+      for (int k = it + 1; k < max_iter; ++k) w[k] = hi - lo;
+      root[i] = 0.5 * (lo + hi);
+      okp[i] = 1;
+      usedp[i] = used;
+      return;
+    }
+  }
+  root[i] = 0.5 * (lo + hi);
+  okp[i] = 1;
+  usedp[i] = used;
+}
+
+__global__ void cubic_points_kernel(const double* P, const double* u, int64_t n, int d,
+                                    double* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double uu = u[i];
+  for (int k = 0; k < d; ++k)
+    out[i * d + k] = decasteljau1(P[(i * 4 + 0) * d + k], P[(i * 4 + 1) * d + k],
+                                  P[(i * 4 + 2) * d + k], P[(i * 4 + 3) * d + k], uu);
+}
+
+__global__ void rebase_kernel(const double* e, int64_t n, double* b) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double ee[6], bb[6];
+  for (int k = 0; k < 6; ++k) ee[k] = e[i * 6 + k];
+  rebase5(ee, bb);
+  for (int k = 0; k < 6; ++k) b[i * 6 + k] = bb[k];
+}
+
+// ------------------------------------------------------------ launch helpers
+template <int D>
+static int launch_project(const ProjParams& p, unsigned flags, cudaStream_t st) {
+  unsigned grid = grid_for(p.n, BLOCK);
+  bool screen = (flags & MREP_SCREEN) && !(flags & MREP_STATS);
+  bool stats = (flags & MREP_STATS) != 0;
+  if (screen) project_kernel<D, true, false><<<grid, BLOCK, 0, st>>>(p);
+  else if (stats) project_kernel<D, false, true><<<grid, BLOCK, 0, st>>>(p);
+  else project_kernel<D, false, false><<<grid, BLOCK, 0, st>>>(p);
+  MREP_LAUNCH_CHECK();
+  unsigned g2 = grid < 148u * 4u ? grid : 148u * 4u;
+  if (screen) project_pass2_kernel<D, true><<<g2, BLOCK, 0, st>>>(p);
+  else project_pass2_kernel<D, false><<<g2, BLOCK, 0, st>>>(p);
+  MREP_LAUNCH_CHECK();
+  return MREP_OK;
+}
+
+}  // namespace mrep
+
+using namespace mrep;
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* mrep_last_error(void) { return g_last_error.c_str(); }
+int mrep_version(void) { return 100; }
+int mrep_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int64_t mrep_table_bytes(int64_t S) {
+  if (S < 1) return -1;
+  return table_layout(S).total_doubles * (int64_t)sizeof(double);
+}
+
+int mrep_table_pack(const double* seg_pts, const double* seg_ta, const double* seg_tb,
+                    const double* seam_t, const double* seam_pt, int64_t S, int d, void* table,
+                    void* stream) {
+  if (S < 1 || (d != 2 && d != 3) || !table) {
+    set_error("mrep_table_pack: need S >= 1, d in {2,3}");
+    return MREP_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  TableLayout L = table_layout(S);
+  double* base = (double*)table;
+  MREP_CUDA_CHECK(cudaMemsetAsync(base, 0, HDR * sizeof(double), st));
+  double* box = base + L.box_off;
+  pack_records_kernel<<<grid_for(S, 128), 128, 0, st>>>(seg_pts, seg_ta, seg_tb, seam_t, seam_pt,
+                                                        S, d, base, base + L.rec_off,
+                                                        box + L.lvl_off[0]);
+  MREP_LAUNCH_CHECK();
+  for (int lv = 1; lv <= L.top; ++lv) {
+    reduce_boxes_kernel<<<grid_for(L.lvl_cnt[lv], 128), 128, 0, st>>>(
+        box + L.lvl_off[lv - 1] * 6, L.lvl_cnt[lv - 1], box + L.lvl_off[lv] * 6, L.lvl_cnt[lv]);
+    MREP_LAUNCH_CHECK();
+  }
+  return MREP_OK;
+}
+
+int mrep_project(const void* table, int64_t S, int d, const double* queries, int64_t n,
+                 double clip_tol, int max_iter, int soundness_samples, unsigned flags,
+                 double* out_t, double* out_foot, double* out_dist, int64_t* out_cand,
+                 int32_t* out_seg, int64_t* out_stats, double* out_sound, uint64_t* counters,
+                 void* stream) {
+  if (S < 1 || (d != 2 && d != 3) || n < 0 || max_iter < 1 || !table) {
+    set_error("mrep_project: bad arguments (S >= 1, d in {2,3}, max_iter >= 1)");
+    return MREP_ERR_ARG;
+  }
+  if (n == 0) return MREP_OK;
+  if (!queries || !out_t || !out_foot || !out_dist) {
+    set_error("mrep_project: null query/output pointer");
+    return MREP_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  ProjParams p{};
+  p.tab = table_view(table, S);
+  p.q = queries;
+  p.n = n;
+  p.clip_tol = clip_tol;
+  p.max_iter = max_iter;
+  p.soundness = soundness_samples;
+  p.out_t = out_t;
+  p.out_foot = out_foot;
+  p.out_dist = out_dist;
+  p.out_cand = out_cand;
+  p.out_seg = out_seg;
+  p.out_stats = out_stats;
+  p.out_sound = out_sound;
+  p.counters = counters;
+  void* ws = nullptr;
+  size_t wsb = sizeof(unsigned long long) * 2 + sizeof(int64_t) * (size_t)n;
+  MREP_CUDA_CHECK(cudaMallocAsync(&ws, wsb, st));
+  p.pass2_count = (unsigned long long*)ws;
+  p.pass2_list = (int64_t*)((char*)ws + 16);
+  MREP_CUDA_CHECK(cudaMemsetAsync(ws, 0, 16, st));
+  int rc = d == 3 ? launch_project<3>(p, flags, st) : launch_project<2>(p, flags, st);
+  MREP_CUDA_CHECK(cudaFreeAsync(ws, st));
+  return rc;
+}
+
+int mrep_project_block(const double* seg_pts, const double* seg_ta, const double* seg_tb,
+                       const double* seam_t, const double* seam_pt, int64_t S, int d,
+                       const double* queries, int64_t n, double clip_tol, int max_iter,
+                       int soundness_samples, double* out_t, double* out_foot, double* out_dist,
+                       int64_t* out_cand, int64_t* out_stats, double* out_sound, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t bytes = mrep_table_bytes(S);
+  if (bytes < 0) {
+    set_error("mrep_project_block: S must be >= 1");
+    return MREP_ERR_ARG;
+  }
+  void* table = nullptr;
+  MREP_CUDA_CHECK(cudaMallocAsync(&table, (size_t)bytes, st));
+  int rc = mrep_table_pack(seg_pts, seg_ta, seg_tb, seam_t, seam_pt, S, d, table, stream);
+  if (rc == MREP_OK)
+    rc = mrep_project(table, S, d, queries, n, clip_tol, max_iter, soundness_samples, MREP_STATS,
+                      out_t, out_foot, out_dist, out_cand, nullptr, out_stats, out_sound, nullptr,
+                      stream);
+  cudaFreeAsync(table, st);
+  return rc;
+}
+
+int mrep_knot_span(const double* knots, int64_t m, int p, const double* t, int64_t n,
+                   int32_t* span, void* stream) {
+  if (n <= 0) return MREP_OK;
+  knot_span_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(knots, m, p, t, n, span);
+  MREP_LAUNCH_CHECK();
+  return MREP_OK;
+}
+
+#define MREP_SIMPLE_LAUNCH(kern, n, ...)                                           \
+  do {                                                                             \
+    if ((n) <= 0) return MREP_OK;                                                  \
+    kern<<<grid_for((n), 128), 128, 0, (cudaStream_t)stream>>>(__VA_ARGS__);       \
+    MREP_LAUNCH_CHECK();                                                           \
+    return MREP_OK;                                                                \
+  } while (0)
+
+int mrep_quartic_roots(const double* c, int64_t n, double* roots, int64_t* counts, void* stream) {
+  MREP_SIMPLE_LAUNCH(quartic_kernel, n, c, n, roots, counts);
+}
+int mrep_newton_quartic_roots(const double* c, int64_t n, double* roots, int64_t* counts,
+                              void* stream) {
+  MREP_SIMPLE_LAUNCH(newton_quartic_kernel, n, c, n, roots, counts);
+}
+int mrep_distance_poly(const double* P, const double* q, int64_t n, int d, double* e,
+                       void* stream) {
+  if (d != 2 && d != 3) {
+    set_error("mrep_distance_poly: d must be 2 or 3");
+    return MREP_ERR_ARG;
+  }
+  MREP_SIMPLE_LAUNCH(distance_poly_kernel, n, P, q, n, d, e);
+}
+int mrep_restrict_ordinates(const double* b, const double* lo, const double* hi, int64_t n,
+                            double* out, void* stream) {
+  MREP_SIMPLE_LAUNCH(restrict_kernel, n, b, lo, hi, n, out);
+}
+int mrep_eval_ordinates(const double* b, const double* u, int64_t n, double* out, void* stream) {
+  MREP_SIMPLE_LAUNCH(eval_ord_kernel, n, b, u, n, out);
+}
+int mrep_hull_cross(const double* b, int64_t n, int32_t* found, double* z, void* stream) {
+  MREP_SIMPLE_LAUNCH(hull_kernel, n, b, n, found, z);
+}
+int mrep_clip_root(const double* b, int64_t n, double tol, int max_iter, double* root, int32_t* ok,
+                   int32_t* used, double* widths, void* stream) {
+  if (max_iter < 1) {
+    set_error("mrep_clip_root: max_iter must be >= 1");
+    return MREP_ERR_ARG;
+  }
+  MREP_SIMPLE_LAUNCH(clip_kernel, n, b, n, tol, max_iter, root, ok, used, widths);
+}
+int mrep_cubic_points(const double* P, const double* u, int64_t n, int d, double* out,
+                      void* stream) {
+  MREP_SIMPLE_LAUNCH(cubic_points_kernel, n, P, u, n, d, out);
+}
+int mrep_rebase(const double* e, int64_t n, double* b, void* stream) {
+  MREP_SIMPLE_LAUNCH(rebase_kernel, n, e, n, b);
+}
+
+}  // extern "C"
