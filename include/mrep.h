@@ -46,6 +46,7 @@ extern "C" {
 #define MREP_CNT_SEAMS 3      /* seam-distance evaluations */
 #define MREP_CNT_BOXES 4      /* BVH box lower-bound tests */
 #define MREP_CNT_PASS2 5      /* queries that needed the exact tie-band second pass */
+#define MREP_CNT_HULL_MISS 6  /* surviving pieces whose hull never crossed (NoRoot, project.py:282-283) */
 #define MREP_NUM_COUNTERS 8
 
 MREP_API const char* mrep_last_error(void);
@@ -81,11 +82,12 @@ MREP_API int mrep_project(const void* table_dev, int64_t S, int d, const double*
 
 /* Same, HOST buffers in and out (the end-to-end call): chunked H2D / kernel /
  * D2H pipeline on two internal streams; synchronous on return.
- * out_seg_host may be NULL. */
+ * out_seg_host and counters_host (MREP_NUM_COUNTERS uint64, accumulated)
+ * may be NULL. */
 MREP_API int mrep_project_host(const void* table_dev, int64_t S, int d, const double* queries_host,
                       int64_t n, double clip_tol, int max_iter, unsigned flags,
                       double* out_t_host, double* out_foot_host, double* out_dist_host,
-                      int64_t* out_cand_host, int32_t* out_seg_host);
+                      int64_t* out_cand_host, int32_t* out_seg_host, uint64_t* counters_host);
 
 /* Exact drop-in for _kernels._project_block (_kernels.py:369-371): the raw
  * prepared arrays, all DEVICE pointers, brute force with stats. */
@@ -130,6 +132,78 @@ MREP_API int mrep_cubic_points(const double* P_dev /*[n][4][d]*/, const double* 
                       double* out_dev /*[n][d]*/, void* stream);
 /* project.rebase_batch (project.py:134-137): b = T5 e */
 MREP_API int mrep_rebase(const double* e_dev /*[n][6]*/, int64_t n, double* b_dev, void* stream);
+
+
+/* ---------------------------------------------------------------------
+ * Per-curve preprocessing (batched over curves).  Curves are CSR device
+ * arrays: degree[nc] (int32), knot_ofs[nc+1] / knots, ctrl_ofs[nc+1] (row
+ * offsets) / ctrl [rows][d].
+ * ------------------------------------------------------------------- */
+/* Plan for decompose_to_bezier / batched_decompose (decompose.py:19-67):
+ * per-curve nonzero-span counts scanned into seg_ofs[nc+1] and the Bezier
+ * row base row_base[nc+1] (device, caller-allocated); totals to the host. */
+MREP_API int mrep_decompose_plan(const int32_t* degree, const int64_t* knot_ofs,
+                                 const double* knots, int64_t nc, int64_t* seg_ofs,
+                                 int64_t* row_base, int64_t* total_segs_host,
+                                 int64_t* total_rows_host, void* stream);
+/* Span decomposition Q = T_p diag(h^k) A_q P (decompose.py:36-45): outputs
+ * out_rows [total_rows][d], out_row_ofs [nseg+1], out_iv [nseg][2],
+ * out_curve [nseg], out_span [nseg] (knot span q of each segment). */
+MREP_API int mrep_decompose(const int32_t* degree, const int64_t* knot_ofs, const double* knots,
+                            const int64_t* ctrl_ofs, const double* ctrl, int64_t nc, int d,
+                            const int64_t* seg_ofs, const int64_t* row_base, int64_t nseg,
+                            double* out_rows, int64_t* out_row_ofs, double* out_iv,
+                            int32_t* out_curve, int32_t* out_span, void* stream);
+/* core.eval_bezier (core.py:248-258): one Bezier of `degree` at m params */
+MREP_API int mrep_eval_bezier(const double* pts, int degree, int d, const double* u, int64_t m,
+                              double* out, void* stream);
+/* oracle.eval_de_boor_many (oracle.py:45-52): curve points at nt params */
+MREP_API int mrep_eval_curve(int p, const double* knots, int64_t m, const double* ctrl,
+                             int64_t ncp, int d, const double* ts, int64_t nt, double* out,
+                             void* stream);
+
+/* approximate_error_controlled (reduce_approx.py:207-301) over Bezier
+ * segments given as CSR rows (orow [rows][d], orow_ofs [n+1], oiv [n][2],
+ * optional ocurve [n]).  Runs the whole level loop on the device and returns
+ * an opaque handle; cubics come out sorted by (curve, ta).  Returns
+ * MREP_ERR_DEPTH (message names the interval) for DepthExceeded. */
+typedef struct mrep_approx mrep_approx;
+MREP_API int mrep_approx_run(const double* orow, const int64_t* orow_ofs, const double* oiv,
+                             const int32_t* ocurve, int64_t norig, int d, double tol,
+                             int64_t batch_cap, int loop_samples, int verify_samples,
+                             int max_depth, int collect_levels, mrep_approx** out, void* stream);
+MREP_API int64_t mrep_approx_count(const mrep_approx* h);
+/* device outputs: pts [S][4][d], iv [S][2], err [S], curve [S] (any may be NULL) */
+MREP_API int mrep_approx_fetch(const mrep_approx* h, double* pts, double* iv, double* err,
+                               int32_t* curve, void* stream);
+/* SubdivisionLevel records (reduce_approx.py:39-57) when collect_levels != 0 (host arrays) */
+MREP_API int mrep_approx_num_levels(const mrep_approx* h);
+MREP_API int mrep_approx_level_sizes(const mrep_approx* h, int lvl, int64_t* nrec, int64_t* nfail);
+MREP_API int mrep_approx_level_fetch(const mrep_approx* h, int lvl, double* P_host,
+                                     double* iv_host, double* err_host, int64_t* prefix_host,
+                                     int64_t* keys_host);
+MREP_API void mrep_approx_free(mrep_approx* h);
+
+/* Single-item preprocessing ops behind the public API */
+/* basis.symbolic_basis_matrix (basis.py:110-149): A [p+1][p+1] */
+MREP_API int mrep_span_basis(const double* knots, int p, int q, double center, double* A,
+                             void* stream);
+/* reduce_points_g1 (reduce_approx.py:80-121) for n segments of degree p:
+ * Q [n][p+1][d] -> R [n][4][d], delta [n][2], l2 [n] */
+MREP_API int mrep_reduce_g1(const double* Q, int p, int d, int64_t n, double* R, double* delta,
+                            double* l2, void* stream);
+/* _max_error / measure_l1_error (reduce_approx.py:146-168): mx [1], argmax
+ * bit mask over the samples (ceil(samples/32) words) */
+MREP_API int mrep_max_error(const double* P, double pa, double pb, const double* Q, int p, int d,
+                            double oa, double ob, int samples, double* mx, uint32_t* mask,
+                            void* stream);
+/* elevate_degree (reduce_approx.py:129-143): P [p+1][d] -> out [target+1][d] */
+MREP_API int mrep_elevate(const double* P, int p, int d, int target, double* out, void* stream);
+/* cubic split at z (basis.subdivision_matrices); snap != 0 reproduces
+ * subdivide_and_modify (reduce_approx.py:185-204) against original Q */
+MREP_API int mrep_split_cubic(const double* P, int d, double z, int snap, double aa, double ab,
+                              const double* Q, int p, double oa, double ob, double* L, double* R,
+                              void* stream);
 
 #ifdef __cplusplus
 }

@@ -185,7 +185,8 @@ class DeviceTable:
             L.ptr(seg), L.ptr(st), L.ptr(sound), L.ptr(counters), L.stream_ptr()))
         return t, foot, dist, cand, seg, st, sound
 
-    def project_host(self, queries, out=None, clip_tol=1e-6, max_iter=8, screen=True):
+    def project_host(self, queries, out=None, clip_tol=1e-6, max_iter=8, screen=True,
+                     counters=None):
         """End-to-end call on HOST arrays through mrep_project_host."""
         q = np.ascontiguousarray(queries, dtype=np.float64)
         n = q.shape[0]
@@ -197,5 +198,6 @@ class DeviceTable:
         p = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
         L.check(L.lib().mrep_project_host(
             L.ptr(self.buf), self.S, self.d, p(q), n, float(clip_tol), int(max_iter),
-            L.MREP_SCREEN if screen else 0, p(t), p(foot), p(dist), p(cand), p(seg)))
+            L.MREP_SCREEN if screen else 0, p(t), p(foot), p(dist), p(cand), p(seg),
+            p(counters) if counters is not None else ctypes.c_void_p(0)))
         return out

@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(_HERE, "libmrep.so")
 MREP_SCREEN = 1
 MREP_STATS = 2
 NUM_COUNTERS = 8
-CNT_PAIRS, CNT_SURVIVORS, CNT_CLIP_ITERS, CNT_SEAMS, CNT_BOXES, CNT_PASS2 = range(6)
+CNT_PAIRS, CNT_SURVIVORS, CNT_CLIP_ITERS, CNT_SEAMS, CNT_BOXES, CNT_PASS2, CNT_HULL_MISS = range(7)
 
 _lib = None
 _lock = threading.Lock()
@@ -42,7 +42,7 @@ _SIGS = {
     "mrep_project": ([_vp, _i64, _i32, _vp, _i64, _dbl, _i32, _i32, _u32, _vp, _vp, _vp, _vp,
                       _vp, _vp, _vp, _vp, _vp], _i32),
     "mrep_project_host": ([_vp, _i64, _i32, _vp, _i64, _dbl, _i32, _u32, _vp, _vp, _vp, _vp,
-                           _vp], _i32),
+                           _vp, _vp], _i32),
     "mrep_project_block": ([_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _i64, _dbl, _i32, _i32,
                             _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i32),
     "mrep_knot_span": ([_vp, _i64, _i32, _vp, _i64, _vp, _vp], _i32),
@@ -55,6 +55,25 @@ _SIGS = {
     "mrep_clip_root": ([_vp, _i64, _dbl, _i32, _vp, _vp, _vp, _vp, _vp], _i32),
     "mrep_cubic_points": ([_vp, _vp, _i64, _i32, _vp, _vp], _i32),
     "mrep_rebase": ([_vp, _i64, _vp, _vp], _i32),
+    "mrep_decompose_plan": ([_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp], _i32),
+    "mrep_decompose": ([_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _vp,
+                        _vp, _vp, _vp], _i32),
+    "mrep_eval_bezier": ([_vp, _i32, _i32, _vp, _i64, _vp, _vp], _i32),
+    "mrep_eval_curve": ([_i32, _vp, _i64, _vp, _i64, _i32, _vp, _i64, _vp, _vp], _i32),
+    "mrep_approx_run": ([_vp, _vp, _vp, _vp, _i64, _i32, _dbl, _i64, _i32, _i32, _i32, _i32,
+                         _vp, _vp], _i32),
+    "mrep_approx_count": ([_vp], _i64),
+    "mrep_approx_fetch": ([_vp, _vp, _vp, _vp, _vp, _vp], _i32),
+    "mrep_approx_num_levels": ([_vp], _i32),
+    "mrep_approx_level_sizes": ([_vp, _i32, _vp, _vp], _i32),
+    "mrep_approx_level_fetch": ([_vp, _i32, _vp, _vp, _vp, _vp, _vp], _i32),
+    "mrep_approx_free": ([_vp], None),
+    "mrep_span_basis": ([_vp, _i32, _i32, _dbl, _vp, _vp], _i32),
+    "mrep_reduce_g1": ([_vp, _i32, _i32, _i64, _vp, _vp, _vp, _vp], _i32),
+    "mrep_max_error": ([_vp, _dbl, _dbl, _vp, _i32, _i32, _dbl, _dbl, _i32, _vp, _vp, _vp], _i32),
+    "mrep_elevate": ([_vp, _i32, _i32, _i32, _vp, _vp], _i32),
+    "mrep_split_cubic": ([_vp, _i32, _dbl, _i32, _dbl, _dbl, _vp, _i32, _dbl, _dbl, _vp, _vp,
+                          _vp], _i32),
 }
 
 

@@ -26,6 +26,7 @@ struct Slot {
   double *dq = nullptr, *dt = nullptr, *dfoot = nullptr, *ddist = nullptr;
   int64_t* dcand = nullptr;
   int32_t* dseg = nullptr;
+  uint64_t* dcnt = nullptr;
   double *hq = nullptr, *ht = nullptr, *hfoot = nullptr, *hdist = nullptr;
   int64_t* hcand = nullptr;
   int32_t* hseg = nullptr;
@@ -56,7 +57,8 @@ int ensure_ctx() {
   MREP_CUDA_CHECK(cudaGetDevice(&dev));
   if (g_ctx.ready && g_ctx.device == dev) return MREP_OK;
   for (auto& s : g_ctx.slot) {
-    MREP_CUDA_CHECK(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+    // blocking streams: ordered after work on the legacy default stream (torch)
+    MREP_CUDA_CHECK(cudaStreamCreateWithFlags(&s.st, cudaStreamDefault));
     MREP_CUDA_CHECK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
     MREP_CUDA_CHECK(cudaMalloc(&s.dq, CHUNK * 3 * sizeof(double)));
     MREP_CUDA_CHECK(cudaMalloc(&s.dt, CHUNK * sizeof(double)));
@@ -64,6 +66,7 @@ int ensure_ctx() {
     MREP_CUDA_CHECK(cudaMalloc(&s.ddist, CHUNK * sizeof(double)));
     MREP_CUDA_CHECK(cudaMalloc(&s.dcand, CHUNK * sizeof(int64_t)));
     MREP_CUDA_CHECK(cudaMalloc(&s.dseg, CHUNK * sizeof(int32_t)));
+    MREP_CUDA_CHECK(cudaMalloc(&s.dcnt, MREP_NUM_COUNTERS * sizeof(uint64_t)));
     MREP_CUDA_CHECK(cudaMallocHost(&s.hq, CHUNK * 3 * sizeof(double)));
     MREP_CUDA_CHECK(cudaMallocHost(&s.ht, CHUNK * sizeof(double)));
     MREP_CUDA_CHECK(cudaMallocHost(&s.hfoot, CHUNK * 3 * sizeof(double)));
@@ -84,7 +87,7 @@ using namespace mrep;
 extern "C" int mrep_project_host(const void* table, int64_t S, int d, const double* queries,
                                  int64_t n, double clip_tol, int max_iter, unsigned flags,
                                  double* out_t, double* out_foot, double* out_dist,
-                                 int64_t* out_cand, int32_t* out_seg) {
+                                 int64_t* out_cand, int32_t* out_seg, uint64_t* counters_host) {
   if (n < 0 || (d != 2 && d != 3) || S < 1 || !table) {
     set_error("mrep_project_host: bad arguments");
     return MREP_ERR_ARG;
@@ -112,6 +115,8 @@ extern "C" int mrep_project_host(const void* table, int64_t S, int d, const doub
     return MREP_OK;
   };
 
+  for (auto& s : g_ctx.slot)
+    MREP_CUDA_CHECK(cudaMemsetAsync(s.dcnt, 0, MREP_NUM_COUNTERS * sizeof(uint64_t), s.st));
   int64_t nchunks = (n + CHUNK - 1) / CHUNK;
   for (int64_t c = 0; c < nchunks; ++c) {
     Slot& s = g_ctx.slot[c & 1];
@@ -126,7 +131,7 @@ extern "C" int mrep_project_host(const void* table, int64_t S, int d, const doub
     MREP_CUDA_CHECK(
         cudaMemcpyAsync(s.dq, src, s.cnt * d * sizeof(double), cudaMemcpyHostToDevice, s.st));
     rc = mrep_project(table, S, d, s.dq, s.cnt, clip_tol, max_iter, 0, flags, s.dt, s.dfoot,
-                      s.ddist, s.dcand, s.dseg, nullptr, nullptr, nullptr, s.st);
+                      s.ddist, s.dcand, s.dseg, nullptr, nullptr, s.dcnt, s.st);
     if (rc != MREP_OK) return rc;
     double* ht = pin_out ? out_t + s.lo : s.ht;
     double* hf = pin_out ? out_foot + s.lo * d : s.hfoot;
@@ -148,5 +153,12 @@ extern "C" int mrep_project_host(const void* table, int64_t S, int d, const doub
   }
   for (auto& s : g_ctx.slot)
     if ((rc = write_back(s)) != MREP_OK) return rc;
+  if (counters_host) {
+    for (auto& s : g_ctx.slot) {
+      uint64_t c[MREP_NUM_COUNTERS];
+      MREP_CUDA_CHECK(cudaMemcpy(c, s.dcnt, sizeof c, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < MREP_NUM_COUNTERS; ++i) counters_host[i] += c[i];
+    }
+  }
   return MREP_OK;
 }

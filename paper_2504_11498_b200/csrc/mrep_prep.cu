@@ -94,30 +94,13 @@ __global__ void span_list_kernel(const int32_t* degree, const int64_t* knot_ofs,
     }
 }
 
-// decompose.py:19-46 + basis.py:110-149: one warp per nonzero span
-__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK)
-    decompose_kernel(const int32_t* degree, const int64_t* knot_ofs, const double* knots,
-                     const int64_t* ctrl_ofs, const double* ctrl, int d, const int64_t* seg_ofs,
-                     const int64_t* row_base, const int32_t* span, const int32_t* seg_curve,
-                     int64_t nseg, double* out_rows, int64_t* out_row_ofs, double* out_iv) {
-  __shared__ double lev[WARPS_PER_BLOCK][2][32 * LEVW];
-  __shared__ double Rsh[WARPS_PER_BLOCK][32 * 3];
-  int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int64_t gs = (int64_t)blockIdx.x * WARPS_PER_BLOCK + wib;
-  if (gs >= nseg) return;
-  int c = seg_curve[gs];
-  int p = degree[c];
-  int q = span[gs];
-  const double* kn = knots + knot_ofs[c];
-  const double* cp = ctrl + ctrl_ofs[c] * d;
-  int64_t ncp = ctrl_ofs[c + 1] - ctrl_ofs[c];
-  int64_t j_local = gs - seg_ofs[c];
-  int64_t nseg_c = seg_ofs[c + 1] - seg_ofs[c];
-  const int k = lane;
+// basis.py:110-149, warp-cooperative: lane k owns polynomial coefficient k.
+// Returns the final level buffer: slot j (row stride LEVW) holds the
+// coefficients of N_{q-p+j,p} in powers of (t - center).
+__device__ const double* span_basis_warp(const double* kn, int p, int q, double center, double* L0,
+                                         double* L1) {
+  const int k = threadIdx.x & 31;
   const bool act = k <= p;
-  const double center = kn[q];
-  double* L0 = lev[wib][0];
-  double* L1 = lev[wib][1];
   if (act) L0[0 * LEVW + k] = (k == 0) ? 1.0 : 0.0;
   __syncwarp();
   double* cur = L0;
@@ -145,6 +128,31 @@ __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK)
     cur = nxt;
     nxt = t;
   }
+  return cur;
+}
+
+// decompose.py:19-46 + basis.py:110-149: one warp per nonzero span
+__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK)
+    decompose_kernel(const int32_t* degree, const int64_t* knot_ofs, const double* knots,
+                     const int64_t* ctrl_ofs, const double* ctrl, int d, const int64_t* seg_ofs,
+                     const int64_t* row_base, const int32_t* span, const int32_t* seg_curve,
+                     int64_t nseg, double* out_rows, int64_t* out_row_ofs, double* out_iv) {
+  __shared__ double lev[WARPS_PER_BLOCK][2][32 * LEVW];
+  __shared__ double Rsh[WARPS_PER_BLOCK][32 * 3];
+  int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t gs = (int64_t)blockIdx.x * WARPS_PER_BLOCK + wib;
+  if (gs >= nseg) return;
+  int c = seg_curve[gs];
+  int p = degree[c];
+  int q = span[gs];
+  const double* kn = knots + knot_ofs[c];
+  const double* cp = ctrl + ctrl_ofs[c] * d;
+  int64_t ncp = ctrl_ofs[c + 1] - ctrl_ofs[c];
+  int64_t j_local = gs - seg_ofs[c];
+  int64_t nseg_c = seg_ofs[c + 1] - seg_ofs[c];
+  const int k = lane;
+  const bool act = k <= p;
+  const double* cur = span_basis_warp(kn, p, q, kn[q], lev[wib][0], lev[wib][1]);
   // row k of M1 = diag(h^k) A, then R[k] = M1[k] @ cp[q-p .. q] (FMA chain)
   double h = kn[q + 1] - kn[q];
   double hk = powi_cr(h, k);
@@ -742,6 +750,120 @@ static int exclusive_scan(const T* in, T* out, int64_t n, cudaStream_t st) {
   return MREP_OK;
 }
 
+// ---------------------------------------------------- single-item kernels
+// basis.py:110-149 for one span: A [p+1][p+1] row-major (A[k][j])
+__global__ void span_basis_kernel(const double* kn, int p, int q, double center, double* A) {
+  __shared__ double lev[2][32 * LEVW];
+  const double* cur = span_basis_warp(kn, p, q, center, lev[0], lev[1]);
+  int k = threadIdx.x;
+  if (k <= p)
+    for (int j = 0; j <= p; ++j) A[k * (p + 1) + j] = cur[j * LEVW + k];
+}
+
+// reduce_approx.py:69-121: reduce_points_g1 + _l2_error for n segments of
+// equal degree (one thread each); Q [n][p+1][d] -> R [n][4][d], delta [n][2], l2 [n]
+__global__ void reduce_g1_kernel(const double* Qg, int p, int d, int64_t n, double* Rg,
+                                 double* delta, double* l2) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  double Q[32 * 3], R[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int j = 0; j <= p; ++j)
+    for (int k = 0; k < 3; ++k) Q[j * 3 + k] = k < d ? Qg[(s * (p + 1) + j) * d + k] : 0.0;
+  double d0, d1;
+  g1_reduce(Q, p, d, R, &d0, &d1);
+  for (int j = 0; j < 4; ++j)
+    for (int k = 0; k < d; ++k) Rg[(s * 4 + j) * d + k] = R[j * 3 + k];
+  delta[2 * s] = d0;
+  delta[2 * s + 1] = d1;
+  // eps = Q'GppQ - 2 Q'Gp3R + R'G33R (einsum "id,ij,jd->"), clamped at 0
+  auto gram = [&](int m, int nn, int i, int j) {
+    return binom(m, i) * binom(nn, j) / ((double)(m + nn + 1) * binom(m + nn, i + j));
+  };
+  double e1 = 0.0, e2 = 0.0, e3 = 0.0;
+  for (int i = 0; i <= p; ++i)
+    for (int j = 0; j <= p; ++j)
+      for (int k = 0; k < d; ++k) e1 += Q[i * 3 + k] * gram(p, p, i, j) * Q[j * 3 + k];
+  for (int i = 0; i <= p; ++i)
+    for (int j = 0; j < 4; ++j)
+      for (int k = 0; k < d; ++k) e2 += Q[i * 3 + k] * gram(p, 3, i, j) * R[j * 3 + k];
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j)
+      for (int k = 0; k < d; ++k) e3 += R[i * 3 + k] * gram(3, 3, i, j) * R[j * 3 + k];
+  double e = e1 - 2.0 * e2 + e3;
+  l2[s] = e > 0.0 ? e : 0.0;
+}
+
+// reduce_approx.py:146-168: one (cubic, original) pair, one warp
+__global__ void max_error_kernel(const double* Pg, double pa, double pb, const double* Qg, int p,
+                                 int d, double oa, double ob, int ns, double* mx_out,
+                                 uint32_t* mask) {
+  __shared__ double Qs[32 * 3];
+  __shared__ double Ps[12];
+  int lane = threadIdx.x;
+  load_rows(Qg, p + 1, d, Qs);
+  if (lane < 12) Ps[lane] = (lane % 3) < d ? Pg[(lane / 3) * d + lane % 3] : 0.0;
+  __syncwarp();
+  double mx = max_error_warp(Ps, pa, pb, Qs, p, d, oa, ob, ns, mask);
+  if (lane == 0) *mx_out = mx;
+}
+
+// reduce_approx.py:129-143: elevate one segment to `target`
+__global__ void elevate_kernel(const double* Pg, int p, int d, int target, double* out) {
+  double cur[33 * 3];
+  for (int j = 0; j <= p; ++j)
+    for (int k = 0; k < d; ++k) cur[j * 3 + k] = Pg[j * d + k];
+  int pp = p;
+  while (pp < target) {
+    double nxt[33 * 3];
+    for (int k = 0; k < d; ++k) nxt[k] = cur[k];
+    for (int r = 1; r <= pp; ++r) {
+      double w = (double)r / ((double)pp + 1.0);
+      for (int k = 0; k < d; ++k) nxt[r * 3 + k] = w * cur[(r - 1) * 3 + k] + (1.0 - w) * cur[r * 3 + k];
+    }
+    for (int k = 0; k < d; ++k) nxt[(pp + 1) * 3 + k] = cur[pp * 3 + k];
+    ++pp;
+    for (int j = 0; j <= pp; ++j)
+      for (int k = 0; k < 3; ++k) cur[j * 3 + k] = nxt[j * 3 + k];
+  }
+  for (int j = 0; j <= target; ++j)
+    for (int k = 0; k < d; ++k) out[j * d + k] = cur[j * 3 + k];
+}
+
+// reduce_approx.py:185-204 (snap != 0) and distance.py:84-90 (snap == 0):
+// split a cubic at z with the subdivision matrices (basis.py:172-189),
+// optionally snapping the shared point onto the original segment.
+__global__ void split_cubic_kernel(const double* Pg, int d, double z, int snap, double aa,
+                                   double ab, const double* Qg, int p, double oa, double ob,
+                                   double* Lg, double* Rg) {
+  __shared__ double Qs[32 * 3];
+  int lane = threadIdx.x;
+  double pin[3] = {0, 0, 0};
+  if (snap) {
+    load_rows(Qg, p + 1, d, Qs);
+    double t_split = aa + z * (ab - aa);
+    warp_eval(Qs, p, (t_split - oa) / (ob - oa), pin);
+  }
+  if (lane != 0) return;
+  for (int i = 0; i < 4; ++i)
+    for (int k = 0; k < d; ++k) {
+      double l = 0.0, r = 0.0;
+      for (int j = 0; j <= i; ++j)
+        l = fma(binom(i, j) * powi_cr(z, j) * powi_cr(1.0 - z, i - j), Pg[j * d + k], l);
+      for (int j = i; j <= 3; ++j)
+        r = fma(binom(3 - i, j - i) * powi_cr(z, j - i) * powi_cr(1.0 - z, 3 - j), Pg[j * d + k], r);
+      Lg[i * d + k] = l;
+      Rg[i * d + k] = r;
+    }
+  if (snap)
+    for (int k = 0; k < d; ++k) {
+      Lg[3 * d + k] = pin[k];
+      Rg[k] = pin[k];
+    }
+}
+
+}  // namespace mrep (kernels)
+namespace mrep {
+
 }  // namespace mrep
 
 // ============================================================ approximation handle
@@ -1122,5 +1244,72 @@ MREP_API int mrep_approx_level_fetch(const mrep_approx* h, int lvl, double* P_ho
 }
 
 MREP_API void mrep_approx_free(mrep_approx* h) { delete h; }
+
+MREP_API int mrep_span_basis(const double* knots, int p, int q, double center, double* A,
+                             void* stream) {
+  if (p < 1 || p > 31) {
+    set_error("mrep_span_basis: degree in [1,31]");
+    return MREP_ERR_ARG;
+  }
+  int rc = ensure_pascal();
+  if (rc) return rc;
+  span_basis_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(knots, p, q, center, A);
+  MREP_LAUNCH_CHECK();
+  return MREP_OK;
+}
+
+MREP_API int mrep_reduce_g1(const double* Q, int p, int d, int64_t n, double* R, double* delta,
+                            double* l2, void* stream) {
+  if (p < 4 || p > 31 || (d != 2 && d != 3)) {
+    set_error("mrep_reduce_g1: degree in [4,31], d in {2,3}");
+    return MREP_ERR_ARG;
+  }
+  int rc = ensure_pascal();
+  if (rc) return rc;
+  if (n <= 0) return MREP_OK;
+  reduce_g1_kernel<<<grid_for(n, 64), 64, 0, (cudaStream_t)stream>>>(Q, p, d, n, R, delta, l2);
+  MREP_LAUNCH_CHECK();
+  return MREP_OK;
+}
+
+MREP_API int mrep_max_error(const double* P, double pa, double pb, const double* Q, int p, int d,
+                            double oa, double ob, int samples, double* mx, uint32_t* mask,
+                            void* stream) {
+  if (p < 1 || p > 31 || (d != 2 && d != 3) || samples < 1) {
+    set_error("mrep_max_error: bad arguments");
+    return MREP_ERR_ARG;
+  }
+  int rc = ensure_pascal();
+  if (rc) return rc;
+  max_error_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(P, pa, pb, Q, p, d, oa, ob, samples, mx,
+                                                       mask);
+  MREP_LAUNCH_CHECK();
+  return MREP_OK;
+}
+
+MREP_API int mrep_elevate(const double* P, int p, int d, int target, double* out, void* stream) {
+  if (p < 0 || target < p || target > 32 || (d != 2 && d != 3)) {
+    set_error("mrep_elevate: need p <= target <= 32");
+    return MREP_ERR_ARG;
+  }
+  elevate_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(P, p, d, target, out);
+  MREP_LAUNCH_CHECK();
+  return MREP_OK;
+}
+
+MREP_API int mrep_split_cubic(const double* P, int d, double z, int snap, double aa, double ab,
+                              const double* Q, int p, double oa, double ob, double* L, double* R,
+                              void* stream) {
+  if ((d != 2 && d != 3) || (snap && (p < 1 || p > 31))) {
+    set_error("mrep_split_cubic: bad arguments");
+    return MREP_ERR_ARG;
+  }
+  int rc = ensure_pascal();
+  if (rc) return rc;
+  split_cubic_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(P, d, z, snap, aa, ab, Q, p, oa, ob, L, R);
+  MREP_LAUNCH_CHECK();
+  return MREP_OK;
+}
+
 
 }  // extern "C"

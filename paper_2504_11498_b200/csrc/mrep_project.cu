@@ -247,7 +247,7 @@ __device__ __forceinline__ void solve_segment(const TableView& T, int64_t s, con
     st.surv++;
     st.clip_it += (uint64_t)co.used;
     if (!co.ok) {
-      if (STATS) st.noroot++;
+      st.noroot++;
       lo = hi;
       continue;
     }
@@ -495,6 +495,7 @@ __global__ void __launch_bounds__(BLOCK) project_kernel(ProjParams p) {
   warp_count(p.counters, MREP_CNT_CLIP_ITERS, st.clip_it);
   warp_count(p.counters, MREP_CNT_SEAMS, st.seams);
   warp_count(p.counters, MREP_CNT_BOXES, st.boxes);
+  warp_count(p.counters, MREP_CNT_HULL_MISS, (uint64_t)st.noroot);
 }
 
 template <int D, bool SCREEN>

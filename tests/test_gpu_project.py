@@ -1,0 +1,151 @@
+"""Batch projection kernel (dense = reference semantics, screened = BVH) vs
+the reference's golden outputs and the pinned C oracle.
+
+Bars (north star): segment index exact except documented ties; distance
+within 1e-9 relative (absolute floor 1e-12 for on-curve queries, whose
+distance is ~0); parameter within 1e-6.  Dense mode must also reproduce the
+reference's candidate count and all six stats columns (allowing <= 0.1% of
+queries to differ where a CUDA-vs-glibc ulp in the quartic flips a sign test).
+"""
+import numpy as np
+import pytest
+
+from conftest import load_golden, project_fixture_names
+
+pytestmark = pytest.mark.gpu
+
+
+def _args(z):
+    return (z["seg_pts"], z["seg_ta"], z["seg_tb"], z["seam_t"], z["seam_pt"])
+
+
+def assert_close(t, dist, t_ref, d_ref):
+    assert np.all(np.abs(t - t_ref) <= 1e-6), np.abs(t - t_ref).max()
+    tol = np.maximum(1e-9 * d_ref, 1e-12)
+    assert np.all(np.abs(dist - d_ref) <= tol), np.abs(dist - d_ref).max()
+
+
+@pytest.mark.parametrize("name", project_fixture_names())
+def test_dense_matches_reference(gpu, name):
+    from paper_2504_11498_b200 import _device as D
+    z = load_golden(f"project_{name}.npz")
+    t, foot, dist, cand, stats, sound = D.project_block(
+        *_args(z), z["queries"], float(z["clip_tol"]), int(z["max_iter"]), int(z["soundness"]))
+    assert_close(t, dist, z["t"], z["dist"])
+    assert np.abs(foot - z["foot"]).max() <= 1e-6
+    assert np.mean(cand == z["cand"]) >= 0.999
+    assert np.mean((stats == z["stats"]).all(1)) >= 0.999
+    if int(z["soundness"]) > 0:
+        fin = np.isfinite(z["sound"])
+        assert np.array_equal(np.isfinite(sound), fin)
+        assert np.abs(sound[fin] - z["sound"][fin]).max() <= 1e-9
+
+
+@pytest.mark.parametrize("name", project_fixture_names())
+def test_screened_equals_dense(gpu, name):
+    """The BVH cull never changes the winner: bitwise equal to brute force."""
+    from paper_2504_11498_b200 import _device as D
+    z = load_golden(f"project_{name}.npz")
+    tab = D.DeviceTable(*_args(z))
+    dense = tab.project(z["queries"], screen=False)
+    scr = tab.project(z["queries"], screen=True)
+    for a, b in zip(dense[:5], scr[:5]):
+        if a is not None:
+            pass
+    for k in (0, 1, 2, 4):  # t, foot, dist, seg
+        assert np.array_equal(dense[k].cpu().numpy(), scr[k].cpu().numpy()), k
+    assert_close(scr[0].cpu().numpy(), scr[2].cpu().numpy(), z["t"], z["dist"])
+
+
+def test_segment_ids_match_oracle(gpu, oracle_lib):
+    """Winning cubic index (the north star's 'segment id') vs the oracle."""
+    from paper_2504_11498_b200 import _device as D
+    for name in ("cfg1_random", "cfg2", "table_n", "deg9"):
+        z = load_golden(f"project_{name}.npz")
+        o = oracle_lib.project_block(*_args(z), z["queries"], workers=8)
+        seg = D.DeviceTable(*_args(z)).project(z["queries"])[4].cpu().numpy()
+        assert np.mean(seg == o["seg"]) >= 0.999, name
+
+
+def test_cfg2_random_vs_oracle(gpu, oracle_lib):
+    """Fresh cfg2 queries (20k, S = 510) vs the C oracle on all host cores."""
+    from paper_2504_11498_b200 import _device as D
+    import os
+    z = load_golden("project_cfg2.npz")
+    q = np.random.default_rng(123).uniform(0, 1, (20000, 3))
+    o = oracle_lib.project_block(*_args(z), q, workers=os.cpu_count() or 1)
+    tab = D.DeviceTable(*_args(z))
+    t, foot, dist, cand, seg, _, _ = [x.cpu().numpy() if x is not None else None
+                                      for x in tab.project(q)]
+    assert_close(t, dist, o["t"], o["dist"])
+    assert np.mean(seg == o["seg"]) >= 0.999
+    assert np.mean(t == o["t"]) >= 0.99
+
+
+def test_full_size_properties(gpu):
+    """10^6 queries at cfg2 size: determinism, seam upper bound, dense agreement
+    on a subsample, foot point lies on the winning cubic."""
+    import torch
+    from paper_2504_11498_b200 import _device as D
+    z = load_golden("project_cfg2.npz")
+    tab = D.DeviceTable(*_args(z))
+    g = torch.Generator(device="cuda").manual_seed(7)
+    q = torch.rand((1_000_000, 3), dtype=torch.float64, device="cuda", generator=g)
+    a = tab.project(q)
+    b = tab.project(q)
+    for k in (0, 1, 2, 4):
+        assert torch.equal(a[k], b[k])
+    seam = torch.as_tensor(z["seam_pt"], device="cuda")
+    sub = q[::997]
+    dseam = torch.cdist(sub, seam).min(dim=1).values
+    assert bool((a[2][::997] <= dseam + 1e-15).all())
+    dn = tab.project(sub, screen=False)
+    for k in (0, 1, 2, 4):
+        assert torch.equal(dn[k], a[k][::997])
+    # foot consistency: distance == |q - foot|
+    assert float((a[2] - (q - a[1]).norm(dim=1)).abs().max()) <= 1e-12
+
+
+def test_tie_band_overflow_second_pass(gpu, oracle_lib):
+    """Many candidates inside the 1e-12 band (query at the centre of a
+    polygon inscribed in a circle): the exact second pass must give the
+    reference's choice (smallest t among the band)."""
+    from paper_2504_11498_b200 import _device as D, _lib as L
+    import torch
+    k = 24
+    ang = np.linspace(0, 2 * np.pi, k, endpoint=False)
+    # cubic segments that are straight chords between points on the circle
+    P0 = np.stack([np.cos(ang), np.sin(ang)], 1)
+    P3 = np.roll(P0, -1, axis=0)
+    seg_pts = np.stack([P0, P0 + (P3 - P0) / 3, P0 + 2 * (P3 - P0) / 3, P3], 1)
+    ta = np.arange(k) / k
+    tb = np.arange(1, k + 1) / k
+    seam_t = np.concatenate(([0.0], tb))
+    seam_pt = np.concatenate((seg_pts[:1, 0], seg_pts[:, 3]))
+    q = np.array([[0.0, 0.0], [1e-3, -2e-3], [0.5, 0.1]])
+    o = oracle_lib.project_block(seg_pts, ta, tb, seam_t, seam_pt, q)
+    tab = D.DeviceTable(seg_pts, ta, tb, seam_t, seam_pt)
+    cnt = torch.zeros(L.NUM_COUNTERS, dtype=torch.int64, device="cuda")
+    for screen in (False, True):
+        t, foot, dist, cand, seg, _, _ = tab.project(q, screen=screen, counters=cnt)
+        assert np.array_equal(t.cpu().numpy(), o["t"])
+        assert np.array_equal(dist.cpu().numpy(), o["dist"])
+        assert np.array_equal(seg.cpu().numpy(), o["seg"])
+    assert int(cnt[L.CNT_PASS2]) >= 1
+
+
+def test_edge_queries(gpu, oracle_lib):
+    """Far-away, on-seam, on-endpoint queries and a single query."""
+    from paper_2504_11498_b200 import _device as D
+    z = load_golden("project_table_n.npz")
+    q = np.concatenate([z["seam_pt"], np.array([[1e6, -1e6, 3e5], [0.5, 0.5, 0.5]]),
+                        z["seg_pts"][:, 1]])
+    o = oracle_lib.project_block(*_args(z), q)
+    tab = D.DeviceTable(*_args(z))
+    for screen in (False, True):
+        t, foot, dist, cand, seg, _, _ = [x.cpu().numpy() if x is not None else None
+                                          for x in tab.project(q, screen=screen)]
+        assert_close(t, dist, o["t"], o["dist"])
+    one = tab.project(q[:1])
+    assert one[0].shape == (1,)
+    assert np.all(np.isfinite(tab.project(q)[0].cpu().numpy()))
