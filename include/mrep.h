@@ -38,6 +38,7 @@ extern "C" {
 /* mrep_project flags */
 #define MREP_SCREEN 1u   /* BVH-culled exact solve (t/foot/dist/seg identical; cand = candidates examined) */
 #define MREP_STATS 2u    /* brute-force mode with per-query stats + soundness (forces !MREP_SCREEN) */
+#define MREP_NO_SORT 4u  /* process queries in input order (default: Morton order for warp coherence) */
 
 /* Work counters written (accumulated) by mrep_project when `counters_dev` != NULL. */
 #define MREP_CNT_PAIRS 0      /* (query, cubic) pairs solved: E, quartic, rebase, pieces */
@@ -50,6 +51,8 @@ extern "C" {
 #define MREP_NUM_COUNTERS 8
 
 MREP_API const char* mrep_last_error(void);
+/* measured FP64 FMA throughput of the current device, TFLOP/s (roofline peak) */
+MREP_API int mrep_fp64_peak(double* tflops);
 MREP_API int mrep_version(void);
 MREP_API int mrep_device_count(void);
 

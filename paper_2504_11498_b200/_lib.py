@@ -36,6 +36,7 @@ _u32 = ctypes.c_uint
 _SIGS = {
     "mrep_last_error": ([], ctypes.c_char_p),
     "mrep_version": ([], _i32),
+    "mrep_fp64_peak": ([_vp], _i32),
     "mrep_device_count": ([], _i32),
     "mrep_table_bytes": ([_i64], _i64),
     "mrep_table_pack": ([_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp], _i32),

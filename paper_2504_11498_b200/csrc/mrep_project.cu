@@ -26,6 +26,8 @@
 #include <mutex>
 #include <string>
 
+#include <cub/cub.cuh>
+
 #include "mrep_common.cuh"
 #include "mrep_math.cuh"
 
@@ -56,6 +58,7 @@ struct ProjParams {
   uint64_t* counters;
   unsigned long long* pass2_count;
   int64_t* pass2_list;
+  const uint32_t* perm;  // Morton order of the queries (nullptr = identity)
 };
 
 // ------------------------------------------------------------ tie band
@@ -447,26 +450,354 @@ __device__ __forceinline__ void write_winner(const ProjParams& p, int64_t qi, co
   if (p.out_seg) p.out_seg[qi] = seg;
 }
 
+// =================================================================
+// Warp-cooperative projection kernel.
+//
+// Queries arrive in Morton order (p.perm), so the 32 queries of a warp are
+// spatial neighbours and visit the same cubics.  Three mechanisms keep the
+// FP64 pipe busy despite the reference's data-dependent control flow:
+//  * dense mode walks the cubics warp-uniformly (broadcast record loads);
+//  * screened mode pools the (query, cubic) pairs of all 32 lanes' BVH
+//    candidate lists and deals them out 32 at a time (a lane with 8
+//    candidates no longer stalls 31 lanes with 1);
+//  * surviving monotone pieces go to a per-warp ring queue in shared memory
+//    and are Bezier-clipped 32 at a time, instead of one lane clipping while
+//    31 wait.  Each clipped candidate is handed back to its owner lane's tie
+//    band with a shuffle.
+// =================================================================
+constexpr int WARPS_PB = BLOCK / 32;
+constexpr int SVQ = 64;        // survivor ring (power of two)
+constexpr int PAIRCAP = 512;   // pair pool per warp
+constexpr int SLIST = 16;      // per-lane candidate list in screened mode
+
+struct WarpShared {
+  double sb[SVQ][6];
+  double slo[SVQ], shi[SVQ];
+  int sseg[SVQ];
+  int smeta[SVQ];  // owner lane | piece index << 8
+  double q[32][3];
+  double dmin[32];
+  int cnt[32][6];  // per owner: ok candidates, c3l, c3g, cfl, cfg, noroot
+  int pseg[PAIRCAP];
+  unsigned char powner[PAIRCAP];
+};
+
+enum { C_OK = 0, C_C3L, C_C3G, C_CFL, C_CFG, C_NOROOT };
+
+// Clip up to 32 queued survivors (one per lane) and deliver the candidates.
+template <int D, bool STATS>
+__device__ __forceinline__ void flush_survivors(WarpShared& W, int& head, int tail,
+                                                const TableView& T, double clip_tol, int max_iter,
+                                                Band& B, QStats& st, int lane) {
+  int m = tail - head;
+  if (m > 32) m = 32;
+  bool has = lane < m;
+  double t = 0.0, d = 0.0, v = 0.0;
+  uint64_t ord = 0;
+  int owner = 0;
+  bool ok = false;
+  if (has) {
+    int slot = (head + lane) & (SVQ - 1);
+    double bp[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) bp[i] = W.sb[slot][i];
+    double lo = W.slo[slot], hi = W.shi[slot];
+    int s = W.sseg[slot];
+    int meta = W.smeta[slot];
+    owner = meta & 0xff;
+    int k = meta >> 8;
+    ClipOut co = clip_root(bp, clip_tol, max_iter);
+    st.surv++;
+    st.clip_it += (uint64_t)co.used;
+    ok = co.ok;
+    if (!ok) {
+      atomicAdd(&W.cnt[owner][C_NOROOT], 1);
+      st.noroot++;
+    } else {
+      const double* r = T.rec + (int64_t)s * REC;
+      double ta = __ldg(r + 24), tb = __ldg(r + 25);
+      if (STATS) {
+        double gscale = (hi - lo) * (tb - ta);
+        if (co.w3 <= clip_tol) atomicAdd(&W.cnt[owner][C_C3L], 1);
+        if (co.w3 * gscale <= clip_tol) atomicAdd(&W.cnt[owner][C_C3G], 1);
+        if (co.wf <= clip_tol) atomicAdd(&W.cnt[owner][C_CFL], 1);
+        if (co.wf * gscale <= clip_tol) atomicAdd(&W.cnt[owner][C_CFG], 1);
+      }
+      v = lo + co.root * (hi - lo);
+      double acc = 0.0;
+#pragma unroll
+      for (int dim = 0; dim < D; ++dim) {
+        double f = decasteljau1(__ldg(r + 12 + dim), __ldg(r + 15 + dim), __ldg(r + 18 + dim),
+                                __ldg(r + 21 + dim), v);
+        double diff = W.q[owner][dim] - f;
+        acc += diff * diff;
+      }
+      t = ta + v * (tb - ta);
+      d = sqrt(acc);
+      ord = SURV_BIT | ((uint64_t)s << 3) | (uint64_t)k;
+    }
+  }
+  head += m;
+  __syncwarp();
+  // hand each candidate to its owner's tie band
+  for (int j = 0; j < m; ++j) {
+    int oj = __shfl_sync(0xffffffffu, owner, j);
+    bool okj = __shfl_sync(0xffffffffu, ok, j);
+    double tj = __shfl_sync(0xffffffffu, t, j);
+    double dj = __shfl_sync(0xffffffffu, d, j);
+    double vj = __shfl_sync(0xffffffffu, v, j);
+    uint64_t oj_ord = __shfl_sync(0xffffffffu, ord, j);
+    if (okj && lane == oj) {
+      st.offers++;
+      band_offer(B, tj, dj, vj, oj_ord);
+      W.dmin[lane] = B.dmin;
+    }
+  }
+  __syncwarp();
+}
+
+// E, E' roots, interior split points and the rebased ordinates of one pair
+struct PairPrep {
+  double bseg[6];
+  double b1, b2, b3, b4;
+  int nin;
+};
+
+template <int D>
+__device__ __forceinline__ void prep_pair(const TableView& T, int64_t s, const double (&q)[D],
+                                          PairPrep& P) {
+  const double* r = T.rec + s * REC;
+  double w[4][D];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int dim = 0; dim < D; ++dim) w[k][dim] = __ldg(r + k * 3 + dim);
+  double e[6];
+  distance_poly_w<D>(w, q, e);
+  double ep[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) ep[k] = (double)(k + 1) * e[k + 1];
+  Roots4 rt = quartic_roots_01(ep);
+  P.b1 = P.b2 = P.b3 = P.b4 = 1.0;
+  P.nin = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double x = rt.r[i];
+    if (i < rt.count && 1e-10 < x && x < 1.0 - 1e-10) {
+      P.b1 = (P.nin == 0) ? x : P.b1;
+      P.b2 = (P.nin == 1) ? x : P.b2;
+      P.b3 = (P.nin == 2) ? x : P.b3;
+      P.b4 = (P.nin == 3) ? x : P.b4;
+      ++P.nin;
+    }
+  }
+  rebase5(e, P.bseg);
+}
+
+// Walk the monotone pieces of the warp's current pairs in lock step
+// (piece k of every pair together), queue survivors, flush full batches.
+template <int D, bool STATS>
+__device__ __forceinline__ void pieces_step(WarpShared& W, int& head, int& tail, bool has,
+                                            int64_t s, int owner, const PairPrep& P,
+                                            const double (&q)[D], const TableView& T,
+                                            double clip_tol, int max_iter, int soundness,
+                                            Band& B, QStats& st, int lane) {
+  int K = __reduce_max_sync(0xffffffffu, has ? P.nin + 1 : 0);
+  double lo = 0.0;
+  for (int k = 0; k < K; ++k) {
+    bool act = has && k <= P.nin;
+    double hi = (k == P.nin) ? 1.0 : (k == 0 ? P.b1 : (k == 1 ? P.b2 : (k == 2 ? P.b3 : P.b4)));
+    bool surv = false;
+    double bp[6];
+    if (act) {
+      restrict_ordinates(P.bseg, lo, hi, bp);
+      surv = bp[0] < 0.0 && bp[0] * bp[5] <= 0.0;
+      if (!surv && STATS && soundness > 0) {
+        const double* r = T.rec + s * REC;
+        for (int si = 0; si < soundness; ++si) {
+          double v = lo + (hi - lo) * (double)si / ((double)soundness - 1.0);
+          double acc = 0.0;
+#pragma unroll
+          for (int dim = 0; dim < D; ++dim) {
+            double f = decasteljau1(__ldg(r + 12 + dim), __ldg(r + 15 + dim),
+                                    __ldg(r + 18 + dim), __ldg(r + 21 + dim), v);
+            double diff = q[dim] - f;
+            acc += diff * diff;
+          }
+          if (acc < st.sound) st.sound = acc;
+        }
+      }
+      if (surv && STATS) st.pieces++;
+    }
+    unsigned bal = __ballot_sync(0xffffffffu, surv);
+    if (surv) {
+      int slot = (tail + __popc(bal & ((1u << lane) - 1))) & (SVQ - 1);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) W.sb[slot][i] = bp[i];
+      W.slo[slot] = lo;
+      W.shi[slot] = hi;
+      W.sseg[slot] = (int)s;
+      W.smeta[slot] = owner | (k << 8);
+    }
+    tail += __popc(bal);
+    __syncwarp();
+    if (tail - head >= 32) flush_survivors<D, STATS>(W, head, tail, T, clip_tol, max_iter, B, st, lane);
+    lo = hi;
+  }
+}
+
 template <int D, bool SCREEN, bool STATS>
 __global__ void __launch_bounds__(BLOCK) project_kernel(ProjParams p) {
-  int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  bool active = qi < p.n;
+  __shared__ WarpShared wsh[WARPS_PB];
+  const int lane = threadIdx.x & 31;
+  WarpShared& W = wsh[threadIdx.x >> 5];
+  int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool active = gi < p.n;
+  int64_t qi = active ? (p.perm ? (int64_t)p.perm[gi] : gi) : 0;
   QStats st{};
   st.sound = __longlong_as_double(0x7ff0000000000000LL);
-  if (active) {
-    double q[D];
+  const TableView& T = p.tab;
+  double q[D];
 #pragma unroll
-    for (int k = 0; k < D; ++k) q[k] = p.q[qi * D + k];
-    Band B;
-    band_init(B, false, 0.0);
-    if (SCREEN) {
-      double scale = p.tab.hdr[4];
+  for (int k = 0; k < D; ++k) q[k] = active ? p.q[qi * D + k] : 0.0;
 #pragma unroll
-      for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
-      gen_screened<D, STATS>(p.tab, q, scale, p.clip_tol, p.max_iter, B, st);
-    } else {
-      gen_dense<D, STATS>(p.tab, q, p.clip_tol, p.max_iter, p.soundness, B, st);
+  for (int k = 0; k < D; ++k) W.q[lane][k] = q[k];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) W.cnt[lane][c] = 0;
+  Band B;
+  band_init(B, false, 0.0);
+  int head = 0, tail = 0;
+  __syncwarp();
+  if (!SCREEN) {
+    if (active)
+      for (int64_t s = 0; s <= T.S; ++s) offer_seam<D>(T, s, q, B, st);
+    for (int64_t s = 0; s < T.S; ++s) {
+      PairPrep P;
+      if (active) {
+        prep_pair<D>(T, s, q, P);
+        st.pairs++;
+      }
+      pieces_step<D, STATS>(W, head, tail, active, s, lane, P, q, T, p.clip_tol, p.max_iter,
+                            p.soundness, B, st, lane);
     }
+  } else {
+    double scale = T.hdr[4];
+#pragma unroll
+    for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
+    // greedy descent: first upper bound from the seams of a nearby cubic
+    if (active) {
+      int level = T.top;
+      int64_t idx = 0;
+      while (level > 0) {
+        int64_t first = idx * FANOUT, cnt = T.lvl_cnt[level - 1], off = T.lvl_off[level - 1];
+        double best = 0.0;
+        int64_t bi = first;
+        for (int c = 0; c < FANOUT; ++c) {
+          int64_t ch = first + c;
+          if (ch < cnt) {
+            st.boxes++;
+            double lb = box_lb2<D>(T, off + ch, q);
+            if (c == 0 || lb < best) {
+              best = lb;
+              bi = ch;
+            }
+          }
+        }
+        idx = bi;
+        --level;
+      }
+      offer_seam<D>(T, idx, q, B, st);
+      offer_seam<D>(T, idx + 1, q, B, st);
+    }
+    uint64_t masks = 0;
+    int level = T.top;
+    int64_t idx = 0;
+    if (active) masks = (uint64_t)child_mask<D>(T, level, 0, q, cut2(B.dmin, scale), st) << (8 * level);
+    bool done = !active;
+    int64_t list[SLIST];
+    while (__any_sync(0xffffffffu, !done)) {
+      // 1) each lane extends its traversal until its list is full or it is done
+      int nlist = 0;
+      while (!done && nlist < SLIST) {
+        uint32_t mk = (uint32_t)(masks >> (8 * level)) & 0xffu;
+        if (mk == 0) {
+          if (level == T.top) {
+            done = true;
+            break;
+          }
+          ++level;
+          idx /= FANOUT;
+          continue;
+        }
+        int c = __ffs(mk) - 1;
+        masks &= ~(1ull << (8 * level + c));
+        int64_t ch = idx * FANOUT + c;
+        double c2 = cut2(B.dmin, scale);
+        st.boxes++;
+        if (level - 1 == 0) {
+          if (box_lb2<D>(T, T.lvl_off[0] + ch, q) <= c2) {
+            offer_seam<D>(T, ch, q, B, st);
+            offer_seam<D>(T, ch + 1, q, B, st);
+            list[nlist++] = ch;
+          }
+        } else if (box_lb2<D>(T, T.lvl_off[level - 1] + ch, q) <= c2) {
+          --level;
+          idx = ch;
+          masks |= (uint64_t)child_mask<D>(T, level, idx, q, c2, st) << (8 * level);
+        }
+      }
+      __syncwarp();
+      W.dmin[lane] = B.dmin;
+      // 2) pool the warp's pairs
+      int incl = nlist;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += y;
+      }
+      int total = __shfl_sync(0xffffffffu, incl, 31);
+      int base = incl - nlist;
+      for (int i = 0; i < nlist; ++i) {
+        W.pseg[base + i] = (int)list[i];
+        W.powner[base + i] = (unsigned char)lane;
+      }
+      __syncwarp();
+      // 3) deal the pairs out 32 at a time
+      for (int c0 = 0; c0 < total; c0 += 32) {
+        int pi = c0 + lane;
+        bool has = pi < total;
+        int owner = 0;
+        int64_t s = 0;
+        double qq[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) qq[k] = 0.0;
+        if (has) {
+          owner = W.powner[pi];
+          s = W.pseg[pi];
+#pragma unroll
+          for (int k = 0; k < D; ++k) qq[k] = W.q[owner][k];
+          double sc = T.hdr[4];
+#pragma unroll
+          for (int k = 0; k < D; ++k) sc = fmax(sc, fabs(qq[k]));
+          st.boxes++;
+          // re-test with the owner's current bound (survivors may have tightened it)
+          has = box_lb2<D>(T, T.lvl_off[0] + s, qq) <= cut2(W.dmin[owner], sc);
+        }
+        PairPrep P;
+        if (has) {
+          prep_pair<D>(T, s, qq, P);
+          st.pairs++;
+        }
+        pieces_step<D, STATS>(W, head, tail, has, s, owner, P, qq, T, p.clip_tol, p.max_iter, 0,
+                              B, st, lane);
+      }
+      __syncwarp();
+    }
+  }
+  while (tail > head)
+    flush_survivors<D, STATS>(W, head, tail, T, p.clip_tol, p.max_iter, B, st, lane);
+  __syncwarp();
+  if (active) {
     if (B.overflow) {
       // more than BAND_K candidates inside the tie band: exact second pass
       p.out_dist[qi] = B.dmin;
@@ -476,16 +807,18 @@ __global__ void __launch_bounds__(BLOCK) project_kernel(ProjParams p) {
     } else {
       write_winner<D>(p, qi, band_pick(B));
     }
-    if (p.out_cand) p.out_cand[qi] = (int64_t)(SCREEN ? st.offers : (uint64_t)(p.tab.S + 1) + st.offers - st.seams);
+    if (p.out_cand)
+      p.out_cand[qi] = SCREEN ? (int64_t)st.offers
+                              : (int64_t)(T.S + 1) + (int64_t)(st.offers - st.seams);
     if (STATS) {
       if (p.out_stats) {
         int64_t* o = p.out_stats + qi * 6;
         o[0] = st.pieces;
-        o[1] = st.c3l;
-        o[2] = st.c3g;
-        o[3] = st.cfl;
-        o[4] = st.cfg;
-        o[5] = st.noroot;
+        o[1] = W.cnt[lane][C_C3L];
+        o[2] = W.cnt[lane][C_C3G];
+        o[3] = W.cnt[lane][C_CFL];
+        o[4] = W.cnt[lane][C_CFG];
+        o[5] = W.cnt[lane][C_NOROOT];
       }
       if (p.out_sound) p.out_sound[qi] = st.sound;
     }
@@ -496,6 +829,26 @@ __global__ void __launch_bounds__(BLOCK) project_kernel(ProjParams p) {
   warp_count(p.counters, MREP_CNT_SEAMS, st.seams);
   warp_count(p.counters, MREP_CNT_BOXES, st.boxes);
   warp_count(p.counters, MREP_CNT_HULL_MISS, (uint64_t)st.noroot);
+}
+
+// Morton key (10 bits per axis) of each query inside the table's padded box
+template <int D>
+__global__ void morton_kernel(const double* q, int64_t n, const double* box_root, uint32_t* key,
+                              uint32_t* idx) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t code = 0;
+  for (int k = 0; k < D; ++k) {
+    double lo = box_root[k], hi = box_root[3 + k];
+    double ext = fmax(hi - lo, 1e-300);
+    double u = (q[i * D + k] - (lo - ext)) / (3.0 * ext);
+    u = fmin(fmax(u, 0.0), 1.0);
+    uint32_t c = (uint32_t)(u * 1023.0);
+    // spread 10 bits with stride D
+    for (int b = 0; b < 10; ++b) code |= ((c >> b) & 1u) << (b * D + k);
+  }
+  key[i] = code;
+  idx[i] = (uint32_t)i;
 }
 
 template <int D, bool SCREEN>
@@ -884,12 +1237,33 @@ int mrep_project(const void* table, int64_t S, int d, const double* queries, int
   p.out_stats = out_stats;
   p.out_sound = out_sound;
   p.counters = counters;
+  // workspace: pass-2 list + Morton keys / permutation + sort scratch
+  size_t sort_tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 30, st);
+  size_t off_list = 16, off_keys = off_list + sizeof(int64_t) * (size_t)n;
+  size_t off_tmp = off_keys + 4 * sizeof(uint32_t) * (size_t)n;
+  size_t wsb = off_tmp + sort_tmp + 256;
   void* ws = nullptr;
-  size_t wsb = sizeof(unsigned long long) * 2 + sizeof(int64_t) * (size_t)n;
   MREP_CUDA_CHECK(cudaMallocAsync(&ws, wsb, st));
-  p.pass2_count = (unsigned long long*)ws;
-  p.pass2_list = (int64_t*)((char*)ws + 16);
+  char* wc = (char*)ws;
+  p.pass2_count = (unsigned long long*)wc;
+  p.pass2_list = (int64_t*)(wc + off_list);
   MREP_CUDA_CHECK(cudaMemsetAsync(ws, 0, 16, st));
+  p.perm = nullptr;
+  if (!(flags & MREP_NO_SORT) && n > 64) {
+    uint32_t* k_in = (uint32_t*)(wc + off_keys);
+    uint32_t* k_out = k_in + n;
+    uint32_t* i_in = k_out + n;
+    uint32_t* i_out = i_in + n;
+    const double* root = p.tab.box + p.tab.lvl_off[p.tab.top] * 6;
+    if (d == 3) morton_kernel<3><<<grid_for(n, 256), 256, 0, st>>>(queries, n, root, k_in, i_in);
+    else morton_kernel<2><<<grid_for(n, 256), 256, 0, st>>>(queries, n, root, k_in, i_in);
+    MREP_LAUNCH_CHECK();
+    MREP_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(wc + off_tmp, sort_tmp, k_in, k_out, i_in, i_out,
+                                                    (int)n, 0, d * 10, st));
+    p.perm = i_out;
+  }
   int rc = d == 3 ? launch_project<3>(p, flags, st) : launch_project<2>(p, flags, st);
   MREP_CUDA_CHECK(cudaFreeAsync(ws, st));
   return rc;
