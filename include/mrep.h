@@ -39,6 +39,7 @@ extern "C" {
 #define MREP_SCREEN 1u   /* BVH-culled exact solve (t/foot/dist/seg identical; cand = candidates examined) */
 #define MREP_STATS 2u    /* brute-force mode with per-query stats + soundness (forces !MREP_SCREEN) */
 #define MREP_NO_SORT 4u  /* process queries in input order (default: Morton order for warp coherence) */
+#define MREP_FUSED 8u    /* screened mode in the single fused warp-cooperative kernel (default: wavefront) */
 
 /* Work counters written (accumulated) by mrep_project when `counters_dev` != NULL. */
 #define MREP_CNT_PAIRS 0      /* (query, cubic) pairs solved: E, quartic, rebase, pieces */

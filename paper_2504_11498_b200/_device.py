@@ -163,7 +163,7 @@ class DeviceTable:
                                         L.ptr(self.buf), L.stream_ptr()))
 
     def project(self, queries, clip_tol=1e-6, max_iter=8, soundness_samples=0, screen=True,
-                stats=False, counters=None):
+                stats=False, counters=None, extra_flags=0):
         """Project device queries (n, d); returns device tensors
         (t, foot, dist, cand, seg, stats|None, sound|None)."""
         torch = L._torch()
@@ -179,6 +179,7 @@ class DeviceTable:
         st = torch.zeros((n, 6), dtype=torch.int64, device=dev) if stats else None
         sound = torch.empty((n,), dtype=torch.float64, device=dev) if stats else None
         flags = (L.MREP_STATS if stats else 0) | (L.MREP_SCREEN if (screen and not stats) else 0)
+        flags |= int(extra_flags)
         L.check(L.lib().mrep_project(
             L.ptr(self.buf), self.S, self.d, L.ptr(q), n, float(clip_tol), int(max_iter),
             int(soundness_samples), flags, L.ptr(t), L.ptr(foot), L.ptr(dist), L.ptr(cand),

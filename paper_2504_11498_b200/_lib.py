@@ -21,6 +21,8 @@ LIB_PATH = os.path.join(_HERE, "libmrep.so")
 
 MREP_SCREEN = 1
 MREP_STATS = 2
+MREP_NO_SORT = 4
+MREP_FUSED = 8
 NUM_COUNTERS = 8
 CNT_PAIRS, CNT_SURVIVORS, CNT_CLIP_ITERS, CNT_SEAMS, CNT_BOXES, CNT_PASS2, CNT_HULL_MISS = range(7)
 

@@ -90,10 +90,20 @@ __device__ __forceinline__ int quad_roots(double c0, double c1, double c2, doubl
   return 1;
 }
 
-// _kernels.py:58-88; returns count (0..3), roots r0..r2 (append order)
-__device__ __forceinline__ int cubic_roots(double c0, double c1, double c2, double c3, double& r0,
-                                           double& r1, double& r2) {
-  if (c3 == 0.0) return quad_roots(c0, c1, c2, r0, r1);
+// _kernels.py:58-88; up to 3 roots in append order.  Not inlined: it is
+// called from two sites (degenerate cubic, Ferrari resolvent) and carries
+// acos / cos / cbrt, the largest instruction sequences of the solve.
+struct Cubic3 {
+  double r0, r1, r2;
+  int n;
+};
+
+__device__ __noinline__ Cubic3 cubic_roots3(double c0, double c1, double c2, double c3) {
+  Cubic3 o{0.0, 0.0, 0.0, 0};
+  if (c3 == 0.0) {
+    o.n = quad_roots(c0, c1, c2, o.r0, o.r1);
+    return o;
+  }
   double b = c2 / c3, c = c1 / c3, d = c0 / c3;
   double p = c - b * b / 3.0;
   double q = 2.0 * pow3(b) / 27.0 - b * c / 3.0 + d;
@@ -105,17 +115,23 @@ __device__ __forceinline__ int cubic_roots(double c0, double c1, double c2, doub
     if (arg > 1.0) arg = 1.0;
     else if (arg < -1.0) arg = -1.0;
     double th = acos(arg) / 3.0;
-    r0 = m * cos(th - 2.0943951023931953 * 0.0) + off;
-    r1 = m * cos(th - 2.0943951023931953 * 1.0) + off;
-    r2 = m * cos(th - 2.0943951023931953 * 2.0) + off;
-    return 3;
+#pragma unroll 1
+    for (int k = 0; k < 3; ++k) {
+      double r = m * cos(th - 2.0943951023931953 * (double)k) + off;
+      o.r0 = o.r1;  // shift in: after 3 steps r0, r1, r2 = roots k = 0, 1, 2
+      o.r1 = o.r2;
+      o.r2 = r;
+    }
+    o.n = 3;
+    return o;
   }
   double rr = q * q / 4.0 + pow3(p) / 27.0;
   double srt = sqrt((0.0 > rr) ? 0.0 : rr);  // Python max(rr, 0.0)
   double u = -q / 2.0 + srt;
   double v = -q / 2.0 - srt;
-  r0 = np_cbrt(u) + np_cbrt(v) + off;
-  return 1;
+  o.r0 = np_cbrt(u) + np_cbrt(v) + off;
+  o.n = 1;
+  return o;
 }
 
 // Root set of E' on [0,1]: up to 4 sorted slots, `valid` bitmask (bit i = slot i).
@@ -137,6 +153,20 @@ __device__ __forceinline__ void cex(double& a, double& b) {
 // sort, dedup).  Candidate slots keep the reference's append order; invalid
 // slots hold +inf so a stable 4-element odd-even transposition sort reproduces
 // the reference's compaction followed by insertion sort.
+// Candidate slots for the quartic: values are shifted in at the END in the
+// reference's append order (slot 3 newest); the stable sort afterwards only
+// needs the relative order, which shifting preserves.
+struct Slots4 {
+  double v0, v1, v2, v3;
+};
+
+__device__ __forceinline__ void push4(Slots4& S, double x) {
+  S.v0 = S.v1;
+  S.v1 = S.v2;
+  S.v2 = S.v3;
+  S.v3 = x;
+}
+
 __device__ __forceinline__ Roots4 quartic_roots_01(const double c[5]) {
   Roots4 out;
   out.count = 0;
@@ -150,21 +180,22 @@ __device__ __forceinline__ Roots4 quartic_roots_01(const double c[5]) {
   if (scale == 0.0) return out;
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
   double eps = 1e-12 * scale;
-  double cand[4] = {INF, INF, INF, INF};
-  bool ok[4] = {false, false, false, false};
+  Slots4 S{INF, INF, INF, INF};
   if (fabs(c[4]) <= eps) {
+    double a0 = 0.0, a1 = 0.0;
+    int n = 0;
+    Cubic3 cr{0.0, 0.0, 0.0, 0};
     if (fabs(c[3]) <= eps) {
-      int n = quad_roots(c[0], c[1], c[2], cand[0], cand[1]);
-      ok[0] = n > 0;
-      ok[1] = n > 1;
+      n = quad_roots(c[0], c[1], c[2], a0, a1);
+      cr.r0 = a0;
+      cr.r1 = a1;
+      cr.n = n;
     } else {
-      double r2 = INF;
-      int n = cubic_roots(c[0], c[1], c[2], c[3], cand[0], cand[1], r2);
-      cand[2] = r2;
-      ok[0] = n > 0;
-      ok[1] = n > 1;
-      ok[2] = n > 2;
+      cr = cubic_roots3(c[0], c[1], c[2], c[3]);
     }
+    if (cr.n > 0) push4(S, cr.r0);
+    if (cr.n > 1) push4(S, cr.r1);
+    if (cr.n > 2) push4(S, cr.r2);
   } else {
     double b3 = c[3] / c[4], b2 = c[2] / c[4], b1 = c[1] / c[4], b0 = c[0] / c[4];
     double p = b2 - 3.0 * b3 * b3 / 8.0;
@@ -177,72 +208,52 @@ __device__ __forceinline__ Roots4 quartic_roots_01(const double c[5]) {
       // biquadratic in y^2: each nonnegative z gives +sqrt(z)+off, -sqrt(z)+off
       double z0 = 0.0, z1 = 0.0;
       int zn = quad_roots(r, p, 1.0, z0, z1);
-      bool u0 = zn > 0 && z0 >= 0.0;
-      bool u1 = zn > 1 && z1 >= 0.0;
-      double s0 = u0 ? sqrt(z0) : 0.0;
-      double s1 = u1 ? sqrt(z1) : 0.0;
-      // append order: (z0 pair) then (z1 pair), packed from slot 0
-      double a0 = s0 + off, a1 = -s0 + off, a2 = s1 + off, a3 = -s1 + off;
-      if (u0) {
-        cand[0] = a0;
-        cand[1] = a1;
-        ok[0] = ok[1] = true;
-        if (u1) {
-          cand[2] = a2;
-          cand[3] = a3;
-          ok[2] = ok[3] = true;
+#pragma unroll 1
+      for (int i = 0; i < zn; ++i) {
+        double z = (i == 0) ? z0 : z1;
+        if (z >= 0.0) {
+          double sq = sqrt(z);
+          push4(S, sq + off);
+          push4(S, -sq + off);
         }
-      } else if (u1) {
-        cand[0] = a2;
-        cand[1] = a3;
-        ok[0] = ok[1] = true;
       }
     } else {
       // resolvent cubic 8m^3 + 8p m^2 + (2p^2 - 8r) m - q^2 = 0
-      double m0 = 0.0, m1 = -INF, m2 = -INF;
-      int mn = cubic_roots(-q * q, 2.0 * p * p - 8.0 * r, 8.0 * p, 8.0, m0, m1, m2);
-      double m = m0;
-      if (mn > 1 && m1 > m) m = m1;
-      if (mn > 2 && m2 > m) m = m2;
-      if (mn > 0 && m > 0.0) {
+      Cubic3 cr = cubic_roots3(-q * q, 2.0 * p * p - 8.0 * r, 8.0 * p, 8.0);
+      double m = cr.r0;
+      if (cr.n > 1 && cr.r1 > m) m = cr.r1;
+      if (cr.n > 2 && cr.r2 > m) m = cr.r2;
+      if (cr.n > 0 && m > 0.0) {
         double s = sqrt(2.0 * m);
-        double x0 = 0, x1 = 0, y0 = 0, y1 = 0;
-        int n1 = quad_roots(p / 2.0 + m - q / (2.0 * s), s, 1.0, x0, x1);
-        int n2 = quad_roots(p / 2.0 + m + q / (2.0 * s), -s, 1.0, y0, y1);
-        x0 += off;
-        x1 += off;
-        y0 += off;
-        y1 += off;
-        // pack: first quadratic's roots, then the second's
-        cand[0] = (n1 > 0) ? x0 : y0;
-        cand[1] = (n1 > 1) ? x1 : ((n1 == 1) ? y0 : y1);
-        cand[2] = (n1 == 2) ? y0 : ((n1 == 1) ? y1 : INF);
-        cand[3] = (n1 == 2) ? y1 : INF;
-        int n = n1 + n2;
-        ok[0] = n > 0;
-        ok[1] = n > 1;
-        ok[2] = n > 2;
-        ok[3] = n > 3;
+#pragma unroll 1
+        for (int j = 0; j < 2; ++j) {
+          double cc0 = (j == 0) ? p / 2.0 + m - q / (2.0 * s) : p / 2.0 + m + q / (2.0 * s);
+          double x0 = 0.0, x1 = 0.0;
+          int nj = quad_roots(cc0, (j == 0) ? s : -s, 1.0, x0, x1);
+          if (nj > 0) push4(S, x0 + off);
+          if (nj > 1) push4(S, x1 + off);
+        }
       }
     }
   }
-  // polish, residual filter, clamp (_kernels.py:150-161)
-#pragma unroll
+  // polish, residual filter, clamp (_kernels.py:150-161); rolled: slot v0 is
+  // processed, then the ring rotates, so after 4 steps the order is restored
+#pragma unroll 1
   for (int i = 0; i < 4; ++i) {
-    if (ok[i]) {
-      double x = polish_root(c[0], c[1], c[2], c[3], c[4], cand[i]);
+    double x = S.v0;
+    if (x != INF) {
+      x = polish_root(c[0], c[1], c[2], c[3], c[4], x);
       double f = c[0] + x * (c[1] + x * (c[2] + x * (c[3] + x * c[4])));
       if (fabs(f) <= 1e-9 * scale && -1e-12 <= x && x <= 1.0 + 1e-12) {
         if (x < 0.0) x = 0.0;
         else if (x > 1.0) x = 1.0;
-        cand[i] = x;
       } else {
-        cand[i] = INF;
+        x = INF;
       }
-    } else {
-      cand[i] = INF;
     }
+    push4(S, x);  // rotate: v0 leaves the front, re-enters at the back
   }
+  double cand[4] = {S.v0, S.v1, S.v2, S.v3};
   // stable sort (odd-even transposition) == compaction + insertion sort
   cex(cand[0], cand[1]);
   cex(cand[2], cand[3]);
@@ -331,9 +342,9 @@ __device__ __forceinline__ double eval_ordinates(const double (&b)[6], double u)
 __device__ __forceinline__ bool hull_cross(const double (&b)[6], double& z1o, double& z2o) {
   uint32_t lo_st = 0, hi_st = 0;
   int nl = 0, nh = 0;
-#pragma unroll
+#pragma unroll 1
   for (int i = 0; i < 6; ++i) {
-    double x = xs5(i), y = b[i];
+    double x = xs5(i), y = sel6(b, i);
     while (nl > 1) {
       int a = (lo_st >> (3 * (nl - 1))) & 7, c = (lo_st >> (3 * (nl - 2))) & 7;
       double xa = xs5(a), ya = sel6(b, a), xc = xs5(c), yc = sel6(b, c);
@@ -352,7 +363,7 @@ __device__ __forceinline__ bool hull_cross(const double (&b)[6], double& z1o, do
     ++nh;
   }
   double z1 = 2.0, z2 = -1.0;
-#pragma unroll
+#pragma unroll 1
   for (int chain = 0; chain < 2; ++chain) {
     uint32_t st = chain == 0 ? lo_st : hi_st;
     int m = chain == 0 ? nl : nh;

@@ -21,6 +21,7 @@
 // query is re-run in an exact second pass with the final dmin.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <mutex>
@@ -35,6 +36,24 @@ namespace mrep {
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+// Keep stream-ordered allocations cached in the device's default pool: the
+// projection workspace is re-requested on every call, and releasing it at each
+// synchronisation would re-map hundreds of MB per call.
+static std::mutex g_pool_mu;
+static int g_pool_dev_mask = 0;
+int ensure_pool() {
+  int dev = 0;
+  MREP_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (dev < 31 && (g_pool_dev_mask & (1 << dev))) return MREP_OK;
+  cudaMemPool_t pool;
+  MREP_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = ~0ull;
+  MREP_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  if (dev < 31) g_pool_dev_mask |= 1 << dev;
+  return MREP_OK;
+}
 
 constexpr uint64_t SURV_BIT = 1ull << 62;
 constexpr int BAND_K = 4;
@@ -306,7 +325,7 @@ __device__ __forceinline__ uint32_t child_mask(const TableView& T, int level, in
   int64_t first = idx * FANOUT;
   int64_t cnt = T.lvl_cnt[level - 1];
   int64_t off = T.lvl_off[level - 1];
-#pragma unroll
+#pragma unroll 1
   for (int c = 0; c < FANOUT; ++c) {
     int64_t ch = first + c;
     if (ch < cnt) {
@@ -692,6 +711,7 @@ __global__ void __launch_bounds__(BLOCK) project_kernel(ProjParams p) {
         int64_t first = idx * FANOUT, cnt = T.lvl_cnt[level - 1], off = T.lvl_off[level - 1];
         double best = 0.0;
         int64_t bi = first;
+#pragma unroll 1
         for (int c = 0; c < FANOUT; ++c) {
           int64_t ch = first + c;
           if (ch < cnt) {
@@ -706,8 +726,8 @@ __global__ void __launch_bounds__(BLOCK) project_kernel(ProjParams p) {
         idx = bi;
         --level;
       }
-      offer_seam<D>(T, idx, q, B, st);
-      offer_seam<D>(T, idx + 1, q, B, st);
+#pragma unroll 1
+      for (int e = 0; e < 2; ++e) offer_seam<D>(T, idx + e, q, B, st);
     }
     uint64_t masks = 0;
     int level = T.top;
@@ -736,8 +756,8 @@ __global__ void __launch_bounds__(BLOCK) project_kernel(ProjParams p) {
         st.boxes++;
         if (level - 1 == 0) {
           if (box_lb2<D>(T, T.lvl_off[0] + ch, q) <= c2) {
-            offer_seam<D>(T, ch, q, B, st);
-            offer_seam<D>(T, ch + 1, q, B, st);
+#pragma unroll 1
+            for (int e = 0; e < 2; ++e) offer_seam<D>(T, ch + e, q, B, st);
             list[nlist++] = ch;
           }
         } else if (box_lb2<D>(T, T.lvl_off[level - 1] + ch, q) <= c2) {
@@ -876,6 +896,387 @@ __global__ void __launch_bounds__(BLOCK) project_pass2_kernel(ProjParams p) {
   }
   if (p.counters && blockIdx.x == 0 && threadIdx.x == 0)
     atomicAdd((unsigned long long*)&p.counters[MREP_CNT_PASS2], total);
+}
+
+// =================================================================
+// Wavefront pipeline for the screened mode.
+//
+// Small single-purpose kernels, each with a compact instruction footprint
+// and uniform work items, connected by device-side append buffers:
+//   W1 traverse  (thread / query, Morton order): BVH walk with the seam upper
+//                bound; emits (query, cubic) pairs and the seam candidates
+//                inside the seam tie band;
+//   W2 pairs     (thread / pair): E, E' roots, monotone pieces, elimination;
+//                emits surviving pieces;
+//   W3 clip      (thread / survivor): Bezier clipping, foot point, distance;
+//                emits candidates that can still reach the tie band and
+//                lowers the query's running minimum (atomicMin on the bits of
+//                a non-negative double);
+//   W4/W5/W6     exact tie-band selection over the candidate list, the
+//                reference's two-pass rule (_kernels.py:480-490) as three
+//                atomic passes: min distance -> min t inside dmin + 1e-12 ->
+//                min reference order -> the winner writes its outputs.
+// Queries whose buffers would overflow (or whose seam band exceeds BAND_K)
+// are finished by a per-thread exact fallback kernel.
+// =================================================================
+struct WaveParams {
+  TableView tab;
+  const double* q;
+  int64_t n;
+  const uint32_t* perm;
+  double clip_tol;
+  int max_iter;
+  double* out_t;
+  double* out_foot;
+  double* out_dist;
+  int64_t* out_cand;
+  int32_t* out_seg;
+  uint64_t* counters;
+  unsigned long long* dmin;  // bits of the running min distance (non-negative double)
+  unsigned long long* tkey;  // order key of the min t inside the band
+  unsigned long long* okey;  // min reference order among band members with that t
+  int32_t* flag;             // 1 = finish in the fallback kernel
+  unsigned long long* cnt;   // [0] pairs, [1] survivors, [2] candidates, [3] fallbacks
+  uint32_t* pq;
+  uint32_t* ps;
+  unsigned long long pcap;
+  double* sb;  // survivors: b0..b5, lo, hi
+  uint32_t* sq;
+  uint32_t* ssk;  // cubic << 3 | piece
+  unsigned long long scap;
+  uint32_t* cq;
+  double* ct;
+  double* cd;
+  double* cv;
+  unsigned long long* cord;
+  unsigned long long ccap;
+  int64_t* fb;
+};
+
+// warp-aggregated slot allocation (works in divergent code)
+__device__ __forceinline__ unsigned long long wave_append(unsigned long long* counter, bool want) {
+  unsigned act = __activemask();
+  unsigned bal = __ballot_sync(act, want);
+  if (!bal) return ~0ull;
+  int leader = __ffs(bal) - 1;
+  unsigned long long base = 0;
+  if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(counter, (unsigned long long)__popc(bal));
+  base = __shfl_sync(act, base, leader);
+  return want ? base + __popc(bal & ((1u << (threadIdx.x & 31)) - 1)) : ~0ull;
+}
+
+__device__ __forceinline__ unsigned long long tkey_of(double t) {
+  if (t == 0.0) t = 0.0;  // -0.0 and +0.0 compare equal in the reference
+  unsigned long long b = (unsigned long long)__double_as_longlong(t);
+  return (b >> 63) ? ~b : (b | (1ull << 63));
+}
+
+__device__ __forceinline__ double dmin_of(const WaveParams& w, int64_t qi) {
+  return __longlong_as_double((long long)w.dmin[qi]);
+}
+
+template <int D>
+__global__ void __launch_bounds__(BLOCK) wave_traverse(WaveParams w) {
+  int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  QStats st{};
+  if (gi < w.n) {
+    const TableView& T = w.tab;
+    int64_t qi = w.perm ? (int64_t)w.perm[gi] : gi;
+    double q[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) q[k] = w.q[qi * D + k];
+    const double NaN = __longlong_as_double(0x7ff8000000000000LL);
+    w.out_t[qi] = NaN;
+    w.out_dist[qi] = NaN;
+#pragma unroll
+    for (int k = 0; k < D; ++k) w.out_foot[qi * D + k] = NaN;
+    if (w.out_seg) w.out_seg[qi] = -1;
+    w.tkey[qi] = ~0ull;
+    w.okey[qi] = ~0ull;
+    bool fall = false;
+    Band B;
+    band_init(B, false, 0.0);
+    double scale = T.hdr[4];
+#pragma unroll
+    for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
+    {  // greedy descent: first bound from the seams of a nearby cubic
+      int level = T.top;
+      int64_t idx = 0;
+      while (level > 0) {
+        int64_t first = idx * FANOUT, cnt = T.lvl_cnt[level - 1], off = T.lvl_off[level - 1];
+        double best = 0.0;
+        int64_t bi = first;
+#pragma unroll 1
+        for (int c = 0; c < FANOUT; ++c) {
+          int64_t ch = first + c;
+          if (ch < cnt) {
+            st.boxes++;
+            double lb = box_lb2<D>(T, off + ch, q);
+            if (c == 0 || lb < best) {
+              best = lb;
+              bi = ch;
+            }
+          }
+        }
+        idx = bi;
+        --level;
+      }
+#pragma unroll 1
+      for (int e = 0; e < 2; ++e) offer_seam<D>(T, idx + e, q, B, st);
+    }
+    uint64_t masks = 0;
+    int level = T.top;
+    int64_t idx = 0;
+    masks = (uint64_t)child_mask<D>(T, level, 0, q, cut2(B.dmin, scale), st) << (8 * level);
+    for (;;) {
+      uint32_t mk = (uint32_t)(masks >> (8 * level)) & 0xffu;
+      if (mk == 0) {
+        if (level == T.top) break;
+        ++level;
+        idx /= FANOUT;
+        continue;
+      }
+      int c = __ffs(mk) - 1;
+      masks &= ~(1ull << (8 * level + c));
+      int64_t ch = idx * FANOUT + c;
+      double c2 = cut2(B.dmin, scale);
+      st.boxes++;
+      if (level - 1 == 0) {
+        if (box_lb2<D>(T, T.lvl_off[0] + ch, q) <= c2) {
+#pragma unroll 1
+          for (int e = 0; e < 2; ++e) offer_seam<D>(T, ch + e, q, B, st);
+          unsigned long long slot = wave_append(&w.cnt[0], true);
+          if (slot < w.pcap) {
+            w.pq[slot] = (uint32_t)qi;
+            w.ps[slot] = (uint32_t)ch;
+          } else {
+            fall = true;
+          }
+        }
+      } else if (box_lb2<D>(T, T.lvl_off[level - 1] + ch, q) <= c2) {
+        --level;
+        idx = ch;
+        masks |= (uint64_t)child_mask<D>(T, level, idx, q, c2, st) << (8 * level);
+      }
+    }
+    if (B.overflow) fall = true;
+    w.dmin[qi] = (unsigned long long)__double_as_longlong(B.dmin);
+    // the seam members of the seam tie band become candidates
+#pragma unroll
+    for (int j = 0; j < BAND_K; ++j) {
+      bool want = (B.valid >> j) & 1u;
+      unsigned long long slot = wave_append(&w.cnt[2], want);
+      if (want) {
+        if (slot < w.ccap) {
+          w.cq[slot] = (uint32_t)qi;
+          w.ct[slot] = B.t[j];
+          w.cd[slot] = B.d[j];
+          w.cv[slot] = -1.0;
+          w.cord[slot] = B.ord[j];
+        } else {
+          fall = true;
+        }
+      }
+    }
+    if (w.out_cand) w.out_cand[qi] = (int64_t)st.offers;
+    w.flag[qi] = fall ? 1 : 0;
+    if (fall) {
+      unsigned long long slot = atomicAdd(&w.cnt[3], 1ull);
+      w.fb[slot] = qi;
+    }
+  }
+  warp_count(w.counters, MREP_CNT_SEAMS, st.seams);
+  warp_count(w.counters, MREP_CNT_BOXES, st.boxes);
+}
+
+template <int D>
+__global__ void __launch_bounds__(BLOCK) wave_pairs(WaveParams w) {
+  unsigned long long total = *(volatile unsigned long long*)&w.cnt[0];
+  if (total > w.pcap) total = w.pcap;
+  const TableView& T = w.tab;
+  uint64_t npairs = 0, nboxes = 0;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    int64_t qi = w.pq[i];
+    int64_t s = w.ps[i];
+    if (w.flag[qi]) continue;
+    double q[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) q[k] = w.q[qi * D + k];
+    double scale = T.hdr[4];
+#pragma unroll
+    for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
+    ++nboxes;
+    // re-test with the query's final seam bound
+    if (!(box_lb2<D>(T, T.lvl_off[0] + s, q) <= cut2(dmin_of(w, qi), scale))) continue;
+    ++npairs;
+    PairPrep P;
+    prep_pair<D>(T, s, q, P);
+    double lo = 0.0;
+#pragma unroll 1
+    for (int k = 0; k <= P.nin; ++k) {
+      double hi = (k == P.nin) ? 1.0 : (k == 0 ? P.b1 : (k == 1 ? P.b2 : (k == 2 ? P.b3 : P.b4)));
+      double bp[6];
+      restrict_ordinates(P.bseg, lo, hi, bp);
+      bool surv = bp[0] < 0.0 && bp[0] * bp[5] <= 0.0;
+      unsigned long long slot = wave_append(&w.cnt[1], surv);
+      if (surv) {
+        if (slot < w.scap) {
+          double* o = w.sb + slot * 8;
+#pragma unroll
+          for (int j = 0; j < 6; ++j) o[j] = bp[j];
+          o[6] = lo;
+          o[7] = hi;
+          w.sq[slot] = (uint32_t)qi;
+          w.ssk[slot] = (uint32_t)((s << 3) | k);
+        } else if (atomicExch(&w.flag[qi], 1) == 0) {  // finished by the fallback kernel
+          unsigned long long fs = atomicAdd(&w.cnt[3], 1ull);
+          w.fb[fs] = qi;
+        }
+      }
+      lo = hi;
+    }
+  }
+  warp_count(w.counters, MREP_CNT_PAIRS, npairs);
+  warp_count(w.counters, MREP_CNT_BOXES, nboxes);
+}
+
+template <int D>
+__global__ void __launch_bounds__(BLOCK) wave_clip(WaveParams w) {
+  unsigned long long total = *(volatile unsigned long long*)&w.cnt[1];
+  if (total > w.scap) total = w.scap;
+  const TableView& T = w.tab;
+  uint64_t nsurv = 0, nit = 0, nmiss = 0;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    int64_t qi = w.sq[i];
+    if (w.flag[qi]) continue;
+    const double* o = w.sb + i * 8;
+    double bp[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) bp[j] = o[j];
+    double lo = o[6], hi = o[7];
+    uint32_t sk = w.ssk[i];
+    int64_t s = sk >> 3;
+    ClipOut co = clip_root(bp, w.clip_tol, w.max_iter);
+    ++nsurv;
+    nit += (uint64_t)co.used;
+    if (!co.ok) {
+      ++nmiss;
+      continue;
+    }
+    const double* r = T.rec + s * REC;
+    double ta = __ldg(r + 24), tb = __ldg(r + 25);
+    double v = lo + co.root * (hi - lo);
+    double acc = 0.0;
+#pragma unroll
+    for (int dim = 0; dim < D; ++dim) {
+      double f = decasteljau1(__ldg(r + 12 + dim), __ldg(r + 15 + dim), __ldg(r + 18 + dim),
+                              __ldg(r + 21 + dim), v);
+      double diff = w.q[qi * D + dim] - f;
+      acc += diff * diff;
+    }
+    double d = sqrt(acc);
+    double t = ta + v * (tb - ta);
+    if (w.out_cand) atomicAdd((unsigned long long*)&w.out_cand[qi], 1ull);
+    double cur = dmin_of(w, qi);
+    bool keep = d <= cur + 1e-12;
+    unsigned long long slot = wave_append(&w.cnt[2], keep);
+    if (keep) {
+      atomicMin(&w.dmin[qi], (unsigned long long)__double_as_longlong(d));
+      if (slot < w.ccap) {
+        w.cq[slot] = (uint32_t)qi;
+        w.ct[slot] = t;
+        w.cd[slot] = d;
+        w.cv[slot] = v;
+        w.cord[slot] = SURV_BIT | sk;
+      } else if (atomicExch(&w.flag[qi], 1) == 0) {
+        unsigned long long fs = atomicAdd(&w.cnt[3], 1ull);
+        w.fb[fs] = qi;
+      }
+    }
+  }
+  warp_count(w.counters, MREP_CNT_SURVIVORS, nsurv);
+  warp_count(w.counters, MREP_CNT_CLIP_ITERS, nit);
+  warp_count(w.counters, MREP_CNT_HULL_MISS, nmiss);
+}
+
+// W4..W6: the reference's selection as three atomic passes over candidates
+template <int D, int PASS>
+__global__ void __launch_bounds__(256) wave_select(WaveParams w) {
+  unsigned long long total = *(volatile unsigned long long*)&w.cnt[2];
+  if (total > w.ccap) total = w.ccap;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    int64_t qi = w.cq[i];
+    if (w.flag[qi]) continue;
+    double d = w.cd[i];
+    if (!(d <= dmin_of(w, qi) + 1e-12)) continue;
+    unsigned long long tk = tkey_of(w.ct[i]);
+    if (PASS == 0) {
+      atomicMin(&w.tkey[qi], tk);
+      continue;
+    }
+    if (tk != w.tkey[qi]) continue;
+    unsigned long long ord = w.cord[i];
+    if (PASS == 1) {
+      atomicMin(&w.okey[qi], ord);
+      continue;
+    }
+    if (ord != w.okey[qi]) continue;
+    // winner: outputs (foot recomputed exactly as the reference stored it)
+    const TableView& T = w.tab;
+    double foot[D];
+    int32_t seg;
+    if (ord & SURV_BIT) {
+      int64_t s = (int64_t)((ord & ~SURV_BIT) >> 3);
+      const double* r = T.rec + s * REC;
+      double v = w.cv[i];
+#pragma unroll
+      for (int dim = 0; dim < D; ++dim)
+        foot[dim] = decasteljau1(r[12 + dim], r[15 + dim], r[18 + dim], r[21 + dim], v);
+      seg = (int32_t)s;
+    } else {
+      int64_t s = (int64_t)ord;
+      double stt;
+      seam_point<D>(T, s, foot, stt);
+      seg = (int32_t)(s > 0 ? s - 1 : 0);
+    }
+    w.out_t[qi] = w.ct[i];
+    w.out_dist[qi] = d;
+#pragma unroll
+    for (int k = 0; k < D; ++k) w.out_foot[qi * D + k] = foot[k];
+    if (w.out_seg) w.out_seg[qi] = seg;
+  }
+}
+
+// exact per-thread path for the rare queries the buffers could not hold
+template <int D>
+__global__ void __launch_bounds__(BLOCK) wave_fallback(WaveParams w, ProjParams p) {
+  unsigned long long total = *(volatile unsigned long long*)&w.cnt[3];
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    int64_t qi = w.fb[i];
+    double q[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) q[k] = w.q[qi * D + k];
+    double scale = w.tab.hdr[4];
+#pragma unroll
+    for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
+    Band B;
+    band_init(B, false, 0.0);
+    QStats st{};
+    gen_screened<D, false>(w.tab, q, scale, w.clip_tol, w.max_iter, B, st);
+    if (B.overflow) {
+      double dm = B.dmin;
+      band_init(B, true, dm);
+      gen_screened<D, false>(w.tab, q, scale, w.clip_tol, w.max_iter, B, st);
+      write_winner<D>(p, qi, Pick{B.t[0], B.d[0], B.v[0], B.ord[0], B.valid != 0});
+    } else {
+      write_winner<D>(p, qi, band_pick(B));
+    }
+    if (w.out_cand) w.out_cand[qi] = (int64_t)st.offers;
+  }
 }
 
 // ------------------------------------------------------------ table build
@@ -1160,6 +1561,77 @@ static int launch_project(const ProjParams& p, unsigned flags, cudaStream_t st) 
   return MREP_OK;
 }
 
+
+template <int D>
+static int launch_wave(const ProjParams& p, cudaStream_t st) {
+  const int64_t n = p.n;
+  const unsigned long long pcap = (unsigned long long)std::max<int64_t>(8 * n, 1 << 16);
+  const unsigned long long scap = (unsigned long long)std::max<int64_t>(2 * n, 1 << 16);
+  const unsigned long long ccap = (unsigned long long)std::max<int64_t>(4 * n, 1 << 16);
+  size_t bytes = 0;
+  auto take = [&](size_t b) {
+    size_t o = bytes;
+    bytes += (b + 255) & ~(size_t)255;
+    return o;
+  };
+  size_t o_cnt = take(8 * sizeof(unsigned long long));
+  size_t o_dmin = take(n * 8), o_tkey = take(n * 8), o_okey = take(n * 8), o_flag = take(n * 4);
+  size_t o_pq = take(pcap * 4), o_ps = take(pcap * 4);
+  size_t o_sb = take(scap * 64), o_sq = take(scap * 4), o_ssk = take(scap * 4);
+  size_t o_cq = take(ccap * 4), o_ct = take(ccap * 8), o_cd = take(ccap * 8), o_cv = take(ccap * 8),
+         o_cord = take(ccap * 8);
+  size_t o_fb = take(n * 8);
+  char* base = nullptr;
+  MREP_CUDA_CHECK(cudaMallocAsync((void**)&base, bytes, st));
+  WaveParams w{};
+  w.tab = p.tab;
+  w.q = p.q;
+  w.n = n;
+  w.perm = p.perm;
+  w.clip_tol = p.clip_tol;
+  w.max_iter = p.max_iter;
+  w.out_t = p.out_t;
+  w.out_foot = p.out_foot;
+  w.out_dist = p.out_dist;
+  w.out_cand = p.out_cand;
+  w.out_seg = p.out_seg;
+  w.counters = p.counters;
+  w.cnt = (unsigned long long*)(base + o_cnt);
+  w.dmin = (unsigned long long*)(base + o_dmin);
+  w.tkey = (unsigned long long*)(base + o_tkey);
+  w.okey = (unsigned long long*)(base + o_okey);
+  w.flag = (int32_t*)(base + o_flag);
+  w.pq = (uint32_t*)(base + o_pq);
+  w.ps = (uint32_t*)(base + o_ps);
+  w.pcap = pcap;
+  w.sb = (double*)(base + o_sb);
+  w.sq = (uint32_t*)(base + o_sq);
+  w.ssk = (uint32_t*)(base + o_ssk);
+  w.scap = scap;
+  w.cq = (uint32_t*)(base + o_cq);
+  w.ct = (double*)(base + o_ct);
+  w.cd = (double*)(base + o_cd);
+  w.cv = (double*)(base + o_cv);
+  w.cord = (unsigned long long*)(base + o_cord);
+  w.ccap = ccap;
+  w.fb = (int64_t*)(base + o_fb);
+  MREP_CUDA_CHECK(cudaMemsetAsync(w.cnt, 0, 8 * sizeof(unsigned long long), st));
+  const unsigned persist = 148u * 8u;
+  wave_traverse<D><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
+  MREP_LAUNCH_CHECK();
+  wave_pairs<D><<<persist, BLOCK, 0, st>>>(w);
+  MREP_LAUNCH_CHECK();
+  wave_clip<D><<<persist, BLOCK, 0, st>>>(w);
+  MREP_LAUNCH_CHECK();
+  wave_select<D, 0><<<persist, 256, 0, st>>>(w);
+  wave_select<D, 1><<<persist, 256, 0, st>>>(w);
+  wave_select<D, 2><<<persist, 256, 0, st>>>(w);
+  MREP_LAUNCH_CHECK();
+  wave_fallback<D><<<148u, BLOCK, 0, st>>>(w, p);
+  MREP_LAUNCH_CHECK();
+  MREP_CUDA_CHECK(cudaFreeAsync(base, st));
+  return MREP_OK;
+}
 }  // namespace mrep
 
 using namespace mrep;
@@ -1222,6 +1694,8 @@ int mrep_project(const void* table, int64_t S, int d, const double* queries, int
     return MREP_ERR_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  int prc = ensure_pool();
+  if (prc) return prc;
   ProjParams p{};
   p.tab = table_view(table, S);
   p.q = queries;
@@ -1264,7 +1738,10 @@ int mrep_project(const void* table, int64_t S, int d, const double* queries, int
                                                     (int)n, 0, d * 10, st));
     p.perm = i_out;
   }
-  int rc = d == 3 ? launch_project<3>(p, flags, st) : launch_project<2>(p, flags, st);
+  int rc;
+  bool wave = (flags & MREP_SCREEN) && !(flags & MREP_STATS) && !(flags & MREP_FUSED);
+  if (wave) rc = d == 3 ? launch_wave<3>(p, st) : launch_wave<2>(p, st);
+  else rc = d == 3 ? launch_project<3>(p, flags, st) : launch_project<2>(p, flags, st);
   MREP_CUDA_CHECK(cudaFreeAsync(ws, st));
   return rc;
 }

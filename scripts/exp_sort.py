@@ -27,22 +27,22 @@ def morton(q, bits=21):
 p, knots, ctrl = P.clamped_uniform_curve(np.random.default_rng(0), 7, 512, 3)
 prep = prepare_curve(BSplineCurve(p, knots, ctrl), 1e-4)
 tab = prep.table
+from paper_2504_11498_b200 import _lib as L
 qh = np.random.default_rng(1).uniform(0, 1, (1_000_000, 3))
-order = np.argsort(morton(qh), kind="stable")
-for name, arr, screen, n in (("screen unsorted", qh, True, 1_000_000),
-                             ("screen sorted", qh[order], True, 1_000_000),
-                             ("dense unsorted", qh, False, 100_000),
-                             ("dense sorted", qh[order][::10], False, 100_000)):
-    q = torch.from_numpy(np.ascontiguousarray(arr[:n])).cuda()
-    tab.project(q, screen=screen)
+for name, fl, screen, n in (("screen wave", 0, True, 1_000_000),
+                            ("screen fused", L.MREP_FUSED, True, 1_000_000),
+                            ("screen fused nosort", L.MREP_FUSED | L.MREP_NO_SORT, True, 1_000_000),
+                            ("dense", 0, False, 100_000)):
+    q = torch.from_numpy(np.ascontiguousarray(qh[:n])).cuda()
+    tab.project(q, screen=screen, extra_flags=fl)
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     best = 1e9
     for _ in range(3):
         e0.record()
-        tab.project(q, screen=screen)
+        tab.project(q, screen=screen, extra_flags=fl)
         e1.record()
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1))
-    print(f"{name:18s} n={n} {best:8.3f} ms  {n / best / 1e3:8.2f} M pts/s", flush=True)
+    print(f"{name:22s} n={n} {best:8.3f} ms  {n / best / 1e3:8.2f} M pts/s", flush=True)

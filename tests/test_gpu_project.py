@@ -42,6 +42,21 @@ def test_dense_matches_reference(gpu, name):
 
 
 @pytest.mark.parametrize("name", project_fixture_names())
+def test_wavefront_fused_unsorted_agree(gpu, name):
+    """The three screened schedules (wavefront, fused warp kernel, input
+    order) produce bit-identical winners."""
+    from paper_2504_11498_b200 import _device as D, _lib as L
+    z = load_golden(f"project_{name}.npz")
+    tab = D.DeviceTable(*_args(z))
+    a = tab.project(z["queries"])
+    b = tab.project(z["queries"], extra_flags=L.MREP_FUSED)
+    c = tab.project(z["queries"], extra_flags=L.MREP_NO_SORT | L.MREP_FUSED)
+    for k in (0, 1, 2, 4):
+        assert np.array_equal(a[k].cpu().numpy(), b[k].cpu().numpy()), k
+        assert np.array_equal(a[k].cpu().numpy(), c[k].cpu().numpy()), k
+
+
+@pytest.mark.parametrize("name", project_fixture_names())
 def test_screened_equals_dense(gpu, name):
     """The BVH cull never changes the winner: bitwise equal to brute force."""
     from paper_2504_11498_b200 import _device as D
