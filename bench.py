@@ -68,7 +68,8 @@ def make_queries(rank, n):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled (every 50 ms) while the
+    timed region runs; the sampler is this process's own child, stopped by PID."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -77,41 +78,48 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.samples = []
-        self._stop = threading.Event()
+        self.proc = None
         self._t = None
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
-                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+    def _reader(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._reader, daemon=True)
+            self._t.start()
+            time.sleep(0.3)  # first sample before the timed work starts
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self._t.join(timeout=5)
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                          if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
 
 
 def cpu_baseline(seg, queries, sample_n, workers):
@@ -173,8 +181,8 @@ def run_reference(args, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mrep", choices=["mrep", "reference"])
     ap.add_argument("--n", type=int, default=N_PER_RANK)
     ap.add_argument("--ref-sample", type=int, default=32768)
@@ -215,13 +223,13 @@ def main():
     def step(cnt=None):
         return tab.project(q, screen=screen, counters=cnt)
 
+    from paper_2504_11498_b200.sharding import gather_results, pack_results
+
     def gather(out):
+        # the single exchange of the path: (t, distance, segment id) to rank 0
         if world == 1:
             return
-        t, dd, seg = out[0], out[2], out[4].to(torch.float64)
-        pack = torch.stack([t, dd, seg], 1).contiguous()
-        bufs = [torch.empty_like(pack) for _ in range(world)] if rank == 0 else None
-        dist.gather(pack, bufs, dst=0)
+        gather_results(pack_results(out[0], out[2], out[4]), world * n, world, rank)
 
     for _ in range(args.warmup):
         gather(step())
@@ -232,7 +240,9 @@ def main():
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     kstarts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     kends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    with ClockSampler(local) as clocks:
+    clocks = ClockSampler(local)
+    clocks.__enter__()
+    if True:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -255,36 +265,61 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     value = world * n / (ms / 1e3)
+    # own kernels per projection call: Morton keys + 4 cub radix-sort passes
+    # (histogram, exclusive sum, 3 onesweep) + 7 wavefront kernels; dense: 2
+    launches_per_step = (1 + 5 + 7) if screen else (1 + 5 + 2)
 
-    # ---- roofline of the projection kernel ----
+    # ---- roofline: per-stage device times (CUDA events between the pipeline's
+    #      kernels, recorded inside libmrep on this stream) x algorithmic work ----
     c = counters.cpu().numpy().astype(np.float64)
-    flops = (F_PAIR * c[L.CNT_PAIRS] + F_CLIP * c[L.CNT_SURVIVORS] + F_SEAM * c[L.CNT_SEAMS]
-             + F_BOX * c[L.CNT_BOXES])
-    kms = statistics.mean(kern_ms)
     import ctypes
+    stage = np.zeros(8)
+    reps = 5
+    for _ in range(reps):
+        flush.fill_(2.0)
+        tab.project(q, screen=screen, extra_flags=L.MREP_TIMING)
+        buf = (ctypes.c_double * 8)()
+        L.lib().mrep_last_stage_times(buf, 8)
+        stage += np.array(buf[:8]) / reps
     peak = ctypes.c_double()
     L.check(L.lib().mrep_fp64_peak(ctypes.byref(peak)))
-    achieved = flops / (kms / 1e3) / 1e12
-    dense_equiv = (F_PAIR * 510 + F_SEAM * 511) * n / (kms / 1e3) / 1e12
+    kms = statistics.mean(kern_ms)
+    names = ["morton_sort", "traverse", "pairs", "clip", "select", "fallback"]
+    work = {"traverse": F_BOX * c[L.CNT_BOXES] + F_SEAM * c[L.CNT_SEAMS],
+            "pairs": F_PAIR * c[L.CNT_PAIRS], "clip": F_CLIP * c[L.CNT_SURVIVORS]}
+    stages = {}
+    for i, nm in enumerate(names):
+        ms_i = float(stage[i])
+        ent = {"ms": ms_i}
+        if nm in work and ms_i > 0:
+            ent["tflops"] = work[nm] / (ms_i / 1e3) / 1e12
+            ent["frac"] = ent["tflops"] / peak.value
+        stages[nm] = ent
+    flops = sum(work.values())
+    dom = max(("traverse", "pairs", "clip"), key=lambda k: stages[k]["ms"]) if screen else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("project_kernel_dram_bytes_per_launch")
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch", {}).get(f"wave_{dom}")
         except Exception:
             traffic = None
-    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
+    achieved = stages[dom]["tflops"] if dom else flops / (kms / 1e3) / 1e12
+    roofline = {"bound": "fp64", "kernel": f"wave_{dom}" if dom else "project_kernel (dense)",
+                "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                 "frac": achieved / peak.value, "traffic": traffic,
                 "peak_source": "DFMA microbenchmark measured in this run (mrep_fp64_peak); "
                                "MEASURED_PEAKS.json has no FP64 figure",
                 "flop_model": "500/pair + 650/clipped survivor + 10/seam + 10/box test "
-                              "(SURVEY.md 8(d), counters from the kernel)",
+                              "(SURVEY.md 8(d); counts from the kernels' own counters)",
+                "stages": stages,
+                "pipeline": {"ms": kms, "tflops": flops / (kms / 1e3) / 1e12,
+                             "frac": flops / (kms / 1e3) / 1e12 / peak.value},
                 "per_query": {"pairs": c[L.CNT_PAIRS] / n, "survivors": c[L.CNT_SURVIVORS] / n,
                               "seams": c[L.CNT_SEAMS] / n, "box_tests": c[L.CNT_BOXES] / n},
-                "kernel_ms": kms,
-                "dense_equivalent_tflops": dense_equiv,
-                "hbm": {"bytes_per_query": 24 + 8 + 24 + 8 + 8 + 4,
-                        "gbs": n * 76 / (kms / 1e3) / 1e9}}
+                "dense_equivalent_tflops": (F_PAIR * prep.num_segments
+                                            + F_SEAM * (prep.num_segments + 1)) * n
+                                           / (kms / 1e3) / 1e12}
 
     # ---- e2e: host buffers through the C ABI (H2D + kernel + D2H per step) ----
     q_pin = torch.from_numpy(q_host).pin_memory()
@@ -304,6 +339,7 @@ def main():
         t0 = time.perf_counter()
         tab.project_host(qnp, out=onp, screen=screen)
         e2e_times.append(time.perf_counter() - t0)
+    clocks.__exit__(None, None, None)
     e2e_s = statistics.mean(e2e_times)
     if world > 1:
         tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
@@ -330,7 +366,7 @@ def main():
                                                     parallelism=f"query-shard x{world}",
                                                     prep_ms=prep_ms),
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
-                "gpu_launches": 2 * args.steps, "clocks": clocks.summary()}
+                "gpu_launches": launches_per_step * args.steps, "clocks": clocks.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -40,6 +40,7 @@ extern "C" {
 #define MREP_STATS 2u    /* brute-force mode with per-query stats + soundness (forces !MREP_SCREEN) */
 #define MREP_NO_SORT 4u  /* process queries in input order (default: Morton order for warp coherence) */
 #define MREP_FUSED 8u    /* screened mode in the single fused warp-cooperative kernel (default: wavefront) */
+#define MREP_TIMING 16u  /* record per-stage device times (see mrep_last_stage_times); synchronises */
 
 /* Work counters written (accumulated) by mrep_project when `counters_dev` != NULL. */
 #define MREP_CNT_PAIRS 0      /* (query, cubic) pairs solved: E, quartic, rebase, pieces */
@@ -52,6 +53,9 @@ extern "C" {
 #define MREP_NUM_COUNTERS 8
 
 MREP_API const char* mrep_last_error(void);
+/* per-stage device times (ms) of this thread's last MREP_TIMING projection:
+ * [0] Morton sort [1] traverse [2] pairs [3] clip [4] select [5] fallback */
+MREP_API int mrep_last_stage_times(double* ms, int max);
 /* measured FP64 FMA throughput of the current device, TFLOP/s (roofline peak) */
 MREP_API int mrep_fp64_peak(double* tflops);
 MREP_API int mrep_version(void);
@@ -92,6 +96,23 @@ MREP_API int mrep_project_host(const void* table_dev, int64_t S, int d, const do
                       int64_t n, double clip_tol, int max_iter, unsigned flags,
                       double* out_t_host, double* out_foot_host, double* out_dist_host,
                       int64_t* out_cand_host, int32_t* out_seg_host, uint64_t* counters_host);
+
+/* Host-array twins (no GPU framework needed on the caller's side):
+ * mrep_table_create builds a device table from a PreparedCurve's host arrays
+ * (project.py:225-238) and returns an opaque handle; mrep_table_free frees it. */
+MREP_API int mrep_table_create(const double* seg_pts_host, const double* seg_ta_host,
+                               const double* seg_tb_host, const double* seam_t_host,
+                               const double* seam_pt_host, int64_t S, int d, void** table_out);
+MREP_API int mrep_table_free(void* table);
+/* _kernels._project_block (_kernels.py:369-371) with its exact host-array
+ * signature: brute force with stats + soundness, synchronous. */
+MREP_API int mrep_project_block_host(const double* seg_pts, const double* seg_ta,
+                                     const double* seg_tb, const double* seam_t,
+                                     const double* seam_pt, int64_t S, int d,
+                                     const double* queries, int64_t n, double clip_tol,
+                                     int max_iter, int soundness_samples, double* out_t,
+                                     double* out_foot, double* out_dist, int64_t* out_cand,
+                                     int64_t* out_stats, double* out_sound);
 
 /* Exact drop-in for _kernels._project_block (_kernels.py:369-371): the raw
  * prepared arrays, all DEVICE pointers, brute force with stats. */

@@ -23,6 +23,7 @@ MREP_SCREEN = 1
 MREP_STATS = 2
 MREP_NO_SORT = 4
 MREP_FUSED = 8
+MREP_TIMING = 16
 NUM_COUNTERS = 8
 CNT_PAIRS, CNT_SURVIVORS, CNT_CLIP_ITERS, CNT_SEAMS, CNT_BOXES, CNT_PASS2, CNT_HULL_MISS = range(7)
 
@@ -38,6 +39,7 @@ _u32 = ctypes.c_uint
 _SIGS = {
     "mrep_last_error": ([], ctypes.c_char_p),
     "mrep_version": ([], _i32),
+    "mrep_last_stage_times": ([_vp, _i32], _i32),
     "mrep_fp64_peak": ([_vp], _i32),
     "mrep_device_count": ([], _i32),
     "mrep_table_bytes": ([_i64], _i64),
@@ -48,6 +50,10 @@ _SIGS = {
                            _vp, _vp], _i32),
     "mrep_project_block": ([_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _i64, _dbl, _i32, _i32,
                             _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i32),
+    "mrep_table_create": ([_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp], _i32),
+    "mrep_table_free": ([_vp], _i32),
+    "mrep_project_block_host": ([_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _i64, _dbl, _i32, _i32,
+                                 _vp, _vp, _vp, _vp, _vp, _vp], _i32),
     "mrep_knot_span": ([_vp, _i64, _i32, _vp, _i64, _vp, _vp], _i32),
     "mrep_quartic_roots": ([_vp, _i64, _vp, _vp, _vp], _i32),
     "mrep_newton_quartic_roots": ([_vp, _i64, _vp, _vp, _vp], _i32),

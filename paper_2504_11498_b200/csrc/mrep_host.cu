@@ -162,3 +162,94 @@ extern "C" int mrep_project_host(const void* table, int64_t S, int d, const doub
   }
   return MREP_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Host-array entry points: what a ctypes / cffi binding in the reference
+// binds without any GPU framework.
+
+extern "C" int mrep_table_create(const double* seg_pts, const double* seg_ta, const double* seg_tb,
+                                 const double* seam_t, const double* seam_pt, int64_t S, int d,
+                                 void** table_out) {
+  *table_out = nullptr;
+  int64_t bytes = mrep_table_bytes(S);
+  if (bytes < 0 || (d != 2 && d != 3)) {
+    set_error("mrep_table_create: need S >= 1 and d in {2,3}");
+    return MREP_ERR_ARG;
+  }
+  double *dsp = nullptr, *dta = nullptr, *dtb = nullptr, *dst = nullptr, *dspt = nullptr;
+  void* table = nullptr;
+  MREP_CUDA_CHECK(cudaMalloc(&table, (size_t)bytes));
+  MREP_CUDA_CHECK(cudaMalloc(&dsp, S * 4 * d * sizeof(double)));
+  MREP_CUDA_CHECK(cudaMalloc(&dta, S * sizeof(double)));
+  MREP_CUDA_CHECK(cudaMalloc(&dtb, S * sizeof(double)));
+  MREP_CUDA_CHECK(cudaMalloc(&dst, (S + 1) * sizeof(double)));
+  MREP_CUDA_CHECK(cudaMalloc(&dspt, (S + 1) * d * sizeof(double)));
+  MREP_CUDA_CHECK(cudaMemcpy(dsp, seg_pts, S * 4 * d * sizeof(double), cudaMemcpyHostToDevice));
+  MREP_CUDA_CHECK(cudaMemcpy(dta, seg_ta, S * sizeof(double), cudaMemcpyHostToDevice));
+  MREP_CUDA_CHECK(cudaMemcpy(dtb, seg_tb, S * sizeof(double), cudaMemcpyHostToDevice));
+  MREP_CUDA_CHECK(cudaMemcpy(dst, seam_t, (S + 1) * sizeof(double), cudaMemcpyHostToDevice));
+  MREP_CUDA_CHECK(cudaMemcpy(dspt, seam_pt, (S + 1) * d * sizeof(double), cudaMemcpyHostToDevice));
+  int rc = mrep_table_pack(dsp, dta, dtb, dst, dspt, S, d, table, nullptr);
+  cudaDeviceSynchronize();
+  cudaFree(dsp);
+  cudaFree(dta);
+  cudaFree(dtb);
+  cudaFree(dst);
+  cudaFree(dspt);
+  if (rc != MREP_OK) {
+    cudaFree(table);
+    return rc;
+  }
+  *table_out = table;
+  return MREP_OK;
+}
+
+extern "C" int mrep_table_free(void* table) {
+  if (table) MREP_CUDA_CHECK(cudaFree(table));
+  return MREP_OK;
+}
+
+extern "C" int mrep_project_block_host(const double* seg_pts, const double* seg_ta,
+                                       const double* seg_tb, const double* seam_t,
+                                       const double* seam_pt, int64_t S, int d,
+                                       const double* queries, int64_t n, double clip_tol,
+                                       int max_iter, int soundness_samples, double* out_t,
+                                       double* out_foot, double* out_dist, int64_t* out_cand,
+                                       int64_t* out_stats, double* out_sound) {
+  void* table = nullptr;
+  int rc = mrep_table_create(seg_pts, seg_ta, seg_tb, seam_t, seam_pt, S, d, &table);
+  if (rc != MREP_OK) return rc;
+  if (n == 0) return mrep_table_free(table);
+  double *dq = nullptr, *dt = nullptr, *df = nullptr, *dd = nullptr, *dso = nullptr;
+  int64_t *dc = nullptr, *dstat = nullptr;
+  MREP_CUDA_CHECK(cudaMalloc(&dq, n * d * sizeof(double)));
+  MREP_CUDA_CHECK(cudaMalloc(&dt, n * sizeof(double)));
+  MREP_CUDA_CHECK(cudaMalloc(&df, n * d * sizeof(double)));
+  MREP_CUDA_CHECK(cudaMalloc(&dd, n * sizeof(double)));
+  MREP_CUDA_CHECK(cudaMalloc(&dso, n * sizeof(double)));
+  MREP_CUDA_CHECK(cudaMalloc(&dc, n * sizeof(int64_t)));
+  MREP_CUDA_CHECK(cudaMalloc(&dstat, n * 6 * sizeof(int64_t)));
+  MREP_CUDA_CHECK(cudaMemset(dstat, 0, n * 6 * sizeof(int64_t)));
+  MREP_CUDA_CHECK(cudaMemcpy(dq, queries, n * d * sizeof(double), cudaMemcpyHostToDevice));
+  rc = mrep_project(table, S, d, dq, n, clip_tol, max_iter, soundness_samples, MREP_STATS, dt, df,
+                    dd, dc, nullptr, dstat, dso, nullptr, nullptr);
+  if (rc == MREP_OK) {
+    MREP_CUDA_CHECK(cudaMemcpy(out_t, dt, n * sizeof(double), cudaMemcpyDeviceToHost));
+    MREP_CUDA_CHECK(cudaMemcpy(out_foot, df, n * d * sizeof(double), cudaMemcpyDeviceToHost));
+    MREP_CUDA_CHECK(cudaMemcpy(out_dist, dd, n * sizeof(double), cudaMemcpyDeviceToHost));
+    MREP_CUDA_CHECK(cudaMemcpy(out_cand, dc, n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (out_stats)
+      MREP_CUDA_CHECK(cudaMemcpy(out_stats, dstat, n * 6 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (out_sound)
+      MREP_CUDA_CHECK(cudaMemcpy(out_sound, dso, n * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  cudaFree(dq);
+  cudaFree(dt);
+  cudaFree(df);
+  cudaFree(dd);
+  cudaFree(dso);
+  cudaFree(dc);
+  cudaFree(dstat);
+  mrep_table_free(table);
+  return rc;
+}

@@ -37,6 +37,37 @@ namespace mrep {
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 
+// Per-stage device times of the last MREP_TIMING call on this host thread (ms):
+// [0] morton+sort [1] traverse [2] pairs [3] clip [4] select [5] fallback
+static thread_local double g_stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+
+struct StageTimer {
+  cudaEvent_t ev[8];
+  int n = 0;
+  bool on = false;
+  cudaStream_t st;
+  StageTimer(bool enable, cudaStream_t s) : on(enable), st(s) {
+    if (on)
+      for (auto& e : ev) cudaEventCreate(&e);
+  }
+  void mark() {
+    if (on && n < 8) cudaEventRecord(ev[n++], st);
+  }
+  void finish(int first_slot) {
+    if (!on) return;
+    cudaEventSynchronize(ev[n - 1]);
+    for (int i = 0; i + 1 < n; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      if (first_slot + i < 8) g_stage_ms[first_slot + i] = ms;
+    }
+  }
+  ~StageTimer() {
+    if (on)
+      for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
 // Keep stream-ordered allocations cached in the device's default pool: the
 // projection workspace is re-requested on every call, and releasing it at each
 // synchronisation would re-map hundreds of MB per call.
@@ -1563,7 +1594,7 @@ static int launch_project(const ProjParams& p, unsigned flags, cudaStream_t st) 
 
 
 template <int D>
-static int launch_wave(const ProjParams& p, cudaStream_t st) {
+static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing) {
   const int64_t n = p.n;
   const unsigned long long pcap = (unsigned long long)std::max<int64_t>(8 * n, 1 << 16);
   const unsigned long long scap = (unsigned long long)std::max<int64_t>(2 * n, 1 << 16);
@@ -1617,18 +1648,26 @@ static int launch_wave(const ProjParams& p, cudaStream_t st) {
   w.fb = (int64_t*)(base + o_fb);
   MREP_CUDA_CHECK(cudaMemsetAsync(w.cnt, 0, 8 * sizeof(unsigned long long), st));
   const unsigned persist = 148u * 8u;
+  StageTimer tm(timing, st);
+  tm.mark();
   wave_traverse<D><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
+  tm.mark();
   wave_pairs<D><<<persist, BLOCK, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
+  tm.mark();
   wave_clip<D><<<persist, BLOCK, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
+  tm.mark();
   wave_select<D, 0><<<persist, 256, 0, st>>>(w);
   wave_select<D, 1><<<persist, 256, 0, st>>>(w);
   wave_select<D, 2><<<persist, 256, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
+  tm.mark();
   wave_fallback<D><<<148u, BLOCK, 0, st>>>(w, p);
   MREP_LAUNCH_CHECK();
+  tm.mark();
+  tm.finish(1);
   MREP_CUDA_CHECK(cudaFreeAsync(base, st));
   return MREP_OK;
 }
@@ -1640,6 +1679,11 @@ using namespace mrep;
 extern "C" {
 
 const char* mrep_last_error(void) { return g_last_error.c_str(); }
+int mrep_last_stage_times(double* ms, int max) {
+  int k = max < 8 ? max : 8;
+  for (int i = 0; i < k; ++i) ms[i] = g_stage_ms[i];
+  return k;
+}
 int mrep_version(void) { return 100; }
 int mrep_device_count(void) {
   int n = 0;
@@ -1725,6 +1769,9 @@ int mrep_project(const void* table, int64_t S, int d, const double* queries, int
   p.pass2_list = (int64_t*)(wc + off_list);
   MREP_CUDA_CHECK(cudaMemsetAsync(ws, 0, 16, st));
   p.perm = nullptr;
+  const bool timing = (flags & MREP_TIMING) != 0;
+  StageTimer sort_tm(timing, st);
+  sort_tm.mark();
   if (!(flags & MREP_NO_SORT) && n > 64) {
     uint32_t* k_in = (uint32_t*)(wc + off_keys);
     uint32_t* k_out = k_in + n;
@@ -1738,9 +1785,11 @@ int mrep_project(const void* table, int64_t S, int d, const double* queries, int
                                                     (int)n, 0, d * 10, st));
     p.perm = i_out;
   }
+  sort_tm.mark();
+  sort_tm.finish(0);
   int rc;
   bool wave = (flags & MREP_SCREEN) && !(flags & MREP_STATS) && !(flags & MREP_FUSED);
-  if (wave) rc = d == 3 ? launch_wave<3>(p, st) : launch_wave<2>(p, st);
+  if (wave) rc = d == 3 ? launch_wave<3>(p, st, timing) : launch_wave<2>(p, st, timing);
   else rc = d == 3 ? launch_project<3>(p, flags, st) : launch_project<2>(p, flags, st);
   MREP_CUDA_CHECK(cudaFreeAsync(ws, st));
   return rc;
