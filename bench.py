@@ -266,8 +266,8 @@ def main():
         ms = float(tt.item())
     value = world * n / (ms / 1e3)
     # own kernels per projection call: Morton keys + 4 cub radix-sort passes
-    # (histogram, exclusive sum, 3 onesweep) + 7 wavefront kernels; dense: 2
-    launches_per_step = (1 + 5 + 7) if screen else (1 + 5 + 2)
+    # (histogram, exclusive sum, 3 onesweep) + 8 wavefront kernels; dense: 2
+    launches_per_step = (1 + 5 + 8) if screen else (1 + 5 + 2)
 
     # ---- roofline: per-stage device times (CUDA events between the pipeline's
     #      kernels, recorded inside libmrep on this stream) x algorithmic work ----

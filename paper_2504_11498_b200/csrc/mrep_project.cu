@@ -644,6 +644,57 @@ __device__ __forceinline__ void prep_pair(const TableView& T, int64_t s, const d
   rebase5(e, P.bseg);
 }
 
+// prep_pair with a rigorous early exit: the degree-6 Bernstein coefficients
+// of D(u) = |C(u) - q|^2 follow from E = D' by d_0 = D(0), d_{i+1} = d_i + b_i/6
+// (b = Bernstein ordinates of E); min_i d_i <= min_u D(u).  If that bound
+// (minus a generous rounding allowance) exceeds the cut, no candidate of this
+// cubic can reach the tie band and the quartic is skipped.
+template <int D>
+__device__ __forceinline__ bool prep_pair_cut(const TableView& T, int64_t s, const double (&q)[D],
+                                              double cut_sq, PairPrep& P) {
+  const double* r = T.rec + s * REC;
+  double w[4][D];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int dim = 0; dim < D; ++dim) w[k][dim] = __ldg(r + k * 3 + dim);
+  double e[6];
+  distance_poly_w<D>(w, q, e);
+  rebase5(e, P.bseg);
+  double d0 = 0.0;
+#pragma unroll
+  for (int dim = 0; dim < D; ++dim) {
+    double df = w[0][dim] - q[dim];
+    d0 += df * df;
+  }
+  double di = d0, dmin_b = d0, mag = fabs(d0);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    di += P.bseg[i] * (1.0 / 6.0);
+    dmin_b = fmin(dmin_b, di);
+    mag += fabs(P.bseg[i]);
+  }
+  if (dmin_b - 1e-9 * mag > cut_sq) return false;
+  double ep[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) ep[k] = (double)(k + 1) * e[k + 1];
+  Roots4 rt = quartic_roots_01(ep);
+  P.b1 = P.b2 = P.b3 = P.b4 = 1.0;
+  P.nin = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double x = rt.r[i];
+    if (i < rt.count && 1e-10 < x && x < 1.0 - 1e-10) {
+      P.b1 = (P.nin == 0) ? x : P.b1;
+      P.b2 = (P.nin == 1) ? x : P.b2;
+      P.b3 = (P.nin == 2) ? x : P.b3;
+      P.b4 = (P.nin == 3) ? x : P.b4;
+      ++P.nin;
+    }
+  }
+  return true;
+}
+
 // Walk the monotone pieces of the warp's current pairs in lock step
 // (piece k of every pair together), queue survivors, flush full batches.
 template <int D, bool STATS>
@@ -967,6 +1018,11 @@ struct WaveParams {
   unsigned long long* tkey;  // order key of the min t inside the band
   unsigned long long* okey;  // min reference order among band members with that t
   int32_t* flag;             // 1 = finish in the fallback kernel
+  double* qs;                // queries gathered into Morton order [n][D]
+  double* win_t;             // winner record per sorted position
+  double* win_d;
+  double* win_v;
+  int64_t* scnt;             // candidate count per sorted position
   unsigned long long* cnt;   // [0] pairs, [1] survivors, [2] candidates, [3] fallbacks
   uint32_t* pq;
   uint32_t* ps;
@@ -1002,118 +1058,158 @@ __device__ __forceinline__ unsigned long long tkey_of(double t) {
   return (b >> 63) ? ~b : (b | (1ull << 63));
 }
 
-__device__ __forceinline__ double dmin_of(const WaveParams& w, int64_t qi) {
-  return __longlong_as_double((long long)w.dmin[qi]);
+// every per-query array below is indexed by the SORTED position g; only the
+// final emit kernel touches the caller's order (one scattered write pass)
+__device__ __forceinline__ double dmin_of(const WaveParams& w, int64_t g) {
+  return __longlong_as_double((long long)w.dmin[g]);
+}
+
+// Packet traversal: the 32 (Morton-adjacent) queries of a warp walk the AABB
+// tree together.  One DFS stack per warp lives in shared memory; each entry
+// carries the lane mask of the queries that still need the node, so control
+// flow is warp-uniform and every box is one broadcast load.
+constexpr int PSTACK = 72;  // >= 8 entries per level x 9 levels
+
+__device__ __forceinline__ unsigned long long pk(unsigned mask, int level, int64_t idx) {
+  return ((unsigned long long)mask << 32) | ((unsigned long long)level << 28) |
+         (unsigned long long)idx;
 }
 
 template <int D>
 __global__ void __launch_bounds__(BLOCK) wave_traverse(WaveParams w) {
+  __shared__ unsigned long long stk[BLOCK / 32][PSTACK];
+  const int lane = threadIdx.x & 31;
+  unsigned long long* S = stk[threadIdx.x >> 5];
   int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = gi < w.n;
   QStats st{};
-  if (gi < w.n) {
-    const TableView& T = w.tab;
-    int64_t qi = w.perm ? (int64_t)w.perm[gi] : gi;
-    double q[D];
+  const TableView& T = w.tab;
+  int64_t qi = active ? (w.perm ? (int64_t)w.perm[gi] : gi) : 0;
+  double q[D];
 #pragma unroll
-    for (int k = 0; k < D; ++k) q[k] = w.q[qi * D + k];
-    const double NaN = __longlong_as_double(0x7ff8000000000000LL);
-    w.out_t[qi] = NaN;
-    w.out_dist[qi] = NaN;
+  for (int k = 0; k < D; ++k) q[k] = active ? w.q[qi * D + k] : 0.0;
+  bool fall = false;
+  Band B;
+  band_init(B, false, 0.0);
+  double scale = T.hdr[4];
 #pragma unroll
-    for (int k = 0; k < D; ++k) w.out_foot[qi * D + k] = NaN;
-    if (w.out_seg) w.out_seg[qi] = -1;
-    w.tkey[qi] = ~0ull;
-    w.okey[qi] = ~0ull;
-    bool fall = false;
-    Band B;
-    band_init(B, false, 0.0);
-    double scale = T.hdr[4];
+  for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
+  if (active) {
 #pragma unroll
-    for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
-    {  // greedy descent: first bound from the seams of a nearby cubic
-      int level = T.top;
-      int64_t idx = 0;
-      while (level > 0) {
-        int64_t first = idx * FANOUT, cnt = T.lvl_cnt[level - 1], off = T.lvl_off[level - 1];
-        double best = 0.0;
-        int64_t bi = first;
+    for (int k = 0; k < D; ++k) w.qs[gi * D + k] = q[k];
+    w.tkey[gi] = ~0ull;
+    w.okey[gi] = ~0ull;
+  }
+  {  // greedy descent (uniform trip counts): first bound from a nearby cubic
+    int level = T.top;
+    int64_t idx = 0;
+    while (level > 0) {
+      int64_t first = idx * FANOUT, cnt = T.lvl_cnt[level - 1], off = T.lvl_off[level - 1];
+      double best = 0.0;
+      int64_t bi = first;
 #pragma unroll 1
-        for (int c = 0; c < FANOUT; ++c) {
-          int64_t ch = first + c;
-          if (ch < cnt) {
-            st.boxes++;
-            double lb = box_lb2<D>(T, off + ch, q);
-            if (c == 0 || lb < best) {
-              best = lb;
-              bi = ch;
-            }
+      for (int c = 0; c < FANOUT; ++c) {
+        int64_t ch = first + c;
+        if (ch < cnt) {
+          st.boxes++;
+          double lb = box_lb2<D>(T, off + ch, q);
+          if (c == 0 || lb < best) {
+            best = lb;
+            bi = ch;
           }
         }
-        idx = bi;
-        --level;
       }
+      idx = bi;
+      --level;
+    }
+    if (active) {
 #pragma unroll 1
       for (int e = 0; e < 2; ++e) offer_seam<D>(T, idx + e, q, B, st);
     }
-    uint64_t masks = 0;
-    int level = T.top;
-    int64_t idx = 0;
-    masks = (uint64_t)child_mask<D>(T, level, 0, q, cut2(B.dmin, scale), st) << (8 * level);
-    for (;;) {
-      uint32_t mk = (uint32_t)(masks >> (8 * level)) & 0xffu;
-      if (mk == 0) {
-        if (level == T.top) break;
-        ++level;
-        idx /= FANOUT;
-        continue;
-      }
-      int c = __ffs(mk) - 1;
-      masks &= ~(1ull << (8 * level + c));
-      int64_t ch = idx * FANOUT + c;
-      double c2 = cut2(B.dmin, scale);
-      st.boxes++;
-      if (level - 1 == 0) {
-        if (box_lb2<D>(T, T.lvl_off[0] + ch, q) <= c2) {
+  }
+  unsigned amask = __ballot_sync(0xffffffffu, active);
+  int sp = 0;
+  if (amask) {
+    if (lane == 0) S[0] = pk(amask, T.top, 0);
+    sp = 1;
+  }
+  __syncwarp();
+  while (sp > 0) {
+    unsigned long long e = S[--sp];
+    unsigned mask = (unsigned)(e >> 32);
+    int level = (int)((e >> 28) & 0xf);
+    int64_t idx = (int64_t)(e & 0xfffffffull);
+    bool mine = (mask >> lane) & 1u;
+    __syncwarp();
+    if (level == 0) {
+      // leaf cubic: re-test with the current bound, offer its seams, emit the pair
+      bool need = false;
+      if (mine) {
+        st.boxes++;
+        need = box_lb2<D>(T, T.lvl_off[0] + idx, q) <= cut2(B.dmin, scale);
+        if (need) {
 #pragma unroll 1
-          for (int e = 0; e < 2; ++e) offer_seam<D>(T, ch + e, q, B, st);
-          unsigned long long slot = wave_append(&w.cnt[0], true);
-          if (slot < w.pcap) {
-            w.pq[slot] = (uint32_t)qi;
-            w.ps[slot] = (uint32_t)ch;
-          } else {
-            fall = true;
-          }
+          for (int k = 0; k < 2; ++k) offer_seam<D>(T, idx + k, q, B, st);
         }
-      } else if (box_lb2<D>(T, T.lvl_off[level - 1] + ch, q) <= c2) {
-        --level;
-        idx = ch;
-        masks |= (uint64_t)child_mask<D>(T, level, idx, q, c2, st) << (8 * level);
       }
-    }
-    if (B.overflow) fall = true;
-    w.dmin[qi] = (unsigned long long)__double_as_longlong(B.dmin);
-    // the seam members of the seam tie band become candidates
-#pragma unroll
-    for (int j = 0; j < BAND_K; ++j) {
-      bool want = (B.valid >> j) & 1u;
-      unsigned long long slot = wave_append(&w.cnt[2], want);
-      if (want) {
-        if (slot < w.ccap) {
-          w.cq[slot] = (uint32_t)qi;
-          w.ct[slot] = B.t[j];
-          w.cd[slot] = B.d[j];
-          w.cv[slot] = -1.0;
-          w.cord[slot] = B.ord[j];
+      unsigned long long slot = wave_append(&w.cnt[0], need);
+      if (need) {
+        if (slot < w.pcap) {
+          w.pq[slot] = (uint32_t)gi;
+          w.ps[slot] = (uint32_t)idx;
         } else {
           fall = true;
         }
       }
+      continue;
     }
-    if (w.out_cand) w.out_cand[qi] = (int64_t)st.offers;
-    w.flag[qi] = fall ? 1 : 0;
+    // children (level-1, idx*8 + c), pushed in reverse so the lowest pops first
+    int64_t first = idx * FANOUT, cnt = T.lvl_cnt[level - 1], off = T.lvl_off[level - 1];
+    double c2 = cut2(B.dmin, scale);
+#pragma unroll 1
+    for (int c = FANOUT - 1; c >= 0; --c) {
+      int64_t ch = first + c;
+      if (ch >= cnt) continue;
+      bool need = false;
+      if (mine) {
+        st.boxes++;
+        need = box_lb2<D>(T, off + ch, q) <= c2;
+      }
+      unsigned m = __ballot_sync(0xffffffffu, need);
+      if (m) {
+        if (lane == 0) S[sp] = pk(m, level - 1, ch);
+        ++sp;
+      }
+    }
+    __syncwarp();
+  }
+  if (active) {
+    if (B.overflow) fall = true;
+    w.dmin[gi] = (unsigned long long)__double_as_longlong(B.dmin);
+  }
+  // the seam members of the seam tie band become candidates
+#pragma unroll
+  for (int j = 0; j < BAND_K; ++j) {
+    bool want = active && ((B.valid >> j) & 1u);
+    unsigned long long slot = wave_append(&w.cnt[2], want);
+    if (want) {
+      if (slot < w.ccap) {
+        w.cq[slot] = (uint32_t)gi;
+        w.ct[slot] = B.t[j];
+        w.cd[slot] = B.d[j];
+        w.cv[slot] = -1.0;
+        w.cord[slot] = B.ord[j];
+      } else {
+        fall = true;
+      }
+    }
+  }
+  if (active) {
+    w.scnt[gi] = (int64_t)st.offers;
+    w.flag[gi] = fall ? 1 : 0;
     if (fall) {
       unsigned long long slot = atomicAdd(&w.cnt[3], 1ull);
-      w.fb[slot] = qi;
+      w.fb[slot] = gi;
     }
   }
   warp_count(w.counters, MREP_CNT_SEAMS, st.seams);
@@ -1128,21 +1224,21 @@ __global__ void __launch_bounds__(BLOCK) wave_pairs(WaveParams w) {
   uint64_t npairs = 0, nboxes = 0;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (unsigned long long)gridDim.x * blockDim.x) {
-    int64_t qi = w.pq[i];
+    int64_t qi = w.pq[i];  // sorted position
     int64_t s = w.ps[i];
     if (w.flag[qi]) continue;
     double q[D];
 #pragma unroll
-    for (int k = 0; k < D; ++k) q[k] = w.q[qi * D + k];
+    for (int k = 0; k < D; ++k) q[k] = w.qs[qi * D + k];
     double scale = T.hdr[4];
 #pragma unroll
     for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
     ++nboxes;
     // re-test with the query's final seam bound
     if (!(box_lb2<D>(T, T.lvl_off[0] + s, q) <= cut2(dmin_of(w, qi), scale))) continue;
-    ++npairs;
     PairPrep P;
-    prep_pair<D>(T, s, q, P);
+    if (!prep_pair_cut<D>(T, s, q, cut2(dmin_of(w, qi), scale), P)) continue;
+    ++npairs;
     double lo = 0.0;
 #pragma unroll 1
     for (int k = 0; k <= P.nin; ++k) {
@@ -1204,12 +1300,12 @@ __global__ void __launch_bounds__(BLOCK) wave_clip(WaveParams w) {
     for (int dim = 0; dim < D; ++dim) {
       double f = decasteljau1(__ldg(r + 12 + dim), __ldg(r + 15 + dim), __ldg(r + 18 + dim),
                               __ldg(r + 21 + dim), v);
-      double diff = w.q[qi * D + dim] - f;
+      double diff = w.qs[qi * D + dim] - f;
       acc += diff * diff;
     }
     double d = sqrt(acc);
     double t = ta + v * (tb - ta);
-    if (w.out_cand) atomicAdd((unsigned long long*)&w.out_cand[qi], 1ull);
+    atomicAdd((unsigned long long*)&w.scnt[qi], 1ull);
     double cur = dmin_of(w, qi);
     bool keep = d <= cur + 1e-12;
     unsigned long long slot = wave_append(&w.cnt[2], keep);
@@ -1255,30 +1351,54 @@ __global__ void __launch_bounds__(256) wave_select(WaveParams w) {
       continue;
     }
     if (ord != w.okey[qi]) continue;
-    // winner: outputs (foot recomputed exactly as the reference stored it)
-    const TableView& T = w.tab;
-    double foot[D];
-    int32_t seg;
-    if (ord & SURV_BIT) {
-      int64_t s = (int64_t)((ord & ~SURV_BIT) >> 3);
-      const double* r = T.rec + s * REC;
-      double v = w.cv[i];
-#pragma unroll
-      for (int dim = 0; dim < D; ++dim)
-        foot[dim] = decasteljau1(r[12 + dim], r[15 + dim], r[18 + dim], r[21 + dim], v);
-      seg = (int32_t)s;
-    } else {
-      int64_t s = (int64_t)ord;
-      double stt;
-      seam_point<D>(T, s, foot, stt);
-      seg = (int32_t)(s > 0 ? s - 1 : 0);
-    }
-    w.out_t[qi] = w.ct[i];
-    w.out_dist[qi] = d;
-#pragma unroll
-    for (int k = 0; k < D; ++k) w.out_foot[qi * D + k] = foot[k];
-    if (w.out_seg) w.out_seg[qi] = seg;
+    // winner record (identical duplicates write identical values)
+    w.win_t[qi] = w.ct[i];
+    w.win_d[qi] = d;
+    w.win_v[qi] = w.cv[i];
   }
+}
+
+// Final pass in sorted order: foot point of each winner (recomputed exactly
+// as the reference stored it) and one scattered write of the outputs.
+template <int D>
+__global__ void __launch_bounds__(256) wave_emit(WaveParams w) {
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= w.n) return;
+  if (w.flag[g]) return;  // written by the fallback kernel
+  int64_t qi = w.perm ? (int64_t)w.perm[g] : g;
+  const TableView& T = w.tab;
+  unsigned long long ord = w.okey[g];
+  if (w.out_cand) w.out_cand[qi] = w.scnt[g];
+  if (ord == ~0ull) {
+    const double NaN = __longlong_as_double(0x7ff8000000000000LL);
+    w.out_t[qi] = NaN;
+    w.out_dist[qi] = NaN;
+#pragma unroll
+    for (int k = 0; k < D; ++k) w.out_foot[qi * D + k] = NaN;
+    if (w.out_seg) w.out_seg[qi] = -1;
+    return;
+  }
+  double foot[D];
+  int32_t seg;
+  if (ord & SURV_BIT) {
+    int64_t s = (int64_t)((ord & ~SURV_BIT) >> 3);
+    const double* r = T.rec + s * REC;
+    double v = w.win_v[g];
+#pragma unroll
+    for (int dim = 0; dim < D; ++dim)
+      foot[dim] = decasteljau1(r[12 + dim], r[15 + dim], r[18 + dim], r[21 + dim], v);
+    seg = (int32_t)s;
+  } else {
+    int64_t s = (int64_t)ord;
+    double stt;
+    seam_point<D>(T, s, foot, stt);
+    seg = (int32_t)(s > 0 ? s - 1 : 0);
+  }
+  w.out_t[qi] = w.win_t[g];
+  w.out_dist[qi] = w.win_d[g];
+#pragma unroll
+  for (int k = 0; k < D; ++k) w.out_foot[qi * D + k] = foot[k];
+  if (w.out_seg) w.out_seg[qi] = seg;
 }
 
 // exact per-thread path for the rare queries the buffers could not hold
@@ -1287,10 +1407,11 @@ __global__ void __launch_bounds__(BLOCK) wave_fallback(WaveParams w, ProjParams 
   unsigned long long total = *(volatile unsigned long long*)&w.cnt[3];
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (unsigned long long)gridDim.x * blockDim.x) {
-    int64_t qi = w.fb[i];
+    int64_t g = w.fb[i];
+    int64_t qi = w.perm ? (int64_t)w.perm[g] : g;
     double q[D];
 #pragma unroll
-    for (int k = 0; k < D; ++k) q[k] = w.q[qi * D + k];
+    for (int k = 0; k < D; ++k) q[k] = w.qs[g * D + k];
     double scale = w.tab.hdr[4];
 #pragma unroll
     for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
@@ -1612,6 +1733,8 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing) {
   size_t o_cq = take(ccap * 4), o_ct = take(ccap * 8), o_cd = take(ccap * 8), o_cv = take(ccap * 8),
          o_cord = take(ccap * 8);
   size_t o_fb = take(n * 8);
+  size_t o_qs = take(n * D * 8), o_wt = take(n * 8), o_wd = take(n * 8), o_wv = take(n * 8),
+         o_sc = take(n * 8);
   char* base = nullptr;
   MREP_CUDA_CHECK(cudaMallocAsync((void**)&base, bytes, st));
   WaveParams w{};
@@ -1646,6 +1769,11 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing) {
   w.cord = (unsigned long long*)(base + o_cord);
   w.ccap = ccap;
   w.fb = (int64_t*)(base + o_fb);
+  w.qs = (double*)(base + o_qs);
+  w.win_t = (double*)(base + o_wt);
+  w.win_d = (double*)(base + o_wd);
+  w.win_v = (double*)(base + o_wv);
+  w.scnt = (int64_t*)(base + o_sc);
   MREP_CUDA_CHECK(cudaMemsetAsync(w.cnt, 0, 8 * sizeof(unsigned long long), st));
   const unsigned persist = 148u * 8u;
   StageTimer tm(timing, st);
@@ -1662,6 +1790,8 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing) {
   wave_select<D, 0><<<persist, 256, 0, st>>>(w);
   wave_select<D, 1><<<persist, 256, 0, st>>>(w);
   wave_select<D, 2><<<persist, 256, 0, st>>>(w);
+  MREP_LAUNCH_CHECK();
+  wave_emit<D><<<grid_for(n, 256), 256, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
   tm.mark();
   wave_fallback<D><<<148u, BLOCK, 0, st>>>(w, p);
