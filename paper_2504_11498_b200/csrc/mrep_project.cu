@@ -234,6 +234,9 @@ __device__ __forceinline__ void offer_seam(const TableView& T, int64_t s, const 
   }
   st.seams++;
   st.offers++;
+  // sqrt is monotone and correctly rounded: acc > lim^2 (rounded up by a
+  // relative 1e-15) implies sqrt(acc) > lim, the band's first rejection test
+  if (acc > B.lim * B.lim * (1.0 + 1e-15)) return;
   band_offer(B, stt, sqrt(acc), -1.0, (uint64_t)s);
 }
 
@@ -1018,7 +1021,7 @@ struct WaveParams {
   unsigned long long* tkey;  // order key of the min t inside the band
   unsigned long long* okey;  // min reference order among band members with that t
   int32_t* flag;             // 1 = finish in the fallback kernel
-  double* qs;                // queries gathered into Morton order [n][D]
+  double* qs;                // per sorted query: 4 doubles = coords (D) + running min (slot 3)
   double* win_t;             // winner record per sorted position
   double* win_d;
   double* win_v;
@@ -1059,9 +1062,14 @@ __device__ __forceinline__ unsigned long long tkey_of(double t) {
 }
 
 // every per-query array below is indexed by the SORTED position g; only the
-// final emit kernel touches the caller's order (one scattered write pass)
+// final emit kernel touches the caller's order (one scattered write pass).
+// The running minimum lives in slot 3 of the query's 32-byte record, so a
+// pair / survivor fetches coordinates and bound in one sector.
+__device__ __forceinline__ unsigned long long* dmin_ptr(const WaveParams& w, int64_t g) {
+  return (unsigned long long*)(w.qs + g * 4 + 3);
+}
 __device__ __forceinline__ double dmin_of(const WaveParams& w, int64_t g) {
-  return __longlong_as_double((long long)w.dmin[g]);
+  return __longlong_as_double((long long)*dmin_ptr(w, g));
 }
 
 // Packet traversal: the 32 (Morton-adjacent) queries of a warp walk the AABB
@@ -1095,8 +1103,6 @@ __global__ void __launch_bounds__(BLOCK) wave_traverse(WaveParams w) {
 #pragma unroll
   for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
   if (active) {
-#pragma unroll
-    for (int k = 0; k < D; ++k) w.qs[gi * D + k] = q[k];
     w.tkey[gi] = ~0ull;
     w.okey[gi] = ~0ull;
   }
@@ -1185,7 +1191,12 @@ __global__ void __launch_bounds__(BLOCK) wave_traverse(WaveParams w) {
   }
   if (active) {
     if (B.overflow) fall = true;
-    w.dmin[gi] = (unsigned long long)__double_as_longlong(B.dmin);
+    double4 rec;
+    rec.x = q[0];
+    rec.y = q[1];
+    rec.z = D == 3 ? q[D - 1] : 0.0;
+    rec.w = B.dmin;
+    *(double4*)(w.qs + gi * 4) = rec;
   }
   // the seam members of the seam tie band become candidates
 #pragma unroll
@@ -1226,18 +1237,19 @@ __global__ void __launch_bounds__(BLOCK) wave_pairs(WaveParams w) {
        i += (unsigned long long)gridDim.x * blockDim.x) {
     int64_t qi = w.pq[i];  // sorted position
     int64_t s = w.ps[i];
-    if (w.flag[qi]) continue;
+    double4 rec = *(const double4*)(w.qs + qi * 4);
     double q[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) q[k] = w.qs[qi * D + k];
+    q[0] = rec.x;
+    q[1] = rec.y;
+    if (D == 3) q[D - 1] = rec.z;
     double scale = T.hdr[4];
 #pragma unroll
     for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
+    const double c2 = cut2(rec.w, scale);  // the query's final seam bound
     ++nboxes;
-    // re-test with the query's final seam bound
-    if (!(box_lb2<D>(T, T.lvl_off[0] + s, q) <= cut2(dmin_of(w, qi), scale))) continue;
+    if (!(box_lb2<D>(T, T.lvl_off[0] + s, q) <= c2)) continue;
     PairPrep P;
-    if (!prep_pair_cut<D>(T, s, q, cut2(dmin_of(w, qi), scale), P)) continue;
+    if (!prep_pair_cut<D>(T, s, q, c2, P)) continue;
     ++npairs;
     double lo = 0.0;
 #pragma unroll 1
@@ -1300,7 +1312,7 @@ __global__ void __launch_bounds__(BLOCK) wave_clip(WaveParams w) {
     for (int dim = 0; dim < D; ++dim) {
       double f = decasteljau1(__ldg(r + 12 + dim), __ldg(r + 15 + dim), __ldg(r + 18 + dim),
                               __ldg(r + 21 + dim), v);
-      double diff = w.qs[qi * D + dim] - f;
+      double diff = w.qs[qi * 4 + dim] - f;
       acc += diff * diff;
     }
     double d = sqrt(acc);
@@ -1310,7 +1322,7 @@ __global__ void __launch_bounds__(BLOCK) wave_clip(WaveParams w) {
     bool keep = d <= cur + 1e-12;
     unsigned long long slot = wave_append(&w.cnt[2], keep);
     if (keep) {
-      atomicMin(&w.dmin[qi], (unsigned long long)__double_as_longlong(d));
+      atomicMin(dmin_ptr(w, qi), (unsigned long long)__double_as_longlong(d));
       if (slot < w.ccap) {
         w.cq[slot] = (uint32_t)qi;
         w.ct[slot] = t;
@@ -1411,7 +1423,7 @@ __global__ void __launch_bounds__(BLOCK) wave_fallback(WaveParams w, ProjParams 
     int64_t qi = w.perm ? (int64_t)w.perm[g] : g;
     double q[D];
 #pragma unroll
-    for (int k = 0; k < D; ++k) q[k] = w.qs[g * D + k];
+    for (int k = 0; k < D; ++k) q[k] = w.qs[g * 4 + k];
     double scale = w.tab.hdr[4];
 #pragma unroll
     for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
@@ -1733,7 +1745,7 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing) {
   size_t o_cq = take(ccap * 4), o_ct = take(ccap * 8), o_cd = take(ccap * 8), o_cv = take(ccap * 8),
          o_cord = take(ccap * 8);
   size_t o_fb = take(n * 8);
-  size_t o_qs = take(n * D * 8), o_wt = take(n * 8), o_wd = take(n * 8), o_wv = take(n * 8),
+  size_t o_qs = take(n * 4 * 8), o_wt = take(n * 8), o_wd = take(n * 8), o_wv = take(n * 8),
          o_sc = take(n * 8);
   char* base = nullptr;
   MREP_CUDA_CHECK(cudaMallocAsync((void**)&base, bytes, st));
@@ -1775,16 +1787,25 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing) {
   w.win_v = (double*)(base + o_wv);
   w.scnt = (int64_t*)(base + o_sc);
   MREP_CUDA_CHECK(cudaMemsetAsync(w.cnt, 0, 8 * sizeof(unsigned long long), st));
-  const unsigned persist = 148u * 8u;
+  auto persist_grid = [](const void* fn, int block) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, block, 0);
+    return (unsigned)(sms * (per > 0 ? per : 1));
+  };
+  const unsigned g_pairs = persist_grid((const void*)wave_pairs<D>, BLOCK);
+  const unsigned g_clip = persist_grid((const void*)wave_clip<D>, BLOCK);
+  const unsigned persist = persist_grid((const void*)wave_select<D, 2>, 256);
   StageTimer tm(timing, st);
   tm.mark();
   wave_traverse<D><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
   tm.mark();
-  wave_pairs<D><<<persist, BLOCK, 0, st>>>(w);
+  wave_pairs<D><<<g_pairs, BLOCK, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
   tm.mark();
-  wave_clip<D><<<persist, BLOCK, 0, st>>>(w);
+  wave_clip<D><<<g_clip, BLOCK, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
   tm.mark();
   wave_select<D, 0><<<persist, 256, 0, st>>>(w);
