@@ -49,22 +49,49 @@ N_PER_RANK = 1_000_000
 F_PAIR, F_CLIP, F_SEAM, F_BOX = 500.0, 650.0, 10.0, 10.0
 
 
-def workload_config(n):
-    return {"workload": "cfg2: 1e6 random points/GPU onto a degree-7 B-spline, 512 ctrl pts "
-                        "(510 cubic Beziers after 1e-4 approximation)",
-            "queries_per_gpu": n, "degree": 7, "control_points": 512, "tolerance": 1e-4,
-            "clip_tol": 1e-6, "max_iterations": 8, "dim": 3,
+CONFIGS = {
+    # BASELINE.json configs[0]: inversion of 1e4 on-curve points, degree 3, 64 ctrl
+    "cfg1": dict(degree=3, ctrl=64, n=10_000, queries="on-curve", scaling="weak",
+                 desc="cfg1: 1e4 on-curve points (inversion) onto a degree-3 B-spline, "
+                      "64 ctrl pts (61 cubics)"),
+    # configs[1]: the headline
+    "cfg2": dict(degree=7, ctrl=512, n=1_000_000, queries="uniform", scaling="weak",
+                 desc="cfg2: 1e6 random points/GPU onto a degree-7 B-spline, 512 ctrl pts "
+                      "(510 cubic Beziers after 1e-4 approximation)"),
+    # configs[4]: 1e8 points onto 1e5 cubics, query-sharded (strong scaling)
+    "cfg5": dict(degree=3, ctrl=100_003, n=100_000_000, queries="uniform", scaling="strong",
+                 desc="cfg5: 1e8 random points onto a degree-3 B-spline with 100003 ctrl pts "
+                      "(1e5 cubics), sharded across GPUs"),
+}
+
+
+def workload_config(cfg, n):
+    c = CONFIGS[cfg]
+    return {"workload": c["desc"], "queries_per_gpu": n, "degree": c["degree"],
+            "control_points": c["ctrl"], "tolerance": 1e-4, "clip_tol": 1e-6,
+            "max_iterations": 8, "dim": 3, "queries": c["queries"],
             "l2": "flushed (256 MB write) before each timed step",
             "mode": "BVH-screened exact solve (t/dist/segment identical to brute force)"}
 
 
-def make_curve():
-    from oracle import prep as P
-    return P.clamped_uniform_curve(np.random.default_rng(0), 7, 512, 3)
+def make_curve(cfg="cfg2"):
+    """(degree, knots, ctrl): random_clamped_curve(default_rng(0), p, n, 3,
+    uniform_knots=True) -- the reference fixture generator's call sequence."""
+    from paper_2504_11498_b200.fixtures import random_clamped_curve
+    c = CONFIGS[cfg]
+    cv = random_clamped_curve(np.random.default_rng(0), c["degree"], c["ctrl"], 3,
+                              uniform_knots=True)
+    return cv.degree, np.array(cv.knots.knots), np.array(cv.control_points)
 
 
-def make_queries(rank, n):
-    return np.random.default_rng(1 + rank).uniform(0.0, 1.0, (n, 3))
+def make_queries(cfg, rank, n, curve=None):
+    rng = np.random.default_rng(1 + rank)
+    if CONFIGS[cfg]["queries"] == "on-curve":
+        from paper_2504_11498_b200 import BSplineCurve, eval_de_boor_many
+        p, knots, ctrl = curve
+        return eval_de_boor_many(BSplineCurve(p, knots, ctrl),
+                                 rng.uniform(knots[0], knots[-1], n))
+    return rng.uniform(0.0, 1.0, (n, 3))
 
 
 class ClockSampler:
@@ -133,10 +160,10 @@ def cpu_baseline(seg, queries, sample_n, workers):
     return sample_n / dt, dt
 
 
-def prepared_arrays():
-    """Segment table of the cfg2 curve, built by the GPU prep pipeline."""
+def prepared_arrays(cfg):
+    """Segment table of the workload's curve, built by the GPU prep pipeline."""
     from paper_2504_11498_b200 import BSplineCurve, prepare_curve
-    p, knots, ctrl = make_curve()
+    p, knots, ctrl = make_curve(cfg)
     curve = BSplineCurve(p, knots, ctrl)
     import torch
     torch.cuda.synchronize()
@@ -151,12 +178,17 @@ def run_reference(args, rank):
         return
     import oracle
     from oracle import prep as P
-    p, knots, ctrl = make_curve()
-    pr = P.prepare(p, knots, ctrl, 1e-4)
+    curve = make_curve(args.config)
+    pr = P.prepare(*curve, 1e-4)
     seg = (pr["seg_pts"], pr["seg_ta"], pr["seg_tb"], pr["seam_t"], pr["seam_pt"])
     cores = len(os.sched_getaffinity(0))
-    sample = args.ref_sample
-    q = make_queries(0, sample)
+    S = len(pr["seg_ta"])
+    sample = args.ref_sample if args.config == "cfg2" else max(64, int(args.ref_sample * 510 / S))
+    if CONFIGS[args.config]["queries"] == "on-curve":
+        p_, k_, c_ = curve
+        q = P.eval_curve(p_, k_, c_, np.random.default_rng(1).uniform(k_[0], k_[-1], sample))
+    else:
+        q = make_queries(args.config, 0, sample)
     for _ in range(args.warmup):
         oracle.project_block(*seg, q[: max(1000, sample // 10)], workers=cores)
     times = []
@@ -169,11 +201,13 @@ def run_reference(args, rank):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(N_PER_RANK), "impl": "reference",
+            "data": "synthetic", "config": workload_config(args.config, CONFIGS[args.config]["n"]),
+            "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{sample} of the cfg2 queries per step, brute force over "
-                                       f"all 510 cubics (C restatement of _kernels._project_block, "
-                                       f"bit-exact vs the reference), {cores} threads"},
+                             "sample": f"{sample} of the {args.config} queries per step, brute force "
+                                       f"over all {S} cubics (C restatement of "
+                                       f"_kernels._project_block, bit-exact vs the reference), "
+                                       f"{cores} threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -184,7 +218,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mrep", choices=["mrep", "reference"])
-    ap.add_argument("--n", type=int, default=N_PER_RANK)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=0, help="queries per GPU (default: the config's)")
     ap.add_argument("--ref-sample", type=int, default=32768)
     ap.add_argument("--cpu-sample", type=int, default=65536)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -210,10 +245,18 @@ def main():
     from paper_2504_11498_b200 import _lib as L
     from paper_2504_11498_b200 import _device as D
 
-    prep, prep_ms = prepared_arrays()
+    cfg = CONFIGS[args.config]
+    prep, prep_ms = prepared_arrays(args.config)
     tab = prep.table
-    n = args.n
-    q_host = make_queries(rank, n)
+    if args.n:
+        n = args.n
+    elif cfg["scaling"] == "strong":
+        from paper_2504_11498_b200.sharding import shard_range
+        lo, hi = shard_range(cfg["n"], rank, world)
+        n = hi - lo
+    else:
+        n = cfg["n"]
+    q_host = make_queries(args.config, rank, n, make_curve(args.config))
     q = torch.from_numpy(q_host).cuda()
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -229,7 +272,8 @@ def main():
         # the single exchange of the path: (t, distance, segment id) to rank 0
         if world == 1:
             return
-        gather_results(pack_results(out[0], out[2], out[4]), world * n, world, rank)
+        total = cfg["n"] if cfg["scaling"] == "strong" and not args.n else world * n
+        gather_results(pack_results(out[0], out[2], out[4]), total, world, rank)
 
     for _ in range(args.warmup):
         gather(step())
@@ -264,7 +308,8 @@ def main():
         tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    value = world * n / (ms / 1e3)
+    n_total = (cfg["n"] if cfg["scaling"] == "strong" and not args.n else world * n)
+    value = n_total / (ms / 1e3)
     # own kernels per projection call: Morton keys + 4 cub radix-sort passes
     # (histogram, exclusive sum, 3 onesweep) + 8 wavefront kernels; dense: 2
     launches_per_step = (1 + 5 + 8) if screen else (1 + 5 + 2)
@@ -345,7 +390,7 @@ def main():
         tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
-    e2e = {"value": world * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": n * 24,
+    e2e = {"value": n_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": n * 24,
            "d2h_bytes_per_step": n * (8 + 24 + 8 + 8 + 4),
            "path": "mrep_project_host (C ABI, pinned host buffers, 2-stream chunked pipeline)"}
 
@@ -354,15 +399,17 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             seg = (prep.seg_pts, prep.seg_ta, prep.seg_tb, prep.seam_t, prep.seam_pt)
             cores = len(os.sched_getaffinity(0))
-            v, dt = cpu_baseline(seg, q_host, args.cpu_sample, cores)
+            sample = max(256, min(args.cpu_sample, int(args.cpu_sample * 510 / prep.num_segments)))
+            v, dt = cpu_baseline(seg, q_host, sample, cores)
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                   "sample": f"first {args.cpu_sample} of the 1e6 queries, brute force over all "
-                             f"510 cubics ({dt:.1f} s wall on {cores} threads); C restatement of "
-                             f"_kernels._project_block, bit-exact vs the reference"}
+                   "sample": f"first {sample} of the {n} queries, brute force over all "
+                             f"{prep.num_segments} cubics ({dt:.1f} s wall on {cores} threads); "
+                             f"C restatement of _kernels._project_block, bit-exact vs the "
+                             f"reference"}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": dict(workload_config(n),
+                "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "config": dict(workload_config(args.config, n),
                                                     parallelism=f"query-shard x{world}",
                                                     prep_ms=prep_ms),
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,

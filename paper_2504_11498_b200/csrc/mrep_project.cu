@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -647,6 +648,36 @@ __device__ __forceinline__ void prep_pair(const TableView& T, int64_t s, const d
   rebase5(e, P.bseg);
 }
 
+// Rigorous lower bound on min_u |C_s(u) - q|^2 from the Bernstein
+// coefficients of D = |C - q|^2 (see prep_pair_cut); true if it can reach cut_sq.
+template <int D>
+__device__ __forceinline__ bool bern_may_reach(const TableView& T, int64_t s, const double (&q)[D],
+                                               double cut_sq) {
+  const double* r = T.rec + s * REC;
+  double w[4][D];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int dim = 0; dim < D; ++dim) w[k][dim] = __ldg(r + k * 3 + dim);
+  double e[6], b[6];
+  distance_poly_w<D>(w, q, e);
+  rebase5(e, b);
+  double d0 = 0.0;
+#pragma unroll
+  for (int dim = 0; dim < D; ++dim) {
+    double df = w[0][dim] - q[dim];
+    d0 += df * df;
+  }
+  double di = d0, dmin_b = d0, mag = fabs(d0);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    di += b[i] * (1.0 / 6.0);
+    dmin_b = fmin(dmin_b, di);
+    mag += fabs(b[i]);
+  }
+  return !(dmin_b - 1e-9 * mag > cut_sq);
+}
+
 // prep_pair with a rigorous early exit: the degree-6 Bernstein coefficients
 // of D(u) = |C(u) - q|^2 follow from E = D' by d_0 = D(0), d_{i+1} = d_i + b_i/6
 // (b = Bernstein ordinates of E); min_i d_i <= min_u D(u).  If that bound
@@ -1156,6 +1187,9 @@ __global__ void __launch_bounds__(BLOCK) wave_traverse(WaveParams w) {
         if (need) {
 #pragma unroll 1
           for (int k = 0; k < 2; ++k) offer_seam<D>(T, idx + k, q, B, st);
+          // emit the pair only if the cubic's Bernstein distance bound can
+          // still reach the tie band (with the bound its own seams just set)
+          need = bern_may_reach<D>(T, idx, q, cut2(B.dmin, scale));
         }
       }
       unsigned long long slot = wave_append(&w.cnt[0], need);
@@ -1169,21 +1203,55 @@ __global__ void __launch_bounds__(BLOCK) wave_traverse(WaveParams w) {
       }
       continue;
     }
-    // children (level-1, idx*8 + c), pushed in reverse so the lowest pops first
+    // children (level-1, idx*8 + c): best-first -- pushed in decreasing order
+    // of the packet leader's box distance so the nearest child pops first and
+    // the seam bound tightens before the far leaves are reached
     int64_t first = idx * FANOUT, cnt = T.lvl_cnt[level - 1], off = T.lvl_off[level - 1];
     double c2 = cut2(B.dmin, scale);
-#pragma unroll 1
-    for (int c = FANOUT - 1; c >= 0; --c) {
+    double key[FANOUT];
+    unsigned msk[FANOUT];
+#pragma unroll
+    for (int c = 0; c < FANOUT; ++c) {
       int64_t ch = first + c;
-      if (ch >= cnt) continue;
       bool need = false;
-      if (mine) {
+      double lb = 0.0;
+      if (ch < cnt && mine) {
         st.boxes++;
-        need = box_lb2<D>(T, off + ch, q) <= c2;
+        lb = box_lb2<D>(T, off + ch, q);
+        need = lb <= c2;
       }
       unsigned m = __ballot_sync(0xffffffffu, need);
-      if (m) {
-        if (lane == 0) S[sp] = pk(m, level - 1, ch);
+      msk[c] = m;
+      key[c] = m ? __shfl_sync(0xffffffffu, lb, __ffs(m) - 1) : -1.0;
+    }
+    // sort (key, child) descending: 8-input network, uniform across the warp
+    int ord8[FANOUT];
+#pragma unroll
+    for (int c = 0; c < FANOUT; ++c) ord8[c] = c;
+#define MREP_CEX(a, b)                                   \
+  if (key[a] < key[b]) {                                 \
+    double tk = key[a];                                  \
+    key[a] = key[b];                                     \
+    key[b] = tk;                                         \
+    unsigned tm = msk[a];                                \
+    msk[a] = msk[b];                                     \
+    msk[b] = tm;                                         \
+    int to = ord8[a];                                    \
+    ord8[a] = ord8[b];                                   \
+    ord8[b] = to;                                        \
+  }
+    MREP_CEX(0, 1) MREP_CEX(2, 3) MREP_CEX(4, 5) MREP_CEX(6, 7)
+    MREP_CEX(0, 2) MREP_CEX(1, 3) MREP_CEX(4, 6) MREP_CEX(5, 7)
+    MREP_CEX(1, 2) MREP_CEX(5, 6) MREP_CEX(0, 4) MREP_CEX(3, 7)
+    MREP_CEX(1, 5) MREP_CEX(2, 6)
+    MREP_CEX(1, 4) MREP_CEX(3, 6)
+    MREP_CEX(2, 4) MREP_CEX(3, 5)
+    MREP_CEX(3, 4)
+#undef MREP_CEX
+#pragma unroll
+    for (int c = 0; c < FANOUT; ++c) {
+      if (msk[c]) {
+        if (lane == 0) S[sp] = pk(msk[c], level - 1, first + ord8[c]);
         ++sp;
       }
     }
@@ -1413,6 +1481,15 @@ __global__ void __launch_bounds__(256) wave_emit(WaveParams w) {
   if (w.out_seg) w.out_seg[qi] = seg;
 }
 
+// diagnostics: emitted pairs / survivors / candidates into counters[7] (packed 21 bits each)
+__global__ void wave_diag(WaveParams w) {
+  if (w.counters && threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long a = w.cnt[0] >> 10, b = w.cnt[1] >> 10, c = w.cnt[2] >> 10;
+    atomicAdd((unsigned long long*)&w.counters[7], (a & 0x1fffff) | ((b & 0x1fffff) << 21) |
+                                                       ((c & 0x1fffff) << 42));
+  }
+}
+
 // exact per-thread path for the rare queries the buffers could not hold
 template <int D>
 __global__ void __launch_bounds__(BLOCK) wave_fallback(WaveParams w, ProjParams p) {
@@ -1441,6 +1518,8 @@ __global__ void __launch_bounds__(BLOCK) wave_fallback(WaveParams w, ProjParams 
     }
     if (w.out_cand) w.out_cand[qi] = (int64_t)st.offers;
   }
+  if (w.counters && blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd((unsigned long long*)&w.counters[MREP_CNT_PASS2], total);
 }
 
 // ------------------------------------------------------------ table build
@@ -1729,7 +1808,7 @@ static int launch_project(const ProjParams& p, unsigned flags, cudaStream_t st) 
 template <int D>
 static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing) {
   const int64_t n = p.n;
-  const unsigned long long pcap = (unsigned long long)std::max<int64_t>(8 * n, 1 << 16);
+  const unsigned long long pcap = (unsigned long long)std::max<int64_t>(16 * n, 1 << 16);
   const unsigned long long scap = (unsigned long long)std::max<int64_t>(2 * n, 1 << 16);
   const unsigned long long ccap = (unsigned long long)std::max<int64_t>(4 * n, 1 << 16);
   size_t bytes = 0;
@@ -1817,6 +1896,7 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing) {
   tm.mark();
   wave_fallback<D><<<148u, BLOCK, 0, st>>>(w, p);
   MREP_LAUNCH_CHECK();
+  if (getenv("MREP_DIAG")) wave_diag<<<1, 32, 0, st>>>(w);
   tm.mark();
   tm.finish(1);
   MREP_CUDA_CHECK(cudaFreeAsync(base, st));
@@ -1874,11 +1954,41 @@ int mrep_table_pack(const double* seg_pts, const double* seg_ta, const double* s
   return MREP_OK;
 }
 
+static int project_chunk(const void* table, int64_t S, int d, const double* queries, int64_t n,
+                         double clip_tol, int max_iter, int soundness_samples, unsigned flags,
+                         double* out_t, double* out_foot, double* out_dist, int64_t* out_cand,
+                         int32_t* out_seg, int64_t* out_stats, double* out_sound,
+                         uint64_t* counters, void* stream);
+
+// Large batches run as independent chunks (workspace is ~0.5 KB per query),
+// each with its own Morton sort; results do not depend on the chunking.
 int mrep_project(const void* table, int64_t S, int d, const double* queries, int64_t n,
                  double clip_tol, int max_iter, int soundness_samples, unsigned flags,
                  double* out_t, double* out_foot, double* out_dist, int64_t* out_cand,
                  int32_t* out_seg, int64_t* out_stats, double* out_sound, uint64_t* counters,
                  void* stream) {
+  const int64_t CHUNK_Q = (int64_t)1 << 23;
+  if (n <= CHUNK_Q)
+    return project_chunk(table, S, d, queries, n, clip_tol, max_iter, soundness_samples, flags,
+                         out_t, out_foot, out_dist, out_cand, out_seg, out_stats, out_sound,
+                         counters, stream);
+  for (int64_t lo = 0; lo < n; lo += CHUNK_Q) {
+    int64_t m = n - lo < CHUNK_Q ? n - lo : CHUNK_Q;
+    int rc = project_chunk(table, S, d, queries + lo * d, m, clip_tol, max_iter,
+                           soundness_samples, flags, out_t + lo, out_foot + lo * d, out_dist + lo,
+                           out_cand ? out_cand + lo : nullptr, out_seg ? out_seg + lo : nullptr,
+                           out_stats ? out_stats + lo * 6 : nullptr,
+                           out_sound ? out_sound + lo : nullptr, counters, stream);
+    if (rc != MREP_OK) return rc;
+  }
+  return MREP_OK;
+}
+
+static int project_chunk(const void* table, int64_t S, int d, const double* queries, int64_t n,
+                         double clip_tol, int max_iter, int soundness_samples, unsigned flags,
+                         double* out_t, double* out_foot, double* out_dist, int64_t* out_cand,
+                         int32_t* out_seg, int64_t* out_stats, double* out_sound,
+                         uint64_t* counters, void* stream) {
   if (S < 1 || (d != 2 && d != 3) || n < 0 || max_iter < 1 || !table) {
     set_error("mrep_project: bad arguments (S >= 1, d in {2,3}, max_iter >= 1)");
     return MREP_ERR_ARG;
