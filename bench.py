@@ -58,6 +58,11 @@ CONFIGS = {
     "cfg2": dict(degree=7, ctrl=512, n=1_000_000, queries="uniform", scaling="weak",
                  desc="cfg2: 1e6 random points/GPU onto a degree-7 B-spline, 512 ctrl pts "
                       "(510 cubic Beziers after 1e-4 approximation)"),
+    # configs[2]: 1e4 curves, mixed degree 3-9, 8-2048 ctrl pts, 100 points per curve
+    "cfg3": dict(degree="3-9", ctrl="8-2048", n=1_000_000, queries="uniform", scaling="weak",
+                 curves=10_000, per_curve=100,
+                 desc="cfg3: 1e6 random points/GPU, 100 per curve, onto a batch of 1e4 "
+                      "B-splines (degree 3-9, 8-2048 ctrl pts, log-uniform), one batched call"),
     # configs[4]: 1e8 points onto 1e5 cubics, query-sharded (strong scaling)
     "cfg5": dict(degree=3, ctrl=100_003, n=100_000_000, queries="uniform", scaling="strong",
                  desc="cfg5: 1e8 random points onto a degree-3 B-spline with 100003 ctrl pts "
@@ -149,28 +154,120 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
-def cpu_baseline(seg, queries, sample_n, workers):
-    """The reference kernel restated in C (oracle/), all host cores."""
+def cpu_time(jobs, workers):
+    """The reference kernel restated in C (oracle/), all host cores, over a
+    list of (seg arrays, queries) jobs; returns (queries, seconds)."""
     import oracle
-    q = queries[:sample_n]
-    oracle.project_block(*seg, q[: min(2000, sample_n)], workers=workers)  # warm
+    seg, q = jobs[0]
+    oracle.project_block(*seg, q[: min(200, len(q))], workers=workers)  # warm
     t0 = time.perf_counter()
-    oracle.project_block(*seg, q, workers=workers)
-    dt = time.perf_counter() - t0
-    return sample_n / dt, dt
+    nq = 0
+    for seg, q in jobs:
+        oracle.project_block(*seg, q, workers=workers)
+        nq += len(q)
+    return nq, time.perf_counter() - t0
 
 
-def prepared_arrays(cfg):
-    """Segment table of the workload's curve, built by the GPU prep pipeline."""
-    from paper_2504_11498_b200 import BSplineCurve, prepare_curve
-    p, knots, ctrl = make_curve(cfg)
-    curve = BSplineCurve(p, knots, ctrl)
-    import torch
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    prep = prepare_curve(curve, 1e-4)
-    torch.cuda.synchronize()
-    return prep, (time.perf_counter() - t0) * 1e3
+def _seg(prep):
+    return (prep.seg_pts, prep.seg_ta, prep.seg_tb, prep.seam_t, prep.seam_pt)
+
+
+class SingleCurve:
+    """cfg1 / cfg2 / cfg5: one prepared curve, the rank's query shard."""
+
+    def __init__(self, cfg, rank, world, n_override):
+        import torch
+        from paper_2504_11498_b200 import BSplineCurve, prepare_curve
+        c = CONFIGS[cfg]
+        self.curve = make_curve(cfg)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        self.prep = prepare_curve(BSplineCurve(*self.curve), 1e-4)
+        torch.cuda.synchronize()
+        self.prep_ms = (time.perf_counter() - t0) * 1e3
+        self.tab = self.prep.table
+        if n_override:
+            self.n = n_override
+        elif c["scaling"] == "strong":
+            from paper_2504_11498_b200.sharding import shard_range
+            lo, hi = shard_range(c["n"], rank, world)
+            self.n = hi - lo
+        else:
+            self.n = c["n"]
+        self.n_total = c["n"] if c["scaling"] == "strong" and not n_override else world * self.n
+        self.q_host = make_queries(cfg, rank, self.n, self.curve)
+        self.q = torch.from_numpy(self.q_host).cuda()
+        self.num_segments = self.prep.num_segments
+        self.h2d = self.n * 24
+
+    def step(self, counters=None, extra_flags=0, dense=False):
+        return self.tab.project(self.q, screen=not dense, counters=counters,
+                                extra_flags=extra_flags)
+
+    def pinned(self):
+        import torch
+        self.q_pin = torch.from_numpy(self.q_host).pin_memory().numpy()
+
+    def host(self, out, dense=False):
+        self.tab.project_host(self.q_pin, out=out, screen=not dense)
+
+    def cpu_jobs(self, sample):
+        sample = max(256, min(sample, int(sample * 510 / self.num_segments)))
+        desc = (f"first {sample} of the {self.n} queries, brute force over all "
+                f"{self.num_segments} cubics")
+        return [(_seg(self.prep), self.q_host[:sample])], desc
+
+
+class CurveSetWorkload:
+    """cfg3: 1e4 mixed curves prepared as one device set, 100 queries per
+    curve in random order, one batched projection call per step."""
+
+    def __init__(self, cfg, rank, world, n_override):
+        import torch
+        from paper_2504_11498_b200 import prepare_curve_set
+        from paper_2504_11498_b200.fixtures import mixed_curve_batch
+        c = CONFIGS[cfg]
+        self.curves = mixed_curve_batch(c["curves"])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        self.cset = prepare_curve_set(self.curves, 1e-4)
+        torch.cuda.synchronize()
+        self.prep_ms = (time.perf_counter() - t0) * 1e3
+        self.n = n_override or c["n"]
+        self.n_total = world * self.n
+        rng = np.random.default_rng(1 + rank)
+        self.cid_host = (np.arange(self.n) % c["curves"]).astype(np.int32)
+        rng.shuffle(self.cid_host)
+        self.q_host = rng.uniform(0.0, 1.0, (self.n, 3))
+        self.q = torch.from_numpy(self.q_host).cuda()
+        self.cid = torch.from_numpy(self.cid_host).cuda()
+        self.num_segments = self.cset.num_segments
+        self.h2d = self.n * (24 + 4)
+
+    def step(self, counters=None, extra_flags=0, dense=False):
+        return self.cset.project_device(self.q, self.cid, counters=counters,
+                                        extra_flags=extra_flags)
+
+    def pinned(self):
+        import torch
+        self.q_pin = torch.from_numpy(self.q_host).pin_memory().numpy()
+        self.cid_pin = torch.from_numpy(self.cid_host).pin_memory().numpy()
+
+    def host(self, out, dense=False):
+        self.cset.project_host(self.q_pin, self.cid_pin, out=out)
+
+    def cpu_jobs(self, sample):
+        stride = max(1, len(self.curves) // 50)
+        jobs, nq, ns = [], 0, 0
+        for c in range(0, len(self.curves), stride):
+            pr = self.cset[c]
+            m = self.cid_host == c
+            jobs.append((_seg(pr), self.q_host[m]))
+            nq += int(m.sum())
+            ns += pr.num_segments
+        desc = (f"{nq} queries of {len(jobs)} stratified curves (every {stride}th, {ns} cubics), "
+                f"brute force per curve")
+        return jobs, desc
 
 
 def run_reference(args, rank):
@@ -178,36 +275,60 @@ def run_reference(args, rank):
         return
     import oracle
     from oracle import prep as P
-    curve = make_curve(args.config)
-    pr = P.prepare(*curve, 1e-4)
-    seg = (pr["seg_pts"], pr["seg_ta"], pr["seg_tb"], pr["seam_t"], pr["seam_pt"])
     cores = len(os.sched_getaffinity(0))
-    S = len(pr["seg_ta"])
-    sample = args.ref_sample if args.config == "cfg2" else max(64, int(args.ref_sample * 510 / S))
-    if CONFIGS[args.config]["queries"] == "on-curve":
-        p_, k_, c_ = curve
-        q = P.eval_curve(p_, k_, c_, np.random.default_rng(1).uniform(k_[0], k_[-1], sample))
+    if args.config == "cfg3":
+        from paper_2504_11498_b200.fixtures import mixed_curve_batch
+        c = CONFIGS["cfg3"]
+        curves = mixed_curve_batch(c["curves"])
+        rng = np.random.default_rng(1)
+        cid = (np.arange(c["n"]) % c["curves"]).astype(np.int32)
+        rng.shuffle(cid)
+        q_all = rng.uniform(0.0, 1.0, (c["n"], 3))
+        stride = len(curves) // 50
+        jobs, ns = [], 0
+        for ci in range(0, len(curves), stride):
+            cv = curves[ci]
+            pr = P.prepare(cv.degree, np.array(cv.knots.knots), np.array(cv.control_points), 1e-4)
+            jobs.append(((pr["seg_pts"], pr["seg_ta"], pr["seg_tb"], pr["seam_t"], pr["seam_pt"]),
+                         q_all[cid == ci]))
+            ns += len(pr["seg_ta"])
+        sample = sum(len(j[1]) for j in jobs)
+        desc = (f"{sample} queries of {len(jobs)} stratified curves (every {stride}th of "
+                f"{len(curves)}, {ns} cubics, numpy restatement of prepare_curve), brute force "
+                f"per curve")
     else:
-        q = make_queries(args.config, 0, sample)
+        curve = make_curve(args.config)
+        pr = P.prepare(*curve, 1e-4)
+        seg = (pr["seg_pts"], pr["seg_ta"], pr["seg_tb"], pr["seam_t"], pr["seam_pt"])
+        S = len(pr["seg_ta"])
+        sample = args.ref_sample if args.config == "cfg2" else max(64, int(args.ref_sample * 510 / S))
+        if CONFIGS[args.config]["queries"] == "on-curve":
+            p_, k_, c_ = curve
+            q = P.eval_curve(p_, k_, c_, np.random.default_rng(1).uniform(k_[0], k_[-1], sample))
+        else:
+            q = make_queries(args.config, 0, sample)
+        jobs = [(seg, q)]
+        desc = f"{sample} of the {args.config} queries per step, brute force over all {S} cubics"
     for _ in range(args.warmup):
-        oracle.project_block(*seg, q[: max(1000, sample // 10)], workers=cores)
+        for seg, q in jobs:
+            oracle.project_block(*seg, q[: max(100, len(q) // 10)], workers=cores)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.project_block(*seg, q, workers=cores)
+        for seg, q in jobs:
+            oracle.project_block(*seg, q, workers=cores)
         times.append(time.perf_counter() - t0)
     ms = statistics.mean(times) * 1e3
     value = sample / (ms / 1e3)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": CONFIGS[args.config]["scaling"],
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(args.config, CONFIGS[args.config]["n"]),
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{sample} of the {args.config} queries per step, brute force "
-                                       f"over all {S} cubics (C restatement of "
-                                       f"_kernels._project_block, bit-exact vs the reference), "
-                                       f"{cores} threads"},
+                             "sample": desc + " (C restatement of _kernels._project_block, "
+                                              f"bit-exact vs the reference), {cores} threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -243,28 +364,15 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2504_11498_b200 import _lib as L
-    from paper_2504_11498_b200 import _device as D
 
     cfg = CONFIGS[args.config]
-    prep, prep_ms = prepared_arrays(args.config)
-    tab = prep.table
-    if args.n:
-        n = args.n
-    elif cfg["scaling"] == "strong":
-        from paper_2504_11498_b200.sharding import shard_range
-        lo, hi = shard_range(cfg["n"], rank, world)
-        n = hi - lo
-    else:
-        n = cfg["n"]
-    q_host = make_queries(args.config, rank, n, make_curve(args.config))
-    q = torch.from_numpy(q_host).cuda()
+    wl = (CurveSetWorkload if args.config == "cfg3" else SingleCurve)(args.config, rank, world,
+                                                                     args.n)
+    n, n_total = wl.n, wl.n_total
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     counters = torch.zeros(L.NUM_COUNTERS, dtype=torch.int64, device="cuda")
-    screen = not args.dense
-
-    def step(cnt=None):
-        return tab.project(q, screen=screen, counters=cnt)
+    dense = args.dense and args.config != "cfg3"
 
     from paper_2504_11498_b200.sharding import gather_results, pack_results
 
@@ -272,11 +380,10 @@ def main():
         # the single exchange of the path: (t, distance, segment id) to rank 0
         if world == 1:
             return
-        total = cfg["n"] if cfg["scaling"] == "strong" and not args.n else world * n
-        gather_results(pack_results(out[0], out[2], out[4]), total, world, rank)
+        gather_results(pack_results(out[0], out[2], out[4]), n_total, world, rank)
 
     for _ in range(args.warmup):
-        gather(step())
+        gather(wl.step(dense=dense))
     torch.cuda.synchronize()
 
     # ---- timed device steps (inputs resident in HBM) ----
@@ -286,21 +393,20 @@ def main():
     kends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     clocks = ClockSampler(local)
     clocks.__enter__()
-    if True:
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        for i in range(args.steps):
-            flush.fill_(float(i))
-            starts[i].record(stream)
-            kstarts[i].record(stream)
-            out = step(counters if i == 0 else None)
-            kends[i].record(stream)
-            gather(out)
-            ends[i].record(stream)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        starts[i].record(stream)
+        kstarts[i].record(stream)
+        out = wl.step(counters if i == 0 else None, dense=dense)
+        kends[i].record(stream)
+        gather(out)
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     kern_ms = [s.elapsed_time(e) for s, e in zip(kstarts, kends)]
     ms = statistics.mean(step_ms)
@@ -308,11 +414,12 @@ def main():
         tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    n_total = (cfg["n"] if cfg["scaling"] == "strong" and not args.n else world * n)
     value = n_total / (ms / 1e3)
-    # own kernels per projection call: Morton keys + 4 cub radix-sort passes
-    # (histogram, exclusive sum, 3 onesweep) + 8 wavefront kernels; dense: 2
-    launches_per_step = (1 + 5 + 8) if screen else (1 + 5 + 2)
+    # own kernels per projection call: Morton keys + 5 cub radix-sort kernels
+    # (histogram, exclusive sum, onesweep passes) + 8 wavefront kernels; dense: 2
+    passes = (30 + (14 if args.config == "cfg3" else 0) + 7) // 8
+    launches_per_step = 1 + 2 + passes + (8 if not dense else 2)
+    launches_per_step *= max(1, -(-n // (1 << 23)))
 
     # ---- roofline: per-stage device times (CUDA events between the pipeline's
     #      kernels, recorded inside libmrep on this stream) x algorithmic work ----
@@ -322,7 +429,7 @@ def main():
     reps = 5
     for _ in range(reps):
         flush.fill_(2.0)
-        tab.project(q, screen=screen, extra_flags=L.MREP_TIMING)
+        wl.step(extra_flags=L.MREP_TIMING, dense=dense)
         buf = (ctypes.c_double * 8)()
         L.lib().mrep_last_stage_times(buf, 8)
         stage += np.array(buf[:8]) / reps
@@ -341,12 +448,16 @@ def main():
             ent["frac"] = ent["tflops"] / peak.value
         stages[nm] = ent
     flops = sum(work.values())
-    dom = max(("traverse", "pairs", "clip"), key=lambda k: stages[k]["ms"]) if screen else None
+    dom = max(("traverse", "pairs", "clip"), key=lambda k: stages[k]["ms"]) if not dense else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and dom:
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch", {}).get(f"wave_{dom}")
+            pj = json.load(open(prof))
+            traffic = (pj.get("dram_bytes_per_launch_by_config", {}).get(args.config, {})
+                       .get(f"wave_{dom}"))
+            if traffic is None and args.config == pj.get("config", "cfg2"):
+                traffic = pj.get("dram_bytes_per_launch", {}).get(f"wave_{dom}")
         except Exception:
             traffic = None
     achieved = stages[dom]["tflops"] if dom else flops / (kms / 1e3) / 1e12
@@ -361,28 +472,28 @@ def main():
                 "pipeline": {"ms": kms, "tflops": flops / (kms / 1e3) / 1e12,
                              "frac": flops / (kms / 1e3) / 1e12 / peak.value},
                 "per_query": {"pairs": c[L.CNT_PAIRS] / n, "survivors": c[L.CNT_SURVIVORS] / n,
-                              "seams": c[L.CNT_SEAMS] / n, "box_tests": c[L.CNT_BOXES] / n},
-                "dense_equivalent_tflops": (F_PAIR * prep.num_segments
-                                            + F_SEAM * (prep.num_segments + 1)) * n
-                                           / (kms / 1e3) / 1e12}
+                              "seams": c[L.CNT_SEAMS] / n, "box_tests": c[L.CNT_BOXES] / n}}
+    if args.config != "cfg3":
+        roofline["dense_equivalent_tflops"] = ((F_PAIR * wl.num_segments
+                                               + F_SEAM * (wl.num_segments + 1)) * n
+                                               / (kms / 1e3) / 1e12)
 
     # ---- e2e: host buffers through the C ABI (H2D + kernel + D2H per step) ----
-    q_pin = torch.from_numpy(q_host).pin_memory()
+    wl.pinned()
     outs = (torch.empty(n, dtype=torch.float64).pin_memory(),
             torch.empty((n, 3), dtype=torch.float64).pin_memory(),
             torch.empty(n, dtype=torch.float64).pin_memory(),
             torch.empty(n, dtype=torch.int64).pin_memory(),
             torch.empty(n, dtype=torch.int32).pin_memory())
     onp = tuple(o.numpy() for o in outs)
-    qnp = q_pin.numpy()
     for _ in range(2):
-        tab.project_host(qnp, out=onp, screen=screen)
+        wl.host(onp, dense=dense)
     e2e_times = []
     for _ in range(args.steps):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        tab.project_host(qnp, out=onp, screen=screen)
+        wl.host(onp, dense=dense)
         e2e_times.append(time.perf_counter() - t0)
     clocks.__exit__(None, None, None)
     e2e_s = statistics.mean(e2e_times)
@@ -390,28 +501,26 @@ def main():
         tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
-    e2e = {"value": n_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": n * 24,
+    e2e = {"value": n_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": wl.h2d,
            "d2h_bytes_per_step": n * (8 + 24 + 8 + 8 + 4),
-           "path": "mrep_project_host (C ABI, pinned host buffers, 2-stream chunked pipeline)"}
+           "path": ("mrep_project_batch_host" if args.config == "cfg3" else "mrep_project_host")
+           + " (C ABI, pinned host buffers, 2-stream chunked pipeline)"}
 
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            seg = (prep.seg_pts, prep.seg_ta, prep.seg_tb, prep.seam_t, prep.seam_pt)
             cores = len(os.sched_getaffinity(0))
-            sample = max(256, min(args.cpu_sample, int(args.cpu_sample * 510 / prep.num_segments)))
-            v, dt = cpu_baseline(seg, q_host, sample, cores)
-            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                   "sample": f"first {sample} of the {n} queries, brute force over all "
-                             f"{prep.num_segments} cubics ({dt:.1f} s wall on {cores} threads); "
-                             f"C restatement of _kernels._project_block, bit-exact vs the "
-                             f"reference"}
+            jobs, desc = wl.cpu_jobs(args.cpu_sample)
+            nq, dt = cpu_time(jobs, cores)
+            cpu = {"value": nq / dt, "unit": UNIT, "cores": cores, "kind": "port",
+                   "sample": f"{desc} ({dt:.1f} s wall on {cores} threads); C restatement of "
+                             f"_kernels._project_block, bit-exact vs the reference"}
+        conf = dict(workload_config(args.config, n), parallelism=f"query-shard x{world}",
+                    prep_ms=wl.prep_ms, cubics=wl.num_segments)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic", "config": dict(workload_config(args.config, n),
-                                                    parallelism=f"query-shard x{world}",
-                                                    prep_ms=prep_ms),
+                "dtype": "f64", "data": "synthetic", "config": conf,
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks.summary()}
         print(json.dumps(line), flush=True)

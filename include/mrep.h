@@ -41,6 +41,8 @@ extern "C" {
 #define MREP_NO_SORT 4u  /* process queries in input order (default: Morton order for warp coherence) */
 #define MREP_FUSED 8u    /* screened mode in the single fused warp-cooperative kernel (default: wavefront) */
 #define MREP_TIMING 16u  /* record per-stage device times (see mrep_last_stage_times); synchronises */
+#define MREP_PACKET 32u   /* screened traversal: force warp-packet BVH walks (default: by query density) */
+#define MREP_PER_LANE 64u /* screened traversal: force per-lane BVH walks */
 
 /* Work counters written (accumulated) by mrep_project when `counters_dev` != NULL. */
 #define MREP_CNT_PAIRS 0      /* (query, cubic) pairs solved: E, quartic, rebase, pieces */
@@ -121,6 +123,55 @@ MREP_API int mrep_project_block(const double* seg_pts, const double* seg_ta, con
                        const double* queries, int64_t n, double clip_tol, int max_iter,
                        int soundness_samples, double* out_t, double* out_foot, double* out_dist,
                        int64_t* out_cand, int64_t* out_stats, double* out_sound, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Curve sets: many prepared curves resident at once, projected in ONE batch
+ * where every query names its curve (BASELINE.json configs[2]; the reference
+ * runs prepare_curve + project_prepared per curve, project.py:220-289, with
+ * batched_decompose, decompose.py:49-67, for the decomposition).  The handle
+ * owns one device allocation: per-curve table descriptors (same records and
+ * AABB hierarchy as mrep_table_pack), plus the scheduler rank of each curve
+ * (decreasing cubic count).  seg_* are the curves' PreparedCurve arrays
+ * concatenated in curve order; seg_ofs[c]..seg_ofs[c+1] are curve c's cubics
+ * (seg_ofs is a HOST array of ncurves+1 int64, seg_ofs[0] = 0, every curve
+ * >= 1 cubic).  Seams are derived exactly as project.py:234-237 does.
+ * ------------------------------------------------------------------- */
+MREP_API int mrep_curveset_create_dev(const double* seg_pts_dev /*[S][4][d]*/,
+                                      const double* seg_ta_dev, const double* seg_tb_dev,
+                                      const int64_t* seg_ofs_host, int64_t ncurves, int d,
+                                      void* stream, void** set_out);
+/* host-array twin (no GPU framework on the caller's side) */
+MREP_API int mrep_curveset_create(const double* seg_pts_host, const double* seg_ta_host,
+                                  const double* seg_tb_host, const int64_t* seg_ofs_host,
+                                  int64_t ncurves, int d, void** set_out);
+MREP_API int mrep_curveset_free(void* set);
+MREP_API int mrep_curveset_info(const void* set, int64_t* ncurves, int64_t* total_cubics, int* d,
+                                int64_t* device_bytes);
+/* Screened exact projection of query i onto curve curve_ids[i] (int32).
+ * Per query, t / foot / dist / segment are those project_prepared returns for
+ * that curve alone.  Scheduling (the paper's task scheduler): queries sorted
+ * by (curve rank, Morton code), persistent traversal warps drain an atomic
+ * task queue heaviest curve first.  A query with an out-of-range curve id gets
+ * NaN outputs and segment -1. */
+MREP_API int mrep_project_batch(const void* set, const double* queries_dev,
+                                const int32_t* curve_ids_dev, int64_t n, double clip_tol,
+                                int max_iter, unsigned flags, double* out_t_dev,
+                                double* out_foot_dev, double* out_dist_dev,
+                                int64_t* out_cand_dev, int32_t* out_seg_dev,
+                                uint64_t* counters_dev, void* stream);
+/* Same from HOST buffers (chunked H2D / kernel / D2H pipeline, synchronous). */
+MREP_API int mrep_project_batch_host(const void* set, const double* queries_host,
+                                     const int32_t* curve_ids_host, int64_t n, double clip_tol,
+                                     int max_iter, unsigned flags, double* out_t_host,
+                                     double* out_foot_host, double* out_dist_host,
+                                     int64_t* out_cand_host, int32_t* out_seg_host,
+                                     uint64_t* counters_host);
+
+/* Synthetic-input helper, host only (no GPU): the reference fixture
+ * generator's momentum walk (_fixtures.py _walk_points) for n points, given
+ * v0 (already unit length) and the n-1 normal draws g [n-1][d]; writes the
+ * un-normalised walk pts [n][d].  Bit-identical to the numpy loop. */
+MREP_API int mrep_synth_walk(const double* v0, const double* g, int64_t n, int d, double* pts);
 
 /* Knot span of each parameter: searchsorted(knots, t, 'right') - 1 clipped
  * to [p, m - p - 2] (the span convention of core.py:108-112). */

@@ -24,6 +24,8 @@ MREP_STATS = 2
 MREP_NO_SORT = 4
 MREP_FUSED = 8
 MREP_TIMING = 16
+MREP_PACKET = 32
+MREP_PER_LANE = 64
 NUM_COUNTERS = 8
 CNT_PAIRS, CNT_SURVIVORS, CNT_CLIP_ITERS, CNT_SEAMS, CNT_BOXES, CNT_PASS2, CNT_HULL_MISS = range(7)
 
@@ -54,6 +56,15 @@ _SIGS = {
     "mrep_table_free": ([_vp], _i32),
     "mrep_project_block_host": ([_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _i64, _dbl, _i32, _i32,
                                  _vp, _vp, _vp, _vp, _vp, _vp], _i32),
+    "mrep_curveset_create_dev": ([_vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp], _i32),
+    "mrep_curveset_create": ([_vp, _vp, _vp, _vp, _i64, _i32, _vp], _i32),
+    "mrep_curveset_free": ([_vp], _i32),
+    "mrep_curveset_info": ([_vp, _vp, _vp, _vp, _vp], _i32),
+    "mrep_project_batch": ([_vp, _vp, _vp, _i64, _dbl, _i32, _u32, _vp, _vp, _vp, _vp, _vp, _vp,
+                            _vp], _i32),
+    "mrep_project_batch_host": ([_vp, _vp, _vp, _i64, _dbl, _i32, _u32, _vp, _vp, _vp, _vp, _vp,
+                                 _vp], _i32),
+    "mrep_synth_walk": ([_vp, _vp, _i64, _i32, _vp], _i32),
     "mrep_knot_span": ([_vp, _i64, _i32, _vp, _i64, _vp, _vp], _i32),
     "mrep_quartic_roots": ([_vp, _i64, _vp, _vp, _vp], _i32),
     "mrep_newton_quartic_roots": ([_vp, _i64, _vp, _vp, _vp], _i32),

@@ -26,10 +26,12 @@ struct Slot {
   double *dq = nullptr, *dt = nullptr, *dfoot = nullptr, *ddist = nullptr;
   int64_t* dcand = nullptr;
   int32_t* dseg = nullptr;
+  int32_t* dcur = nullptr;
   uint64_t* dcnt = nullptr;
   double *hq = nullptr, *ht = nullptr, *hfoot = nullptr, *hdist = nullptr;
   int64_t* hcand = nullptr;
   int32_t* hseg = nullptr;
+  int32_t* hcur = nullptr;
   int64_t lo = 0, cnt = 0;  // chunk in flight (for staged write-back)
   bool busy = false;
 };
@@ -66,6 +68,7 @@ int ensure_ctx() {
     MREP_CUDA_CHECK(cudaMalloc(&s.ddist, CHUNK * sizeof(double)));
     MREP_CUDA_CHECK(cudaMalloc(&s.dcand, CHUNK * sizeof(int64_t)));
     MREP_CUDA_CHECK(cudaMalloc(&s.dseg, CHUNK * sizeof(int32_t)));
+    MREP_CUDA_CHECK(cudaMalloc(&s.dcur, CHUNK * sizeof(int32_t)));
     MREP_CUDA_CHECK(cudaMalloc(&s.dcnt, MREP_NUM_COUNTERS * sizeof(uint64_t)));
     MREP_CUDA_CHECK(cudaMallocHost(&s.hq, CHUNK * 3 * sizeof(double)));
     MREP_CUDA_CHECK(cudaMallocHost(&s.ht, CHUNK * sizeof(double)));
@@ -73,6 +76,7 @@ int ensure_ctx() {
     MREP_CUDA_CHECK(cudaMallocHost(&s.hdist, CHUNK * sizeof(double)));
     MREP_CUDA_CHECK(cudaMallocHost(&s.hcand, CHUNK * sizeof(int64_t)));
     MREP_CUDA_CHECK(cudaMallocHost(&s.hseg, CHUNK * sizeof(int32_t)));
+    MREP_CUDA_CHECK(cudaMallocHost(&s.hcur, CHUNK * sizeof(int32_t)));
   }
   g_ctx.device = dev;
   g_ctx.ready = true;
@@ -84,20 +88,18 @@ int ensure_ctx() {
 
 using namespace mrep;
 
-extern "C" int mrep_project_host(const void* table, int64_t S, int d, const double* queries,
-                                 int64_t n, double clip_tol, int max_iter, unsigned flags,
-                                 double* out_t, double* out_foot, double* out_dist,
-                                 int64_t* out_cand, int32_t* out_seg, uint64_t* counters_host) {
-  if (n < 0 || (d != 2 && d != 3) || S < 1 || !table) {
-    set_error("mrep_project_host: bad arguments");
-    return MREP_ERR_ARG;
-  }
-  if (n == 0) return MREP_OK;
-  std::lock_guard<std::mutex> lock(g_ctx.mu);
+namespace mrep {
+namespace {
+
+// Chunked H2D -> kernel -> D2H pipeline over the two slots.  `launch` runs the
+// projection of one chunk already resident in the slot's device buffers.
+template <class Launch>
+int host_pipeline(int d, const double* queries, const int32_t* curve_ids, int64_t n,
+                  double* out_t, double* out_foot, double* out_dist, int64_t* out_cand,
+                  int32_t* out_seg, uint64_t* counters_host, Launch launch) {
   int rc = ensure_ctx();
   if (rc != MREP_OK) return rc;
-  flags &= ~MREP_STATS;
-  const bool pin_in = is_pinned(queries);
+  const bool pin_in = is_pinned(queries) && (!curve_ids || is_pinned(curve_ids));
   const bool pin_out = is_pinned(out_t) && is_pinned(out_foot) && is_pinned(out_dist) &&
                        is_pinned(out_cand) && (!out_seg || is_pinned(out_seg));
 
@@ -124,14 +126,21 @@ extern "C" int mrep_project_host(const void* table, int64_t S, int d, const doub
     s.lo = c * CHUNK;
     s.cnt = (s.lo + CHUNK <= n) ? CHUNK : n - s.lo;
     const double* src = queries + s.lo * d;
+    const int32_t* csrc = curve_ids ? curve_ids + s.lo : nullptr;
     if (!pin_in) {
       std::memcpy(s.hq, src, s.cnt * d * sizeof(double));
       src = s.hq;
+      if (csrc) {
+        std::memcpy(s.hcur, csrc, s.cnt * sizeof(int32_t));
+        csrc = s.hcur;
+      }
     }
     MREP_CUDA_CHECK(
         cudaMemcpyAsync(s.dq, src, s.cnt * d * sizeof(double), cudaMemcpyHostToDevice, s.st));
-    rc = mrep_project(table, S, d, s.dq, s.cnt, clip_tol, max_iter, 0, flags, s.dt, s.dfoot,
-                      s.ddist, s.dcand, s.dseg, nullptr, nullptr, s.dcnt, s.st);
+    if (csrc)
+      MREP_CUDA_CHECK(
+          cudaMemcpyAsync(s.dcur, csrc, s.cnt * sizeof(int32_t), cudaMemcpyHostToDevice, s.st));
+    rc = launch(s);
     if (rc != MREP_OK) return rc;
     double* ht = pin_out ? out_t + s.lo : s.ht;
     double* hf = pin_out ? out_foot + s.lo * d : s.hfoot;
@@ -161,6 +170,48 @@ extern "C" int mrep_project_host(const void* table, int64_t S, int d, const doub
     }
   }
   return MREP_OK;
+}
+
+}  // namespace
+}  // namespace mrep
+
+extern "C" int mrep_project_host(const void* table, int64_t S, int d, const double* queries,
+                                 int64_t n, double clip_tol, int max_iter, unsigned flags,
+                                 double* out_t, double* out_foot, double* out_dist,
+                                 int64_t* out_cand, int32_t* out_seg, uint64_t* counters_host) {
+  if (n < 0 || (d != 2 && d != 3) || S < 1 || !table) {
+    set_error("mrep_project_host: bad arguments");
+    return MREP_ERR_ARG;
+  }
+  if (n == 0) return MREP_OK;
+  std::lock_guard<std::mutex> lock(g_ctx.mu);
+  flags &= ~MREP_STATS;
+  return host_pipeline(d, queries, nullptr, n, out_t, out_foot, out_dist, out_cand, out_seg,
+                       counters_host, [&](Slot& s) {
+                         return mrep_project(table, S, d, s.dq, s.cnt, clip_tol, max_iter, 0,
+                                             flags, s.dt, s.dfoot, s.ddist, s.dcand, s.dseg,
+                                             nullptr, nullptr, s.dcnt, s.st);
+                       });
+}
+
+extern "C" int mrep_project_batch_host(const void* set, const double* queries,
+                                       const int32_t* curve_ids, int64_t n, double clip_tol,
+                                       int max_iter, unsigned flags, double* out_t,
+                                       double* out_foot, double* out_dist, int64_t* out_cand,
+                                       int32_t* out_seg, uint64_t* counters_host) {
+  int d = 0;
+  if (!set || n < 0 || mrep_curveset_info(set, nullptr, nullptr, &d, nullptr) != MREP_OK) {
+    set_error("mrep_project_batch_host: bad arguments");
+    return MREP_ERR_ARG;
+  }
+  if (n == 0) return MREP_OK;
+  std::lock_guard<std::mutex> lock(g_ctx.mu);
+  return host_pipeline(d, queries, curve_ids, n, out_t, out_foot, out_dist, out_cand, out_seg,
+                       counters_host, [&](Slot& s) {
+                         return mrep_project_batch(set, s.dq, s.dcur, s.cnt, clip_tol, max_iter,
+                                                   flags, s.dt, s.dfoot, s.ddist, s.dcand, s.dseg,
+                                                   s.dcnt, s.st);
+                       });
 }
 
 // ---------------------------------------------------------------------------
@@ -252,4 +303,38 @@ extern "C" int mrep_project_block_host(const double* seg_pts, const double* seg_
   cudaFree(dstat);
   mrep_table_free(table);
   return rc;
+}
+
+// ---------------------------------------------------------------------------
+// Synthetic-input helper (host only): the sequential momentum walk of the
+// reference fixture generator (_fixtures.py _walk_points): v <- v + 0.55 g_i,
+// v <- v / ||v||, p_i = p_{i-1} + v, with ||v|| computed as numpy does for a
+// short vector (BLAS ddot = FMA chain, then sqrt).  The caller draws v0 and
+// the normals g with numpy (same RNG stream) and normalises the result.
+#include <cmath>
+extern "C" int mrep_synth_walk(const double* v0, const double* g, int64_t n, int d, double* pts) {
+  if (n < 1 || (d != 2 && d != 3) || !v0 || !pts || (n > 1 && !g)) {
+    set_error("mrep_synth_walk: bad arguments");
+    return MREP_ERR_ARG;
+  }
+  double v[3] = {v0[0], v0[1], d == 3 ? v0[2] : 0.0};
+  double cur[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < d; ++k) pts[k] = 0.0;
+  for (int64_t i = 1; i < n; ++i) {
+    double w[3];
+    for (int k = 0; k < d; ++k) {
+      volatile double prod = 0.55 * g[(i - 1) * d + k];  // no contraction into an FMA
+      w[k] = v[k] + prod;
+    }
+    volatile double sq0 = w[0] * w[0];
+    double s = std::fma(w[1], w[1], sq0);
+    if (d == 3) s = std::fma(w[2], w[2], s);
+    double nr = std::sqrt(s);
+    for (int k = 0; k < d; ++k) {
+      v[k] = w[k] / nr;
+      cur[k] = cur[k] + v[k];
+      pts[i * d + k] = cur[k];
+    }
+  }
+  return MREP_OK;
 }

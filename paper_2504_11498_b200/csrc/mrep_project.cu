@@ -27,6 +27,7 @@
 #include <cstdint>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include <cub/cub.cuh>
 
@@ -469,8 +470,8 @@ __device__ __forceinline__ void warp_count(uint64_t* counters, int slot, uint64_
 }
 
 template <int D>
-__device__ __forceinline__ void write_winner(const ProjParams& p, int64_t qi, const Pick& w) {
-  const TableView& T = p.tab;
+__device__ __forceinline__ void write_winner(const TableView& T, const ProjParams& p, int64_t qi,
+                                             const Pick& w) {
   const double NaN = __longlong_as_double(0x7ff8000000000000LL);
   if (!w.ok) {
     p.out_t[qi] = NaN;
@@ -941,7 +942,7 @@ __global__ void __launch_bounds__(BLOCK) project_kernel(ProjParams p) {
       p.pass2_list[slot] = qi;
       if (p.out_seg) p.out_seg[qi] = -2;
     } else {
-      write_winner<D>(p, qi, band_pick(B));
+      write_winner<D>(T, p, qi, band_pick(B));
     }
     if (p.out_cand)
       p.out_cand[qi] = SCREEN ? (int64_t)st.offers
@@ -1008,7 +1009,7 @@ __global__ void __launch_bounds__(BLOCK) project_pass2_kernel(ProjParams p) {
     } else {
       gen_dense<D, false>(p.tab, q, p.clip_tol, p.max_iter, 0, B, st);
     }
-    write_winner<D>(p, qi, Pick{B.t[0], B.d[0], B.v[0], B.ord[0], B.valid != 0});
+    write_winner<D>(p.tab, p, qi, Pick{B.t[0], B.d[0], B.v[0], B.ord[0], B.valid != 0});
   }
   if (p.counters && blockIdx.x == 0 && threadIdx.x == 0)
     atomicAdd((unsigned long long*)&p.counters[MREP_CNT_PASS2], total);
@@ -1072,7 +1073,22 @@ struct WaveParams {
   unsigned long long* cord;
   unsigned long long ccap;
   int64_t* fb;
+  // multi-curve batch (mrep_project_batch): per-curve table descriptors, the
+  // curve of each query (caller order) and of each sorted position, and the
+  // persistent traversal's task counter
+  const TableView* tabs;
+  const int32_t* qcurve;
+  int64_t ncurves;
+  int32_t* gcur;
+  unsigned long long* queue;
 };
+
+// table of sorted position g: the single curve, or its curve in a batch
+template <bool MULTI>
+__device__ __forceinline__ const TableView& tab_of(const WaveParams& w, int64_t g) {
+  if (MULTI) return w.tabs[w.gcur[g]];
+  return w.tab;
+}
 
 // warp-aggregated slot allocation (works in divergent code)
 __device__ __forceinline__ unsigned long long wave_append(unsigned long long* counter, bool want) {
@@ -1114,16 +1130,31 @@ __device__ __forceinline__ unsigned long long pk(unsigned mask, int level, int64
          (unsigned long long)idx;
 }
 
-template <int D>
-__global__ void __launch_bounds__(BLOCK) wave_traverse(WaveParams w) {
-  __shared__ unsigned long long stk[BLOCK / 32][PSTACK];
-  const int lane = threadIdx.x & 31;
-  unsigned long long* S = stk[threadIdx.x >> 5];
-  int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = gi < w.n;
+// One warp-task: sorted positions base .. base+31.  Per-lane greedy descent,
+// then packet traversal.  In a multi-curve batch the lanes of one warp may
+// belong to different curves (queries are sorted by curve, so a warp spans at
+// most a few): the packet walk runs once per distinct curve of the warp with
+// that curve's lanes as the packet mask, so control flow stays warp-uniform.
+template <int D, bool MULTI, bool PACKET>
+__device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
+                                              unsigned long long* S, int lane) {
+  bool active = gi < w.n;
   QStats st{};
-  const TableView& T = w.tab;
   int64_t qi = active ? (w.perm ? (int64_t)w.perm[gi] : gi) : 0;
+  int32_t cid = 0;
+  if (MULTI && active) {
+    cid = w.qcurve[qi];
+    if (cid < 0 || cid >= w.ncurves) cid = -1;
+    w.gcur[gi] = cid;
+    if (cid < 0) {  // out-of-range curve id (sorted last): NaN result, no work
+      w.tkey[gi] = ~0ull;
+      w.okey[gi] = ~0ull;
+      w.scnt[gi] = 0;
+      w.flag[gi] = 0;
+      active = false;
+    }
+  }
+  const TableView& T = MULTI ? w.tabs[cid < 0 ? 0 : cid] : w.tab;
   double q[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) q[k] = active ? w.q[qi * D + k] : 0.0;
@@ -1137,7 +1168,7 @@ __global__ void __launch_bounds__(BLOCK) wave_traverse(WaveParams w) {
     w.tkey[gi] = ~0ull;
     w.okey[gi] = ~0ull;
   }
-  {  // greedy descent (uniform trip counts): first bound from a nearby cubic
+  if (active) {  // greedy descent: first bound from the seams of a nearby cubic
     int level = T.top;
     int64_t idx = 0;
     while (level > 0) {
@@ -1159,75 +1190,126 @@ __global__ void __launch_bounds__(BLOCK) wave_traverse(WaveParams w) {
       idx = bi;
       --level;
     }
-    if (active) {
 #pragma unroll 1
-      for (int e = 0; e < 2; ++e) offer_seam<D>(T, idx + e, q, B, st);
-    }
+    for (int e = 0; e < 2; ++e) offer_seam<D>(T, idx + e, q, B, st);
   }
-  unsigned amask = __ballot_sync(0xffffffffu, active);
-  int sp = 0;
-  if (amask) {
-    if (lane == 0) S[0] = pk(amask, T.top, 0);
-    sp = 1;
-  }
-  __syncwarp();
-  while (sp > 0) {
-    unsigned long long e = S[--sp];
-    unsigned mask = (unsigned)(e >> 32);
-    int level = (int)((e >> 28) & 0xf);
-    int64_t idx = (int64_t)(e & 0xfffffffull);
-    bool mine = (mask >> lane) & 1u;
-    __syncwarp();
-    if (level == 0) {
-      // leaf cubic: re-test with the current bound, offer its seams, emit the pair
-      bool need = false;
-      if (mine) {
-        st.boxes++;
-        need = box_lb2<D>(T, T.lvl_off[0] + idx, q) <= cut2(B.dmin, scale);
+  unsigned todo = PACKET ? __ballot_sync(0xffffffffu, active) : 0u;
+  if (!PACKET && active) {
+    // Per-lane depth-first walk, for incoherent queries (a warp's lanes far
+    // apart, e.g. ~100 random queries per curve in a batch): a packet would
+    // drag every lane through the union of 32 paths.  8-bit child masks per
+    // level (top <= 7, checked at launch); each child is re-tested against
+    // the bound current when it is reached.
+    int level = T.top;
+    int64_t idx = 0;
+    uint64_t masks = (uint64_t)child_mask<D>(T, level, 0, q, cut2(B.dmin, scale), st)
+                     << (8 * level);
+    for (;;) {
+      uint32_t mk = (uint32_t)(masks >> (8 * level)) & 0xffu;
+      if (mk == 0) {
+        if (level == T.top) break;
+        ++level;
+        idx /= FANOUT;
+        continue;
+      }
+      int c = __ffs(mk) - 1;
+      masks &= ~(1ull << (8 * level + c));
+      int64_t ch = idx * FANOUT + c;
+      double c2 = cut2(B.dmin, scale);
+      st.boxes++;
+      if (level == 1) {
+        bool need = box_lb2<D>(T, T.lvl_off[0] + ch, q) <= c2;
         if (need) {
 #pragma unroll 1
-          for (int k = 0; k < 2; ++k) offer_seam<D>(T, idx + k, q, B, st);
-          // emit the pair only if the cubic's Bernstein distance bound can
-          // still reach the tie band (with the bound its own seams just set)
-          need = bern_may_reach<D>(T, idx, q, cut2(B.dmin, scale));
+          for (int k = 0; k < 2; ++k) offer_seam<D>(T, ch + k, q, B, st);
+          need = bern_may_reach<D>(T, ch, q, cut2(B.dmin, scale));
         }
-      }
-      unsigned long long slot = wave_append(&w.cnt[0], need);
-      if (need) {
-        if (slot < w.pcap) {
-          w.pq[slot] = (uint32_t)gi;
-          w.ps[slot] = (uint32_t)idx;
-        } else {
-          fall = true;
+        unsigned long long slot = wave_append(&w.cnt[0], need);
+        if (need) {
+          if (slot < w.pcap) {
+            w.pq[slot] = (uint32_t)gi;
+            w.ps[slot] = (uint32_t)ch;
+          } else {
+            fall = true;
+          }
         }
+      } else if (box_lb2<D>(T, T.lvl_off[level - 1] + ch, q) <= c2) {
+        --level;
+        idx = ch;
+        masks |= (uint64_t)child_mask<D>(T, level, idx, q, c2, st) << (8 * level);
       }
-      continue;
     }
-    // children (level-1, idx*8 + c): best-first -- pushed in decreasing order
-    // of the packet leader's box distance so the nearest child pops first and
-    // the seam bound tightens before the far leaves are reached
-    int64_t first = idx * FANOUT, cnt = T.lvl_cnt[level - 1], off = T.lvl_off[level - 1];
-    double c2 = cut2(B.dmin, scale);
-    double key[FANOUT];
-    unsigned msk[FANOUT];
-#pragma unroll
-    for (int c = 0; c < FANOUT; ++c) {
-      int64_t ch = first + c;
-      bool need = false;
-      double lb = 0.0;
-      if (ch < cnt && mine) {
-        st.boxes++;
-        lb = box_lb2<D>(T, off + ch, q);
-        need = lb <= c2;
+  }
+  while (todo) {
+    // packet = the lanes of one curve (all active lanes for a single curve)
+    unsigned amask = todo;
+    int32_t lc = 0;
+    if (MULTI) {
+      lc = __shfl_sync(0xffffffffu, cid, __ffs(todo) - 1);
+      amask = __ballot_sync(0xffffffffu, active && cid == lc);
+    }
+    todo &= ~amask;
+    const TableView& TG = MULTI ? w.tabs[lc] : w.tab;
+    if (lane == 0) S[0] = pk(amask, TG.top, 0);
+    int sp = 1;
+    __syncwarp();
+    while (sp > 0) {
+      unsigned long long e = S[--sp];
+      unsigned mask = (unsigned)(e >> 32);
+      int level = (int)((e >> 28) & 0xf);
+      int64_t idx = (int64_t)(e & 0xfffffffull);
+      bool mine = (mask >> lane) & 1u;
+      __syncwarp();
+      if (level == 0) {
+        // leaf cubic: re-test with the current bound, offer its seams, emit the pair
+        bool need = false;
+        if (mine) {
+          st.boxes++;
+          need = box_lb2<D>(TG, TG.lvl_off[0] + idx, q) <= cut2(B.dmin, scale);
+          if (need) {
+#pragma unroll 1
+            for (int k = 0; k < 2; ++k) offer_seam<D>(TG, idx + k, q, B, st);
+            // emit the pair only if the cubic's Bernstein distance bound can
+            // still reach the tie band (with the bound its own seams just set)
+            need = bern_may_reach<D>(TG, idx, q, cut2(B.dmin, scale));
+          }
+        }
+        unsigned long long slot = wave_append(&w.cnt[0], need);
+        if (need) {
+          if (slot < w.pcap) {
+            w.pq[slot] = (uint32_t)gi;
+            w.ps[slot] = (uint32_t)idx;
+          } else {
+            fall = true;
+          }
+        }
+        continue;
       }
-      unsigned m = __ballot_sync(0xffffffffu, need);
-      msk[c] = m;
-      key[c] = m ? __shfl_sync(0xffffffffu, lb, __ffs(m) - 1) : -1.0;
-    }
-    // sort (key, child) descending: 8-input network, uniform across the warp
-    int ord8[FANOUT];
+      // children (level-1, idx*8 + c): best-first -- pushed in decreasing order
+      // of the packet leader's box distance so the nearest child pops first and
+      // the seam bound tightens before the far leaves are reached
+      int64_t first = idx * FANOUT, cnt = TG.lvl_cnt[level - 1], off = TG.lvl_off[level - 1];
+      double c2 = cut2(B.dmin, scale);
+      double key[FANOUT];
+      unsigned msk[FANOUT];
 #pragma unroll
-    for (int c = 0; c < FANOUT; ++c) ord8[c] = c;
+      for (int c = 0; c < FANOUT; ++c) {
+        int64_t ch = first + c;
+        bool need = false;
+        double lb = 0.0;
+        if (ch < cnt && mine) {
+          st.boxes++;
+          lb = box_lb2<D>(TG, off + ch, q);
+          need = lb <= c2;
+        }
+        unsigned m = __ballot_sync(0xffffffffu, need);
+        msk[c] = m;
+        key[c] = m ? __shfl_sync(0xffffffffu, lb, __ffs(m) - 1) : -1.0;
+      }
+      // sort (key, child) descending: 8-input network, uniform across the warp
+      int ord8[FANOUT];
+#pragma unroll
+      for (int c = 0; c < FANOUT; ++c) ord8[c] = c;
 #define MREP_CEX(a, b)                                   \
   if (key[a] < key[b]) {                                 \
     double tk = key[a];                                  \
@@ -1240,22 +1322,23 @@ __global__ void __launch_bounds__(BLOCK) wave_traverse(WaveParams w) {
     ord8[a] = ord8[b];                                   \
     ord8[b] = to;                                        \
   }
-    MREP_CEX(0, 1) MREP_CEX(2, 3) MREP_CEX(4, 5) MREP_CEX(6, 7)
-    MREP_CEX(0, 2) MREP_CEX(1, 3) MREP_CEX(4, 6) MREP_CEX(5, 7)
-    MREP_CEX(1, 2) MREP_CEX(5, 6) MREP_CEX(0, 4) MREP_CEX(3, 7)
-    MREP_CEX(1, 5) MREP_CEX(2, 6)
-    MREP_CEX(1, 4) MREP_CEX(3, 6)
-    MREP_CEX(2, 4) MREP_CEX(3, 5)
-    MREP_CEX(3, 4)
+      MREP_CEX(0, 1) MREP_CEX(2, 3) MREP_CEX(4, 5) MREP_CEX(6, 7)
+      MREP_CEX(0, 2) MREP_CEX(1, 3) MREP_CEX(4, 6) MREP_CEX(5, 7)
+      MREP_CEX(1, 2) MREP_CEX(5, 6) MREP_CEX(0, 4) MREP_CEX(3, 7)
+      MREP_CEX(1, 5) MREP_CEX(2, 6)
+      MREP_CEX(1, 4) MREP_CEX(3, 6)
+      MREP_CEX(2, 4) MREP_CEX(3, 5)
+      MREP_CEX(3, 4)
 #undef MREP_CEX
 #pragma unroll
-    for (int c = 0; c < FANOUT; ++c) {
-      if (msk[c]) {
-        if (lane == 0) S[sp] = pk(msk[c], level - 1, first + ord8[c]);
-        ++sp;
+      for (int c = 0; c < FANOUT; ++c) {
+        if (msk[c]) {
+          if (lane == 0) S[sp] = pk(msk[c], level - 1, first + ord8[c]);
+          ++sp;
+        }
       }
+      __syncwarp();
     }
-    __syncwarp();
   }
   if (active) {
     if (B.overflow) fall = true;
@@ -1295,16 +1378,40 @@ __global__ void __launch_bounds__(BLOCK) wave_traverse(WaveParams w) {
   warp_count(w.counters, MREP_CNT_BOXES, st.boxes);
 }
 
-template <int D>
-__global__ void __launch_bounds__(BLOCK) wave_pairs(WaveParams w) {
+// W1.  Single curve: one thread per sorted query, hardware block scheduling.
+// Multi-curve batch (the paper's task scheduler): queries are sorted by
+// curve, heaviest curve (most cubics) first, Morton order inside a curve;
+// persistent warps pull 32-position tasks from an atomic work queue, so the
+// long tasks start first and the short ones fill the tail (LPT order).
+template <int D, bool MULTI, bool PACKET>
+__global__ void __launch_bounds__(BLOCK) wave_traverse(const __grid_constant__ WaveParams w) {
+  __shared__ unsigned long long stk[BLOCK / 32][PSTACK];
+  const int lane = threadIdx.x & 31;
+  unsigned long long* S = stk[threadIdx.x >> 5];
+  if (!MULTI) {
+    traverse_task<D, false, PACKET>(w, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, S, lane);
+  } else {
+    for (;;) {
+      unsigned long long task = 0;
+      if (lane == 0) task = atomicAdd(w.queue, 1ull);
+      task = __shfl_sync(0xffffffffu, task, 0);
+      int64_t base = (int64_t)task * 32;
+      if (base >= w.n) break;
+      traverse_task<D, true, PACKET>(w, base + lane, S, lane);
+    }
+  }
+}
+
+template <int D, bool MULTI>
+__global__ void __launch_bounds__(BLOCK) wave_pairs(const __grid_constant__ WaveParams w) {
   unsigned long long total = *(volatile unsigned long long*)&w.cnt[0];
   if (total > w.pcap) total = w.pcap;
-  const TableView& T = w.tab;
   uint64_t npairs = 0, nboxes = 0;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     int64_t qi = w.pq[i];  // sorted position
     int64_t s = w.ps[i];
+    const TableView& T = tab_of<MULTI>(w, qi);
     double4 rec = *(const double4*)(w.qs + qi * 4);
     double q[D];
     q[0] = rec.x;
@@ -1348,16 +1455,16 @@ __global__ void __launch_bounds__(BLOCK) wave_pairs(WaveParams w) {
   warp_count(w.counters, MREP_CNT_BOXES, nboxes);
 }
 
-template <int D>
-__global__ void __launch_bounds__(BLOCK) wave_clip(WaveParams w) {
+template <int D, bool MULTI>
+__global__ void __launch_bounds__(BLOCK) wave_clip(const __grid_constant__ WaveParams w) {
   unsigned long long total = *(volatile unsigned long long*)&w.cnt[1];
   if (total > w.scap) total = w.scap;
-  const TableView& T = w.tab;
   uint64_t nsurv = 0, nit = 0, nmiss = 0;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     int64_t qi = w.sq[i];
     if (w.flag[qi]) continue;
+    const TableView& T = tab_of<MULTI>(w, qi);
     const double* o = w.sb + i * 8;
     double bp[6];
 #pragma unroll
@@ -1410,7 +1517,7 @@ __global__ void __launch_bounds__(BLOCK) wave_clip(WaveParams w) {
 
 // W4..W6: the reference's selection as three atomic passes over candidates
 template <int D, int PASS>
-__global__ void __launch_bounds__(256) wave_select(WaveParams w) {
+__global__ void __launch_bounds__(256) wave_select(const __grid_constant__ WaveParams w) {
   unsigned long long total = *(volatile unsigned long long*)&w.cnt[2];
   if (total > w.ccap) total = w.ccap;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -1440,13 +1547,12 @@ __global__ void __launch_bounds__(256) wave_select(WaveParams w) {
 
 // Final pass in sorted order: foot point of each winner (recomputed exactly
 // as the reference stored it) and one scattered write of the outputs.
-template <int D>
-__global__ void __launch_bounds__(256) wave_emit(WaveParams w) {
+template <int D, bool MULTI>
+__global__ void __launch_bounds__(256) wave_emit(const __grid_constant__ WaveParams w) {
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= w.n) return;
   if (w.flag[g]) return;  // written by the fallback kernel
   int64_t qi = w.perm ? (int64_t)w.perm[g] : g;
-  const TableView& T = w.tab;
   unsigned long long ord = w.okey[g];
   if (w.out_cand) w.out_cand[qi] = w.scnt[g];
   if (ord == ~0ull) {
@@ -1458,6 +1564,7 @@ __global__ void __launch_bounds__(256) wave_emit(WaveParams w) {
     if (w.out_seg) w.out_seg[qi] = -1;
     return;
   }
+  const TableView& T = tab_of<MULTI>(w, g);
   double foot[D];
   int32_t seg;
   if (ord & SURV_BIT) {
@@ -1482,7 +1589,7 @@ __global__ void __launch_bounds__(256) wave_emit(WaveParams w) {
 }
 
 // diagnostics: emitted pairs / survivors / candidates into counters[7] (packed 21 bits each)
-__global__ void wave_diag(WaveParams w) {
+__global__ void wave_diag(const __grid_constant__ WaveParams w) {
   if (w.counters && threadIdx.x == 0 && blockIdx.x == 0) {
     unsigned long long a = w.cnt[0] >> 10, b = w.cnt[1] >> 10, c = w.cnt[2] >> 10;
     atomicAdd((unsigned long long*)&w.counters[7], (a & 0x1fffff) | ((b & 0x1fffff) << 21) |
@@ -1491,30 +1598,32 @@ __global__ void wave_diag(WaveParams w) {
 }
 
 // exact per-thread path for the rare queries the buffers could not hold
-template <int D>
-__global__ void __launch_bounds__(BLOCK) wave_fallback(WaveParams w, ProjParams p) {
+template <int D, bool MULTI>
+__global__ void __launch_bounds__(BLOCK) wave_fallback(const __grid_constant__ WaveParams w,
+                                                       const __grid_constant__ ProjParams p) {
   unsigned long long total = *(volatile unsigned long long*)&w.cnt[3];
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     int64_t g = w.fb[i];
     int64_t qi = w.perm ? (int64_t)w.perm[g] : g;
+    const TableView& T = tab_of<MULTI>(w, g);
     double q[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) q[k] = w.qs[g * 4 + k];
-    double scale = w.tab.hdr[4];
+    double scale = T.hdr[4];
 #pragma unroll
     for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
     Band B;
     band_init(B, false, 0.0);
     QStats st{};
-    gen_screened<D, false>(w.tab, q, scale, w.clip_tol, w.max_iter, B, st);
+    gen_screened<D, false>(T, q, scale, w.clip_tol, w.max_iter, B, st);
     if (B.overflow) {
       double dm = B.dmin;
       band_init(B, true, dm);
-      gen_screened<D, false>(w.tab, q, scale, w.clip_tol, w.max_iter, B, st);
-      write_winner<D>(p, qi, Pick{B.t[0], B.d[0], B.v[0], B.ord[0], B.valid != 0});
+      gen_screened<D, false>(T, q, scale, w.clip_tol, w.max_iter, B, st);
+      write_winner<D>(T, p, qi, Pick{B.t[0], B.d[0], B.v[0], B.ord[0], B.valid != 0});
     } else {
-      write_winner<D>(p, qi, band_pick(B));
+      write_winner<D>(T, p, qi, band_pick(B));
     }
     if (w.out_cand) w.out_cand[qi] = (int64_t)st.offers;
   }
@@ -1805,8 +1914,10 @@ static int launch_project(const ProjParams& p, unsigned flags, cudaStream_t st) 
 }
 
 
-template <int D>
-static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing) {
+template <int D, bool MULTI>
+static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, bool packet,
+                       const TableView* tabs = nullptr, const int32_t* qcurve = nullptr,
+                       int64_t ncurves = 0) {
   const int64_t n = p.n;
   const unsigned long long pcap = (unsigned long long)std::max<int64_t>(16 * n, 1 << 16);
   const unsigned long long scap = (unsigned long long)std::max<int64_t>(2 * n, 1 << 16);
@@ -1826,6 +1937,7 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing) {
   size_t o_fb = take(n * 8);
   size_t o_qs = take(n * 4 * 8), o_wt = take(n * 8), o_wd = take(n * 8), o_wv = take(n * 8),
          o_sc = take(n * 8);
+  size_t o_gc = MULTI ? take(n * 4) : 0;
   char* base = nullptr;
   MREP_CUDA_CHECK(cudaMallocAsync((void**)&base, bytes, st));
   WaveParams w{};
@@ -1865,6 +1977,11 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing) {
   w.win_d = (double*)(base + o_wd);
   w.win_v = (double*)(base + o_wv);
   w.scnt = (int64_t*)(base + o_sc);
+  w.tabs = tabs;
+  w.qcurve = qcurve;
+  w.ncurves = ncurves;
+  w.gcur = MULTI ? (int32_t*)(base + o_gc) : nullptr;
+  w.queue = w.cnt + 5;
   MREP_CUDA_CHECK(cudaMemsetAsync(w.cnt, 0, 8 * sizeof(unsigned long long), st));
   auto persist_grid = [](const void* fn, int block) {
     int dev = 0, sms = 148, per = 1;
@@ -1873,28 +1990,42 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, block, 0);
     return (unsigned)(sms * (per > 0 ? per : 1));
   };
-  const unsigned g_pairs = persist_grid((const void*)wave_pairs<D>, BLOCK);
-  const unsigned g_clip = persist_grid((const void*)wave_clip<D>, BLOCK);
+  const unsigned g_pairs = persist_grid((const void*)wave_pairs<D, MULTI>, BLOCK);
+  const unsigned g_clip = persist_grid((const void*)wave_clip<D, MULTI>, BLOCK);
   const unsigned persist = persist_grid((const void*)wave_select<D, 2>, 256);
   StageTimer tm(timing, st);
   tm.mark();
-  wave_traverse<D><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
+  if (MULTI) {
+    // persistent: one resident wave of warps drains the task queue
+    unsigned need = grid_for(n, BLOCK);
+    if (packet) {
+      unsigned g = persist_grid((const void*)wave_traverse<D, true, true>, BLOCK);
+      wave_traverse<D, true, true><<<g < need ? g : need, BLOCK, 0, st>>>(w);
+    } else {
+      unsigned g = persist_grid((const void*)wave_traverse<D, true, false>, BLOCK);
+      wave_traverse<D, true, false><<<g < need ? g : need, BLOCK, 0, st>>>(w);
+    }
+  } else if (packet) {
+    wave_traverse<D, false, true><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
+  } else {
+    wave_traverse<D, false, false><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
+  }
   MREP_LAUNCH_CHECK();
   tm.mark();
-  wave_pairs<D><<<g_pairs, BLOCK, 0, st>>>(w);
+  wave_pairs<D, MULTI><<<g_pairs, BLOCK, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
   tm.mark();
-  wave_clip<D><<<g_clip, BLOCK, 0, st>>>(w);
+  wave_clip<D, MULTI><<<g_clip, BLOCK, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
   tm.mark();
   wave_select<D, 0><<<persist, 256, 0, st>>>(w);
   wave_select<D, 1><<<persist, 256, 0, st>>>(w);
   wave_select<D, 2><<<persist, 256, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
-  wave_emit<D><<<grid_for(n, 256), 256, 0, st>>>(w);
+  wave_emit<D, MULTI><<<grid_for(n, 256), 256, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
   tm.mark();
-  wave_fallback<D><<<148u, BLOCK, 0, st>>>(w, p);
+  wave_fallback<D, MULTI><<<148u, BLOCK, 0, st>>>(w, p);
   MREP_LAUNCH_CHECK();
   if (getenv("MREP_DIAG")) wave_diag<<<1, 32, 0, st>>>(w);
   tm.mark();
@@ -1902,6 +2033,273 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing) {
   MREP_CUDA_CHECK(cudaFreeAsync(base, st));
   return MREP_OK;
 }
+// ------------------------------------------------------------ curve sets
+// A curve set is the device form of many PreparedCurves (the reference's
+// prepare_curve applied per curve, project.py:220-242): one allocation holding
+// a TableView descriptor per curve, the scheduler rank of each curve, and the
+// per-curve tables (same 256-B records + 8-ary AABB hierarchy as a single
+// table, each 256-B aligned).
+struct CurveSet {
+  int64_t nc = 0, S_total = 0;
+  int d = 3;
+  int rank_bits = 1;
+  int max_top = 1;  // deepest AABB hierarchy of the set
+  char* mem = nullptr;
+  int64_t bytes = 0;
+  TableView* desc = nullptr;  // device, [nc]
+  uint32_t* rank = nullptr;   // device, [nc]: position in decreasing-cubic-count order
+  std::vector<int64_t> ofs;   // host, [nc + 1] cubic offsets
+};
+
+__global__ void set_pack_kernel(const double* seg_pts, const double* seg_ta, const double* seg_tb,
+                                const int64_t* ofs, const int64_t* tab_off, int64_t nc,
+                                int64_t S_total, int d, double* tables) {
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= S_total) return;
+  // curve of cubic g: last c with ofs[c] <= g
+  int64_t lo = 0, hi = nc;
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (ofs[mid] <= g) lo = mid;
+    else hi = mid;
+  }
+  const int64_t c = lo, s = g - ofs[c], S = ofs[c + 1] - ofs[c];
+  double* base = tables + tab_off[c];
+  double* hdr = base;
+  double* r = base + HDR + s * REC;
+  double* box0 = base + HDR + S * REC;
+  double P[4][3];
+  for (int j = 0; j < 4; ++j)
+    for (int k = 0; k < 3; ++k) P[j][k] = k < d ? seg_pts[(g * 4 + j) * d + k] : 0.0;
+  if (s == 0) {  // seam_t[0] = seg_ta[0], seam_pt[0] = seg_pts[0, 0] (project.py:234-235)
+    hdr[0] = seg_ta[g];
+    for (int k = 0; k < 3; ++k) hdr[1 + k] = P[0][k];
+  }
+  double amax = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    double w0, w1, w2, w3;
+    cubic_power_coeffs(P[0][k], P[1][k], P[2][k], P[3][k], w0, w1, w2, w3);
+    r[0 * 3 + k] = w0;
+    r[1 * 3 + k] = w1;
+    r[2 * 3 + k] = w2;
+    r[3 * 3 + k] = w3;
+    double blo = P[0][k], bhi = P[0][k];
+    for (int j = 0; j < 4; ++j) {
+      r[12 + j * 3 + k] = P[j][k];
+      blo = fmin(blo, P[j][k]);
+      bhi = fmax(bhi, P[j][k]);
+      amax = fmax(amax, fabs(P[j][k]));
+    }
+    box0[s * 6 + k] = blo;
+    box0[s * 6 + 3 + k] = bhi;
+  }
+  r[24] = seg_ta[g];
+  r[25] = seg_tb[g];
+  r[26] = seg_tb[g];  // seam_t[s+1] = seg_tb[s], seam_pt[s+1] = seg_pts[s, 3] (project.py:236-237)
+  for (int k = 0; k < 3; ++k) r[27 + k] = P[3][k];
+  r[30] = 0.0;
+  r[31] = 0.0;
+  atomicMax((unsigned long long*)&hdr[4], (unsigned long long)__double_as_longlong(amax));
+}
+
+// one block per curve builds its AABB levels bottom-up
+__global__ void set_boxes_kernel(const TableView* desc) {
+  const TableView& T = desc[blockIdx.x];
+  double* box = const_cast<double*>(T.box);
+  for (int lv = 1; lv <= T.top; ++lv) {
+    const double* child = box + T.lvl_off[lv - 1] * 6;
+    double* parent = box + T.lvl_off[lv] * 6;
+    const int64_t nchild = T.lvl_cnt[lv - 1], npar = T.lvl_cnt[lv];
+    for (int64_t i = threadIdx.x; i < npar; i += blockDim.x) {
+      double lo[3], hi[3];
+      for (int k = 0; k < 3; ++k) {
+        lo[k] = child[i * FANOUT * 6 + k];
+        hi[k] = child[i * FANOUT * 6 + 3 + k];
+      }
+      for (int c = 1; c < FANOUT; ++c) {
+        int64_t ch = i * FANOUT + c;
+        if (ch >= nchild) break;
+        for (int k = 0; k < 3; ++k) {
+          lo[k] = fmin(lo[k], child[ch * 6 + k]);
+          hi[k] = fmax(hi[k], child[ch * 6 + 3 + k]);
+        }
+      }
+      for (int k = 0; k < 3; ++k) {
+        parent[i * 6 + k] = lo[k];
+        parent[i * 6 + 3 + k] = hi[k];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Scheduler key of each query: (rank of its curve, Morton code inside that
+// curve's root box).  Sorting by it groups a curve's queries, orders curves
+// by decreasing cubic count and makes the lanes of a warp spatial neighbours.
+// Queries with an invalid curve id get the largest key (sorted last).
+template <int D>
+__global__ void morton_multi_kernel(const double* q, const int32_t* qcurve, int64_t n,
+                                    const TableView* desc, const uint32_t* rank, int64_t nc,
+                                    int end_bit, uint64_t* key, uint32_t* idx) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  idx[i] = (uint32_t)i;
+  int32_t c = qcurve[i];
+  if (c < 0 || c >= nc) {
+    key[i] = (end_bit >= 64) ? ~0ull : ((1ull << end_bit) - 1ull);
+    return;
+  }
+  const TableView& T = desc[c];
+  const double* box_root = T.box + T.lvl_off[T.top] * 6;
+  uint64_t code = 0;
+  for (int k = 0; k < D; ++k) {
+    double lo = box_root[k], hi = box_root[3 + k];
+    double ext = fmax(hi - lo, 1e-300);
+    double u = (q[i * D + k] - (lo - ext)) / (3.0 * ext);
+    u = fmin(fmax(u, 0.0), 1.0);
+    uint32_t cc = (uint32_t)(u * 1023.0);
+    for (int b = 0; b < 10; ++b) code |= (uint64_t)((cc >> b) & 1u) << (b * D + k);
+  }
+  key[i] = ((uint64_t)rank[c] << (10 * D)) | code;
+}
+
+int set_create(const double* seg_pts, const double* seg_ta, const double* seg_tb,
+               const int64_t* ofs_host, int64_t nc, int d, cudaStream_t st, CurveSet** out) {
+  *out = nullptr;
+  if (nc < 1 || (d != 2 && d != 3) || !ofs_host || ofs_host[0] != 0) {
+    set_error("mrep_curveset_create: need ncurves >= 1, d in {2,3}, seg_ofs[0] == 0");
+    return MREP_ERR_ARG;
+  }
+  for (int64_t c = 0; c < nc; ++c)
+    if (ofs_host[c + 1] - ofs_host[c] < 1) {
+      set_error("mrep_curveset_create: every curve needs at least one cubic (seg_ofs increasing)");
+      return MREP_ERR_ARG;
+    }
+  CurveSet* cs = new CurveSet();
+  cs->nc = nc;
+  cs->d = d;
+  cs->ofs.assign(ofs_host, ofs_host + nc + 1);
+  cs->S_total = ofs_host[nc];
+  // layout: [desc nc][rank nc][ofs nc+1][tab_off nc][tables...]
+  auto al = [](int64_t b) { return (b + 255) & ~(int64_t)255; };
+  const int64_t o_desc = 0, o_rank = al(nc * (int64_t)sizeof(TableView));
+  const int64_t o_ofs = o_rank + al(nc * 4), o_toff = o_ofs + al((nc + 1) * 8);
+  const int64_t o_tab = o_toff + al(nc * 8);
+  std::vector<int64_t> toff(nc);
+  int64_t dbl = 0;
+  for (int64_t c = 0; c < nc; ++c) {
+    toff[c] = dbl;
+    dbl += (table_layout(cs->ofs[c + 1] - cs->ofs[c]).total_doubles + 31) & ~(int64_t)31;
+  }
+  cs->bytes = o_tab + dbl * 8;
+  cudaError_t e = cudaMalloc(&cs->mem, (size_t)cs->bytes);
+  if (e != cudaSuccess) {
+    set_error(std::string("mrep_curveset_create: cudaMalloc: ") + cudaGetErrorString(e));
+    delete cs;
+    return MREP_ERR_CUDA;
+  }
+  double* tables = (double*)(cs->mem + o_tab);
+  std::vector<TableView> desc(nc);
+  for (int64_t c = 0; c < nc; ++c) {
+    desc[c] = table_view(tables + toff[c], cs->ofs[c + 1] - cs->ofs[c]);
+    cs->max_top = std::max(cs->max_top, desc[c].top);
+  }
+  // scheduler rank: curves by decreasing cubic count (ties by index)
+  std::vector<int64_t> order(nc);
+  for (int64_t c = 0; c < nc; ++c) order[c] = c;
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+    return cs->ofs[a + 1] - cs->ofs[a] > cs->ofs[b + 1] - cs->ofs[b];
+  });
+  std::vector<uint32_t> rank(nc);
+  for (int64_t i = 0; i < nc; ++i) rank[order[i]] = (uint32_t)i;
+  cs->rank_bits = 1;
+  while (((int64_t)1 << cs->rank_bits) < nc + 1) ++cs->rank_bits;
+  cs->desc = (TableView*)(cs->mem + o_desc);
+  cs->rank = (uint32_t*)(cs->mem + o_rank);
+  int64_t* ofs_dev = (int64_t*)(cs->mem + o_ofs);
+  int64_t* toff_dev = (int64_t*)(cs->mem + o_toff);
+  int rc = MREP_OK;
+  auto fail = [&](cudaError_t err, const char* what) {
+    set_error(std::string("mrep_curveset_create: ") + what + ": " + cudaGetErrorString(err));
+    rc = MREP_ERR_CUDA;
+  };
+  if ((e = cudaMemcpyAsync(cs->desc, desc.data(), nc * sizeof(TableView), cudaMemcpyHostToDevice, st)) != cudaSuccess) fail(e, "desc");
+  if (!rc && (e = cudaMemcpyAsync(cs->rank, rank.data(), nc * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess) fail(e, "rank");
+  if (!rc && (e = cudaMemcpyAsync(ofs_dev, cs->ofs.data(), (nc + 1) * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) fail(e, "ofs");
+  if (!rc && (e = cudaMemcpyAsync(toff_dev, toff.data(), nc * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) fail(e, "toff");
+  if (!rc && (e = cudaMemsetAsync(tables, 0, dbl * 8, st)) != cudaSuccess) fail(e, "memset");
+  if (!rc) {
+    set_pack_kernel<<<grid_for(cs->S_total, 128), 128, 0, st>>>(seg_pts, seg_ta, seg_tb, ofs_dev,
+                                                                toff_dev, nc, cs->S_total, d, tables);
+    set_boxes_kernel<<<(unsigned)nc, 128, 0, st>>>(cs->desc);
+    if ((e = cudaGetLastError()) != cudaSuccess) fail(e, "pack kernels");
+  }
+  // the host staging vectors die here: finish the copies before returning
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess && !rc) fail(e, "sync");
+  if (rc) {
+    cudaFree(cs->mem);
+    delete cs;
+    return rc;
+  }
+  *out = cs;
+  return MREP_OK;
+}
+
+static int project_batch_chunk(const CurveSet* cs, const double* queries, const int32_t* qcurve,
+                               int64_t n, double clip_tol, int max_iter, unsigned flags,
+                               double* out_t, double* out_foot, double* out_dist,
+                               int64_t* out_cand, int32_t* out_seg, uint64_t* counters,
+                               cudaStream_t st) {
+  int prc = ensure_pool();
+  if (prc) return prc;
+  const int d = cs->d;
+  ProjParams p{};
+  p.q = queries;
+  p.n = n;
+  p.clip_tol = clip_tol;
+  p.max_iter = max_iter;
+  p.out_t = out_t;
+  p.out_foot = out_foot;
+  p.out_dist = out_dist;
+  p.out_cand = out_cand;
+  p.out_seg = out_seg;
+  p.counters = counters;
+  const int end_bit = 10 * d + cs->rank_bits;
+  size_t sort_tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, end_bit,
+                                  st);
+  size_t o_k = 0, o_i = o_k + 16 * (size_t)n, o_tmp = o_i + 8 * (size_t)n + 256;
+  char* ws = nullptr;
+  MREP_CUDA_CHECK(cudaMallocAsync((void**)&ws, o_tmp + sort_tmp + 256, st));
+  uint64_t* k_in = (uint64_t*)(ws + o_k);
+  uint64_t* k_out = k_in + n;
+  uint32_t* i_in = (uint32_t*)(ws + o_i);
+  uint32_t* i_out = i_in + n;
+  const bool timing = (flags & MREP_TIMING) != 0;
+  StageTimer sort_tm(timing, st);
+  sort_tm.mark();
+  if (d == 3)
+    morton_multi_kernel<3><<<grid_for(n, 256), 256, 0, st>>>(queries, qcurve, n, cs->desc, cs->rank,
+                                                             cs->nc, end_bit, k_in, i_in);
+  else
+    morton_multi_kernel<2><<<grid_for(n, 256), 256, 0, st>>>(queries, qcurve, n, cs->desc, cs->rank,
+                                                             cs->nc, end_bit, k_in, i_in);
+  MREP_LAUNCH_CHECK();
+  MREP_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(ws + o_tmp, sort_tmp, k_in, k_out, i_in, i_out,
+                                                  (int)n, 0, end_bit, st));
+  sort_tm.mark();
+  sort_tm.finish(0);
+  p.perm = i_out;
+  const bool packet = ((flags & MREP_PACKET) ? true
+                       : (flags & MREP_PER_LANE) ? false
+                       : n >= 8 * cs->S_total) || cs->max_top > 7;
+  int rc = d == 3 ? launch_wave<3, true>(p, st, timing, packet, cs->desc, qcurve, cs->nc)
+                  : launch_wave<2, true>(p, st, timing, packet, cs->desc, qcurve, cs->nc);
+  MREP_CUDA_CHECK(cudaFreeAsync(ws, st));
+  return rc;
+}
+
 }  // namespace mrep
 
 using namespace mrep;
@@ -2050,7 +2448,14 @@ static int project_chunk(const void* table, int64_t S, int d, const double* quer
   sort_tm.finish(0);
   int rc;
   bool wave = (flags & MREP_SCREEN) && !(flags & MREP_STATS) && !(flags & MREP_FUSED);
-  if (wave) rc = d == 3 ? launch_wave<3>(p, st, timing) : launch_wave<2>(p, st, timing);
+  // packet traversal when the queries are dense along the curve (Morton
+  // neighbours share their BVH path); per-lane walks otherwise
+  const bool packet = (flags & MREP_PACKET) ? true
+                      : (flags & MREP_PER_LANE) ? false
+                      : (n >= 8 * S || p.tab.top > 7);
+  if (wave)
+    rc = d == 3 ? launch_wave<3, false>(p, st, timing, packet || p.tab.top > 7)
+                : launch_wave<2, false>(p, st, timing, packet || p.tab.top > 7);
   else rc = d == 3 ? launch_project<3>(p, flags, st) : launch_project<2>(p, flags, st);
   MREP_CUDA_CHECK(cudaFreeAsync(ws, st));
   return rc;
@@ -2076,6 +2481,102 @@ int mrep_project_block(const double* seg_pts, const double* seg_ta, const double
                       stream);
   cudaFreeAsync(table, st);
   return rc;
+}
+
+
+// ---------------------------------------------------------------- curve sets
+int mrep_curveset_create_dev(const double* seg_pts, const double* seg_ta, const double* seg_tb,
+                             const int64_t* seg_ofs_host, int64_t ncurves, int d, void* stream,
+                             void** set_out) {
+  if (!set_out) {
+    set_error("mrep_curveset_create_dev: null handle pointer");
+    return MREP_ERR_ARG;
+  }
+  CurveSet* cs = nullptr;
+  int rc = set_create(seg_pts, seg_ta, seg_tb, seg_ofs_host, ncurves, d, (cudaStream_t)stream, &cs);
+  *set_out = cs;
+  return rc;
+}
+
+int mrep_curveset_create(const double* seg_pts, const double* seg_ta, const double* seg_tb,
+                         const int64_t* seg_ofs, int64_t ncurves, int d, void** set_out) {
+  if (!set_out || !seg_ofs || ncurves < 1 || (d != 2 && d != 3)) {
+    set_error("mrep_curveset_create: bad arguments");
+    return MREP_ERR_ARG;
+  }
+  *set_out = nullptr;
+  const int64_t S = seg_ofs[ncurves];
+  if (S < 1) {
+    set_error("mrep_curveset_create: no cubics");
+    return MREP_ERR_ARG;
+  }
+  double *dp = nullptr, *da = nullptr, *db = nullptr;
+  MREP_CUDA_CHECK(cudaMalloc(&dp, S * 4 * d * sizeof(double)));
+  MREP_CUDA_CHECK(cudaMalloc(&da, S * sizeof(double)));
+  MREP_CUDA_CHECK(cudaMalloc(&db, S * sizeof(double)));
+  MREP_CUDA_CHECK(cudaMemcpy(dp, seg_pts, S * 4 * d * sizeof(double), cudaMemcpyHostToDevice));
+  MREP_CUDA_CHECK(cudaMemcpy(da, seg_ta, S * sizeof(double), cudaMemcpyHostToDevice));
+  MREP_CUDA_CHECK(cudaMemcpy(db, seg_tb, S * sizeof(double), cudaMemcpyHostToDevice));
+  CurveSet* cs = nullptr;
+  int rc = set_create(dp, da, db, seg_ofs, ncurves, d, nullptr, &cs);
+  cudaFree(dp);
+  cudaFree(da);
+  cudaFree(db);
+  *set_out = cs;
+  return rc;
+}
+
+int mrep_curveset_free(void* set) {
+  CurveSet* cs = (CurveSet*)set;
+  if (!cs) return MREP_OK;
+  cudaError_t e = cudaFree(cs->mem);
+  delete cs;
+  if (e != cudaSuccess) {
+    set_error(std::string("mrep_curveset_free: ") + cudaGetErrorString(e));
+    return MREP_ERR_CUDA;
+  }
+  return MREP_OK;
+}
+
+int mrep_curveset_info(const void* set, int64_t* ncurves, int64_t* total_cubics, int* d,
+                       int64_t* device_bytes) {
+  const CurveSet* cs = (const CurveSet*)set;
+  if (!cs) {
+    set_error("mrep_curveset_info: null set");
+    return MREP_ERR_ARG;
+  }
+  if (ncurves) *ncurves = cs->nc;
+  if (total_cubics) *total_cubics = cs->S_total;
+  if (d) *d = cs->d;
+  if (device_bytes) *device_bytes = cs->bytes;
+  return MREP_OK;
+}
+
+int mrep_project_batch(const void* set, const double* queries, const int32_t* curve_ids, int64_t n,
+                       double clip_tol, int max_iter, unsigned flags, double* out_t,
+                       double* out_foot, double* out_dist, int64_t* out_cand, int32_t* out_seg,
+                       uint64_t* counters, void* stream) {
+  const CurveSet* cs = (const CurveSet*)set;
+  if (!cs || n < 0 || max_iter < 1) {
+    set_error("mrep_project_batch: bad arguments (set, n >= 0, max_iter >= 1)");
+    return MREP_ERR_ARG;
+  }
+  if (n == 0) return MREP_OK;
+  if (!queries || !curve_ids || !out_t || !out_foot || !out_dist) {
+    set_error("mrep_project_batch: null query/curve/output pointer");
+    return MREP_ERR_ARG;
+  }
+  const int64_t CHUNK_Q = (int64_t)1 << 23;
+  const int d = cs->d;
+  for (int64_t lo = 0; lo < n; lo += CHUNK_Q) {
+    int64_t m = n - lo < CHUNK_Q ? n - lo : CHUNK_Q;
+    int rc = project_batch_chunk(cs, queries + lo * d, curve_ids + lo, m, clip_tol, max_iter, flags,
+                                 out_t + lo, out_foot + lo * d, out_dist + lo,
+                                 out_cand ? out_cand + lo : nullptr,
+                                 out_seg ? out_seg + lo : nullptr, counters, (cudaStream_t)stream);
+    if (rc != MREP_OK) return rc;
+  }
+  return MREP_OK;
 }
 
 int mrep_knot_span(const double* knots, int64_t m, int p, const double* t, int64_t n,

@@ -15,6 +15,9 @@ Files:
                  _eval_ordinates, _decasteljau_point, T5, B3
   project_*.npz  prepared tables + queries + every _project_block output
   prep.npz       curves -> decompose_to_bezier -> approximate_error_controlled
+  batch_mixed.npz  a mixed-degree curve set (BASELINE configs[2] shape, small
+                 n): prepare_curve + project_prepared per curve, queries
+                 interleaved across curves
 """
 
 import os
@@ -316,8 +319,47 @@ def make_prep():
           len(cu_iv), "cubics")
 
 
+def make_batch(n_curves=16, max_control=160, per_curve=48):
+    """Curve i: default_rng(i) draws p ~ U{3..9}, n log-uniform on
+    [max(8, p+1), max_control], then random_clamped_curve(rng, p, n, 3,
+    uniform_knots=True) -- the generator of fixtures.mixed_curve_batch."""
+    curves = []
+    for i in range(n_curves):
+        rng = np.random.default_rng(i)
+        p = int(rng.integers(3, 10))
+        lo = max(8, p + 1)
+        n = int(round(np.exp(rng.uniform(np.log(lo), np.log(max_control)))))
+        n = min(max(n, lo), max_control)
+        curves.append(random_clamped_curve(rng, p, n, 3, uniform_knots=True))
+    rng = np.random.default_rng(4242)
+    cid = rng.permutation(np.repeat(np.arange(n_curves), per_curve)).astype(np.int32)
+    q = random_queries(rng, len(cid), 3)
+    N = len(cid)
+    t, foot, dist, cand = np.empty(N), np.empty((N, 3)), np.empty(N), np.empty(N, np.int64)
+    seg_pts, seg_ta, seg_tb, seg_ofs = [], [], [], [0]
+    for c, cu in enumerate(curves):
+        prep = splinemat.prepare_curve(cu, 1e-4)
+        m = cid == c
+        r = splinemat.project_prepared(prep, q[m], workers=1)
+        t[m], foot[m], dist[m], cand[m] = r
+        seg_pts.append(np.array(prep.seg_pts))
+        seg_ta.append(np.array(prep.seg_ta))
+        seg_tb.append(np.array(prep.seg_tb))
+        seg_ofs.append(seg_ofs[-1] + len(prep.seg_ta))
+    np.savez_compressed(
+        os.path.join(OUT, "batch_mixed.npz"),
+        degree=np.array([c.degree for c in curves]),
+        n_control=np.array([c.control_points.shape[0] for c in curves]),
+        knot_ofs=np.concatenate(([0], np.cumsum([len(c.knots.knots) for c in curves]))),
+        knots=np.concatenate([np.array(c.knots.knots) for c in curves]),
+        ctrl=np.concatenate([np.array(c.control_points) for c in curves]),
+        max_control=max_control, seg_pts=np.concatenate(seg_pts), seg_ta=np.concatenate(seg_ta),
+        seg_tb=np.concatenate(seg_tb), seg_ofs=np.array(seg_ofs), queries=q, curve_ids=cid,
+        t=t, foot=foot, dist=dist, cand=cand)
+    print("batch_mixed", n_curves, "curves,", seg_ofs[-1], "cubics,", N, "queries")
+
+
 if __name__ == "__main__":
-    make_quartic()
-    make_ops()
-    make_projection()
-    make_prep()
+    which = sys.argv[1:] or ["quartic", "ops", "projection", "prep", "batch"]
+    for w in which:
+        globals()["make_" + w]()

@@ -51,9 +51,11 @@ def test_wavefront_fused_unsorted_agree(gpu, name):
     a = tab.project(z["queries"])
     b = tab.project(z["queries"], extra_flags=L.MREP_FUSED)
     c = tab.project(z["queries"], extra_flags=L.MREP_NO_SORT | L.MREP_FUSED)
+    d = tab.project(z["queries"], extra_flags=L.MREP_PACKET)
+    e = tab.project(z["queries"], extra_flags=L.MREP_PER_LANE)
     for k in (0, 1, 2, 4):
-        assert np.array_equal(a[k].cpu().numpy(), b[k].cpu().numpy()), k
-        assert np.array_equal(a[k].cpu().numpy(), c[k].cpu().numpy()), k
+        for other in (b, c, d, e):
+            assert np.array_equal(a[k].cpu().numpy(), other[k].cpu().numpy()), k
 
 
 @pytest.mark.parametrize("name", project_fixture_names())
