@@ -43,6 +43,7 @@ extern "C" {
 #define MREP_TIMING 16u  /* record per-stage device times (see mrep_last_stage_times); synchronises */
 #define MREP_PACKET 32u   /* screened traversal: force warp-packet BVH walks (default: by query density) */
 #define MREP_PER_LANE 64u /* screened traversal: force per-lane BVH walks */
+#define MREP_GROUP 128u   /* screened traversal: force one 8-lane group per query */
 
 /* Work counters written (accumulated) by mrep_project when `counters_dev` != NULL. */
 #define MREP_CNT_PAIRS 0      /* (query, cubic) pairs solved: E, quartic, rebase, pieces */

@@ -26,6 +26,7 @@ MREP_FUSED = 8
 MREP_TIMING = 16
 MREP_PACKET = 32
 MREP_PER_LANE = 64
+MREP_GROUP = 128
 NUM_COUNTERS = 8
 CNT_PAIRS, CNT_SURVIVORS, CNT_CLIP_ITERS, CNT_SEAMS, CNT_BOXES, CNT_PASS2, CNT_HULL_MISS = range(7)
 

@@ -31,16 +31,19 @@ void set_error(const std::string& msg);
   } while (0)
 
 // ---------------------------------------------------------------- table
-// One 256-B record per cubic (32 doubles):
-//   [0..11]  w[k][dim], k = 0..3 power coefficients (B3 P), dim-major inside k
-//   [12..23] P[j][dim], control points
-//   [24] ta  [25] tb  [26] seam_t[s+1]  [27..29] seam_pt[s+1]  [30..31] pad
+// One 256-B record per cubic (32 doubles), two 128-B lines:
+//   line 0 (what the BVH traversal touches: seam offers + Bernstein bound)
+//     [0..11]  w[k][dim], k = 0..3 power coefficients (B3 P), dim-major inside k
+//     [12] seam_t[s+1]  [13..15] seam_pt[s+1]
+//   line 1 (pairs / clipping / foot points)
+//     [16..27] P[j][dim], control points  [28] ta  [29] tb  [30..31] pad
 // Header (64 doubles) before the records: [0] seam_t[0], [1..3] seam_pt[0],
 // [4] coordinate scale (max |coord| of the control points).
 // AABB hierarchy after the records: 8-ary over contiguous cubic ranges,
 // level 0 = one box per cubic, top level = 1 box; 6 doubles per box
 // (lo xyz, hi xyz).
 constexpr int REC = 32;
+constexpr int R_W = 0, R_ST = 12, R_SP = 13, R_P = 16, R_TA = 28, R_TB = 29;
 constexpr int HDR = 64;
 constexpr int FANOUT = 8;
 constexpr int MAX_LEVELS = 12;

@@ -216,9 +216,9 @@ __device__ __forceinline__ void seam_point(const TableView& T, int64_t s, double
     for (int k = 0; k < D; ++k) pt[k] = T.hdr[1 + k];
   } else {
     const double* r = T.rec + (s - 1) * REC;
-    st = r[26];
+    st = r[R_ST];
 #pragma unroll
-    for (int k = 0; k < D; ++k) pt[k] = r[27 + k];
+    for (int k = 0; k < D; ++k) pt[k] = r[R_SP + k];
   }
 }
 
@@ -289,8 +289,8 @@ __device__ __forceinline__ void solve_segment(const TableView& T, int64_t s, con
           double acc = 0.0;
 #pragma unroll
           for (int dim = 0; dim < D; ++dim) {
-            double f = decasteljau1(__ldg(r + 12 + dim), __ldg(r + 15 + dim), __ldg(r + 18 + dim),
-                                    __ldg(r + 21 + dim), v);
+            double f = decasteljau1(__ldg(r + R_P + dim), __ldg(r + R_P + 3 + dim), __ldg(r + R_P + 6 + dim),
+                                    __ldg(r + R_P + 9 + dim), v);
             double diff = q[dim] - f;
             acc += diff * diff;
           }
@@ -309,7 +309,7 @@ __device__ __forceinline__ void solve_segment(const TableView& T, int64_t s, con
       lo = hi;
       continue;
     }
-    double ta = __ldg(r + 24), tb = __ldg(r + 25);
+    double ta = __ldg(r + R_TA), tb = __ldg(r + R_TB);
     if (STATS) {
       double gscale = (hi - lo) * (tb - ta);
       if (co.w3 <= clip_tol) st.c3l++;
@@ -321,8 +321,8 @@ __device__ __forceinline__ void solve_segment(const TableView& T, int64_t s, con
     double acc = 0.0;
 #pragma unroll
     for (int dim = 0; dim < D; ++dim) {
-      double f = decasteljau1(__ldg(r + 12 + dim), __ldg(r + 15 + dim), __ldg(r + 18 + dim),
-                              __ldg(r + 21 + dim), v);
+      double f = decasteljau1(__ldg(r + R_P + dim), __ldg(r + R_P + 3 + dim), __ldg(r + R_P + 6 + dim),
+                              __ldg(r + R_P + 9 + dim), v);
       double diff = q[dim] - f;
       acc += diff * diff;
     }
@@ -490,7 +490,7 @@ __device__ __forceinline__ void write_winner(const TableView& T, const ProjParam
     double v = w.v;
 #pragma unroll
     for (int dim = 0; dim < D; ++dim)
-      foot[dim] = decasteljau1(r[12 + dim], r[15 + dim], r[18 + dim], r[21 + dim], v);
+      foot[dim] = decasteljau1(r[R_P + dim], r[R_P + 3 + dim], r[R_P + 6 + dim], r[R_P + 9 + dim], v);
     seg = (int32_t)s;
   } else {
     int64_t s = (int64_t)ord;
@@ -570,7 +570,7 @@ __device__ __forceinline__ void flush_survivors(WarpShared& W, int& head, int ta
       st.noroot++;
     } else {
       const double* r = T.rec + (int64_t)s * REC;
-      double ta = __ldg(r + 24), tb = __ldg(r + 25);
+      double ta = __ldg(r + R_TA), tb = __ldg(r + R_TB);
       if (STATS) {
         double gscale = (hi - lo) * (tb - ta);
         if (co.w3 <= clip_tol) atomicAdd(&W.cnt[owner][C_C3L], 1);
@@ -582,8 +582,8 @@ __device__ __forceinline__ void flush_survivors(WarpShared& W, int& head, int ta
       double acc = 0.0;
 #pragma unroll
       for (int dim = 0; dim < D; ++dim) {
-        double f = decasteljau1(__ldg(r + 12 + dim), __ldg(r + 15 + dim), __ldg(r + 18 + dim),
-                                __ldg(r + 21 + dim), v);
+        double f = decasteljau1(__ldg(r + R_P + dim), __ldg(r + R_P + 3 + dim), __ldg(r + R_P + 6 + dim),
+                                __ldg(r + R_P + 9 + dim), v);
         double diff = W.q[owner][dim] - f;
         acc += diff * diff;
       }
@@ -755,8 +755,8 @@ __device__ __forceinline__ void pieces_step(WarpShared& W, int& head, int& tail,
           double acc = 0.0;
 #pragma unroll
           for (int dim = 0; dim < D; ++dim) {
-            double f = decasteljau1(__ldg(r + 12 + dim), __ldg(r + 15 + dim),
-                                    __ldg(r + 18 + dim), __ldg(r + 21 + dim), v);
+            double f = decasteljau1(__ldg(r + R_P + dim), __ldg(r + R_P + 3 + dim),
+                                    __ldg(r + R_P + 6 + dim), __ldg(r + R_P + 9 + dim), v);
             double diff = q[dim] - f;
             acc += diff * diff;
           }
@@ -1402,6 +1402,209 @@ __global__ void __launch_bounds__(BLOCK) wave_traverse(const __grid_constant__ W
   }
 }
 
+// W1, group mode: one 8-lane group per query, lane c tests child c of the
+// node being expanded (the 8-ary hierarchy maps onto the group: one
+// coalesced 384-B box load per expansion instead of 8 dependent loads).
+// Best-first: a node's kept children are pushed nearest-on-top (each entry
+// carries its box bound, re-tested against the bound current at pop time).
+// Leaves: each lane offers the END seam of its cubic (seam s+1; cubic 0
+// also offers seam 0) -- a seam whose other cubic was pruned lies in that
+// cubic's box, so it cannot reach the tie band -- and the group min-reduces
+// the seam distances into the running bound.  Seams inside the band at
+// that moment become candidates at once (the select passes re-filter with
+// the final minimum), and a kept leaf whose Bernstein bound still reaches
+// the band becomes a (query, cubic) pair.
+constexpr int GSTACK = 64;
+
+template <int D, bool MULTI>
+__device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, bool active,
+                                               unsigned long long* SK, double* SL, int lane) {
+  const int sub = lane & 7;
+  const unsigned gmask = 0xffu << (lane & 24);
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  QStats st{};
+  int64_t qi = active ? (w.perm ? (int64_t)w.perm[g] : g) : 0;
+  int32_t cid = 0;
+  if (MULTI && active) {
+    cid = w.qcurve[qi];
+    if (cid < 0 || cid >= w.ncurves) cid = -1;
+    if (sub == 0) w.gcur[g] = cid;
+    if (cid < 0) {  // out-of-range curve id (sorted last): NaN result, no work
+      if (sub == 0) {
+        w.tkey[g] = ~0ull;
+        w.okey[g] = ~0ull;
+        w.scnt[g] = 0;
+        w.flag[g] = 0;
+      }
+      active = false;
+    }
+  }
+  const TableView& T = MULTI ? w.tabs[cid < 0 ? 0 : cid] : w.tab;
+  double q[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) q[k] = active ? w.q[qi * D + k] : 0.0;
+  double scale = T.hdr[4];
+#pragma unroll
+  for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
+  double dmin = INF;
+  bool fall = false;
+  int sp = 0;
+  if (active) {
+    if (sub == 0) {
+      w.tkey[g] = ~0ull;
+      w.okey[g] = ~0ull;
+      SK[0] = ((unsigned long long)T.top << 40);
+      SL[0] = 0.0;
+    }
+    sp = 1;
+  }
+  __syncwarp(gmask);
+  while (sp > 0) {  // group-uniform control flow
+    --sp;
+    const unsigned long long e = SK[sp];
+    const double elb = SL[sp];
+    __syncwarp(gmask);
+    double c2 = cut2(dmin, scale);
+    if (elb > c2) continue;
+    const int level = (int)(e >> 40);
+    const int64_t idx = (int64_t)(e & 0xffffffffffull);
+    const int64_t ch = idx * FANOUT + sub;
+    const bool ex = ch < T.lvl_cnt[level - 1];
+    double lb = INF;
+    if (ex) {
+      st.boxes++;
+      lb = box_lb2<D>(T, T.lvl_off[level - 1] + ch, q);
+    }
+    bool keep = ex && lb <= c2;
+    if (level == 1) {
+      // leaves: end seams -> bound, band seams -> candidates, pairs
+      double dr = INF, dl = INF, tr = 0.0, tl = 0.0;
+      if (keep) {
+        double pt[D];
+        seam_point<D>(T, ch + 1, pt, tr);
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          double df = q[k] - pt[k];
+          acc += df * df;
+        }
+        dr = sqrt(acc);
+        st.seams++;
+        st.offers++;
+        if (ch == 0) {
+          seam_point<D>(T, 0, pt, tl);
+          acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            double df = q[k] - pt[k];
+            acc += df * df;
+          }
+          dl = sqrt(acc);
+          st.seams++;
+          st.offers++;
+        }
+      }
+      double m = fmin(dr, dl);
+      m = fmin(m, __shfl_xor_sync(gmask, m, 4));
+      m = fmin(m, __shfl_xor_sync(gmask, m, 2));
+      m = fmin(m, __shfl_xor_sync(gmask, m, 1));
+      dmin = fmin(dmin, m);
+      const double lim = dmin + 1e-12;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const bool want = j == 0 ? dr <= lim : dl <= lim;
+        unsigned long long slot = wave_append(&w.cnt[2], want);
+        if (want) {
+          if (slot < w.ccap) {
+            w.cq[slot] = (uint32_t)g;
+            w.ct[slot] = j == 0 ? tr : tl;
+            w.cd[slot] = j == 0 ? dr : dl;
+            w.cv[slot] = -1.0;
+            w.cord[slot] = j == 0 ? (unsigned long long)(ch + 1) : 0ull;
+          } else {
+            fall = true;
+          }
+        }
+      }
+      c2 = cut2(dmin, scale);
+      bool need = keep && lb <= c2 && bern_may_reach<D>(T, ch, q, c2);
+      unsigned long long slot = wave_append(&w.cnt[0], need);
+      if (need) {
+        if (slot < w.pcap) {
+          w.pq[slot] = (uint32_t)g;
+          w.ps[slot] = (uint32_t)ch;
+        } else {
+          fall = true;
+        }
+      }
+      continue;
+    }
+    // push the kept children, nearest on top
+    const unsigned km = (__ballot_sync(gmask, keep) >> (lane & 24)) & 0xffu;
+    int rank = 0;
+#pragma unroll
+    for (int j = 0; j < FANOUT; ++j) {
+      double lj = __shfl_sync(gmask, lb, (lane & 24) | j);
+      rank += ((km >> j) & 1u) && (lj > lb || (lj == lb && j > sub));
+    }
+    if (keep) {
+      SK[sp + rank] = ((unsigned long long)(level - 1) << 40) | (unsigned long long)ch;
+      SL[sp + rank] = lb;
+    }
+    sp += __popc(km);
+    if (sp > GSTACK - FANOUT) {  // cannot happen for top <= 8; stay exact anyway
+      fall = true;
+      sp = 0;
+    }
+    __syncwarp(gmask);
+  }
+  // group totals to the leader lane
+  unsigned long long offers = st.offers;
+  offers += __shfl_xor_sync(gmask, offers, 4);
+  offers += __shfl_xor_sync(gmask, offers, 2);
+  offers += __shfl_xor_sync(gmask, offers, 1);
+  const unsigned fb = __ballot_sync(gmask, fall) & gmask;
+  if (active && sub == 0) {
+    double4 rec;
+    rec.x = q[0];
+    rec.y = q[1];
+    rec.z = D == 3 ? q[D - 1] : 0.0;
+    rec.w = dmin;
+    *(double4*)(w.qs + g * 4) = rec;
+    w.scnt[g] = (int64_t)offers;
+    w.flag[g] = fb ? 1 : 0;
+    if (fb) {
+      unsigned long long slot = atomicAdd(&w.cnt[3], 1ull);
+      w.fb[slot] = g;
+    }
+  }
+  warp_count(w.counters, MREP_CNT_SEAMS, st.seams);
+  warp_count(w.counters, MREP_CNT_BOXES, st.boxes);
+}
+
+template <int D, bool MULTI>
+__global__ void __launch_bounds__(BLOCK) wave_traverse_group(const __grid_constant__ WaveParams w) {
+  __shared__ unsigned long long sk[BLOCK / 8][GSTACK];
+  __shared__ double sl[BLOCK / 8][GSTACK];
+  const int lane = threadIdx.x & 31;
+  const int grp = threadIdx.x >> 3;
+  if (!MULTI) {
+    int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+    traverse_group<D, false>(w, g, g < w.n, sk[grp], sl[grp], lane);
+  } else {
+    for (;;) {  // persistent warps drain 4-query tasks, heaviest curves first
+      unsigned long long task = 0;
+      if (lane == 0) task = atomicAdd(w.queue, 1ull);
+      task = __shfl_sync(0xffffffffu, task, 0);
+      int64_t base = (int64_t)task * 4;
+      if (base >= w.n) break;
+      int64_t g = base + (lane >> 3);
+      traverse_group<D, true>(w, g, g < w.n, sk[grp], sl[grp], lane);
+      __syncwarp();
+    }
+  }
+}
+
 template <int D, bool MULTI>
 __global__ void __launch_bounds__(BLOCK) wave_pairs(const __grid_constant__ WaveParams w) {
   unsigned long long total = *(volatile unsigned long long*)&w.cnt[0];
@@ -1480,13 +1683,13 @@ __global__ void __launch_bounds__(BLOCK) wave_clip(const __grid_constant__ WaveP
       continue;
     }
     const double* r = T.rec + s * REC;
-    double ta = __ldg(r + 24), tb = __ldg(r + 25);
+    double ta = __ldg(r + R_TA), tb = __ldg(r + R_TB);
     double v = lo + co.root * (hi - lo);
     double acc = 0.0;
 #pragma unroll
     for (int dim = 0; dim < D; ++dim) {
-      double f = decasteljau1(__ldg(r + 12 + dim), __ldg(r + 15 + dim), __ldg(r + 18 + dim),
-                              __ldg(r + 21 + dim), v);
+      double f = decasteljau1(__ldg(r + R_P + dim), __ldg(r + R_P + 3 + dim), __ldg(r + R_P + 6 + dim),
+                              __ldg(r + R_P + 9 + dim), v);
       double diff = w.qs[qi * 4 + dim] - f;
       acc += diff * diff;
     }
@@ -1573,7 +1776,7 @@ __global__ void __launch_bounds__(256) wave_emit(const __grid_constant__ WavePar
     double v = w.win_v[g];
 #pragma unroll
     for (int dim = 0; dim < D; ++dim)
-      foot[dim] = decasteljau1(r[12 + dim], r[15 + dim], r[18 + dim], r[21 + dim], v);
+      foot[dim] = decasteljau1(r[R_P + dim], r[R_P + 3 + dim], r[R_P + 6 + dim], r[R_P + 9 + dim], v);
     seg = (int32_t)s;
   } else {
     int64_t s = (int64_t)ord;
@@ -1656,7 +1859,7 @@ __global__ void pack_records_kernel(const double* seg_pts, const double* seg_ta,
     r[3 * 3 + k] = w3;
     double lo = P[0][k], hi = P[0][k];
     for (int j = 0; j < 4; ++j) {
-      r[12 + j * 3 + k] = P[j][k];
+      r[R_P + j * 3 + k] = P[j][k];
       lo = fmin(lo, P[j][k]);
       hi = fmax(hi, P[j][k]);
       amax = fmax(amax, fabs(P[j][k]));
@@ -1664,10 +1867,10 @@ __global__ void pack_records_kernel(const double* seg_pts, const double* seg_ta,
     box0[s * 6 + k] = lo;
     box0[s * 6 + 3 + k] = hi;
   }
-  r[24] = seg_ta[s];
-  r[25] = seg_tb[s];
-  r[26] = seam_t[s + 1];
-  for (int k = 0; k < 3; ++k) r[27 + k] = k < d ? seam_pt[(s + 1) * d + k] : 0.0;
+  r[R_TA] = seg_ta[s];
+  r[R_TB] = seg_tb[s];
+  r[R_ST] = seam_t[s + 1];
+  for (int k = 0; k < 3; ++k) r[R_SP + k] = k < d ? seam_pt[(s + 1) * d + k] : 0.0;
   r[30] = 0.0;
   r[31] = 0.0;
   // header[4]: max |coordinate| (positive doubles order like their bit patterns)
@@ -1914,8 +2117,20 @@ static int launch_project(const ProjParams& p, unsigned flags, cudaStream_t st) 
 }
 
 
+enum { TRAV_PACKET = 0, TRAV_LANE = 1, TRAV_GROUP = 2 };
+
+static int trav_mode(unsigned flags, int64_t n, int64_t S, int top) {
+  if (flags & MREP_PACKET) return TRAV_PACKET;
+  if (flags & MREP_PER_LANE) return top > 7 ? TRAV_PACKET : TRAV_LANE;
+  if (flags & MREP_GROUP) return top > 8 ? TRAV_PACKET : TRAV_GROUP;
+  // packet walks when the queries are dense along the curve (Morton
+  // neighbours share their BVH path); one 8-lane group per query otherwise
+  if (n >= 8 * S || top > 8) return TRAV_PACKET;
+  return TRAV_GROUP;
+}
+
 template <int D, bool MULTI>
-static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, bool packet,
+static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tmode,
                        const TableView* tabs = nullptr, const int32_t* qcurve = nullptr,
                        int64_t ncurves = 0) {
   const int64_t n = p.n;
@@ -1995,17 +2210,25 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, bool p
   const unsigned persist = persist_grid((const void*)wave_select<D, 2>, 256);
   StageTimer tm(timing, st);
   tm.mark();
-  if (MULTI) {
-    // persistent: one resident wave of warps drains the task queue
+  if (tmode == TRAV_GROUP) {
+    if (MULTI) {
+      // persistent: one resident wave of warps drains the task queue
+      unsigned need = grid_for(n * 8, BLOCK);
+      unsigned g = persist_grid((const void*)wave_traverse_group<D, true>, BLOCK);
+      wave_traverse_group<D, true><<<g < need ? g : need, BLOCK, 0, st>>>(w);
+    } else {
+      wave_traverse_group<D, false><<<grid_for(n * 8, BLOCK), BLOCK, 0, st>>>(w);
+    }
+  } else if (MULTI) {
     unsigned need = grid_for(n, BLOCK);
-    if (packet) {
+    if (tmode == TRAV_PACKET) {
       unsigned g = persist_grid((const void*)wave_traverse<D, true, true>, BLOCK);
       wave_traverse<D, true, true><<<g < need ? g : need, BLOCK, 0, st>>>(w);
     } else {
       unsigned g = persist_grid((const void*)wave_traverse<D, true, false>, BLOCK);
       wave_traverse<D, true, false><<<g < need ? g : need, BLOCK, 0, st>>>(w);
     }
-  } else if (packet) {
+  } else if (tmode == TRAV_PACKET) {
     wave_traverse<D, false, true><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
   } else {
     wave_traverse<D, false, false><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
@@ -2085,7 +2308,7 @@ __global__ void set_pack_kernel(const double* seg_pts, const double* seg_ta, con
     r[3 * 3 + k] = w3;
     double blo = P[0][k], bhi = P[0][k];
     for (int j = 0; j < 4; ++j) {
-      r[12 + j * 3 + k] = P[j][k];
+      r[R_P + j * 3 + k] = P[j][k];
       blo = fmin(blo, P[j][k]);
       bhi = fmax(bhi, P[j][k]);
       amax = fmax(amax, fabs(P[j][k]));
@@ -2093,10 +2316,10 @@ __global__ void set_pack_kernel(const double* seg_pts, const double* seg_ta, con
     box0[s * 6 + k] = blo;
     box0[s * 6 + 3 + k] = bhi;
   }
-  r[24] = seg_ta[g];
-  r[25] = seg_tb[g];
-  r[26] = seg_tb[g];  // seam_t[s+1] = seg_tb[s], seam_pt[s+1] = seg_pts[s, 3] (project.py:236-237)
-  for (int k = 0; k < 3; ++k) r[27 + k] = P[3][k];
+  r[R_TA] = seg_ta[g];
+  r[R_TB] = seg_tb[g];
+  r[R_ST] = seg_tb[g];  // seam_t[s+1] = seg_tb[s], seam_pt[s+1] = seg_pts[s, 3] (project.py:236-237)
+  for (int k = 0; k < 3; ++k) r[R_SP + k] = P[3][k];
   r[30] = 0.0;
   r[31] = 0.0;
   atomicMax((unsigned long long*)&hdr[4], (unsigned long long)__double_as_longlong(amax));
@@ -2291,11 +2514,9 @@ static int project_batch_chunk(const CurveSet* cs, const double* queries, const 
   sort_tm.mark();
   sort_tm.finish(0);
   p.perm = i_out;
-  const bool packet = ((flags & MREP_PACKET) ? true
-                       : (flags & MREP_PER_LANE) ? false
-                       : n >= 8 * cs->S_total) || cs->max_top > 7;
-  int rc = d == 3 ? launch_wave<3, true>(p, st, timing, packet, cs->desc, qcurve, cs->nc)
-                  : launch_wave<2, true>(p, st, timing, packet, cs->desc, qcurve, cs->nc);
+  const int tmode = trav_mode(flags, n, cs->S_total, cs->max_top);
+  int rc = d == 3 ? launch_wave<3, true>(p, st, timing, tmode, cs->desc, qcurve, cs->nc)
+                  : launch_wave<2, true>(p, st, timing, tmode, cs->desc, qcurve, cs->nc);
   MREP_CUDA_CHECK(cudaFreeAsync(ws, st));
   return rc;
 }
@@ -2448,14 +2669,10 @@ static int project_chunk(const void* table, int64_t S, int d, const double* quer
   sort_tm.finish(0);
   int rc;
   bool wave = (flags & MREP_SCREEN) && !(flags & MREP_STATS) && !(flags & MREP_FUSED);
-  // packet traversal when the queries are dense along the curve (Morton
-  // neighbours share their BVH path); per-lane walks otherwise
-  const bool packet = (flags & MREP_PACKET) ? true
-                      : (flags & MREP_PER_LANE) ? false
-                      : (n >= 8 * S || p.tab.top > 7);
+  const int tmode = trav_mode(flags, n, S, p.tab.top);
   if (wave)
-    rc = d == 3 ? launch_wave<3, false>(p, st, timing, packet || p.tab.top > 7)
-                : launch_wave<2, false>(p, st, timing, packet || p.tab.top > 7);
+    rc = d == 3 ? launch_wave<3, false>(p, st, timing, tmode)
+                : launch_wave<2, false>(p, st, timing, tmode);
   else rc = d == 3 ? launch_project<3>(p, flags, st) : launch_project<2>(p, flags, st);
   MREP_CUDA_CHECK(cudaFreeAsync(ws, st));
   return rc;

@@ -11,7 +11,7 @@ import bench  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 wl = (bench.CurveSetWorkload if cfg == "cfg3" else bench.SingleCurve)(cfg, 0, 1, 0)
 from paper_2504_11498_b200 import _lib as L  # noqa: E402
-for name, fl in (("packet", L.MREP_PACKET), ("per-lane", L.MREP_PER_LANE)):
+for name, fl in (("packet", L.MREP_PACKET), ("per-lane", L.MREP_PER_LANE), ("group", L.MREP_GROUP)):
     for _ in range(3):
         wl.step(extra_flags=fl)
     torch.cuda.synchronize()

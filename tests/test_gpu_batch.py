@@ -102,7 +102,7 @@ def test_batch_bit_identical_to_single_curve_path(gpu):
     assert np.array_equal(dt.cpu().numpy(), t) and np.array_equal(ds.cpu().numpy(), seg)
     # both traversal schedules (warp packets / per-lane walks) agree bitwise
     from paper_2504_11498_b200 import _lib as L
-    for fl in (L.MREP_PACKET, L.MREP_PER_LANE):
+    for fl in (L.MREP_PACKET, L.MREP_PER_LANE, L.MREP_GROUP):
         r = cs.project_device(torch.from_numpy(q).cuda(), torch.from_numpy(cid).cuda(),
                               extra_flags=fl)
         for k, ref in ((0, t), (1, foot), (2, dist), (4, seg)):

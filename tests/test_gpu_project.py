@@ -53,8 +53,9 @@ def test_wavefront_fused_unsorted_agree(gpu, name):
     c = tab.project(z["queries"], extra_flags=L.MREP_NO_SORT | L.MREP_FUSED)
     d = tab.project(z["queries"], extra_flags=L.MREP_PACKET)
     e = tab.project(z["queries"], extra_flags=L.MREP_PER_LANE)
+    f = tab.project(z["queries"], extra_flags=L.MREP_GROUP)
     for k in (0, 1, 2, 4):
-        for other in (b, c, d, e):
+        for other in (b, c, d, e, f):
             assert np.array_equal(a[k].cpu().numpy(), other[k].cpu().numpy()), k
 
 
