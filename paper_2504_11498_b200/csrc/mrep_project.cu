@@ -61,7 +61,7 @@ struct StageTimer {
     for (int i = 0; i + 1 < n; ++i) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
-      if (first_slot + i < 8) g_stage_ms[first_slot + i] = ms;
+      if (first_slot + i < 8) g_stage_ms[first_slot + i] += ms;  // summed over chunks
     }
   }
   ~StageTimer() {
@@ -1410,15 +1410,68 @@ __global__ void __launch_bounds__(BLOCK) wave_traverse(const __grid_constant__ W
 // Leaves: each lane offers the END seam of its cubic (seam s+1; cubic 0
 // also offers seam 0) -- a seam whose other cubic was pruned lies in that
 // cubic's box, so it cannot reach the tie band -- and the group min-reduces
-// the seam distances into the running bound.  Seams inside the band at
-// that moment become candidates at once (the select passes re-filter with
-// the final minimum), and a kept leaf whose Bernstein bound still reaches
-// the band becomes a (query, cubic) pair.
+// the seam distances into the running bound.  Each lane remembers its two
+// nearest seams; kept leaves are parked in a per-group shared-memory list.
+// Nothing is appended to the global buffers until the warp's four queries
+// are done: then the seams inside each query's final band become
+// candidates and the parked leaves that still pass the final bound (box and
+// Bernstein tests) become (query, cubic) pairs, with one warp-wide atomic
+// per batch of 32 instead of one per group step.  A lane that had to drop a
+// third seam inside the final band sends its query to the exact fallback.
 constexpr int GSTACK = 64;
+constexpr int GPAIRS = 24;  // parked leaves per query (overflow: flushed early)
+
+struct SeamBest {  // a lane's two nearest seams (t re-read at emission)
+  double d1, d2, dropped;
+  int32_t s1, s2;
+};
+
+__device__ __forceinline__ void seam_keep(SeamBest& b, double d, int32_t s) {
+  if (d < b.d1) {
+    b.dropped = fmin(b.dropped, b.d2);
+    b.d2 = b.d1;
+    b.s2 = b.s1;
+    b.d1 = d;
+    b.s1 = s;
+  } else if (d < b.d2) {
+    b.dropped = fmin(b.dropped, b.d2);
+    b.d2 = d;
+    b.s2 = s;
+  } else {
+    b.dropped = fmin(b.dropped, d);
+  }
+}
+
+// emit parked leaves [0, cnt) of a group that pass cut c2 (box + Bernstein)
+template <int D>
+__device__ __forceinline__ void flush_pairs(const WaveParams& w, const TableView& T, int64_t g,
+                                            const double (&q)[D], double c2, const uint32_t* PC,
+                                            const double* PL, int cnt, int rounds, int sub,
+                                            bool& fall) {
+  for (int r = 0; r < rounds; ++r) {
+    const int i = r * 8 + sub;
+    bool need = false;
+    uint32_t ch = 0;
+    if (i < cnt) {
+      ch = PC[i];
+      need = PL[i] <= c2 && bern_may_reach<D>(T, ch, q, c2);
+    }
+    unsigned long long slot = wave_append(&w.cnt[0], need);
+    if (need) {
+      if (slot < w.pcap) {
+        w.pq[slot] = (uint32_t)g;
+        w.ps[slot] = ch;
+      } else {
+        fall = true;
+      }
+    }
+  }
+}
 
 template <int D, bool MULTI>
 __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, bool active,
-                                               unsigned long long* SK, double* SL, int lane) {
+                                               unsigned long long* SK, double* SL, uint32_t* PC,
+                                               double* PL, int lane) {
   const int sub = lane & 7;
   const unsigned gmask = 0xffu << (lane & 24);
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
@@ -1448,7 +1501,8 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
   for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
   double dmin = INF;
   bool fall = false;
-  int sp = 0;
+  SeamBest sb{INF, INF, INF, 0, 0};
+  int sp = 0, npark = 0;
   if (active) {
     if (sub == 0) {
       w.tkey[g] = ~0ull;
@@ -1475,12 +1529,12 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
       st.boxes++;
       lb = box_lb2<D>(T, T.lvl_off[level - 1] + ch, q);
     }
-    bool keep = ex && lb <= c2;
+    const bool keep = ex && lb <= c2;
     if (level == 1) {
-      // leaves: end seams -> bound, band seams -> candidates, pairs
-      double dr = INF, dl = INF, tr = 0.0, tl = 0.0;
+      // leaves: end seams -> bound; kept leaves parked for the final flush
+      double dr = INF;
       if (keep) {
-        double pt[D];
+        double pt[D], tr;
         seam_point<D>(T, ch + 1, pt, tr);
         double acc = 0.0;
 #pragma unroll
@@ -1489,9 +1543,11 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
           acc += df * df;
         }
         dr = sqrt(acc);
+        seam_keep(sb, dr, (int32_t)(ch + 1));
         st.seams++;
         st.offers++;
         if (ch == 0) {
+          double tl;
           seam_point<D>(T, 0, pt, tl);
           acc = 0.0;
 #pragma unroll
@@ -1499,44 +1555,33 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
             double df = q[k] - pt[k];
             acc += df * df;
           }
-          dl = sqrt(acc);
+          double dl = sqrt(acc);
+          dr = fmin(dr, dl);
+          seam_keep(sb, dl, 0);
           st.seams++;
           st.offers++;
         }
       }
-      double m = fmin(dr, dl);
+      double m = dr;
       m = fmin(m, __shfl_xor_sync(gmask, m, 4));
       m = fmin(m, __shfl_xor_sync(gmask, m, 2));
       m = fmin(m, __shfl_xor_sync(gmask, m, 1));
       dmin = fmin(dmin, m);
-      const double lim = dmin + 1e-12;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const bool want = j == 0 ? dr <= lim : dl <= lim;
-        unsigned long long slot = wave_append(&w.cnt[2], want);
-        if (want) {
-          if (slot < w.ccap) {
-            w.cq[slot] = (uint32_t)g;
-            w.ct[slot] = j == 0 ? tr : tl;
-            w.cd[slot] = j == 0 ? dr : dl;
-            w.cv[slot] = -1.0;
-            w.cord[slot] = j == 0 ? (unsigned long long)(ch + 1) : 0ull;
-          } else {
-            fall = true;
-          }
-        }
-      }
       c2 = cut2(dmin, scale);
-      bool need = keep && lb <= c2 && bern_may_reach<D>(T, ch, q, c2);
-      unsigned long long slot = wave_append(&w.cnt[0], need);
-      if (need) {
-        if (slot < w.pcap) {
-          w.pq[slot] = (uint32_t)g;
-          w.ps[slot] = (uint32_t)ch;
-        } else {
-          fall = true;
-        }
+      const bool park = keep && lb <= c2;
+      const unsigned pm = (__ballot_sync(gmask, park) >> (lane & 24)) & 0xffu;
+      if (npark + __popc(pm) > GPAIRS) {  // list full: flush with the current bound
+        flush_pairs<D>(w, T, g, q, c2, PC, PL, npark, (npark + 7) >> 3, sub, fall);
+        __syncwarp(gmask);
+        npark = 0;
       }
+      if (park) {
+        const int at = npark + __popc(pm & ((1u << sub) - 1));
+        PC[at] = (uint32_t)ch;
+        PL[at] = lb;
+      }
+      npark += __popc(pm);
+      __syncwarp(gmask);
       continue;
     }
     // push the kept children, nearest on top
@@ -1558,12 +1603,40 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
     }
     __syncwarp(gmask);
   }
+  // ---- the warp's four queries are done: batched appends (warp converged)
+  __syncwarp();
+  const double c2f = cut2(dmin, scale);
+  const double lim = dmin + 1e-12;
+  // seams inside the final band become candidates
+  if (sb.dropped <= lim) fall = true;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const double d = j == 0 ? sb.d1 : sb.d2;
+    const bool want = active && d <= lim;
+    unsigned long long slot = wave_append(&w.cnt[2], want);
+    if (want) {
+      if (slot < w.ccap) {
+        double pt[D], ts;
+        seam_point<D>(T, j == 0 ? sb.s1 : sb.s2, pt, ts);
+        w.cq[slot] = (uint32_t)g;
+        w.ct[slot] = ts;
+        w.cd[slot] = d;
+        w.cv[slot] = -1.0;
+        w.cord[slot] = (unsigned long long)(j == 0 ? sb.s1 : sb.s2);
+      } else {
+        fall = true;
+      }
+    }
+  }
+  // parked leaves that still pass the final bound become pairs
+  const int rounds = (__reduce_max_sync(0xffffffffu, (unsigned)npark) + 7) >> 3;
+  flush_pairs<D>(w, T, g, q, c2f, PC, PL, npark, rounds, sub, fall);
   // group totals to the leader lane
   unsigned long long offers = st.offers;
-  offers += __shfl_xor_sync(gmask, offers, 4);
-  offers += __shfl_xor_sync(gmask, offers, 2);
-  offers += __shfl_xor_sync(gmask, offers, 1);
-  const unsigned fb = __ballot_sync(gmask, fall) & gmask;
+  offers += __shfl_xor_sync(0xffffffffu, offers, 4);
+  offers += __shfl_xor_sync(0xffffffffu, offers, 2);
+  offers += __shfl_xor_sync(0xffffffffu, offers, 1);
+  const unsigned fb = __ballot_sync(0xffffffffu, fall) & gmask;
   if (active && sub == 0) {
     double4 rec;
     rec.x = q[0];
@@ -1586,21 +1659,27 @@ template <int D, bool MULTI>
 __global__ void __launch_bounds__(BLOCK) wave_traverse_group(const __grid_constant__ WaveParams w) {
   __shared__ unsigned long long sk[BLOCK / 8][GSTACK];
   __shared__ double sl[BLOCK / 8][GSTACK];
+  __shared__ uint32_t pc[BLOCK / 8][GPAIRS];
+  __shared__ double pl[BLOCK / 8][GPAIRS];
   const int lane = threadIdx.x & 31;
   const int grp = threadIdx.x >> 3;
   if (!MULTI) {
     int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
-    traverse_group<D, false>(w, g, g < w.n, sk[grp], sl[grp], lane);
+    traverse_group<D, false>(w, g, g < w.n, sk[grp], sl[grp], pc[grp], pl[grp], lane);
   } else {
-    for (;;) {  // persistent warps drain 4-query tasks, heaviest curves first
-      unsigned long long task = 0;
-      if (lane == 0) task = atomicAdd(w.queue, 1ull);
-      task = __shfl_sync(0xffffffffu, task, 0);
+    // persistent warps drain 4-query tasks, heaviest curves first; the next
+    // task index is fetched while the current one runs
+    unsigned long long task = 0;
+    if (lane == 0) task = atomicAdd(w.queue, 1ull);
+    task = __shfl_sync(0xffffffffu, task, 0);
+    for (;;) {
       int64_t base = (int64_t)task * 4;
       if (base >= w.n) break;
+      unsigned long long next = 0;
+      if (lane == 0) next = atomicAdd(w.queue, 1ull);
       int64_t g = base + (lane >> 3);
-      traverse_group<D, true>(w, g, g < w.n, sk[grp], sl[grp], lane);
-      __syncwarp();
+      traverse_group<D, true>(w, g, g < w.n, sk[grp], sl[grp], pc[grp], pl[grp], lane);
+      task = __shfl_sync(0xffffffffu, next, 0);
     }
   }
 }
@@ -2587,6 +2666,8 @@ int mrep_project(const void* table, int64_t S, int d, const double* queries, int
                  int32_t* out_seg, int64_t* out_stats, double* out_sound, uint64_t* counters,
                  void* stream) {
   const int64_t CHUNK_Q = (int64_t)1 << 23;
+  if (flags & MREP_TIMING)
+    for (double& v : g_stage_ms) v = 0.0;
   if (n <= CHUNK_Q)
     return project_chunk(table, S, d, queries, n, clip_tol, max_iter, soundness_samples, flags,
                          out_t, out_foot, out_dist, out_cand, out_seg, out_stats, out_sound,
@@ -2785,6 +2866,8 @@ int mrep_project_batch(const void* set, const double* queries, const int32_t* cu
   }
   const int64_t CHUNK_Q = (int64_t)1 << 23;
   const int d = cs->d;
+  if (flags & MREP_TIMING)
+    for (double& v : g_stage_ms) v = 0.0;
   for (int64_t lo = 0; lo < n; lo += CHUNK_Q) {
     int64_t m = n - lo < CHUNK_Q ? n - lo : CHUNK_Q;
     int rc = project_batch_chunk(cs, queries + lo * d, curve_ids + lo, m, clip_tol, max_iter, flags,
