@@ -168,6 +168,42 @@ MREP_API int mrep_project_batch_host(const void* set, const double* queries_host
                                      int64_t* out_cand_host, int32_t* out_seg_host,
                                      uint64_t* counters_host);
 
+/* ---------------------------------------------------------------------
+ * Surfaces (BASELINE.json configs[3]).  The reference has no surface code
+ * (SPEC.md:15, 98, 497); this extends its curve path per SURVEY.md 8(c):
+ * tensor-product Bezier patches from the per-direction span matrices of
+ * decompose.py:19-46, and per-patch seeded projected Newton (the local
+ * refinement of oracle.py:95-128).  Parity is pinned to the C oracle
+ * oracle/mrep_surface_oracle.c (same algorithm) and to a dense-grid search.
+ * Supported degree pairs: (p, p) for p = 1..5, (3, 5) and (5, 3).
+ * patch_pts [nus*nvs][pu+1][pv+1][3] row-major over the span grid (patch
+ * i * nvs + j), patch_iv [nus*nvs][4] = (u0, u1, v0, v1).
+ * ------------------------------------------------------------------- */
+MREP_API int64_t mrep_surface_table_bytes(int64_t npatch, int pu, int pv);
+MREP_API int mrep_surface_table_pack(const double* patch_pts_dev, const double* patch_iv_dev,
+                                     int64_t nus, int64_t nvs, int pu, int pv, void* table_dev,
+                                     void* stream);
+/* Closest point on the surface for each of n 3-D queries: global (u, v),
+ * foot [n][3], distance, patch id (i * nvs + j; ties inside dmin + 1e-12 go
+ * to the smallest patch id).  out_patch and counters may be NULL. */
+MREP_API int mrep_project_surface(const void* table_dev, int64_t npatch, int pu, int pv,
+                                  const double* queries_dev, int64_t n, unsigned flags,
+                                  double* out_u_dev, double* out_v_dev, double* out_foot_dev,
+                                  double* out_dist_dev, int32_t* out_patch_dev,
+                                  uint64_t* counters_dev, void* stream);
+/* Same from HOST buffers (chunked H2D / kernel / D2H pipeline, synchronous). */
+MREP_API int mrep_project_surface_host(const void* table_dev, int64_t npatch, int pu, int pv,
+                                       const double* queries_host, int64_t n, unsigned flags,
+                                       double* out_u_host, double* out_v_host,
+                                       double* out_foot_host, double* out_dist_host,
+                                       int32_t* out_patch_host, uint64_t* counters_host);
+
+/* Surface points by tensor Cox-de Boor: uv [n][2] -> out [n][3]; ctrl [nu][nv][3]. */
+MREP_API int mrep_eval_surface(int pu, int pv, const double* knots_u_dev, int64_t mu,
+                               const double* knots_v_dev, int64_t mv, const double* ctrl_dev,
+                               int64_t nu, int64_t nv, const double* uv_dev, int64_t n,
+                               double* out_dev, void* stream);
+
 /* Synthetic-input helper, host only (no GPU): the reference fixture
  * generator's momentum walk (_fixtures.py _walk_points) for n points, given
  * v0 (already unit length) and the n-1 normal draws g [n-1][d]; writes the

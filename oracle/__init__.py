@@ -5,6 +5,10 @@ Two restatements of the reference (`/root/reference/pkg/src/splinemat`):
 * ``mrep_oracle.c`` (loaded here through ctypes): the numba per-query kernels
   of ``_kernels.py``, bit-for-bit on the same libm, multi-threaded with OpenMP
   the way ``project.py:266-281`` fans out over threads.
+* ``mrep_surface_oracle.c``: the surface projection (the reference has none;
+  this file defines the algorithm the GPU implements, brute force over every
+  patch) and ``surface.py``: numpy surface decomposition + a dense-grid
+  global search that checks the minimiser is global.
 * ``prep.py``: the numpy preprocessing of ``basis.py`` / ``decompose.py`` /
   ``reduce_approx.py`` (decomposition and error-controlled cubic
   approximation), same numpy expressions, so it matches the reference
@@ -39,8 +43,9 @@ def build():
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB_PATH) or (
-                os.path.getmtime(_LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "mrep_oracle.c"))):
+        srcs = [os.path.join(_HERE, f) for f in ("mrep_oracle.c", "mrep_surface_oracle.c")]
+        if not os.path.exists(_LIB_PATH) or any(
+                os.path.getmtime(_LIB_PATH) < os.path.getmtime(f) for f in srcs):
             build()
         L = ctypes.CDLL(_LIB_PATH)
         L.oracle_quartic_roots_01.argtypes = [_dp, _dp]
@@ -61,6 +66,11 @@ def lib():
             _dp, _dp, _dp, _i64p, _i64p, _dp, _i64p, _i32p]
         L.oracle_quartic_block.argtypes = [_dp, ctypes.c_int64, _dp, _i64p]
         L.oracle_newton_quartic_block.argtypes = [_dp, ctypes.c_int64, _dp, _i64p]
+        L.oracle_surf_patch_min.argtypes = [_dp, ctypes.c_int, ctypes.c_int, _dp, _dp, _dp, _dp,
+                                            ctypes.POINTER(ctypes.c_int)]
+        L.oracle_surface_project.argtypes = [_dp, _dp, ctypes.c_int64, ctypes.c_int,
+                                             ctypes.c_int, _dp, ctypes.c_int64, ctypes.c_int,
+                                             _dp, _dp, _dp, _dp, _i32p]
         _lib = L
     return _lib
 
@@ -163,3 +173,30 @@ def project_block(seg_pts, seg_ta, seg_tb, seam_t, seam_pt, queries, clip_tol=1e
         _p(out["stats"], _i64p), _p(out["sound"]), _p(out["win"], _i64p),
         _p(out["seg"], _i32p))
     return out
+
+
+def surface_project(patch_pts, patch_iv, pu, pv, queries, workers=1):
+    """Brute-force surface projection (mrep_surface_oracle.c): patch_pts
+    [np][pu+1][pv+1][3] and patch_iv [np][4] in patch-id order.
+    Returns dict(u, v, foot, dist, patch)."""
+    P = _f64(patch_pts).reshape(-1)
+    I = _f64(patch_iv).reshape(-1)
+    q = _f64(np.atleast_2d(queries))
+    npat = P.size // ((pu + 1) * (pv + 1) * 3)
+    n = q.shape[0]
+    out = dict(u=np.empty(n), v=np.empty(n), foot=np.empty((n, 3)), dist=np.empty(n),
+               patch=np.empty(n, dtype=np.int32))
+    lib().oracle_surface_project(_p(P), _p(I), npat, pu, pv, _p(q), n, int(workers),
+                                 _p(out["u"]), _p(out["v"]), _p(out["foot"]), _p(out["dist"]),
+                                 _p(out["patch"], _i32p))
+    return out
+
+
+def surf_patch_min(P, pu, pv, q):
+    """(u, v, d2, iters) of one patch (local parameters)."""
+    P = _f64(P).reshape(-1)
+    q = _f64(q)
+    u, v, d2, it = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+    lib().oracle_surf_patch_min(_p(P), pu, pv, _p(q), ctypes.byref(u), ctypes.byref(v),
+                                ctypes.byref(d2), ctypes.byref(it))
+    return u.value, v.value, d2.value, it.value

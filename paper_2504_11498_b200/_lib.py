@@ -65,6 +65,14 @@ _SIGS = {
                             _vp], _i32),
     "mrep_project_batch_host": ([_vp, _vp, _vp, _i64, _dbl, _i32, _u32, _vp, _vp, _vp, _vp, _vp,
                                  _vp], _i32),
+    "mrep_surface_table_bytes": ([_i64, _i32, _i32], _i64),
+    "mrep_surface_table_pack": ([_vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp], _i32),
+    "mrep_project_surface": ([_vp, _i64, _i32, _i32, _vp, _i64, _u32, _vp, _vp, _vp, _vp, _vp,
+                              _vp, _vp], _i32),
+    "mrep_project_surface_host": ([_vp, _i64, _i32, _i32, _vp, _i64, _u32, _vp, _vp, _vp, _vp,
+                                   _vp, _vp], _i32),
+    "mrep_eval_surface": ([_i32, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _vp],
+                          _i32),
     "mrep_synth_walk": ([_vp, _vp, _i64, _i32, _vp], _i32),
     "mrep_knot_span": ([_vp, _i64, _i32, _vp, _i64, _vp, _vp], _i32),
     "mrep_quartic_roots": ([_vp, _i64, _vp, _vp, _vp], _i32),

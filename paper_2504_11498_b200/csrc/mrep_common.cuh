@@ -12,6 +12,38 @@ namespace mrep {
 
 void set_error(const std::string& msg);
 
+// Per-stage device times of the last MREP_TIMING call on this host thread (ms):
+// [0] morton+sort [1] traverse [2] pairs [3] clip [4] select [5] fallback
+extern thread_local double g_stage_ms[8];
+
+struct StageTimer {
+  cudaEvent_t ev[8];
+  int n = 0;
+  bool on = false;
+  cudaStream_t st;
+  StageTimer(bool enable, cudaStream_t s) : on(enable), st(s) {
+    if (on)
+      for (auto& e : ev) cudaEventCreate(&e);
+  }
+  void mark() {
+    if (on && n < 8) cudaEventRecord(ev[n++], st);
+  }
+  void finish(int first_slot) {
+    if (!on) return;
+    cudaEventSynchronize(ev[n - 1]);
+    for (int i = 0; i + 1 < n; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      if (first_slot + i < 8) g_stage_ms[first_slot + i] += ms;  // summed over chunks
+    }
+  }
+  ~StageTimer() {
+    if (on)
+      for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
+
 #define MREP_CUDA_CHECK(expr)                                                        \
   do {                                                                               \
     cudaError_t _e = (expr);                                                         \
@@ -59,7 +91,7 @@ struct TableLayout {
   int64_t total_doubles;
 };
 
-inline TableLayout table_layout(int64_t S) {
+inline TableLayout table_layout(int64_t S, int rec = REC) {
   TableLayout L{};
   L.S = S;
   int64_t cnt = S, off = 0;
@@ -75,7 +107,7 @@ inline TableLayout table_layout(int64_t S) {
   L.top = lv;
   L.total_boxes = off;
   L.rec_off = HDR;
-  L.box_off = HDR + S * REC;
+  L.box_off = HDR + S * rec;
   L.total_doubles = L.box_off + off * 6;
   return L;
 }
@@ -90,8 +122,8 @@ struct TableView {
   int64_t lvl_cnt[MAX_LEVELS];
 };
 
-inline TableView table_view(const void* table, int64_t S) {
-  TableLayout L = table_layout(S);
+inline TableView table_view(const void* table, int64_t S, int rec = REC) {
+  TableLayout L = table_layout(S, rec);
   TableView v{};
   const double* base = static_cast<const double*>(table);
   v.hdr = base;

@@ -214,6 +214,27 @@ extern "C" int mrep_project_batch_host(const void* set, const double* queries,
                        });
 }
 
+// Surfaces: the same pipeline; the slot's 8-byte candidate-count buffer
+// carries v (u rides in t, the patch id in the segment buffer).
+extern "C" int mrep_project_surface_host(const void* table, int64_t npatch, int pu, int pv,
+                                         const double* queries, int64_t n, unsigned flags,
+                                         double* out_u, double* out_v, double* out_foot,
+                                         double* out_dist, int32_t* out_patch,
+                                         uint64_t* counters_host) {
+  if (!table || npatch < 1 || n < 0) {
+    set_error("mrep_project_surface_host: bad arguments");
+    return MREP_ERR_ARG;
+  }
+  if (n == 0) return MREP_OK;
+  std::lock_guard<std::mutex> lock(g_ctx.mu);
+  return host_pipeline(3, queries, nullptr, n, out_u, out_foot, out_dist, (int64_t*)out_v,
+                       out_patch, counters_host, [&](Slot& s) {
+                         return mrep_project_surface(table, npatch, pu, pv, s.dq, s.cnt, flags,
+                                                     s.dt, (double*)s.dcand, s.dfoot, s.ddist,
+                                                     s.dseg, s.dcnt, s.st);
+                       });
+}
+
 // ---------------------------------------------------------------------------
 // Host-array entry points: what a ctypes / cffi binding in the reference
 // binds without any GPU framework.

@@ -33,42 +33,14 @@
 
 #include "mrep_common.cuh"
 #include "mrep_math.cuh"
+#include "mrep_screen.cuh"
 
 namespace mrep {
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 
-// Per-stage device times of the last MREP_TIMING call on this host thread (ms):
-// [0] morton+sort [1] traverse [2] pairs [3] clip [4] select [5] fallback
-static thread_local double g_stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-
-struct StageTimer {
-  cudaEvent_t ev[8];
-  int n = 0;
-  bool on = false;
-  cudaStream_t st;
-  StageTimer(bool enable, cudaStream_t s) : on(enable), st(s) {
-    if (on)
-      for (auto& e : ev) cudaEventCreate(&e);
-  }
-  void mark() {
-    if (on && n < 8) cudaEventRecord(ev[n++], st);
-  }
-  void finish(int first_slot) {
-    if (!on) return;
-    cudaEventSynchronize(ev[n - 1]);
-    for (int i = 0; i + 1 < n; ++i) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
-      if (first_slot + i < 8) g_stage_ms[first_slot + i] += ms;  // summed over chunks
-    }
-  }
-  ~StageTimer() {
-    if (on)
-      for (auto& e : ev) cudaEventDestroy(e);
-  }
-};
+thread_local double g_stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
 // Keep stream-ordered allocations cached in the device's default pool: the
 // projection workspace is re-requested on every call, and releasing it at each
@@ -333,25 +305,7 @@ __device__ __forceinline__ void solve_segment(const TableView& T, int64_t s, con
 }
 
 // ------------------------------------------------------------ screening
-template <int D>
-__device__ __forceinline__ double box_lb2(const TableView& T, int64_t box, const double (&q)[D]) {
-  const double* b = T.box + box * 6;
-  double acc = 0.0;
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    double g = fmax(0.0, fmax(__ldg(b + k) - q[k], q[k] - __ldg(b + 3 + k)));
-    acc += g * g;
-  }
-  return acc;
-}
 
-// Cut-off radius: a box whose lower bound exceeds it cannot hold a candidate
-// inside dmin + 1e-12 (margins cover rounding of the box bound and of the
-// foot-point evaluation; they only ever keep extra work).
-__device__ __forceinline__ double cut2(double dmin, double scale) {
-  double c = dmin * (1.0 + 1e-7) + 1e-11 + 1e-13 * scale;
-  return c * c;
-}
 
 template <int D>
 __device__ __forceinline__ uint32_t child_mask(const TableView& T, int level, int64_t idx,
@@ -457,17 +411,6 @@ __device__ void gen_dense(const TableView& T, const double (&q)[D], double clip_
     solve_segment<D, STATS>(T, s, q, clip_tol, max_iter, soundness, B, st);
 }
 
-__device__ __forceinline__ void warp_count(uint64_t* counters, int slot, uint64_t v) {
-  if (!counters) return;
-  unsigned lo = (unsigned)(v & 0xffffffffu), hi = (unsigned)(v >> 32);
-  unsigned mask = __activemask();
-  unsigned slo = __reduce_add_sync(mask, lo);
-  unsigned shi = __reduce_add_sync(mask, hi);
-  int leader = __ffs(mask) - 1;
-  if ((threadIdx.x & 31) == leader)
-    atomicAdd((unsigned long long*)&counters[slot], (unsigned long long)slo +
-                                                        ((unsigned long long)shi << 32));
-}
 
 template <int D>
 __device__ __forceinline__ void write_winner(const TableView& T, const ProjParams& p, int64_t qi,
@@ -1090,23 +1033,7 @@ __device__ __forceinline__ const TableView& tab_of(const WaveParams& w, int64_t 
   return w.tab;
 }
 
-// warp-aggregated slot allocation (works in divergent code)
-__device__ __forceinline__ unsigned long long wave_append(unsigned long long* counter, bool want) {
-  unsigned act = __activemask();
-  unsigned bal = __ballot_sync(act, want);
-  if (!bal) return ~0ull;
-  int leader = __ffs(bal) - 1;
-  unsigned long long base = 0;
-  if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(counter, (unsigned long long)__popc(bal));
-  base = __shfl_sync(act, base, leader);
-  return want ? base + __popc(bal & ((1u << (threadIdx.x & 31)) - 1)) : ~0ull;
-}
 
-__device__ __forceinline__ unsigned long long tkey_of(double t) {
-  if (t == 0.0) t = 0.0;  // -0.0 and +0.0 compare equal in the reference
-  unsigned long long b = (unsigned long long)__double_as_longlong(t);
-  return (b >> 63) ? ~b : (b | (1ull << 63));
-}
 
 // every per-query array below is indexed by the SORTED position g; only the
 // final emit kernel touches the caller's order (one scattered write pass).
