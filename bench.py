@@ -63,6 +63,15 @@ CONFIGS = {
                  curves=10_000, per_curve=100,
                  desc="cfg3: 1e6 random points/GPU, 100 per curve, onto a batch of 1e4 "
                       "B-splines (degree 3-9, 8-2048 ctrl pts, log-uniform), one batched call"),
+    # configs[3]: 1e6 points onto a 64x64-net surface, bicubic and degree 5
+    "cfg4": dict(degree=3, ctrl="64x64", n=1_000_000, queries="uniform", scaling="weak",
+                 surface=True,
+                 desc="cfg4: 1e6 random points/GPU onto a bicubic B-spline surface, 64x64 "
+                      "control net (3721 Bezier patches)"),
+    "cfg4q": dict(degree=5, ctrl="64x64", n=1_000_000, queries="uniform", scaling="weak",
+                  surface=True,
+                  desc="cfg4 (degree 5): 1e6 random points/GPU onto a biquintic B-spline "
+                       "surface, 64x64 control net (3481 Bezier patches)"),
     # configs[4]: 1e8 points onto 1e5 cubics, query-sharded (strong scaling)
     "cfg5": dict(degree=3, ctrl=100_003, n=100_000_000, queries="uniform", scaling="strong",
                  desc="cfg5: 1e8 random points onto a degree-3 B-spline with 100003 ctrl pts "
@@ -76,7 +85,9 @@ def workload_config(cfg, n):
             "control_points": c["ctrl"], "tolerance": 1e-4, "clip_tol": 1e-6,
             "max_iterations": 8, "dim": 3, "queries": c["queries"],
             "l2": "flushed (256 MB write) before each timed step",
-            "mode": "BVH-screened exact solve (t/dist/segment identical to brute force)"}
+            "mode": ("BVH-screened per-patch seeded projected Newton (equal to the brute-force "
+                     "surface oracle)" if c.get("surface") else
+                     "BVH-screened exact solve (t/dist/segment identical to brute force)")}
 
 
 def make_curve(cfg="cfg2"):
@@ -156,15 +167,29 @@ class ClockSampler:
 
 def cpu_time(jobs, workers):
     """The reference kernel restated in C (oracle/), all host cores, over a
-    list of (seg arrays, queries) jobs; returns (queries, seconds)."""
+    list of (seg arrays, queries) jobs; returns (queries, seconds).  Surface
+    jobs run the surface oracle (brute force over every patch)."""
     import oracle
-    seg, q = jobs[0]
-    oracle.project_block(*seg, q[: min(200, len(q))], workers=workers)  # warm
+
+    def run(job, q):
+        if isinstance(job, str) and job == "surface":
+            prep, qq = q
+            pu, pv = prep.surface.degree_u, prep.surface.degree_v
+            oracle.surface_project(prep.patch_pts.reshape(-1, pu + 1, pv + 1, 3),
+                                   prep.patch_iv.reshape(-1, 4), pu, pv, qq, workers=workers)
+            return len(qq)
+        oracle.project_block(*job, q, workers=workers)
+        return len(q)
+
+    job, q = jobs[0]
+    if isinstance(job, str):
+        run(job, (q[0], q[1][:16]))
+    else:
+        run(job, q[: min(200, len(q))])  # warm
     t0 = time.perf_counter()
     nq = 0
-    for seg, q in jobs:
-        oracle.project_block(*seg, q, workers=workers)
-        nq += len(q)
+    for job, q in jobs:
+        nq += run(job, q)
     return nq, time.perf_counter() - t0
 
 
@@ -270,13 +295,81 @@ class CurveSetWorkload:
         return jobs, desc
 
 
+class SurfaceWorkload:
+    """cfg4: one prepared surface (64 x 64 net), the rank's 1e6 queries."""
+
+    def __init__(self, cfg, rank, world, n_override):
+        import torch
+        from paper_2504_11498_b200 import prepare_surface
+        from paper_2504_11498_b200.fixtures import random_surface
+        c = CONFIGS[cfg]
+        p = c["degree"]
+        self.surface = random_surface(np.random.default_rng(0), p, p, 64, 64)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        self.prep = prepare_surface(self.surface)
+        torch.cuda.synchronize()
+        self.prep_ms = (time.perf_counter() - t0) * 1e3
+        self.tab = self.prep.table
+        self.n = n_override or c["n"]
+        self.n_total = world * self.n
+        self.q_host = np.random.default_rng(1 + rank).uniform(0.0, 1.0, (self.n, 3))
+        self.q = torch.from_numpy(self.q_host).cuda()
+        self.num_segments = self.prep.num_patches
+        self.h2d = self.n * 24
+        self.p = p
+
+    def step(self, counters=None, extra_flags=0, dense=False):
+        return self.tab.project(self.q, counters=counters, extra_flags=extra_flags)
+
+    def pinned(self):
+        import torch
+        self.q_pin = torch.from_numpy(self.q_host).pin_memory().numpy()
+
+    def host(self, out, dense=False):
+        u, foot, dist, cand, seg = out
+        # (u, v, foot, dist, patch): v rides in the int64 buffer's bytes
+        self.tab.project_host(self.q_pin, out=(u, cand.view(np.float64), foot, dist, seg))
+
+    def cpu_jobs(self, sample):
+        sample = max(64, min(sample, 2048))
+        desc = (f"first {sample} of the {self.n} queries, brute force over all "
+                f"{self.num_segments} patches (mrep_surface_oracle.c)")
+        return [("surface", (self.prep, self.q_host[:sample]))], desc
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
     import oracle
     from oracle import prep as P
     cores = len(os.sched_getaffinity(0))
-    if args.config == "cfg3":
+    if CONFIGS[args.config].get("surface"):
+        from oracle import surface as OS
+        from paper_2504_11498_b200.fixtures import random_surface
+        pp = CONFIGS[args.config]["degree"]
+        sf = random_surface(np.random.default_rng(0), pp, pp, 64, 64)
+        pts, iv = OS.decompose(pp, pp, sf.knots_u.knots, sf.knots_v.knots, sf.control_points)
+        sample = max(64, min(args.ref_sample // 16, 2048))
+        q = np.random.default_rng(1).uniform(0.0, 1.0, (sample, 3))
+        P = pts.reshape(-1, pp + 1, pp + 1, 3)
+        I = iv.reshape(-1, 4)
+
+        def run_one(qq):
+            oracle.surface_project(P, I, pp, pp, qq, workers=cores)
+
+        desc = (f"{sample} of the {args.config} queries per step, brute force over all {len(P)} "
+                f"patches (mrep_surface_oracle.c: the reference has no surface code, this CPU "
+                f"oracle defines the algorithm)")
+        for _ in range(args.warmup):
+            run_one(q[:32])
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            run_one(q)
+            times.append(time.perf_counter() - t0)
+        jobs = None
+    elif args.config == "cfg3":
         from paper_2504_11498_b200.fixtures import mixed_curve_batch
         c = CONFIGS["cfg3"]
         curves = mixed_curve_batch(c["curves"])
@@ -309,15 +402,16 @@ def run_reference(args, rank):
             q = make_queries(args.config, 0, sample)
         jobs = [(seg, q)]
         desc = f"{sample} of the {args.config} queries per step, brute force over all {S} cubics"
-    for _ in range(args.warmup):
-        for seg, q in jobs:
-            oracle.project_block(*seg, q[: max(100, len(q) // 10)], workers=cores)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        for seg, q in jobs:
-            oracle.project_block(*seg, q, workers=cores)
-        times.append(time.perf_counter() - t0)
+    if jobs is not None:
+        for _ in range(args.warmup):
+            for seg, q in jobs:
+                oracle.project_block(*seg, q[: max(100, len(q) // 10)], workers=cores)
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            for seg, q in jobs:
+                oracle.project_block(*seg, q, workers=cores)
+            times.append(time.perf_counter() - t0)
     ms = statistics.mean(times) * 1e3
     value = sample / (ms / 1e3)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -327,8 +421,9 @@ def run_reference(args, rank):
             "data": "synthetic", "config": workload_config(args.config, CONFIGS[args.config]["n"]),
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": desc + " (C restatement of _kernels._project_block, "
-                                              f"bit-exact vs the reference), {cores} threads"},
+                             "sample": desc + (f", {cores} threads" if jobs is None else
+                                               " (C restatement of _kernels._project_block, "
+                                               f"bit-exact vs the reference), {cores} threads")},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -366,8 +461,9 @@ def main():
     from paper_2504_11498_b200 import _lib as L
 
     cfg = CONFIGS[args.config]
-    wl = (CurveSetWorkload if args.config == "cfg3" else SingleCurve)(args.config, rank, world,
-                                                                     args.n)
+    surf = CONFIGS[args.config].get("surface", False)
+    wl = (CurveSetWorkload if args.config == "cfg3" else SurfaceWorkload if surf
+          else SingleCurve)(args.config, rank, world, args.n)
     n, n_total = wl.n, wl.n_total
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -380,7 +476,10 @@ def main():
         # the single exchange of the path: (t, distance, segment id) to rank 0
         if world == 1:
             return
-        gather_results(pack_results(out[0], out[2], out[4]), n_total, world, rank)
+        if surf:  # (u, v, foot, dist, patch): gather (u, dist, patch id)
+            gather_results(pack_results(out[0], out[3], out[4]), n_total, world, rank)
+        else:
+            gather_results(pack_results(out[0], out[2], out[4]), n_total, world, rank)
 
     for _ in range(args.warmup):
         gather(wl.step(dense=dense))
@@ -419,6 +518,8 @@ def main():
     # (histogram, exclusive sum, onesweep passes) + 8 wavefront kernels; dense: 2
     passes = (30 + (14 if args.config == "cfg3" else 0) + 7) // 8
     launches_per_step = 1 + 2 + passes + (8 if not dense else 2)
+    if surf:  # morton + sort + traverse, solve, select x2, fallback
+        launches_per_step = 1 + 2 + passes + 5
     launches_per_step *= max(1, -(-n // (1 << 23)))
 
     # ---- roofline: per-stage device times (CUDA events between the pipeline's
@@ -439,6 +540,16 @@ def main():
     names = ["morton_sort", "traverse", "pairs", "clip", "select", "fallback"]
     work = {"traverse": F_BOX * c[L.CNT_BOXES] + F_SEAM * c[L.CNT_SEAMS],
             "pairs": F_PAIR * c[L.CNT_PAIRS], "clip": F_CLIP * c[L.CNT_SURVIVORS]}
+    if surf:
+        # per (query, patch) solve: (p+1)^2 seed evaluations + per Newton
+        # iteration one jet and one line-search evaluation
+        pp = wl.p
+        f_s0 = 2 * 3 * (pp + 1) ** 2 + 12 * pp
+        f_sj = 6 * 3 * (pp + 1) ** 2 + 40 * pp + 40
+        names = ["morton_sort", "traverse", "solve", "clip", "select", "fallback"]
+        work = {"traverse": F_BOX * c[L.CNT_BOXES] + 30.0 * c[L.CNT_SEAMS],
+                "solve": c[L.CNT_PAIRS] * (pp + 1) ** 2 * f_s0
+                + c[L.CNT_CLIP_ITERS] * (f_sj + f_s0)}
     stages = {}
     for i, nm in enumerate(names):
         ms_i = float(stage[i])
@@ -448,7 +559,8 @@ def main():
             ent["frac"] = ent["tflops"] / peak.value
         stages[nm] = ent
     flops = sum(work.values())
-    dom = max(("traverse", "pairs", "clip"), key=lambda k: stages[k]["ms"]) if not dense else None
+    dom = max((k for k in ("traverse", "pairs", "solve", "clip") if k in stages),
+              key=lambda k: stages[k]["ms"]) if not dense else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof) and dom:
@@ -461,19 +573,28 @@ def main():
         except Exception:
             traffic = None
     achieved = stages[dom]["tflops"] if dom else flops / (kms / 1e3) / 1e12
-    roofline = {"bound": "fp64", "kernel": f"wave_{dom}" if dom else "project_kernel (dense)",
+    kname = (f"surf_{dom}" if surf else f"wave_{dom}") if dom else "project_kernel (dense)"
+    roofline = {"bound": "fp64", "kernel": kname,
                 "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                 "frac": achieved / peak.value, "traffic": traffic,
                 "peak_source": "DFMA microbenchmark measured in this run (mrep_fp64_peak); "
                                "MEASURED_PEAKS.json has no FP64 figure",
-                "flop_model": "500/pair + 650/clipped survivor + 10/seam + 10/box test "
-                              "(SURVEY.md 8(d); counts from the kernels' own counters)",
+                "flop_model": ("surface: (p+1)^2 seeds x (6(p+1)^2 + 12p) + Newton iterations x "
+                               "(24(p+1)^2 + 52p + 40) per pair, 30/upper-bound point, 10/box "
+                               "test (DESIGN.md 3b)" if surf else
+                               "500/pair + 650/clipped survivor + 10/seam + 10/box test "
+                               "(SURVEY.md 8(d); counts from the kernels' own counters)"),
                 "stages": stages,
                 "pipeline": {"ms": kms, "tflops": flops / (kms / 1e3) / 1e12,
                              "frac": flops / (kms / 1e3) / 1e12 / peak.value},
                 "per_query": {"pairs": c[L.CNT_PAIRS] / n, "survivors": c[L.CNT_SURVIVORS] / n,
                               "seams": c[L.CNT_SEAMS] / n, "box_tests": c[L.CNT_BOXES] / n}}
-    if args.config != "cfg3":
+    if surf:
+        roofline["per_query"] = {"patch_solves": c[L.CNT_PAIRS] / n,
+                                 "newton_iters": c[L.CNT_CLIP_ITERS] / n,
+                                 "bound_points": c[L.CNT_SEAMS] / n,
+                                 "box_tests": c[L.CNT_BOXES] / n}
+    elif args.config != "cfg3":
         roofline["dense_equivalent_tflops"] = ((F_PAIR * wl.num_segments
                                                + F_SEAM * (wl.num_segments + 1)) * n
                                                / (kms / 1e3) / 1e12)
@@ -503,7 +624,8 @@ def main():
         e2e_s = float(tt.item())
     e2e = {"value": n_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": wl.h2d,
            "d2h_bytes_per_step": n * (8 + 24 + 8 + 8 + 4),
-           "path": ("mrep_project_batch_host" if args.config == "cfg3" else "mrep_project_host")
+           "path": ("mrep_project_batch_host" if args.config == "cfg3" else
+                    "mrep_project_surface_host" if surf else "mrep_project_host")
            + " (C ABI, pinned host buffers, 2-stream chunked pipeline)"}
 
     if rank == 0:
