@@ -639,6 +639,9 @@ def main():
                              f"_kernels._project_block, bit-exact vs the reference"}
         conf = dict(workload_config(args.config, n), parallelism=f"query-shard x{world}",
                     prep_ms=wl.prep_ms, cubics=wl.num_segments)
+        sm_sorted = sorted(step_ms)
+        conf["step_ms"] = {"median": statistics.median(step_ms), "min": sm_sorted[0],
+                           "max": sm_sorted[-1]}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None,

@@ -44,22 +44,48 @@ int ensure_pool();
 
 // ---------------------------------------------------------------- layout
 // Header (HDR doubles): [0] pu [1] pv [2] nus [3] nvs [4] coordinate scale.
-// Record per patch (rec_size(pu, pv) doubles, 64-B multiple):
-//   [0 .. 3*(pu+1)*(pv+1))  P[a][c][xyz], a along u, c along v
+// Record per patch (surf_rec(pu, pv) doubles, 64-B multiple), NP = (pu+1)(pv+1):
+//   [0, 3 NP)     P[a][c][xyz], a along u, c along v
+//   [3 NP, 6 NP)  G[a][c][xyz] = S(a/pu, c/pv): the Newton seed grid,
+//                 query-independent, evaluated once at pack time with the
+//                 solver's own surf_point (so bit-identical to evaluating
+//                 it per query, as the oracle does)
 //   then u0 u1 v0 v1 (the patch's parameter rectangle) and the patch id
-//   (i * nvs + j, row-major over the span grid).
+//   (i * nvs + j, row-major over the span grid);
+//   then an oriented box enclosing the control net (so the patch): centre
+//   (3), orthonormal axes e1 e2 e3 (9; e1 along u, e3 the net's normal),
+//   half extents (3, inflated by a rounding margin) -- for a nearly flat
+//   patch it is far tighter than the axis-aligned box.
 // Boxes: the same 8-ary hierarchy as the curve tables, over the patches in
 // 2-D Morton order of (i, j).
 __host__ __device__ inline int surf_rec(int pu, int pv) {
-  int n = 3 * (pu + 1) * (pv + 1) + 5;
+  int n = 6 * (pu + 1) * (pv + 1) + 5 + 15;
   return (n + 7) & ~7;
 }
-__host__ __device__ inline int surf_iv(int pu, int pv) { return 3 * (pu + 1) * (pv + 1); }
+__host__ __device__ inline int surf_obb(int pu, int pv) { return 6 * (pu + 1) * (pv + 1) + 5; }
 
-__device__ __forceinline__ double binom_d(int n, int k) {
-  double r = 1.0;
-  for (int i = 1; i <= k; ++i) r = r * (double)(n - k + i) / (double)i;
-  return r;
+// squared distance lower bound from q to the patch's oriented box
+__device__ __forceinline__ double obb_lb2(const double* O, const double (&q)[3]) {
+  double d[3] = {q[0] - __ldg(O), q[1] - __ldg(O + 1), q[2] - __ldg(O + 2)};
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double pr = d[0] * __ldg(O + 3 + 3 * i) + d[1] * __ldg(O + 4 + 3 * i) +
+                d[2] * __ldg(O + 5 + 3 * i);
+    double g = fmax(0.0, fabs(pr) - __ldg(O + 12 + i));
+    acc += g * g;
+  }
+  return acc;
+}
+__host__ __device__ inline int surf_seed(int pu, int pv) { return 3 * (pu + 1) * (pv + 1); }
+__host__ __device__ inline int surf_iv(int pu, int pv) { return 6 * (pu + 1) * (pv + 1); }
+
+// C(n, k) as an exact double (the oracle's running product r*(n-k+i)/i is
+// an exact integer at every step, so the values agree bit for bit)
+__host__ __device__ constexpr double binom_d(int n, int k) {
+  long long r = 1;
+  for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+  return (double)r;
 }
 
 // Bernstein basis of degree P at u with first and second derivatives
@@ -129,6 +155,32 @@ __device__ __forceinline__ void surf_point(const double* P, double u, double v, 
   }
 }
 
+// surf_point with runtime degrees (pack time only): identical operations
+__device__ void surf_point_rt(const double* P, int pu, int pv, double u, double v, double* S) {
+  double Bu[8], Bv[8], up[8], wp[8];
+  double w = 1.0 - u;
+  up[0] = 1.0;
+  wp[0] = 1.0;
+  for (int k = 1; k <= pu; ++k) {
+    up[k] = up[k - 1] * u;
+    wp[k] = wp[k - 1] * w;
+  }
+  for (int a = 0; a <= pu; ++a) Bu[a] = binom_d(pu, a) * up[a] * wp[pu - a];
+  w = 1.0 - v;
+  for (int k = 1; k <= pv; ++k) {
+    up[k] = up[k - 1] * v;
+    wp[k] = wp[k - 1] * w;
+  }
+  for (int c = 0; c <= pv; ++c) Bv[c] = binom_d(pv, c) * up[c] * wp[pv - c];
+  S[0] = S[1] = S[2] = 0.0;
+  for (int a = 0; a <= pu; ++a) {
+    double R[3] = {0.0, 0.0, 0.0};
+    for (int c = 0; c <= pv; ++c)
+      for (int k = 0; k < 3; ++k) R[k] += Bv[c] * P[(a * (pv + 1) + c) * 3 + k];
+    for (int k = 0; k < 3; ++k) S[k] += Bu[a] * R[k];
+  }
+}
+
 struct Jet {
   double S[3], Su[3], Sv[3], Suu[3], Suv[3], Svv[3];
 };
@@ -193,21 +245,19 @@ template <int PU, int PV>
 __device__ PatchMin patch_min(const double* P, const double (&q)[3]) {
   PatchMin r{0.0, 0.0, 0.0, 0};
   double best = __longlong_as_double(0x7ff0000000000000LL);
-#pragma unroll 1
-  for (int a = 0; a <= PU; ++a) {
-#pragma unroll 1
-    for (int c = 0; c <= PV; ++c) {
-      double u = (double)a / (double)PU, v = (double)c / (double)PV;
-      double S[3];
-      surf_point<PU, PV>(P, u, v, S);
-      double f = dist2_to(S, q);
-      if (f < best) {
-        best = f;
-        r.u = u;
-        r.v = v;
-      }
+  const double* G = P + surf_seed(PU, PV);  // precomputed S(a/PU, c/PV)
+  int bk = 0;
+#pragma unroll 4
+  for (int k = 0; k < (PU + 1) * (PV + 1); ++k) {
+    double S[3] = {__ldg(G + 3 * k), __ldg(G + 3 * k + 1), __ldg(G + 3 * k + 2)};
+    double f = dist2_to(S, q);
+    if (f < best) {
+      best = f;
+      bk = k;
     }
   }
+  r.u = (double)(bk / (PV + 1)) / (double)PU;
+  r.v = (double)(bk % (PV + 1)) / (double)PV;
   double u = r.u, v = r.v, f = best;
   int it = 0;
 #pragma unroll 1
@@ -295,6 +345,7 @@ struct SurfParams {
   double* qs;               // per sorted query: xyz + running min distance
   unsigned long long* pkey; // min patch id in the band
   int32_t* flag;
+  int32_t* prim;            // per sorted query: the greedy-descent patch (solved first)
   uint32_t* pq;
   uint32_t* ps;
   unsigned long long pcap;
@@ -317,19 +368,17 @@ __device__ __forceinline__ double smin_of(const SurfParams& w, int64_t g) {
 template <int PU, int PV>
 __device__ __forceinline__ void offer_points(const SurfParams& w, int64_t s, const double (&q)[3],
                                              double& ub, QStatsLite& st) {
-  const double* P = w.tab.rec + s * w.rec;
-  // four corners (exact surface points) and the centre
+  // the patch's seed grid: (pu+1)(pv+1) exact surface points
+  const double* G = w.tab.rec + s * w.rec + surf_seed(PU, PV);
   const int NP = (PU + 1) * (PV + 1);
-  const int cidx[4] = {0, PV, PU * (PV + 1), NP - 1};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    double S[3] = {__ldg(P + cidx[k] * 3), __ldg(P + cidx[k] * 3 + 1), __ldg(P + cidx[k] * 3 + 2)};
-    ub = fmin(ub, sqrt(dist2_to(S, q)));
+  double m = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll 4
+  for (int k = 0; k < NP; ++k) {
+    double S[3] = {__ldg(G + 3 * k), __ldg(G + 3 * k + 1), __ldg(G + 3 * k + 2)};
+    m = fmin(m, dist2_to(S, q));
   }
-  double S[3];
-  surf_point<PU, PV>(P, 0.5, 0.5, S);
-  ub = fmin(ub, sqrt(dist2_to(S, q)));
-  st.points += 5;
+  ub = fmin(ub, sqrt(m));
+  st.points += NP;
 }
 
 // S1: per-thread depth-first walk (queries in Morton order)
@@ -372,6 +421,7 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
       --level;
     }
     offer_points<PU, PV>(w, idx, q, ub, st);
+    w.prim[g] = (int32_t)idx;
     int lv = T.top;
     int64_t node = 0;
     uint64_t masks = 0;
@@ -397,7 +447,8 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
       double c2 = cut2(ub, scale);
       st.boxes++;
       if (lv == 1) {
-        if (box_lb2<3>(T, T.lvl_off[0] + ch, q) <= c2) {
+        if (box_lb2<3>(T, T.lvl_off[0] + ch, q) <= c2 &&
+            obb_lb2(T.rec + ch * w.rec + surf_obb(PU, PV), q) <= c2) {
           offer_points<PU, PV>(w, ch, q, ub, st);
           unsigned long long slot = wave_append(&w.cnt[0], true);
           if (slot < w.pcap) {
@@ -437,26 +488,33 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
   warp_count(w.counters, MREP_CNT_BOXES, st.boxes);
 }
 
-// S2: one thread per (query, patch) pair
-template <int PU, int PV>
+// S2: one thread per (query, patch) pair.  PASS 0 solves each query's
+// greedy-descent patch first (its minimum is a tight bound: most other pairs
+// then fail the box re-test); PASS 1 solves the remaining pairs.
+template <int PU, int PV, int PASS>
 __global__ void __launch_bounds__(128) surf_solve(const __grid_constant__ SurfParams w) {
-  unsigned long long total = *(volatile unsigned long long*)&w.cnt[0];
-  if (total > w.pcap) total = w.pcap;
+  unsigned long long total = PASS == 0 ? (unsigned long long)w.n
+                                       : *(volatile unsigned long long*)&w.cnt[0];
+  if (PASS == 1 && total > w.pcap) total = w.pcap;
   const TableView& T = w.tab;
   uint64_t npairs = 0, nit = 0;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (unsigned long long)gridDim.x * blockDim.x) {
-    int64_t g = w.pq[i];
+    int64_t g = PASS == 0 ? (int64_t)i : (int64_t)w.pq[i];
     if (w.flag[g]) continue;
-    int64_t s = w.ps[i];
+    int64_t s = PASS == 0 ? (int64_t)w.prim[g] : (int64_t)w.ps[i];
+    if (PASS == 1 && s == w.prim[g]) continue;
     double4 rec = *(const double4*)(w.qs + g * 4);
     double q[3] = {rec.x, rec.y, rec.z};
     double scale = T.hdr[4];
 #pragma unroll
     for (int k = 0; k < 3; ++k) scale = fmax(scale, fabs(q[k]));
-    double cur = smin_of(w, g);
-    if (!(box_lb2<3>(T, T.lvl_off[0] + s, q) <= cut2(cur, scale))) continue;
     const double* P = T.rec + s * w.rec;
+    if (PASS == 1) {
+      const double c2 = cut2(smin_of(w, g), scale);
+      if (!(box_lb2<3>(T, T.lvl_off[0] + s, q) <= c2)) continue;
+      if (!(obb_lb2(P + surf_obb(PU, PV), q) <= c2)) continue;
+    }
     PatchMin m = patch_min<PU, PV>(P, q);
     ++npairs;
     nit += (uint64_t)m.iters;
@@ -541,6 +599,7 @@ __global__ void __launch_bounds__(128) surf_fallback(const __grid_constant__ Sur
         double lb = box_lb2<3>(T, T.lvl_off[0] + s, q);
         if (!(lb <= cut2(dmin, scale))) continue;
         const double* P = T.rec + s * w.rec;
+        if (!(obb_lb2(P + surf_obb(PU, PV), q) <= cut2(dmin, scale))) continue;
         PatchMin m = patch_min<PU, PV>(P, q);
         double d = sqrt(m.d2);
         if (pass == 0) {
@@ -613,10 +672,70 @@ __global__ void surf_pack_kernel(const double* pts, const double* iv, const uint
       hi[c] = fmax(hi[c], x);
       amax = fmax(amax, fabs(x));
     }
+  double* G = r + surf_seed(pu, pv);
+  for (int a = 0; a <= pu; ++a)
+    for (int c = 0; c <= pv; ++c)
+      surf_point_rt(r, pu, pv, (double)a / (double)pu, (double)c / (double)pv,
+                    G + (a * (pv + 1) + c) * 3);
   const int o = surf_iv(pu, pv);
   for (int j = 0; j < 4; ++j) r[o + j] = iv[s * 4 + j];
   r[o + 4] = (double)s;
   for (int j = o + 5; j < R; ++j) r[j] = 0.0;
+  {
+    // frame: e1 along u (mean of the two u-edges), e3 normal to e1 and the
+    // mean v-edge, e2 = e3 x e1
+    const double* P00 = r;
+    const double* P0v = r + pv * 3;
+    const double* Pu0 = r + (pu * (pv + 1)) * 3;
+    const double* Puv = r + (pu * (pv + 1) + pv) * 3;
+    double a[3], b[3], e1[3], e2[3], e3[3];
+    for (int k = 0; k < 3; ++k) {
+      a[k] = (Pu0[k] - P00[k]) + (Puv[k] - P0v[k]);
+      b[k] = (P0v[k] - P00[k]) + (Puv[k] - Pu0[k]);
+    }
+    double na = sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+    bool ok = na > 0.0;
+    for (int k = 0; k < 3; ++k) e1[k] = ok ? a[k] / na : (k == 0 ? 1.0 : 0.0);
+    e3[0] = e1[1] * b[2] - e1[2] * b[1];
+    e3[1] = e1[2] * b[0] - e1[0] * b[2];
+    e3[2] = e1[0] * b[1] - e1[1] * b[0];
+    double n3 = sqrt(e3[0] * e3[0] + e3[1] * e3[1] + e3[2] * e3[2]);
+    if (!(n3 > 1e-300)) {  // degenerate: any frame containing e1
+      double t[3] = {fabs(e1[0]) < 0.9 ? 1.0 : 0.0, fabs(e1[0]) < 0.9 ? 0.0 : 1.0, 0.0};
+      e3[0] = e1[1] * t[2] - e1[2] * t[1];
+      e3[1] = e1[2] * t[0] - e1[0] * t[2];
+      e3[2] = e1[0] * t[1] - e1[1] * t[0];
+      n3 = sqrt(e3[0] * e3[0] + e3[1] * e3[1] + e3[2] * e3[2]);
+    }
+    for (int k = 0; k < 3; ++k) e3[k] /= n3;
+    e2[0] = e3[1] * e1[2] - e3[2] * e1[1];
+    e2[1] = e3[2] * e1[0] - e3[0] * e1[2];
+    e2[2] = e3[0] * e1[1] - e3[1] * e1[0];
+    const double* E[3] = {e1, e2, e3};
+    double lo[3], hi[3];
+    for (int i = 0; i < 3; ++i) {
+      lo[i] = 1e300;
+      hi[i] = -1e300;
+    }
+    for (int j = 0; j < NP; ++j)
+      for (int i = 0; i < 3; ++i) {
+        double pr = r[j * 3] * E[i][0] + r[j * 3 + 1] * E[i][1] + r[j * 3 + 2] * E[i][2];
+        lo[i] = fmin(lo[i], pr);
+        hi[i] = fmax(hi[i], pr);
+      }
+    double* O = r + surf_obb(pu, pv);
+    double c[3] = {0.0, 0.0, 0.0};
+    for (int i = 0; i < 3; ++i) {
+      double mid = 0.5 * (lo[i] + hi[i]);
+      for (int k = 0; k < 3; ++k) c[k] += mid * E[i][k];
+    }
+    for (int k = 0; k < 3; ++k) O[k] = c[k];
+    for (int i = 0; i < 3; ++i)
+      for (int k = 0; k < 3; ++k) O[3 + 3 * i + k] = E[i][k];
+    // rounding margin: projections, the centre reconstruction and the
+    // non-orthogonality of the rounded axes all err by O(1e-15 |x|)
+    for (int i = 0; i < 3; ++i) O[12 + i] = 0.5 * (hi[i] - lo[i]) + 1e-12 * (1.0 + amax);
+  }
   for (int c = 0; c < 3; ++c) {
     box0[k * 6 + c] = lo[c];
     box0[k * 6 + 3 + c] = hi[c];
@@ -724,7 +843,8 @@ static int launch_surface(SurfParams& w, cudaStream_t st, bool timing) {
     bytes += (b + 255) & ~(size_t)255;
     return o;
   };
-  size_t o_cnt = take(8 * 8), o_qs = take(n * 32), o_pk = take(n * 8), o_fl = take(n * 4);
+  size_t o_cnt = take(8 * 8), o_qs = take(n * 32), o_pk = take(n * 8), o_fl = take(n * 4),
+         o_pr = take(n * 4);
   size_t o_pq = take(pcap * 4), o_ps = take(pcap * 4);
   size_t o_cq = take(ccap * 4), o_cs = take(ccap * 4), o_cu = take(ccap * 8), o_cv = take(ccap * 8),
          o_cd = take(ccap * 8), o_fb = take(n * 8);
@@ -734,6 +854,7 @@ static int launch_surface(SurfParams& w, cudaStream_t st, bool timing) {
   w.qs = (double*)(base + o_qs);
   w.pkey = (unsigned long long*)(base + o_pk);
   w.flag = (int32_t*)(base + o_fl);
+  w.prim = (int32_t*)(base + o_pr);
   w.pq = (uint32_t*)(base + o_pq);
   w.ps = (uint32_t*)(base + o_ps);
   w.pcap = pcap;
@@ -752,14 +873,15 @@ static int launch_surface(SurfParams& w, cudaStream_t st, bool timing) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, block, 0);
     return (unsigned)(sms * (per > 0 ? per : 1));
   };
-  const unsigned g_solve = persist_grid((const void*)surf_solve<PU, PV>, 128);
+  const unsigned g_solve = persist_grid((const void*)surf_solve<PU, PV, 1>, 128);
   const unsigned g_sel = persist_grid((const void*)surf_select<PU, PV, 1>, 256);
   StageTimer tm(timing, st);
   tm.mark();
   surf_traverse<PU, PV><<<grid_for(n, 128), 128, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
   tm.mark();
-  surf_solve<PU, PV><<<g_solve, 128, 0, st>>>(w);
+  surf_solve<PU, PV, 0><<<g_solve, 128, 0, st>>>(w);
+  surf_solve<PU, PV, 1><<<g_solve, 128, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
   tm.mark();
   tm.mark();  // (no clip stage for surfaces)
