@@ -185,11 +185,39 @@ struct Jet {
   double S[3], Su[3], Sv[3], Suu[3], Suv[3], Svv[3];
 };
 
+// Bernstein value / first / second derivative of index a, degree P, from
+// the power tables (the per-element formulas of bern(): identical values)
+template <int P>
+__device__ __forceinline__ void bern_at(int a, const double (&up)[P + 1], const double (&wp)[P + 1],
+                                        double& B, double& dB, double& ddB) {
+  B = binom_d(P, a) * up[a] * wp[P - a];
+  double b1a = (P >= 1 && a <= P - 1) ? binom_d(P - 1, a) * up[a] * wp[P - 1 - a] : 0.0;
+  double b1m = (P >= 1 && a >= 1) ? binom_d(P - 1, a - 1) * up[a - 1] * wp[P - a] : 0.0;
+  dB = (double)P * (b1m - b1a);
+  double b2a = (P >= 2 && a <= P - 2) ? binom_d(P - 2, a) * up[a] * wp[P - 2 - a] : 0.0;
+  double b2m1 = (P >= 2 && a >= 1 && a - 1 <= P - 2) ? binom_d(P - 2, a - 1) * up[a - 1] * wp[P - 1 - a]
+                                                      : 0.0;
+  double b2m2 = (P >= 2 && a >= 2) ? binom_d(P - 2, a - 2) * up[a - 2] * wp[P - a] : 0.0;
+  ddB = (double)(P * (P - 1)) * ((b2m2 - 2.0 * b2m1) + b2a);
+}
+
+// S and its first / second partials at (u, v).  Register-lean: the u basis
+// is produced one index at a time from the power tables.
 template <int PU, int PV>
 __device__ __forceinline__ void surf_jet(const double* P, double u, double v, Jet& J) {
-  double Bu[PU + 1], dBu[PU + 1], ddBu[PU + 1], Bv[PV + 1], dBv[PV + 1], ddBv[PV + 1];
-  bern<PU>(u, Bu, dBu, ddBu);
+  double Bv[PV + 1], dBv[PV + 1], ddBv[PV + 1];
   bern<PV>(v, Bv, dBv, ddBv);
+  double up[PU + 1], wp[PU + 1];
+  {
+    const double w = 1.0 - u;
+    up[0] = 1.0;
+    wp[0] = 1.0;
+#pragma unroll
+    for (int k = 1; k <= PU; ++k) {
+      up[k] = up[k - 1] * u;
+      wp[k] = wp[k - 1] * w;
+    }
+  }
 #pragma unroll
   for (int k = 0; k < 3; ++k) J.S[k] = J.Su[k] = J.Sv[k] = J.Suu[k] = J.Suv[k] = J.Svv[k] = 0.0;
 #pragma unroll
@@ -204,14 +232,16 @@ __device__ __forceinline__ void surf_jet(const double* P, double u, double v, Je
         Rv[k] += dBv[c] * p;
         Rvv[k] += ddBv[c] * p;
       }
+    double Bu, dBu, ddBu;
+    bern_at<PU>(a, up, wp, Bu, dBu, ddBu);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      J.S[k] += Bu[a] * R[k];
-      J.Su[k] += dBu[a] * R[k];
-      J.Suu[k] += ddBu[a] * R[k];
-      J.Sv[k] += Bu[a] * Rv[k];
-      J.Suv[k] += dBu[a] * Rv[k];
-      J.Svv[k] += Bu[a] * Rvv[k];
+      J.S[k] += Bu * R[k];
+      J.Su[k] += dBu * R[k];
+      J.Suu[k] += ddBu * R[k];
+      J.Sv[k] += Bu * Rv[k];
+      J.Suv[k] += dBu * Rv[k];
+      J.Svv[k] += Bu * Rvv[k];
     }
   }
 }
@@ -234,16 +264,17 @@ struct QStatsLite {
 constexpr int NEWTON_MAX = 30;
 constexpr int LS_MAX = 12;
 
-struct PatchMin {
-  double u, v, d2;
-  int iters;
+// Minimum of |S(u,v) - q|^2 on one patch: best Bernstein seed, then
+// projected Newton (oracle: surf_patch_min in mrep_surface_oracle.c).  Split
+// into seed_init + newton_iter so the solver can interleave many pairs per
+// lane (surf_solve refills a lane as soon as its pair finishes).
+struct NState {
+  double u, v, f;
+  int it;
 };
 
-// Minimum of |S(u,v) - q|^2 on one patch: best Bernstein seed, then
-// projected Newton (oracle: surf_patch_min in mrep_surface_oracle.c).
 template <int PU, int PV>
-__device__ PatchMin patch_min(const double* P, const double (&q)[3]) {
-  PatchMin r{0.0, 0.0, 0.0, 0};
+__device__ __forceinline__ void seed_init(const double* P, const double (&q)[3], NState& n) {
   double best = __longlong_as_double(0x7ff0000000000000LL);
   const double* G = P + surf_seed(PU, PV);  // precomputed S(a/PU, c/PV)
   int bk = 0;
@@ -256,76 +287,91 @@ __device__ PatchMin patch_min(const double* P, const double (&q)[3]) {
       bk = k;
     }
   }
-  r.u = (double)(bk / (PV + 1)) / (double)PU;
-  r.v = (double)(bk % (PV + 1)) / (double)PV;
-  double u = r.u, v = r.v, f = best;
-  int it = 0;
-#pragma unroll 1
-  for (; it < NEWTON_MAX; ++it) {
-    Jet J;
-    surf_jet<PU, PV>(P, u, v, J);
-    double rr[3] = {J.S[0] - q[0], J.S[1] - q[1], J.S[2] - q[2]};
-    f = dot3(rr, rr);
-    double gu = dot3(J.Su, rr), gv = dot3(J.Sv, rr);
-    double guu = dot3(J.Su, J.Su), gvv = dot3(J.Sv, J.Sv), guv = dot3(J.Su, J.Sv);
-    double huu = guu + dot3(J.Suu, rr);
-    double huv = guv + dot3(J.Suv, rr);
-    double hvv = gvv + dot3(J.Svv, rr);
-    bool fu = !((u <= 0.0 && gu > 0.0) || (u >= 1.0 && gu < 0.0));
-    bool fv = !((v <= 0.0 && gv > 0.0) || (v >= 1.0 && gv < 0.0));
-    double du = 0.0, dv = 0.0;
-    if (fu && fv) {
-      double det = huu * hvv - huv * huv;
-      if (huu > 0.0 && det > 0.0) {
-        du = -(hvv * gu - huv * gv) / det;
-        dv = -(huu * gv - huv * gu) / det;
-      } else {
-        double dg = guu * gvv - guv * guv;  // Gauss-Newton (J^T J, PSD)
-        if (guu > 0.0 && dg > 0.0) {
-          du = -(gvv * gu - guv * gv) / dg;
-          dv = -(guu * gv - guv * gu) / dg;
-        } else {
-          break;
-        }
-      }
-    } else if (fu) {
-      double h = huu > 0.0 ? huu : guu;
-      if (!(h > 0.0)) break;
-      du = -gu / h;
-    } else if (fv) {
-      double h = hvv > 0.0 ? hvv : gvv;
-      if (!(h > 0.0)) break;
-      dv = -gv / h;
+  n.u = (double)(bk / (PV + 1)) / (double)PU;
+  n.v = (double)(bk % (PV + 1)) / (double)PV;
+  n.f = best;
+  n.it = 0;
+}
+
+// one iteration of the oracle's loop; true when the solve is finished
+template <int PU, int PV>
+__device__ __forceinline__ bool newton_iter(const double* P, const double (&q)[3], NState& n) {
+  const double u = n.u, v = n.v;
+  Jet J;
+  surf_jet<PU, PV>(P, u, v, J);
+  double rr[3] = {J.S[0] - q[0], J.S[1] - q[1], J.S[2] - q[2]};
+  const double f = dot3(rr, rr);
+  n.f = f;
+  double gu = dot3(J.Su, rr), gv = dot3(J.Sv, rr);
+  double guu = dot3(J.Su, J.Su), gvv = dot3(J.Sv, J.Sv), guv = dot3(J.Su, J.Sv);
+  double huu = guu + dot3(J.Suu, rr);
+  double huv = guv + dot3(J.Suv, rr);
+  double hvv = gvv + dot3(J.Svv, rr);
+  bool fu = !((u <= 0.0 && gu > 0.0) || (u >= 1.0 && gu < 0.0));
+  bool fv = !((v <= 0.0 && gv > 0.0) || (v >= 1.0 && gv < 0.0));
+  double du = 0.0, dv = 0.0;
+  if (fu && fv) {
+    double det = huu * hvv - huv * huv;
+    if (huu > 0.0 && det > 0.0) {
+      du = -(hvv * gu - huv * gv) / det;
+      dv = -(huu * gv - huv * gu) / det;
     } else {
-      break;  // KKT point at a corner
-    }
-    double t = 1.0, un = u, vn = v, fn = f;
-    bool ok = false;
-#pragma unroll 1
-    for (int ls = 0; ls < LS_MAX; ++ls) {
-      un = clamp01(u + t * du);
-      vn = clamp01(v + t * dv);
-      double S[3];
-      surf_point<PU, PV>(P, un, vn, S);
-      fn = dist2_to(S, q);
-      if (fn < f) {
-        ok = true;
-        break;
+      double dg = guu * gvv - guv * guv;  // Gauss-Newton (J^T J, PSD)
+      if (guu > 0.0 && dg > 0.0) {
+        du = -(gvv * gu - guv * gv) / dg;
+        dv = -(guu * gv - guv * gu) / dg;
+      } else {
+        return true;
       }
-      t = t * 0.5;
     }
-    if (!ok) break;
-    bool conv = fabs(un - u) <= 1e-16 && fabs(vn - v) <= 1e-16;
-    u = un;
-    v = vn;
-    f = fn;
-    if (conv) break;
+  } else if (fu) {
+    double h = huu > 0.0 ? huu : guu;
+    if (!(h > 0.0)) return true;
+    du = -gu / h;
+  } else if (fv) {
+    double h = hvv > 0.0 ? hvv : gvv;
+    if (!(h > 0.0)) return true;
+    dv = -gv / h;
+  } else {
+    return true;  // KKT point at a corner
   }
-  r.u = u;
-  r.v = v;
-  r.d2 = f;
-  r.iters = it;
-  return r;
+  double t = 1.0, un = u, vn = v, fn = f;
+  bool ok = false;
+#pragma unroll 1
+  for (int ls = 0; ls < LS_MAX; ++ls) {
+    un = clamp01(u + t * du);
+    vn = clamp01(v + t * dv);
+    double S[3];
+    surf_point<PU, PV>(P, un, vn, S);
+    fn = dist2_to(S, q);
+    if (fn < f) {
+      ok = true;
+      break;
+    }
+    t = t * 0.5;
+  }
+  if (!ok) return true;
+  bool conv = fabs(un - u) <= 1e-16 && fabs(vn - v) <= 1e-16;
+  n.u = un;
+  n.v = vn;
+  n.f = fn;
+  if (conv) return true;
+  return ++n.it >= NEWTON_MAX;
+}
+
+struct PatchMin {
+  double u, v, d2;
+  int iters;
+};
+
+template <int PU, int PV>
+__device__ PatchMin patch_min(const double* P, const double (&q)[3]) {
+  NState n;
+  seed_init<PU, PV>(P, q, n);
+#pragma unroll 1
+  while (!newton_iter<PU, PV>(P, q, n)) {
+  }
+  return PatchMin{n.u, n.v, n.f, n.it};
 }
 
 // ---------------------------------------------------------------- pipeline
@@ -348,6 +394,8 @@ struct SurfParams {
   int32_t* prim;            // per sorted query: the greedy-descent patch (solved first)
   uint32_t* pq;
   uint32_t* ps;
+  uint32_t* fq;  // pairs surviving the post-greedy re-test (compacted)
+  uint32_t* fs;
   unsigned long long pcap;
   uint32_t* cq;
   uint32_t* cs;
@@ -488,46 +536,107 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
   warp_count(w.counters, MREP_CNT_BOXES, st.boxes);
 }
 
-// S2: one thread per (query, patch) pair.  PASS 0 solves each query's
-// greedy-descent patch first (its minimum is a tight bound: most other pairs
-// then fail the box re-test); PASS 1 solves the remaining pairs.
-template <int PU, int PV, int PASS>
-__global__ void __launch_bounds__(128) surf_solve(const __grid_constant__ SurfParams w) {
-  unsigned long long total = PASS == 0 ? (unsigned long long)w.n
-                                       : *(volatile unsigned long long*)&w.cnt[0];
-  if (PASS == 1 && total > w.pcap) total = w.pcap;
+// S2a: re-test every traversal pair against the bound the greedy patches
+// left (box + oriented box) and compact the survivors, so the solver's
+// lanes only ever hold real work.
+template <int PU, int PV>
+__global__ void __launch_bounds__(256) surf_filter(const __grid_constant__ SurfParams w) {
+  unsigned long long total = *(volatile unsigned long long*)&w.cnt[0];
+  if (total > w.pcap) total = w.pcap;
   const TableView& T = w.tab;
-  uint64_t npairs = 0, nit = 0;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (unsigned long long)gridDim.x * blockDim.x) {
-    int64_t g = PASS == 0 ? (int64_t)i : (int64_t)w.pq[i];
-    if (w.flag[g]) continue;
-    int64_t s = PASS == 0 ? (int64_t)w.prim[g] : (int64_t)w.ps[i];
-    if (PASS == 1 && s == w.prim[g]) continue;
-    double4 rec = *(const double4*)(w.qs + g * 4);
-    double q[3] = {rec.x, rec.y, rec.z};
-    double scale = T.hdr[4];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) scale = fmax(scale, fabs(q[k]));
-    const double* P = T.rec + s * w.rec;
-    if (PASS == 1) {
-      const double c2 = cut2(smin_of(w, g), scale);
-      if (!(box_lb2<3>(T, T.lvl_off[0] + s, q) <= c2)) continue;
-      if (!(obb_lb2(P + surf_obb(PU, PV), q) <= c2)) continue;
+    const int64_t g = w.pq[i];
+    const int64_t s = w.ps[i];
+    bool keep = !w.flag[g] && s != w.prim[g];
+    if (keep) {
+      double4 rec = *(const double4*)(w.qs + g * 4);
+      double q[3] = {rec.x, rec.y, rec.z};
+      double scale = fmax(T.hdr[4], fmax(fabs(q[0]), fmax(fabs(q[1]), fabs(q[2]))));
+      const double c2 = cut2(rec.w, scale);
+      keep = box_lb2<3>(T, T.lvl_off[0] + s, q) <= c2 &&
+             obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2;
     }
-    PatchMin m = patch_min<PU, PV>(P, q);
+    unsigned long long slot = wave_append(&w.cnt[6], keep);
+    if (keep) {  // slot < pcap: the compact list is never longer than the input
+      w.fq[slot] = (uint32_t)g;
+      w.fs[slot] = (uint32_t)s;
+    }
+  }
+}
+
+// S2: projected-Newton solves of (query, patch) pairs with lane refill: a
+// persistent warp loop in which every lane runs one Newton iteration of its
+// current pair and a lane whose pair finished takes the next pair from the
+// queue at once (warp-aggregated atomics), so the 1..30 iterations per pair
+// do not leave lanes idle.  PASS 0: each query's greedy-descent patch
+// (its minimum is a tight bound); PASS 1: the compacted survivors.
+template <int PU, int PV, int PASS>
+__global__ void __launch_bounds__(128, (PU + PV <= 6) ? 3 : 1) surf_solve(const __grid_constant__ SurfParams w) {
+  const unsigned long long total =
+      PASS == 0 ? (unsigned long long)w.n : *(volatile unsigned long long*)&w.cnt[6];
+  unsigned long long* queue = &w.cnt[PASS == 0 ? 4 : 5];
+  const TableView& T = w.tab;
+  const int lane = threadIdx.x & 31;
+  uint64_t npairs = 0, nit = 0;
+  bool have = false, done = false;
+  int64_t g = 0, s = 0;
+  double q[3] = {0.0, 0.0, 0.0};
+  const double* P = T.rec;
+  NState ns{0.0, 0.0, 0.0, 0};
+  for (;;) {
+    // refill lanes without a pair
+    const bool want = !have && !done;
+    const unsigned wm = __ballot_sync(0xffffffffu, want);
+    if (wm) {
+      const int leader = __ffs(wm) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(queue, (unsigned long long)__popc(wm));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (want) {
+        const unsigned long long i = base + __popc(wm & ((1u << lane) - 1));
+        if (i >= total) {
+          done = true;
+        } else {
+          g = PASS == 0 ? (int64_t)i : (int64_t)w.fq[i];
+          s = PASS == 0 ? (int64_t)w.prim[g] : (int64_t)w.fs[i];
+          if (!w.flag[g]) {
+            double4 rec = *(const double4*)(w.qs + g * 4);
+            q[0] = rec.x;
+            q[1] = rec.y;
+            q[2] = rec.z;
+            bool go = true;
+            if (PASS == 1) {  // the bound may have tightened since the filter
+              double scale = fmax(T.hdr[4], fmax(fabs(q[0]), fmax(fabs(q[1]), fabs(q[2]))));
+              go = obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <=
+                   cut2(smin_of(w, g), scale);
+            }
+            if (go) {
+              P = T.rec + s * w.rec;
+              seed_init<PU, PV>(P, q, ns);
+              have = true;
+            }
+          }
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
+    if (!have) continue;
+    if (!newton_iter<PU, PV>(P, q, ns)) continue;
+    // pair finished: its candidate
+    have = false;
     ++npairs;
-    nit += (uint64_t)m.iters;
-    double d = sqrt(m.d2);
-    bool keep = d <= smin_of(w, g) + 1e-12;
+    nit += (uint64_t)ns.it;
+    const double d = sqrt(ns.f);
+    const bool keep = d <= smin_of(w, g) + 1e-12;
     unsigned long long slot = wave_append(&w.cnt[1], keep);
     if (keep) {
       atomicMin(smin_ptr(w, g), (unsigned long long)__double_as_longlong(d));
       if (slot < w.ccap) {
         w.cq[slot] = (uint32_t)g;
         w.cs[slot] = (uint32_t)s;
-        w.cu[slot] = m.u;
-        w.cv[slot] = m.v;
+        w.cu[slot] = ns.u;
+        w.cv[slot] = ns.v;
         w.cd[slot] = d;
       } else if (atomicExch(&w.flag[g], 1) == 0) {
         unsigned long long fs = atomicAdd(&w.cnt[2], 1ull);
@@ -845,7 +954,8 @@ static int launch_surface(SurfParams& w, cudaStream_t st, bool timing) {
   };
   size_t o_cnt = take(8 * 8), o_qs = take(n * 32), o_pk = take(n * 8), o_fl = take(n * 4),
          o_pr = take(n * 4);
-  size_t o_pq = take(pcap * 4), o_ps = take(pcap * 4);
+  size_t o_pq = take(pcap * 4), o_ps = take(pcap * 4), o_fq = take(pcap * 4),
+         o_fs = take(pcap * 4);
   size_t o_cq = take(ccap * 4), o_cs = take(ccap * 4), o_cu = take(ccap * 8), o_cv = take(ccap * 8),
          o_cd = take(ccap * 8), o_fb = take(n * 8);
   char* base = nullptr;
@@ -857,6 +967,8 @@ static int launch_surface(SurfParams& w, cudaStream_t st, bool timing) {
   w.prim = (int32_t*)(base + o_pr);
   w.pq = (uint32_t*)(base + o_pq);
   w.ps = (uint32_t*)(base + o_ps);
+  w.fq = (uint32_t*)(base + o_fq);
+  w.fs = (uint32_t*)(base + o_fs);
   w.pcap = pcap;
   w.cq = (uint32_t*)(base + o_cq);
   w.cs = (uint32_t*)(base + o_cs);
@@ -881,6 +993,7 @@ static int launch_surface(SurfParams& w, cudaStream_t st, bool timing) {
   MREP_LAUNCH_CHECK();
   tm.mark();
   surf_solve<PU, PV, 0><<<g_solve, 128, 0, st>>>(w);
+  surf_filter<PU, PV><<<g_sel, 256, 0, st>>>(w);
   surf_solve<PU, PV, 1><<<g_solve, 128, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
   tm.mark();
