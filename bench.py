@@ -234,7 +234,8 @@ class SingleCurve:
         self.q_pin = torch.from_numpy(self.q_host).pin_memory().numpy()
 
     def host(self, out, dense=False):
-        self.tab.project_host(self.q_pin, out=out, screen=not dense)
+        # the reference-facing call returns (t, foot, dist, cand): no segment ids
+        self.tab.project_host(self.q_pin, out=out[:4] + (None,), screen=not dense)
 
     def cpu_jobs(self, sample):
         sample = max(256, min(sample, int(sample * 510 / self.num_segments)))
@@ -279,7 +280,7 @@ class CurveSetWorkload:
         self.cid_pin = torch.from_numpy(self.cid_host).pin_memory().numpy()
 
     def host(self, out, dense=False):
-        self.cset.project_host(self.q_pin, self.cid_pin, out=out)
+        self.cset.project_host(self.q_pin, self.cid_pin, out=out[:4] + (None,))
 
     def cpu_jobs(self, sample):
         stride = max(1, len(self.curves) // 50)
@@ -623,7 +624,8 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
     e2e = {"value": n_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": wl.h2d,
-           "d2h_bytes_per_step": n * (8 + 24 + 8 + 8 + 4),
+           # (t, foot, dist, cand) for curves; (u, v, foot, dist, patch) for surfaces
+           "d2h_bytes_per_step": n * ((8 + 8 + 24 + 8 + 4) if surf else (8 + 24 + 8 + 8)),
            "path": ("mrep_project_batch_host" if args.config == "cfg3" else
                     "mrep_project_surface_host" if surf else "mrep_project_host")
            + " (C ABI, pinned host buffers, 2-stream chunked pipeline)"}

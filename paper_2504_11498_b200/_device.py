@@ -196,7 +196,7 @@ class DeviceTable:
                    np.empty(n, dtype=np.int64), np.empty(n, dtype=np.int32))
         t, foot, dist, cand, seg = out
         import ctypes
-        p = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+        p = lambda a: ctypes.c_void_p(a.ctypes.data if a is not None else 0)  # noqa: E731
         L.check(L.lib().mrep_project_host(
             L.ptr(self.buf), self.S, self.d, p(q), n, float(clip_tol), int(max_iter),
             L.MREP_SCREEN if screen else 0, p(t), p(foot), p(dist), p(cand), p(seg),

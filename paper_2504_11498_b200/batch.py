@@ -124,7 +124,7 @@ class PreparedCurveSet:
             out = (np.empty(n), np.empty((n, self.d)), np.empty(n),
                    np.empty(n, dtype=np.int64), np.empty(n, dtype=np.int32))
         t, foot, dist, cand, seg = out
-        p = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+        p = lambda a: ctypes.c_void_p(a.ctypes.data if a is not None else 0)  # noqa: E731
         L.check(L.lib().mrep_project_batch_host(
             self.handle, p(q), p(cid), n, float(clip_tol), int(max_iter), L.MREP_SCREEN,
             p(t), p(foot), p(dist), p(cand), p(seg),

@@ -9,7 +9,13 @@
 // copied directly; pageable ones are staged through cached pinned buffers.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
+#include <utility>
+#include <vector>
+#include <algorithm>
 #include <mutex>
 
 #include "mrep_common.cuh"
@@ -18,7 +24,26 @@ namespace mrep {
 
 namespace {
 
-constexpr int64_t CHUNK = 1 << 18;  // queries per pipeline slot
+constexpr int64_t CHUNK_MAX = 1 << 19;  // queries per pipeline slot (buffer size)
+constexpr int NSLOT_MAX = 4;
+// pipeline shape: MREP_E2E_CHUNK (queries per chunk, <= 2^19) and
+// MREP_E2E_SLOTS (2..4 chunks in flight) override the defaults
+static int64_t chunk_size() {
+  static int64_t c = [] {
+    const char* e = getenv("MREP_E2E_CHUNK");
+    int64_t v = e ? atoll(e) : (1 << 18);
+    return v < 4096 ? (int64_t)4096 : (v > CHUNK_MAX ? CHUNK_MAX : v);
+  }();
+  return c;
+}
+static int num_slots() {
+  static int n = [] {
+    const char* e = getenv("MREP_E2E_SLOTS");
+    int v = e ? atoi(e) : 4;
+    return v < 2 ? 2 : (v > NSLOT_MAX ? NSLOT_MAX : v);
+  }();
+  return n;
+}
 
 struct Slot {
   cudaStream_t st = nullptr;
@@ -36,10 +61,21 @@ struct Slot {
   bool busy = false;
 };
 
+// whole-batch device buffers for the pinned fast path (grown on demand)
+struct BigBuf {
+  int64_t cap = 0;
+  double *dq = nullptr, *dt = nullptr, *dfoot = nullptr, *ddist = nullptr;
+  int64_t* dcand = nullptr;
+  int32_t *dseg = nullptr, *dcur = nullptr;
+};
+
 struct HostCtx {
   std::mutex mu;
   int device = -1;
-  Slot slot[2];
+  Slot slot[NSLOT_MAX];
+  BigBuf big;
+  cudaStream_t cin = nullptr, cout = nullptr;  // copy-in / copy-out streams (fast path)
+  std::vector<cudaEvent_t> ev_in, ev_comp;     // per-chunk hand-off events (cached)
   bool ready = false;
 };
 
@@ -62,22 +98,24 @@ int ensure_ctx() {
     // blocking streams: ordered after work on the legacy default stream (torch)
     MREP_CUDA_CHECK(cudaStreamCreateWithFlags(&s.st, cudaStreamDefault));
     MREP_CUDA_CHECK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
-    MREP_CUDA_CHECK(cudaMalloc(&s.dq, CHUNK * 3 * sizeof(double)));
-    MREP_CUDA_CHECK(cudaMalloc(&s.dt, CHUNK * sizeof(double)));
-    MREP_CUDA_CHECK(cudaMalloc(&s.dfoot, CHUNK * 3 * sizeof(double)));
-    MREP_CUDA_CHECK(cudaMalloc(&s.ddist, CHUNK * sizeof(double)));
-    MREP_CUDA_CHECK(cudaMalloc(&s.dcand, CHUNK * sizeof(int64_t)));
-    MREP_CUDA_CHECK(cudaMalloc(&s.dseg, CHUNK * sizeof(int32_t)));
-    MREP_CUDA_CHECK(cudaMalloc(&s.dcur, CHUNK * sizeof(int32_t)));
+    MREP_CUDA_CHECK(cudaMalloc(&s.dq, CHUNK_MAX * 3 * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMalloc(&s.dt, CHUNK_MAX * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMalloc(&s.dfoot, CHUNK_MAX * 3 * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMalloc(&s.ddist, CHUNK_MAX * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMalloc(&s.dcand, CHUNK_MAX * sizeof(int64_t)));
+    MREP_CUDA_CHECK(cudaMalloc(&s.dseg, CHUNK_MAX * sizeof(int32_t)));
+    MREP_CUDA_CHECK(cudaMalloc(&s.dcur, CHUNK_MAX * sizeof(int32_t)));
     MREP_CUDA_CHECK(cudaMalloc(&s.dcnt, MREP_NUM_COUNTERS * sizeof(uint64_t)));
-    MREP_CUDA_CHECK(cudaMallocHost(&s.hq, CHUNK * 3 * sizeof(double)));
-    MREP_CUDA_CHECK(cudaMallocHost(&s.ht, CHUNK * sizeof(double)));
-    MREP_CUDA_CHECK(cudaMallocHost(&s.hfoot, CHUNK * 3 * sizeof(double)));
-    MREP_CUDA_CHECK(cudaMallocHost(&s.hdist, CHUNK * sizeof(double)));
-    MREP_CUDA_CHECK(cudaMallocHost(&s.hcand, CHUNK * sizeof(int64_t)));
-    MREP_CUDA_CHECK(cudaMallocHost(&s.hseg, CHUNK * sizeof(int32_t)));
-    MREP_CUDA_CHECK(cudaMallocHost(&s.hcur, CHUNK * sizeof(int32_t)));
+    MREP_CUDA_CHECK(cudaMallocHost(&s.hq, CHUNK_MAX * 3 * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMallocHost(&s.ht, CHUNK_MAX * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMallocHost(&s.hfoot, CHUNK_MAX * 3 * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMallocHost(&s.hdist, CHUNK_MAX * sizeof(double)));
+    MREP_CUDA_CHECK(cudaMallocHost(&s.hcand, CHUNK_MAX * sizeof(int64_t)));
+    MREP_CUDA_CHECK(cudaMallocHost(&s.hseg, CHUNK_MAX * sizeof(int32_t)));
+    MREP_CUDA_CHECK(cudaMallocHost(&s.hcur, CHUNK_MAX * sizeof(int32_t)));
   }
+  MREP_CUDA_CHECK(cudaStreamCreateWithFlags(&g_ctx.cin, cudaStreamDefault));
+  MREP_CUDA_CHECK(cudaStreamCreateWithFlags(&g_ctx.cout, cudaStreamDefault));
   g_ctx.device = dev;
   g_ctx.ready = true;
   return MREP_OK;
@@ -103,6 +141,94 @@ int host_pipeline(int d, const double* queries, const int32_t* curve_ids, int64_
   const bool pin_out = is_pinned(out_t) && is_pinned(out_foot) && is_pinned(out_dist) &&
                        is_pinned(out_cand) && (!out_seg || is_pinned(out_seg));
 
+  const int NS = num_slots();
+  for (auto& s : g_ctx.slot)
+    MREP_CUDA_CHECK(cudaMemsetAsync(s.dcnt, 0, MREP_NUM_COUNTERS * sizeof(uint64_t), s.st));
+  if (pin_in && pin_out && !getenv("MREP_E2E_SLOTTED")) {
+    // Pinned fast path: device buffers for the whole batch, every chunk
+    // enqueued at once round-robin over NS streams (H2D -> kernels -> D2H
+    // straight into the caller's buffers); nothing waits for a free slot.
+    BigBuf& B = g_ctx.big;
+    if (B.cap < n) {
+      cudaFree(B.dq);
+      cudaFree(B.dt);
+      cudaFree(B.dfoot);
+      cudaFree(B.ddist);
+      cudaFree(B.dcand);
+      cudaFree(B.dseg);
+      cudaFree(B.dcur);
+      B = BigBuf{};
+      int64_t cap = std::max<int64_t>(n, (int64_t)1 << 16);
+      MREP_CUDA_CHECK(cudaMalloc(&B.dq, cap * 3 * sizeof(double)));
+      MREP_CUDA_CHECK(cudaMalloc(&B.dt, cap * sizeof(double)));
+      MREP_CUDA_CHECK(cudaMalloc(&B.dfoot, cap * 3 * sizeof(double)));
+      MREP_CUDA_CHECK(cudaMalloc(&B.ddist, cap * sizeof(double)));
+      MREP_CUDA_CHECK(cudaMalloc(&B.dcand, cap * sizeof(int64_t)));
+      MREP_CUDA_CHECK(cudaMalloc(&B.dseg, cap * sizeof(int32_t)));
+      MREP_CUDA_CHECK(cudaMalloc(&B.dcur, cap * sizeof(int32_t)));
+      B.cap = cap;
+    }
+    const int64_t CH = getenv("MREP_E2E_CHUNK") ? chunk_size()
+                                                : std::min<int64_t>(CHUNK_MAX, std::max<int64_t>(
+                                                      (int64_t)1 << 16, (n + 7) / 8));
+    const int64_t nch = (n + CH - 1) / CH;
+    while ((int64_t)g_ctx.ev_in.size() < nch) {
+      cudaEvent_t a, b;
+      MREP_CUDA_CHECK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      MREP_CUDA_CHECK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      g_ctx.ev_in.push_back(a);
+      g_ctx.ev_comp.push_back(b);
+    }
+    // uploads back to back on the copy-in stream; chunk c's kernels (on
+    // compute stream c % NS) wait for its upload; downloads back to back on
+    // the copy-out stream, each waiting for its chunk's kernels
+    int64_t c = 0;
+    for (int64_t lo = 0; lo < n; lo += CH, ++c) {
+      Slot v = g_ctx.slot[c % NS];  // stream + counters of the slot, big-buffer views
+      v.lo = lo;
+      v.cnt = std::min(CH, n - lo);
+      v.dq = B.dq + lo * d;
+      v.dt = B.dt + lo;
+      v.dfoot = B.dfoot + lo * d;
+      v.ddist = B.ddist + lo;
+      v.dcand = B.dcand + lo;
+      v.dseg = B.dseg + lo;
+      v.dcur = B.dcur + lo;
+      cudaStream_t ci = g_ctx.cin, co = g_ctx.cout;
+      MREP_CUDA_CHECK(cudaMemcpyAsync(v.dq, queries + lo * d, v.cnt * d * sizeof(double),
+                                      cudaMemcpyHostToDevice, ci));
+      if (curve_ids)
+        MREP_CUDA_CHECK(cudaMemcpyAsync(v.dcur, curve_ids + lo, v.cnt * sizeof(int32_t),
+                                        cudaMemcpyHostToDevice, ci));
+      MREP_CUDA_CHECK(cudaEventRecord(g_ctx.ev_in[c], ci));
+      MREP_CUDA_CHECK(cudaStreamWaitEvent(v.st, g_ctx.ev_in[c], 0));
+      if ((rc = launch(v)) != MREP_OK) return rc;
+      MREP_CUDA_CHECK(cudaEventRecord(g_ctx.ev_comp[c], v.st));
+      MREP_CUDA_CHECK(cudaStreamWaitEvent(co, g_ctx.ev_comp[c], 0));
+      MREP_CUDA_CHECK(cudaMemcpyAsync(out_t + lo, v.dt, v.cnt * sizeof(double),
+                                      cudaMemcpyDeviceToHost, co));
+      MREP_CUDA_CHECK(cudaMemcpyAsync(out_foot + lo * d, v.dfoot, v.cnt * d * sizeof(double),
+                                      cudaMemcpyDeviceToHost, co));
+      MREP_CUDA_CHECK(cudaMemcpyAsync(out_dist + lo, v.ddist, v.cnt * sizeof(double),
+                                      cudaMemcpyDeviceToHost, co));
+      MREP_CUDA_CHECK(cudaMemcpyAsync(out_cand + lo, v.dcand, v.cnt * sizeof(int64_t),
+                                      cudaMemcpyDeviceToHost, co));
+      if (out_seg)
+        MREP_CUDA_CHECK(cudaMemcpyAsync(out_seg + lo, v.dseg, v.cnt * sizeof(int32_t),
+                                        cudaMemcpyDeviceToHost, co));
+    }
+    MREP_CUDA_CHECK(cudaStreamSynchronize(g_ctx.cout));
+    for (int i = 0; i < NS; ++i) MREP_CUDA_CHECK(cudaStreamSynchronize(g_ctx.slot[i].st));
+    if (counters_host) {
+      for (auto& s : g_ctx.slot) {
+        uint64_t cc[MREP_NUM_COUNTERS];
+        MREP_CUDA_CHECK(cudaMemcpy(cc, s.dcnt, sizeof cc, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < MREP_NUM_COUNTERS; ++i) counters_host[i] += cc[i];
+      }
+    }
+    return MREP_OK;
+  }
+
   auto write_back = [&](Slot& s) -> int {
     if (!s.busy) return MREP_OK;
     MREP_CUDA_CHECK(cudaEventSynchronize(s.done));
@@ -117,14 +243,41 @@ int host_pipeline(int d, const double* queries, const int32_t* curve_ids, int64_
     return MREP_OK;
   };
 
-  for (auto& s : g_ctx.slot)
-    MREP_CUDA_CHECK(cudaMemsetAsync(s.dcnt, 0, MREP_NUM_COUNTERS * sizeof(uint64_t), s.st));
-  int64_t nchunks = (n + CHUNK - 1) / CHUNK;
+  // Chunk schedule: about 8 chunks per call (2^16 .. 2^19 queries each) so
+  // the first upload and the last download are short and up to NS chunks
+  // overlap their copies and kernels; MREP_E2E_CHUNK forces a size.
+  std::vector<std::pair<int64_t, int64_t>> chunks;
+  int64_t CHUNK = getenv("MREP_E2E_CHUNK") ? chunk_size()
+                                            : std::min<int64_t>(CHUNK_MAX, std::max<int64_t>(
+                                                  (int64_t)1 << 16, (n + 7) / 8));
+  for (int64_t lo = 0; lo < n; lo += CHUNK) chunks.push_back({lo, std::min(CHUNK, n - lo)});
+  const int64_t nchunks = (int64_t)chunks.size();
+  // MREP_E2E_TRACE=1: per-chunk device timeline (H2D / kernels / D2H ends)
+  static const bool trace = getenv("MREP_E2E_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  std::vector<double> th;
+  cudaEvent_t t0ev = nullptr;
+  auto host_ms = [] {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  double h0 = host_ms();
+  if (trace) {
+    cudaEventCreate(&t0ev);
+    cudaEventRecord(t0ev, g_ctx.slot[0].st);
+  }
+  auto mark = [&](cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tev.push_back(e);
+  };
   for (int64_t c = 0; c < nchunks; ++c) {
-    Slot& s = g_ctx.slot[c & 1];
+    Slot& s = g_ctx.slot[c % NS];
     if ((rc = write_back(s)) != MREP_OK) return rc;
-    s.lo = c * CHUNK;
-    s.cnt = (s.lo + CHUNK <= n) ? CHUNK : n - s.lo;
+    s.lo = chunks[c].first;
+    s.cnt = chunks[c].second;
     const double* src = queries + s.lo * d;
     const int32_t* csrc = curve_ids ? curve_ids + s.lo : nullptr;
     if (!pin_in) {
@@ -140,8 +293,12 @@ int host_pipeline(int d, const double* queries, const int32_t* curve_ids, int64_
     if (csrc)
       MREP_CUDA_CHECK(
           cudaMemcpyAsync(s.dcur, csrc, s.cnt * sizeof(int32_t), cudaMemcpyHostToDevice, s.st));
+    mark(s.st);
+    if (trace) th.push_back(host_ms() - h0);
     rc = launch(s);
     if (rc != MREP_OK) return rc;
+    mark(s.st);
+    if (trace) th.push_back(host_ms() - h0);
     double* ht = pin_out ? out_t + s.lo : s.ht;
     double* hf = pin_out ? out_foot + s.lo * d : s.hfoot;
     double* hd = pin_out ? out_dist + s.lo : s.hdist;
@@ -158,10 +315,25 @@ int host_pipeline(int d, const double* queries, const int32_t* curve_ids, int64_
       MREP_CUDA_CHECK(
           cudaMemcpyAsync(hs, s.dseg, s.cnt * sizeof(int32_t), cudaMemcpyDeviceToHost, s.st));
     MREP_CUDA_CHECK(cudaEventRecord(s.done, s.st));
+    mark(s.st);
     s.busy = true;
   }
   for (auto& s : g_ctx.slot)
     if ((rc = write_back(s)) != MREP_OK) return rc;
+  if (trace) {
+    cudaDeviceSynchronize();
+    for (int64_t c = 0; c < nchunks; ++c) {
+      float a = 0, b = 0, e = 0;
+      cudaEventElapsedTime(&a, t0ev, tev[3 * c]);
+      cudaEventElapsedTime(&b, t0ev, tev[3 * c + 1]);
+      cudaEventElapsedTime(&e, t0ev, tev[3 * c + 2]);
+      fprintf(stderr, "chunk %lld n=%lld: h2d_end %.3f  kern_end %.3f  d2h_end %.3f  (host enq %.3f..%.3f)\n",
+              (long long)c, (long long)chunks[c].second, a, b, e, th[2 * c], th[2 * c + 1]);
+    }
+    fprintf(stderr, "host total %.3f ms\n", host_ms() - h0);
+    for (auto ev : tev) cudaEventDestroy(ev);
+    cudaEventDestroy(t0ev);
+  }
   if (counters_host) {
     for (auto& s : g_ctx.slot) {
       uint64_t c[MREP_NUM_COUNTERS];

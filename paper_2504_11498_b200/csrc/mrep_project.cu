@@ -653,6 +653,20 @@ __device__ __forceinline__ bool prep_pair_cut(const TableView& T, int64_t s, con
     mag += fabs(P.bseg[i]);
   }
   if (dmin_b - 1e-9 * mag > cut_sq) return false;
+  // E = D'/2 of one strict sign on [0, 1] (all six Bernstein ordinates,
+  // kept clear of underflow): every monotone piece's restricted ordinates
+  // are positively weighted combinations of them, so each piece has
+  // b0 > 0, or b0 < 0 with b0 b5 > 0 -- the elimination of
+  // _kernels.py:427-441 drops them all.  No survivor: skip the quartic.
+  {
+    bool pos = true, neg = true;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      pos = pos && P.bseg[i] > 1e-290;
+      neg = neg && P.bseg[i] < -1e-290;
+    }
+    if (pos || neg) return false;
+  }
   double ep[5];
 #pragma unroll
   for (int k = 0; k < 5; ++k) ep[k] = (double)(k + 1) * e[k + 1];
