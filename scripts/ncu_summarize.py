@@ -1,6 +1,9 @@
 """Summarise ncu captures into profiles/ (JSON + text), run here (no GPU).
 
-    python scripts/ncu_summarize.py <full.ncu-rep> <launches.csv> <tag>
+    python scripts/ncu_summarize.py <full.ncu-rep> <launches.csv> <tag> [config]
+
+The per-kernel DRAM traffic goes into profiles/ncu_summary.json under
+dram_bytes_per_launch_by_config[config] (bench.py reads it as `traffic`).
 """
 import csv
 import json
@@ -52,6 +55,7 @@ def launches(path):
 
 def main():
     rep, ll, tag = sys.argv[1], sys.argv[2], sys.argv[3]
+    config = sys.argv[4] if len(sys.argv) > 4 else "cfg2"
     kern = full(rep)
     lst = launches(ll)
     prof = os.path.join(ROOT, "profiles")
@@ -62,9 +66,15 @@ def main():
             1e9 if k.get("dram__bytes_read.sum.unit") == "Gbyte" else 1e3
             if k.get("dram__bytes_read.sum.unit") == "Kbyte" else 1.0)
         per.setdefault(name, (k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"]) * mult)
-    summary = {"tag": tag, "source": os.path.basename(rep),
-               "dram_bytes_per_launch": per, "kernels": kern}
-    json.dump(summary, open(os.path.join(prof, "ncu_summary.json"), "w"), indent=1)
+    path = os.path.join(prof, "ncu_summary.json")
+    summary = json.load(open(path)) if os.path.exists(path) else {}
+    summary.setdefault("dram_bytes_per_launch_by_config", {})[config] = per
+    summary.setdefault("kernels_by_config", {})[config] = kern
+    summary.setdefault("sources", {})[config] = os.path.basename(rep)
+    if config == "cfg2":
+        summary.update({"tag": tag, "source": os.path.basename(rep),
+                        "dram_bytes_per_launch": per, "kernels": kern})
+    json.dump(summary, open(path, "w"), indent=1)
     with open(os.path.join(prof, f"{tag}_ncu_kernels.txt"), "w") as f:
         for k in kern:
             f.write(k["kernel"][:90] + "\n")
