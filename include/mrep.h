@@ -204,6 +204,17 @@ MREP_API int mrep_eval_surface(int pu, int pv, const double* knots_u_dev, int64_
                                int64_t nu, int64_t nv, const double* uv_dev, int64_t n,
                                double* out_dev, void* stream);
 
+/* oracle.oracle_project_batch (oracle.py:95-128), the CLI's --verify oracle:
+ * dense scan of the grid points (grid_pts [grid][d] = curve at ts[grid],
+ * ts = linspace(domain)), then lock-step ternary search on each query's
+ * bracketing cells while the batch's widest bracket exceeds 1e-10.
+ * Synchronises the stream (the loop condition is checked on the host). */
+MREP_API int mrep_oracle_project_batch(int p, const double* knots_dev, int64_t m,
+                                       const double* ctrl_dev, int64_t ncp, int d,
+                                       const double* ts_dev, const double* grid_pts_dev,
+                                       int64_t grid, const double* queries_dev, int64_t n,
+                                       double* out_t_dev, double* out_dist_dev, void* stream);
+
 /* Synthetic-input helper, host only (no GPU): the reference fixture
  * generator's momentum walk (_fixtures.py _walk_points) for n points, given
  * v0 (already unit length) and the n-1 normal draws g [n-1][d]; writes the

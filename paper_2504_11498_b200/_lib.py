@@ -73,6 +73,8 @@ _SIGS = {
                                    _vp, _vp], _i32),
     "mrep_eval_surface": ([_i32, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _vp],
                           _i32),
+    "mrep_oracle_project_batch": ([_i32, _vp, _i64, _vp, _i64, _i32, _vp, _vp, _i64, _vp, _i64,
+                                   _vp, _vp, _vp], _i32),
     "mrep_synth_walk": ([_vp, _vp, _i64, _i32, _vp], _i32),
     "mrep_knot_span": ([_vp, _i64, _i32, _vp, _i64, _vp, _vp], _i32),
     "mrep_quartic_roots": ([_vp, _i64, _vp, _vp, _vp], _i32),
