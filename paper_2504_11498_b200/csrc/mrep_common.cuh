@@ -73,7 +73,9 @@ struct StageTimer {
 // [4] coordinate scale (max |coord| of the control points).
 // AABB hierarchy after the records: 8-ary over contiguous cubic ranges,
 // level 0 = one box per cubic, top level = 1 box; 6 doubles per box
-// (lo xyz, hi xyz).
+// (lo xyz, hi xyz).  A float copy of every box follows (6 floats, lo
+// rounded down, hi rounded up, so it encloses the double box): the hot
+// traversals test it on the FP32 pipe with a rigorous rounding allowance.
 constexpr int REC = 32;
 constexpr int R_W = 0, R_ST = 12, R_SP = 13, R_P = 16, R_TA = 28, R_TB = 29;
 constexpr int HDR = 64;
@@ -87,7 +89,8 @@ struct TableLayout {
   int64_t lvl_cnt[MAX_LEVELS];
   int64_t total_boxes;
   int64_t rec_off;  // in doubles from table start
-  int64_t box_off;  // in doubles from table start
+  int64_t box_off;   // in doubles from table start
+  int64_t fbox_off;  // in doubles from table start (float boxes, 3 doubles each)
   int64_t total_doubles;
 };
 
@@ -108,7 +111,8 @@ inline TableLayout table_layout(int64_t S, int rec = REC) {
   L.total_boxes = off;
   L.rec_off = HDR;
   L.box_off = HDR + S * rec;
-  L.total_doubles = L.box_off + off * 6;
+  L.fbox_off = L.box_off + off * 6;
+  L.total_doubles = L.fbox_off + off * 3;
   return L;
 }
 
@@ -116,6 +120,7 @@ struct TableView {
   const double* hdr;
   const double* rec;
   const double* box;
+  const float* fbox;
   int64_t S;
   int top;
   int64_t lvl_off[MAX_LEVELS];
@@ -129,6 +134,7 @@ inline TableView table_view(const void* table, int64_t S, int rec = REC) {
   v.hdr = base;
   v.rec = base + L.rec_off;
   v.box = base + L.box_off;
+  v.fbox = reinterpret_cast<const float*>(base + L.fbox_off);
   v.S = S;
   v.top = L.top;
   for (int i = 0; i < MAX_LEVELS; ++i) {

@@ -309,7 +309,8 @@ __device__ __forceinline__ void solve_segment(const TableView& T, int64_t s, con
 
 template <int D>
 __device__ __forceinline__ uint32_t child_mask(const TableView& T, int level, int64_t idx,
-                                               const double (&q)[D], double c2, QStats& st) {
+                                               const double (&q)[D], double c2, QStats& st,
+                                               bool fb = false, const FQ<D>* fq = nullptr) {
   // children of node idx at `level` live at level-1, indices idx*8 + c
   uint32_t m = 0;
   int64_t first = idx * FANOUT;
@@ -320,7 +321,7 @@ __device__ __forceinline__ uint32_t child_mask(const TableView& T, int level, in
     int64_t ch = first + c;
     if (ch < cnt) {
       st.boxes++;
-      if (box_lb2<D>(T, off + ch, q) <= c2) m |= 1u << c;
+      if ((fb ? box_lb2f<D>(T, off + ch, *fq) : box_lb2<D>(T, off + ch, q)) <= c2) m |= 1u << c;
     }
   }
   return m;
@@ -1105,6 +1106,8 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
   double scale = T.hdr[4];
 #pragma unroll
   for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
+  const bool fb = fbox_ok(scale);  // float box tests (see box_lb2f)
+  const FQ<D> fq = make_fq<D>(q, scale);
   if (active) {
     w.tkey[gi] = ~0ull;
     w.okey[gi] = ~0ull;
@@ -1121,7 +1124,7 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
         int64_t ch = first + c;
         if (ch < cnt) {
           st.boxes++;
-          double lb = box_lb2<D>(T, off + ch, q);
+          double lb = fb ? box_lb2f<D>(T, off + ch, fq) : box_lb2<D>(T, off + ch, q);
           if (c == 0 || lb < best) {
             best = lb;
             bi = ch;
@@ -1143,7 +1146,7 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
     // the bound current when it is reached.
     int level = T.top;
     int64_t idx = 0;
-    uint64_t masks = (uint64_t)child_mask<D>(T, level, 0, q, cut2(B.dmin, scale), st)
+    uint64_t masks = (uint64_t)child_mask<D>(T, level, 0, q, cut2(B.dmin, scale), st, fb, &fq)
                      << (8 * level);
     for (;;) {
       uint32_t mk = (uint32_t)(masks >> (8 * level)) & 0xffu;
@@ -1159,7 +1162,7 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
       double c2 = cut2(B.dmin, scale);
       st.boxes++;
       if (level == 1) {
-        bool need = box_lb2<D>(T, T.lvl_off[0] + ch, q) <= c2;
+        bool need = (fb ? box_lb2f<D>(T, T.lvl_off[0] + ch, fq) : box_lb2<D>(T, T.lvl_off[0] + ch, q)) <= c2;
         if (need) {
 #pragma unroll 1
           for (int k = 0; k < 2; ++k) offer_seam<D>(T, ch + k, q, B, st);
@@ -1174,10 +1177,10 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
             fall = true;
           }
         }
-      } else if (box_lb2<D>(T, T.lvl_off[level - 1] + ch, q) <= c2) {
+      } else if ((fb ? box_lb2f<D>(T, T.lvl_off[level - 1] + ch, fq) : box_lb2<D>(T, T.lvl_off[level - 1] + ch, q)) <= c2) {
         --level;
         idx = ch;
-        masks |= (uint64_t)child_mask<D>(T, level, idx, q, c2, st) << (8 * level);
+        masks |= (uint64_t)child_mask<D>(T, level, idx, q, c2, st, fb, &fq) << (8 * level);
       }
     }
   }
@@ -1206,7 +1209,7 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
         bool need = false;
         if (mine) {
           st.boxes++;
-          need = box_lb2<D>(TG, TG.lvl_off[0] + idx, q) <= cut2(B.dmin, scale);
+          need = (fb ? box_lb2f<D>(TG, TG.lvl_off[0] + idx, fq) : box_lb2<D>(TG, TG.lvl_off[0] + idx, q)) <= cut2(B.dmin, scale);
           if (need) {
 #pragma unroll 1
             for (int k = 0; k < 2; ++k) offer_seam<D>(TG, idx + k, q, B, st);
@@ -1240,7 +1243,7 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
         double lb = 0.0;
         if (ch < cnt && mine) {
           st.boxes++;
-          lb = box_lb2<D>(TG, off + ch, q);
+          lb = fb ? box_lb2f<D>(TG, off + ch, fq) : box_lb2<D>(TG, off + ch, q);
           need = lb <= c2;
         }
         unsigned m = __ballot_sync(0xffffffffu, need);
@@ -1440,6 +1443,8 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
   double scale = T.hdr[4];
 #pragma unroll
   for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
+  const bool fb = fbox_ok(scale);
+  const FQ<D> fq = make_fq<D>(q, scale);
   double dmin = INF;
   bool fall = false;
   SeamBest sb{INF, INF, INF, 0, 0};
@@ -1468,7 +1473,7 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
     double lb = INF;
     if (ex) {
       st.boxes++;
-      lb = box_lb2<D>(T, T.lvl_off[level - 1] + ch, q);
+      lb = fb ? box_lb2f<D>(T, T.lvl_off[level - 1] + ch, fq) : box_lb2<D>(T, T.lvl_off[level - 1] + ch, q);
     }
     const bool keep = ex && lb <= c2;
     if (level == 1) {
@@ -1577,7 +1582,7 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
   offers += __shfl_xor_sync(0xffffffffu, offers, 4);
   offers += __shfl_xor_sync(0xffffffffu, offers, 2);
   offers += __shfl_xor_sync(0xffffffffu, offers, 1);
-  const unsigned fb = __ballot_sync(0xffffffffu, fall) & gmask;
+  const unsigned fbal = __ballot_sync(0xffffffffu, fall) & gmask;
   if (active && sub == 0) {
     double4 rec;
     rec.x = q[0];
@@ -1586,8 +1591,8 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
     rec.w = dmin;
     *(double4*)(w.qs + g * 4) = rec;
     w.scnt[g] = (int64_t)offers;
-    w.flag[g] = fb ? 1 : 0;
-    if (fb) {
+    w.flag[g] = fbal ? 1 : 0;
+    if (fbal) {
       unsigned long long slot = atomicAdd(&w.cnt[3], 1ull);
       w.fb[slot] = g;
     }
@@ -1645,7 +1650,7 @@ __global__ void __launch_bounds__(BLOCK) wave_pairs(const __grid_constant__ Wave
     for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
     const double c2 = cut2(rec.w, scale);  // the query's final seam bound
     ++nboxes;
-    if (!(box_lb2<D>(T, T.lvl_off[0] + s, q) <= c2)) continue;
+    if (!((fbox_ok(scale) ? box_lb2f<D>(T, T.lvl_off[0] + s, make_fq<D>(q, scale)) : box_lb2<D>(T, T.lvl_off[0] + s, q)) <= c2)) continue;
     PairPrep P;
     if (!prep_pair_cut<D>(T, s, q, c2, P)) continue;
     ++npairs;
@@ -2374,6 +2379,14 @@ __global__ void set_boxes_kernel(const TableView* desc) {
     }
     __syncthreads();
   }
+  // float copy of every box of this curve (lo down, hi up)
+  const int64_t nb = T.lvl_off[T.top] + T.lvl_cnt[T.top];
+  float* fb = const_cast<float*>(T.fbox);
+  for (int64_t i = threadIdx.x; i < nb; i += blockDim.x)
+    for (int k = 0; k < 3; ++k) {
+      fb[i * 6 + k] = __double2float_rd(box[i * 6 + k]);
+      fb[i * 6 + 3 + k] = __double2float_ru(box[i * 6 + 3 + k]);
+    }
 }
 
 // Scheduler key of each query: (rank of its curve, Morton code inside that
@@ -2590,6 +2603,9 @@ int mrep_table_pack(const double* seg_pts, const double* seg_ta, const double* s
         box + L.lvl_off[lv - 1] * 6, L.lvl_cnt[lv - 1], box + L.lvl_off[lv] * 6, L.lvl_cnt[lv]);
     MREP_LAUNCH_CHECK();
   }
+  boxes_to_float_kernel<<<grid_for(L.total_boxes, 256), 256, 0, st>>>(
+      box, reinterpret_cast<float*>(base + L.fbox_off), L.total_boxes);
+  MREP_LAUNCH_CHECK();
   return MREP_OK;
 }
 

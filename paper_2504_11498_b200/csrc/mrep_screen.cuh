@@ -21,6 +21,57 @@ __device__ __forceinline__ double box_lb2(const TableView& T, int64_t box, const
   return acc;
 }
 
+// The same lower bound from the float copy of the box, on the FP32 pipe.
+// The float box encloses the double box and q is rounded to float once per
+// lane (FQ); every axis gap is shrunk by m = 6e-7 * scale (scale >= |q|
+// and every box coordinate), more than the float roundings of q and of the
+// subtraction can add, and the sum by 1e-6 relative -- so the result never
+// exceeds the exact squared distance: a box it prunes is also pruned by
+// box_lb2.  Tables/queries near the float range use box_lb2 (fbox_ok).
+template <int D>
+struct FQ {
+  float lo[D], hi[D];  // q + m and q - m in float
+};
+
+template <int D>
+__device__ __forceinline__ FQ<D> make_fq(const double (&q)[D], double scale) {
+  FQ<D> f;
+  const float m = (float)(6e-7 * scale);
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const float qf = __double2float_rn(q[k]);
+    f.lo[k] = qf + m;
+    f.hi[k] = qf - m;
+  }
+  return f;
+}
+
+template <int D>
+__device__ __forceinline__ double box_lb2f(const TableView& T, int64_t box, const FQ<D>& f) {
+  const float* b = T.fbox + box * 6;
+  float acc = 0.0f;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    float g = fmaxf(0.0f, fmaxf(__ldg(b + k) - f.lo[k], f.hi[k] - __ldg(b + 3 + k)));
+    acc += g * g;
+  }
+  return (double)acc * (1.0 - 1e-6);
+}
+
+// float copy of n boxes: lo rounded down, hi rounded up (encloses the box)
+static __global__ void boxes_to_float_kernel(const double* box, float* fbox, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    fbox[i * 6 + k] = __double2float_rd(box[i * 6 + k]);
+    fbox[i * 6 + 3 + k] = __double2float_ru(box[i * 6 + 3 + k]);
+  }
+}
+
+// float boxes are usable while every coordinate stays far inside float range
+__device__ __forceinline__ bool fbox_ok(double scale) { return scale < 1e15; }
+
 // Cut-off radius: a box whose lower bound exceeds it cannot hold a candidate
 // inside dmin + 1e-12 (margins cover rounding of the box bound and of the
 // foot-point evaluation; they only ever keep extra work).

@@ -1119,6 +1119,9 @@ int mrep_surface_table_pack(const double* patch_pts, const double* patch_iv, int
         box + L.lvl_off[lv - 1] * 6, L.lvl_cnt[lv - 1], box + L.lvl_off[lv] * 6, L.lvl_cnt[lv]);
     MREP_LAUNCH_CHECK();
   }
+  boxes_to_float_kernel<<<grid_for(L.total_boxes, 256), 256, 0, st>>>(
+      box, reinterpret_cast<float*>(base + L.fbox_off), L.total_boxes);
+  MREP_LAUNCH_CHECK();
   MREP_CUDA_CHECK(cudaFreeAsync(dorder, st));
   MREP_CUDA_CHECK(cudaStreamSynchronize(st));  // the host order vector dies here
   return MREP_OK;

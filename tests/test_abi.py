@@ -56,6 +56,7 @@ def test_table_bytes():
     from paper_2504_11498_b200 import _lib
     lib = _lib.load_library()
     # header 64 + 32 doubles per cubic + 6 per box (8-ary levels incl. root)
-    assert lib.mrep_table_bytes(1) == (64 + 32 + 6 * (1 + 1)) * 8
-    assert lib.mrep_table_bytes(510) == (64 + 32 * 510 + 6 * (510 + 64 + 8 + 1)) * 8
+    # + the float copy of every box (6 floats = 3 doubles)
+    assert lib.mrep_table_bytes(1) == (64 + 32 + 9 * (1 + 1)) * 8
+    assert lib.mrep_table_bytes(510) == (64 + 32 * 510 + 9 * (510 + 64 + 8 + 1)) * 8
     assert lib.mrep_table_bytes(0) < 0
