@@ -517,7 +517,7 @@ def main():
     value = n_total / (ms / 1e3)
     # own kernels per projection call: Morton keys + 5 cub radix-sort kernels
     # (histogram, exclusive sum, onesweep passes) + 8 wavefront kernels; dense: 2
-    passes = (30 + (14 if args.config == "cfg3" else 0) + 7) // 8
+    passes = (24 + 7) // 8 if args.config != "cfg3" else (30 + 14 + 7) // 8
     launches_per_step = 1 + 2 + passes + (8 if not dense else 2)
     if surf:  # morton + sort + traverse, solve, select x2, fallback
         launches_per_step = 1 + 2 + passes + 5

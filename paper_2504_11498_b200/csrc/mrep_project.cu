@@ -2699,8 +2699,16 @@ static int project_chunk(const void* table, int64_t S, int d, const double* quer
     if (d == 3) morton_kernel<3><<<grid_for(n, 256), 256, 0, st>>>(queries, n, root, k_in, i_in);
     else morton_kernel<2><<<grid_for(n, 256), 256, 0, st>>>(queries, n, root, k_in, i_in);
     MREP_LAUNCH_CHECK();
+    // the top 24 key bits (8 per axis) order the queries as well as all 30
+    // do for warp coherence, with 3 radix passes instead of 4
+    static const int sort_bits = [] {
+      const char* e = getenv("MREP_SORT_BITS");
+      return e ? atoi(e) : 24;
+    }();
+    const int end_bit = d * 10;
+    const int begin_bit = (sort_bits > 0 && sort_bits < end_bit) ? end_bit - sort_bits : 0;
     MREP_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(wc + off_tmp, sort_tmp, k_in, k_out, i_in, i_out,
-                                                    (int)n, 0, d * 10, st));
+                                                    (int)n, begin_bit, end_bit, st));
     p.perm = i_out;
   }
   sort_tm.mark();
