@@ -2521,9 +2521,16 @@ static int project_batch_chunk(const CurveSet* cs, const double* queries, const 
   p.out_seg = out_seg;
   p.counters = counters;
   const int end_bit = 10 * d + cs->rank_bits;
+  // curve rank + the top 12 Morton bits: a curve holds ~10^2 queries, so a
+  // 16^3 cell grid already makes warps spatially coherent (fewer passes)
+  static const int morton_bits = [] {
+    const char* e = getenv("MREP_SORT_BITS_MULTI");
+    return e ? atoi(e) : 12;
+  }();
+  const int begin_bit = (morton_bits > 0 && morton_bits < 10 * d) ? 10 * d - morton_bits : 0;
   size_t sort_tmp = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (const uint64_t*)nullptr, (uint64_t*)nullptr,
-                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, end_bit,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, begin_bit, end_bit,
                                   st);
   size_t o_k = 0, o_i = o_k + 16 * (size_t)n, o_tmp = o_i + 8 * (size_t)n + 256;
   char* ws = nullptr;
@@ -2543,7 +2550,7 @@ static int project_batch_chunk(const CurveSet* cs, const double* queries, const 
                                                              cs->nc, end_bit, k_in, i_in);
   MREP_LAUNCH_CHECK();
   MREP_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(ws + o_tmp, sort_tmp, k_in, k_out, i_in, i_out,
-                                                  (int)n, 0, end_bit, st));
+                                                  (int)n, begin_bit, end_bit, st));
   sort_tm.mark();
   sort_tm.finish(0);
   p.perm = i_out;
