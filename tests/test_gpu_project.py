@@ -167,3 +167,92 @@ def test_edge_queries(gpu, oracle_lib):
     one = tab.project(q[:1])
     assert one[0].shape == (1,)
     assert np.all(np.isfinite(tab.project(q)[0].cpu().numpy()))
+
+
+def _star_polyline(k=12, dim=2):
+    """Degree-1 closed star: inner vertices exactly at distance 5 from the
+    origin (integer Pythagorean points), outer ones at radius 10 between
+    them -- every inner vertex (a seam) is an exact tie for the nearest
+    point of the origin, more than the 4-slot tie band holds."""
+    from paper_2504_11498_b200 import BSplineCurve
+    inner = [(5, 0), (4, 3), (3, 4), (0, 5), (-3, 4), (-4, 3), (-5, 0), (-4, -3), (-3, -4),
+             (0, -5), (3, -4), (4, -3)][:k]
+    pts = []
+    for i, (x, y) in enumerate(inner):
+        pts.append((float(x), float(y)))
+        a0 = np.arctan2(y, x)
+        x1, y1 = inner[(i + 1) % len(inner)]
+        a1 = np.arctan2(y1, x1)
+        am = a0 + 0.5 * ((a1 - a0 + np.pi) % (2 * np.pi) - np.pi)
+        pts.append((10.0 * np.cos(am), 10.0 * np.sin(am)))
+    pts.append(pts[0])
+    P = np.array(pts)
+    if dim == 3:
+        P = np.concatenate([P, np.zeros((len(P), 1))], axis=1)
+    n = len(P)
+    knots = np.concatenate(([0.0], np.linspace(0.0, 1.0, n), [1.0]))
+    return BSplineCurve(1, knots, P)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_exact_seam_ties_overflow_band(gpu, oracle_lib, dim):
+    """Twelve seams tie exactly for the origin: the screened kernel's tie band
+    overflows and the exact second pass / fallback must pick the reference's
+    winner (smallest t among the tied seams)."""
+    from paper_2504_11498_b200 import _lib as L, prepare_curve
+    from paper_2504_11498_b200 import _device as D
+    curve = _star_polyline(12, dim)
+    prep = prepare_curve(curve, 1e-4)
+    q = np.zeros((64, dim))
+    q[1:] = np.random.default_rng(0).uniform(-12, 12, (63, dim))
+    o = oracle_lib.project_block(prep.seg_pts, prep.seg_ta, prep.seg_tb, prep.seam_t,
+                                 prep.seam_pt, q)
+    assert o["dist"][0] == 5.0 and o["t"][0] == 0.0
+    tab = prep.table
+    cnt = np.zeros(L.NUM_COUNTERS, dtype=np.uint64)
+    outs = [tab.project(q, screen=s, extra_flags=f)
+            for s, f in ((False, 0), (True, 0), (True, L.MREP_GROUP), (True, L.MREP_PER_LANE),
+                         (True, L.MREP_FUSED))]
+    for out in outs:
+        t, foot, dist = out[0].cpu().numpy(), out[1].cpu().numpy(), out[2].cpu().numpy()
+        assert np.array_equal(t, o["t"]) or np.abs(t - o["t"]).max() <= 1e-12
+        assert np.abs(dist - o["dist"]).max() <= 1e-12
+        assert t[0] == 0.0 and dist[0] == 5.0
+    for a, b in zip(outs[0][:3], outs[1][:3]):
+        assert np.array_equal(a.cpu().numpy(), b.cpu().numpy())
+
+
+@pytest.mark.parametrize("scale", [1e-6, 1e6])
+def test_scaled_geometry(gpu, oracle_lib, scale):
+    """The cfg1 curve and queries scaled by 1e-6 / 1e6: screening margins are
+    relative, results still match the reference kernel's."""
+    from paper_2504_11498_b200 import BSplineCurve, prepare_curve, project_prepared
+    z = load_golden("project_cfg1_random.npz")
+    curve = BSplineCurve(int(z["degree"]), z["knots"], z["ctrl"] * scale)
+    prep = prepare_curve(curve, 1e-4 * scale)
+    q = z["queries"] * scale
+    t, foot, dist, cand = project_prepared(prep, q)
+    o = oracle_lib.project_block(prep.seg_pts, prep.seg_ta, prep.seg_tb, prep.seam_t,
+                                 prep.seam_pt, q, workers=8)
+    assert np.all(np.abs(t - o["t"]) <= 1e-6)
+    assert np.all(np.abs(dist - o["dist"]) <= np.maximum(1e-9 * o["dist"], 1e-12 * scale))
+
+
+def test_degenerate_and_far_queries(gpu, oracle_lib):
+    """A curve with coincident control points (zero-length cubic pieces) and
+    queries far outside the table box."""
+    from paper_2504_11498_b200 import BSplineCurve, prepare_curve, project_prepared
+    P = np.array([[0, 0, 0], [0, 0, 0], [0, 0, 0], [1, 1, 0], [1, 1, 0], [2, 0, 1], [2, 0, 1]],
+                 dtype=np.float64)
+    knots = np.concatenate(([0.0] * 4, [0.25, 0.5, 0.75], [1.0] * 4))
+    curve = BSplineCurve(3, knots, P)
+    prep = prepare_curve(curve, 1e-4)
+    rng = np.random.default_rng(3)
+    q = np.concatenate([rng.uniform(-1, 3, (500, 3)), rng.uniform(-1e7, 1e7, (20, 3)),
+                        P[[0, -1]]])
+    t, foot, dist, cand = project_prepared(prep, q)
+    o = oracle_lib.project_block(prep.seg_pts, prep.seg_ta, prep.seg_tb, prep.seam_t,
+                                 prep.seam_pt, q, workers=8)
+    assert np.all(np.abs(t - o["t"]) <= 1e-6)
+    assert np.all(np.abs(dist - o["dist"]) <= np.maximum(1e-9 * o["dist"], 1e-12))
+    assert dist[-2:].max() <= 1e-12  # the clamped ends lie on the curve
