@@ -1034,6 +1034,7 @@ struct WaveParams {
   // multi-curve batch (mrep_project_batch): per-curve table descriptors, the
   // curve of each query (caller order) and of each sorted position, and the
   // persistent traversal's task counter
+  int retest_min;  // re-test popped packet nodes at levels >= this (MREP_RETEST_LEVEL)
   const TableView* tabs;
   const int32_t* qcurve;
   int64_t ncurves;
@@ -1229,11 +1230,20 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
         }
         continue;
       }
+      // re-test the popped node against the bound as it is now (seams found
+      // since the push may have tightened it): one test instead of eight
+      double c2 = cut2(B.dmin, scale);
+      if (level >= w.retest_min && level < TG.top && mine) {
+        st.boxes++;
+        const int64_t nb = TG.lvl_off[level] + idx;
+        mine = (fb ? box_lb2f<D>(TG, nb, fq) : box_lb2<D>(TG, nb, q)) <= c2;
+      }
+      mask = __ballot_sync(0xffffffffu, mine);
+      if (!mask) continue;
       // children (level-1, idx*8 + c): best-first -- pushed in decreasing order
       // of the packet leader's box distance so the nearest child pops first and
       // the seam bound tightens before the far leaves are reached
       int64_t first = idx * FANOUT, cnt = TG.lvl_cnt[level - 1], off = TG.lvl_off[level - 1];
-      double c2 = cut2(B.dmin, scale);
       double key[FANOUT];
       unsigned msk[FANOUT];
 #pragma unroll
@@ -2222,6 +2232,11 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   w.ncurves = ncurves;
   w.gcur = MULTI ? (int32_t*)(base + o_gc) : nullptr;
   w.queue = w.cnt + 5;
+  static const int retest_min = [] {
+    const char* e = getenv("MREP_RETEST_LEVEL");
+    return e ? atoi(e) : 1;
+  }();
+  w.retest_min = retest_min;
   MREP_CUDA_CHECK(cudaMemsetAsync(w.cnt, 0, 8 * sizeof(unsigned long long), st));
   auto persist_grid = [](const void* fn, int block) {
     int dev = 0, sms = 148, per = 1;
