@@ -1035,6 +1035,8 @@ struct WaveParams {
   // curve of each query (caller order) and of each sorted position, and the
   // persistent traversal's task counter
   int retest_min;  // re-test popped packet nodes at levels >= this (MREP_RETEST_LEVEL)
+  int trav_bern;   // Bernstein distance test at packet leaves (MREP_TRAV_BERN)
+  int trav_sort;   // full best-first child order in packets (MREP_TRAV_SORT)
   const TableView* tabs;
   const int32_t* qcurve;
   int64_t ncurves;
@@ -1063,7 +1065,8 @@ __device__ __forceinline__ double dmin_of(const WaveParams& w, int64_t g) {
 }
 
 // Packet traversal: the 32 (Morton-adjacent) queries of a warp walk the AABB
-// tree together.  One DFS stack per warp lives in shared memory; each entry
+// tree together (nearest child on top of the stack; the Bernstein distance
+// test of a leaf is left to W2, which runs it densely per pair).  One DFS stack per warp lives in shared memory; each entry
 // carries the lane mask of the queries that still need the node, so control
 // flow is warp-uniform and every box is one broadcast load.
 constexpr int PSTACK = 72;  // >= 8 entries per level x 9 levels
@@ -1216,7 +1219,7 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
             for (int k = 0; k < 2; ++k) offer_seam<D>(TG, idx + k, q, B, st);
             // emit the pair only if the cubic's Bernstein distance bound can
             // still reach the tie band (with the bound its own seams just set)
-            need = bern_may_reach<D>(TG, idx, q, cut2(B.dmin, scale));
+            if (w.trav_bern) need = bern_may_reach<D>(TG, idx, q, cut2(B.dmin, scale));
           }
         }
         unsigned long long slot = wave_append(&w.cnt[0], need);
@@ -1259,6 +1262,30 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
         unsigned m = __ballot_sync(0xffffffffu, need);
         msk[c] = m;
         key[c] = m ? __shfl_sync(0xffffffffu, lb, __ffs(m) - 1) : -1.0;
+      }
+      if (!w.trav_sort) {
+        // nearest child on top, the others below in index order
+        int bc = -1;
+        double bk = 0.0;
+#pragma unroll
+        for (int c = 0; c < FANOUT; ++c)
+          if (msk[c] && (bc < 0 || key[c] < bk)) {
+            bc = c;
+            bk = key[c];
+          }
+#pragma unroll
+        for (int c = 0; c < FANOUT; ++c) {
+          if (msk[c] && c != bc) {
+            if (lane == 0) S[sp] = pk(msk[c], level - 1, first + c);
+            ++sp;
+          }
+        }
+        if (bc >= 0) {
+          if (lane == 0) S[sp] = pk(msk[bc], level - 1, first + bc);
+          ++sp;
+        }
+        __syncwarp();
+        continue;
       }
       // sort (key, child) descending: 8-input network, uniform across the warp
       int ord8[FANOUT];
@@ -2237,6 +2264,16 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
     return e ? atoi(e) : 1;
   }();
   w.retest_min = retest_min;
+  static const int trav_bern = [] {
+    const char* e = getenv("MREP_TRAV_BERN");
+    return e ? atoi(e) : 0;
+  }();
+  static const int trav_sort = [] {
+    const char* e = getenv("MREP_TRAV_SORT");
+    return e ? atoi(e) : 0;
+  }();
+  w.trav_bern = trav_bern;
+  w.trav_sort = trav_sort;
   MREP_CUDA_CHECK(cudaMemsetAsync(w.cnt, 0, 8 * sizeof(unsigned long long), st));
   auto persist_grid = [](const void* fn, int block) {
     int dev = 0, sms = 148, per = 1;
