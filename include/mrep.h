@@ -44,6 +44,7 @@ extern "C" {
 #define MREP_PACKET 32u   /* screened traversal: force warp-packet BVH walks (default: by query density) */
 #define MREP_PER_LANE 64u /* screened traversal: force per-lane BVH walks */
 #define MREP_GROUP 128u   /* screened traversal: force one 8-lane group per query */
+#define MREP_CELLS 256u   /* screened traversal: use the table's cell index (mrep_cells_build) */
 
 /* Work counters written (accumulated) by mrep_project when `counters_dev` != NULL. */
 #define MREP_CNT_PAIRS 0      /* (query, cubic) pairs solved: E, quartic, rebase, pieces */
@@ -220,6 +221,18 @@ MREP_API int mrep_oracle_project_batch(int p, const double* knots_dev, int64_t m
  * v0 (already unit length) and the n-1 normal draws g [n-1][d]; writes the
  * un-normalised walk pts [n][d].  Bit-identical to the numpy loop. */
 MREP_API int mrep_synth_walk(const double* v0, const double* g, int64_t n, int d, double* pts);
+
+/* Cell index of a single-curve table (dense query batches): a uniform grid
+ * of grid^d cells over the table box (+10% each side); each cell lists, in
+ * nearest-first order, every cubic that can hold a tie-band candidate for
+ * any query inside it, so projection with MREP_CELLS replaces the tree walk
+ * for in-grid queries (results bit-identical).  mrep_cells_bytes sizes the
+ * caller-owned buffer (synchronous); mrep_cells_build fills it and records
+ * it in the table header (the buffer must outlive the table's use).
+ * S <= 16384, grid <= 256. */
+MREP_API int64_t mrep_cells_bytes(const void* table_dev, int64_t S, int d, int grid, void* stream);
+MREP_API int mrep_cells_build(void* table_dev, int64_t S, int d, int grid, void* cells_dev,
+                              int64_t bytes, void* stream);
 
 /* Knot span of each parameter: searchsorted(knots, t, 'right') - 1 clipped
  * to [p, m - p - 2] (the span convention of core.py:108-112). */

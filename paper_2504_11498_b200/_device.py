@@ -161,6 +161,33 @@ class DeviceTable:
         self.buf = torch.empty((nbytes // 8,), dtype=torch.float64, device=sp.device)
         L.check(L.lib().mrep_table_pack(L.ptr(sp), *[L.ptr(a) for a in args], self.S, self.d,
                                         L.ptr(self.buf), L.stream_ptr()))
+        self.cells = None
+        self.cells_tried = False
+
+    # a cell index pays off for dense batches (queries >> cubics); built once,
+    # lazily, on the first such batch (mrep_cells_build)
+    CELL_MIN_QUERIES = 1 << 16
+    CELL_MAX_CUBICS = 1 << 14
+
+    def build_cells(self, grid=None):
+        torch = L._torch()
+        grid = grid or (64 if self.d == 3 else 256)
+        nb = L.lib().mrep_cells_bytes(L.ptr(self.buf), self.S, self.d, grid, L.stream_ptr())
+        if nb <= 0:
+            L.check(1)
+        self.cells = torch.empty((nb + 3) // 4, dtype=torch.int32, device=self.buf.device)
+        L.check(L.lib().mrep_cells_build(L.ptr(self.buf), self.S, self.d, grid,
+                                          L.ptr(self.cells), nb, L.stream_ptr()))
+        return self
+
+    def _cell_flag(self, n, screen):
+        if not screen or self.S > self.CELL_MAX_CUBICS:
+            return 0
+        if self.cells is None and not self.cells_tried and n >= max(self.CELL_MIN_QUERIES,
+                                                                    8 * self.S):
+            self.cells_tried = True
+            self.build_cells()
+        return L.MREP_CELLS if (self.cells is not None and n >= 8 * self.S) else 0
 
     def project(self, queries, clip_tol=1e-6, max_iter=8, soundness_samples=0, screen=True,
                 stats=False, counters=None, extra_flags=0):
@@ -180,6 +207,8 @@ class DeviceTable:
         sound = torch.empty((n,), dtype=torch.float64, device=dev) if stats else None
         flags = (L.MREP_STATS if stats else 0) | (L.MREP_SCREEN if (screen and not stats) else 0)
         flags |= int(extra_flags)
+        if not (extra_flags & (L.MREP_PACKET | L.MREP_PER_LANE | L.MREP_GROUP)):
+            flags |= self._cell_flag(n, screen and not stats)
         L.check(L.lib().mrep_project(
             L.ptr(self.buf), self.S, self.d, L.ptr(q), n, float(clip_tol), int(max_iter),
             int(soundness_samples), flags, L.ptr(t), L.ptr(foot), L.ptr(dist), L.ptr(cand),
@@ -197,8 +226,9 @@ class DeviceTable:
         t, foot, dist, cand, seg = out
         import ctypes
         p = lambda a: ctypes.c_void_p(a.ctypes.data if a is not None else 0)  # noqa: E731
+        flags = (L.MREP_SCREEN | self._cell_flag(n, True)) if screen else 0
         L.check(L.lib().mrep_project_host(
             L.ptr(self.buf), self.S, self.d, p(q), n, float(clip_tol), int(max_iter),
-            L.MREP_SCREEN if screen else 0, p(t), p(foot), p(dist), p(cand), p(seg),
+            flags, p(t), p(foot), p(dist), p(cand), p(seg),
             p(counters) if counters is not None else ctypes.c_void_p(0)))
         return out

@@ -27,6 +27,7 @@ MREP_TIMING = 16
 MREP_PACKET = 32
 MREP_PER_LANE = 64
 MREP_GROUP = 128
+MREP_CELLS = 256
 NUM_COUNTERS = 8
 CNT_PAIRS, CNT_SURVIVORS, CNT_CLIP_ITERS, CNT_SEAMS, CNT_BOXES, CNT_PASS2, CNT_HULL_MISS = range(7)
 
@@ -76,6 +77,8 @@ _SIGS = {
     "mrep_oracle_project_batch": ([_i32, _vp, _i64, _vp, _i64, _i32, _vp, _vp, _i64, _vp, _i64,
                                    _vp, _vp, _vp], _i32),
     "mrep_synth_walk": ([_vp, _vp, _i64, _i32, _vp], _i32),
+    "mrep_cells_bytes": ([_vp, _i64, _i32, _i32, _vp], _i64),
+    "mrep_cells_build": ([_vp, _i64, _i32, _i32, _vp, _i64, _vp], _i32),
     "mrep_knot_span": ([_vp, _i64, _i32, _vp, _i64, _vp, _vp], _i32),
     "mrep_quartic_roots": ([_vp, _i64, _vp, _vp, _vp], _i32),
     "mrep_newton_quartic_roots": ([_vp, _i64, _vp, _vp, _vp], _i32),

@@ -25,6 +25,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstdint>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -1081,9 +1082,16 @@ __device__ __forceinline__ unsigned long long pk(unsigned mask, int level, int64
 // belong to different curves (queries are sorted by curve, so a warp spans at
 // most a few): the packet walk runs once per distinct curve of the warp with
 // that curve's lanes as the packet mask, so control flow stays warp-uniform.
-template <int D, bool MULTI, bool PACKET>
+// traversal modes of traverse_task
+enum { TM_LANE = 0, TM_PACKET = 1, TM_CELLS = 2 };
+
+// cell index of a table (mrep_cells_build): header slots
+constexpr int H_CELLS = 8, H_GRID = 9, H_GLO = 10, H_GINV = 13, H_GHI = 16;
+
+template <int D, bool MULTI, int TM>
 __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
                                               unsigned long long* S, int lane) {
+  constexpr bool PACKET = TM == TM_PACKET;
   bool active = gi < w.n;
   QStats st{};
   int64_t qi = active ? (w.perm ? (int64_t)w.perm[gi] : gi) : 0;
@@ -1116,7 +1124,25 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
     w.tkey[gi] = ~0ull;
     w.okey[gi] = ~0ull;
   }
-  if (active) {  // greedy descent: first bound from the seams of a nearby cubic
+  // cell mode: the query's cell in the uniform grid over the table box lists
+  // every cubic that can hold a candidate for ANY query of the cell
+  // (mrep_cells_build), nearest first; queries outside the grid walk the tree
+  bool incell = false;
+  int64_t cell = 0;
+  if (TM == TM_CELLS && active) {
+    const int G = (int)T.hdr[H_GRID];
+    incell = G > 0;
+    int64_t ci[3] = {0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      incell = incell && q[k] >= T.hdr[H_GLO + k] && q[k] < T.hdr[H_GHI + k];
+      double u = (q[k] - T.hdr[H_GLO + k]) * T.hdr[H_GINV + k];
+      int64_t c = (int64_t)u;
+      ci[k] = c < 0 ? 0 : (c >= G ? G - 1 : c);
+    }
+    cell = (ci[0] * G + ci[1]) * (D == 3 ? G : 1) + (D == 3 ? ci[2] : 0);
+  }
+  if (active && !incell) {  // greedy descent: first bound from the seams of a nearby cubic
     int level = T.top;
     int64_t idx = 0;
     while (level > 0) {
@@ -1141,8 +1167,36 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
 #pragma unroll 1
     for (int e = 0; e < 2; ++e) offer_seam<D>(T, idx + e, q, B, st);
   }
+  if (TM == TM_CELLS && incell) {
+    const int G = (int)T.hdr[H_GRID];
+    const int64_t ncell = (int64_t)G * G * (D == 3 ? G : 1);
+    const int32_t* off = reinterpret_cast<const int32_t*>(
+        (uintptr_t)__double_as_longlong(T.hdr[H_CELLS]));
+    const int32_t* ids = off + ncell + 1;
+    const int32_t a = __ldg(off + cell), b = __ldg(off + cell + 1);
+#pragma unroll 1
+    for (int32_t k = a; k < b; ++k) {
+      const int64_t ch = __ldg(ids + k);
+      st.boxes++;
+      bool need = (fb ? box_lb2f<D>(T, T.lvl_off[0] + ch, fq) : box_lb2<D>(T, T.lvl_off[0] + ch, q)) <=
+                  cut2(B.dmin, scale);
+      if (need) {
+#pragma unroll 1
+        for (int e = 0; e < 2; ++e) offer_seam<D>(T, ch + e, q, B, st);
+      }
+      unsigned long long slot = wave_append(&w.cnt[0], need);
+      if (need) {
+        if (slot < w.pcap) {
+          w.pq[slot] = (uint32_t)gi;
+          w.ps[slot] = (uint32_t)ch;
+        } else {
+          fall = true;
+        }
+      }
+    }
+  }
   unsigned todo = PACKET ? __ballot_sync(0xffffffffu, active) : 0u;
-  if (!PACKET && active) {
+  if ((TM == TM_LANE || (TM == TM_CELLS && !incell)) && active) {
     // Per-lane depth-first walk, for incoherent queries (a warp's lanes far
     // apart, e.g. ~100 random queries per curve in a batch): a packet would
     // drag every lane through the union of 32 paths.  8-bit child masks per
@@ -1364,13 +1418,13 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
 // curve, heaviest curve (most cubics) first, Morton order inside a curve;
 // persistent warps pull 32-position tasks from an atomic work queue, so the
 // long tasks start first and the short ones fill the tail (LPT order).
-template <int D, bool MULTI, bool PACKET>
+template <int D, bool MULTI, int TM>
 __global__ void __launch_bounds__(BLOCK) wave_traverse(const __grid_constant__ WaveParams w) {
   __shared__ unsigned long long stk[BLOCK / 32][PSTACK];
   const int lane = threadIdx.x & 31;
   unsigned long long* S = stk[threadIdx.x >> 5];
   if (!MULTI) {
-    traverse_task<D, false, PACKET>(w, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, S, lane);
+    traverse_task<D, false, TM>(w, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, S, lane);
   } else {
     for (;;) {
       unsigned long long task = 0;
@@ -1378,7 +1432,7 @@ __global__ void __launch_bounds__(BLOCK) wave_traverse(const __grid_constant__ W
       task = __shfl_sync(0xffffffffu, task, 0);
       int64_t base = (int64_t)task * 32;
       if (base >= w.n) break;
-      traverse_task<D, true, PACKET>(w, base + lane, S, lane);
+      traverse_task<D, true, TM>(w, base + lane, S, lane);
     }
   }
 }
@@ -2179,9 +2233,12 @@ static int launch_project(const ProjParams& p, unsigned flags, cudaStream_t st) 
 }
 
 
-enum { TRAV_PACKET = 0, TRAV_LANE = 1, TRAV_GROUP = 2 };
+enum { TRAV_PACKET = 0, TRAV_LANE = 1, TRAV_GROUP = 2, TRAV_CELLS = 3 };
 
 static int trav_mode(unsigned flags, int64_t n, int64_t S, int top) {
+  // MREP_CELLS: the caller built a cell index (mrep_cells_build) for this table
+  if ((flags & MREP_CELLS) && !(flags & (MREP_PACKET | MREP_PER_LANE | MREP_GROUP)))
+    return top > 7 ? TRAV_PACKET : TRAV_CELLS;
   if (flags & MREP_PACKET) return TRAV_PACKET;
   if (flags & MREP_PER_LANE) return top > 7 ? TRAV_PACKET : TRAV_LANE;
   if (flags & MREP_GROUP) return top > 8 ? TRAV_PACKET : TRAV_GROUP;
@@ -2299,16 +2356,18 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   } else if (MULTI) {
     unsigned need = grid_for(n, BLOCK);
     if (tmode == TRAV_PACKET) {
-      unsigned g = persist_grid((const void*)wave_traverse<D, true, true>, BLOCK);
-      wave_traverse<D, true, true><<<g < need ? g : need, BLOCK, 0, st>>>(w);
+      unsigned g = persist_grid((const void*)wave_traverse<D, true, TM_PACKET>, BLOCK);
+      wave_traverse<D, true, TM_PACKET><<<g < need ? g : need, BLOCK, 0, st>>>(w);
     } else {
-      unsigned g = persist_grid((const void*)wave_traverse<D, true, false>, BLOCK);
-      wave_traverse<D, true, false><<<g < need ? g : need, BLOCK, 0, st>>>(w);
+      unsigned g = persist_grid((const void*)wave_traverse<D, true, TM_LANE>, BLOCK);
+      wave_traverse<D, true, TM_LANE><<<g < need ? g : need, BLOCK, 0, st>>>(w);
     }
   } else if (tmode == TRAV_PACKET) {
-    wave_traverse<D, false, true><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
+    wave_traverse<D, false, TM_PACKET><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
+  } else if (tmode == TRAV_CELLS) {
+    wave_traverse<D, false, TM_CELLS><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
   } else {
-    wave_traverse<D, false, false><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
+    wave_traverse<D, false, TM_LANE><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
   }
   MREP_LAUNCH_CHECK();
   tm.mark();
@@ -2668,6 +2727,151 @@ int mrep_table_pack(const double* seg_pts, const double* seg_ta, const double* s
   return MREP_OK;
 }
 
+
+// ------------------------------------------------------------ cell index
+// A uniform grid over the table's root box (+10% each side).  For every
+// cell C the list holds each cubic s with
+//   boxdist(C', box_s)^2 <= cut2(UB_C, scale_C),
+//   UB_C = min over seams of the farthest distance from C' to the seam,
+// where C' is C grown by a rounding allowance.  Any query q in C has a seam
+// within UB_C, so dmin(q) <= UB_C, and a cubic that can hold a candidate
+// inside dmin(q) + 1e-12 has boxdist(q, box_s) <= cut(dmin(q)) and is in
+// the list: the cell list replaces the tree walk exactly.
+struct CellGrid {
+  int G, d;
+  double glo[3], h[3];
+  double eps;     // growth of every cell box (rounding of the cell mapping)
+  double hscale;  // table coordinate scale
+  int64_t ncell;
+};
+
+__device__ __forceinline__ void cell_box(const CellGrid& g, int64_t c, double* lo, double* hi) {
+  int64_t ci[3];
+  if (g.d == 3) {
+    ci[2] = c % g.G;
+    ci[1] = (c / g.G) % g.G;
+    ci[0] = c / ((int64_t)g.G * g.G);
+  } else {
+    ci[1] = c % g.G;
+    ci[0] = c / g.G;
+    ci[2] = 0;
+  }
+  for (int k = 0; k < 3; ++k) {
+    if (k < g.d) {
+      lo[k] = g.glo[k] + (double)ci[k] * g.h[k] - g.eps;
+      hi[k] = g.glo[k] + (double)(ci[k] + 1) * g.h[k] + g.eps;
+    } else {
+      lo[k] = hi[k] = 0.0;
+    }
+  }
+}
+
+__device__ double cell_cut2(const TableView& T, const CellGrid& g, const double* lo,
+                            const double* hi) {
+  // UB: min over seams of the farthest point of the cell from the seam
+  double ub2 = __longlong_as_double(0x7ff0000000000000LL);
+  for (int64_t s = 0; s <= T.S; ++s) {
+    double pt[3] = {0.0, 0.0, 0.0};
+    if (s == 0) {
+      for (int k = 0; k < g.d; ++k) pt[k] = T.hdr[1 + k];
+    } else {
+      for (int k = 0; k < g.d; ++k) pt[k] = T.rec[(s - 1) * REC + R_SP + k];
+    }
+    double acc = 0.0;
+    for (int k = 0; k < g.d; ++k) {
+      double f = fmax(fabs(pt[k] - lo[k]), fabs(pt[k] - hi[k]));
+      acc += f * f;
+    }
+    ub2 = fmin(ub2, acc);
+  }
+  double scale = g.hscale;
+  for (int k = 0; k < g.d; ++k) scale = fmax(scale, fmax(fabs(lo[k]), fabs(hi[k])));
+  return cut2(sqrt(ub2) * (1.0 + 1e-12), scale);
+}
+
+__device__ __forceinline__ double cellbox_lb2(const TableView& T, int d, int64_t s, const double* lo,
+                                              const double* hi) {
+  const double* b = T.box + (T.lvl_off[0] + s) * 6;
+  double acc = 0.0;
+  for (int k = 0; k < d; ++k) {
+    double gk = fmax(0.0, fmax(b[k] - hi[k], lo[k] - b[3 + k]));
+    acc += gk * gk;
+  }
+  return acc;
+}
+
+__global__ void cells_count_kernel(const __grid_constant__ TableView T,
+                                   const __grid_constant__ CellGrid g, int32_t* cnt) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= g.ncell) return;
+  double lo[3], hi[3];
+  cell_box(g, c, lo, hi);
+  const double c2 = cell_cut2(T, g, lo, hi);
+  int32_t n = 0;
+  for (int64_t s = 0; s < T.S; ++s) n += cellbox_lb2(T, g.d, s, lo, hi) <= c2;
+  cnt[c] = n;
+}
+
+__global__ void cells_fill_kernel(const __grid_constant__ TableView T,
+                                  const __grid_constant__ CellGrid g, const int32_t* off,
+                                  int32_t* ids) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= g.ncell) return;
+  double lo[3], hi[3];
+  cell_box(g, c, lo, hi);
+  const double c2 = cell_cut2(T, g, lo, hi);
+  int32_t* out = ids + off[c];
+  int32_t n = 0;
+  for (int64_t s = 0; s < T.S; ++s)
+    if (cellbox_lb2(T, g.d, s, lo, hi) <= c2) out[n++] = (int32_t)s;
+  // nearest first (from the cell centre): the running bound tightens early
+  double ctr[3];
+  for (int k = 0; k < 3; ++k) ctr[k] = 0.5 * (lo[k] + hi[k]);
+  for (int32_t i = 1; i < n; ++i) {
+    int32_t v = out[i];
+    double kv = cellbox_lb2(T, g.d, v, ctr, ctr);
+    int32_t j = i - 1;
+    while (j >= 0 && cellbox_lb2(T, g.d, out[j], ctr, ctr) > kv) {
+      out[j + 1] = out[j];
+      --j;
+    }
+    out[j + 1] = v;
+  }
+}
+
+static int cell_grid(const void* table, int64_t S, int d, int grid, cudaStream_t st,
+                     TableView& T, CellGrid& g) {
+  if (S < 1 || S > (1 << 14) || (d != 2 && d != 3) || grid < 1 || grid > 256 || !table) {
+    set_error("mrep_cells: need 1 <= S <= 16384, d in {2,3}, 1 <= grid <= 256");
+    return MREP_ERR_ARG;
+  }
+  T = table_view(table, S);
+  double root[6], hdr5[5];
+  MREP_CUDA_CHECK(cudaMemcpyAsync(root, T.box + T.lvl_off[T.top] * 6, sizeof root,
+                                  cudaMemcpyDeviceToHost, st));
+  MREP_CUDA_CHECK(cudaMemcpyAsync(hdr5, T.hdr, sizeof hdr5, cudaMemcpyDeviceToHost, st));
+  MREP_CUDA_CHECK(cudaStreamSynchronize(st));
+  g = CellGrid{};
+  g.G = grid;
+  g.d = d;
+  g.hscale = hdr5[4];
+  double ext_max = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    if (k < d) {
+      double ext = fmax(root[3 + k] - root[k], 1e-300);
+      g.glo[k] = root[k] - 0.1 * ext;
+      g.h[k] = 1.2 * ext / grid;
+      ext_max = fmax(ext_max, 1.2 * ext);
+    } else {
+      g.glo[k] = 0.0;
+      g.h[k] = 1.0;
+    }
+  }
+  g.eps = 1e-9 * (ext_max + g.hscale);
+  g.ncell = (int64_t)grid * grid * (d == 3 ? grid : 1);
+  return MREP_OK;
+}
+
 static int project_chunk(const void* table, int64_t S, int d, const double* queries, int64_t n,
                          double clip_tol, int max_iter, int soundness_samples, unsigned flags,
                          double* out_t, double* out_foot, double* out_dist, int64_t* out_cand,
@@ -2900,6 +3104,69 @@ int mrep_project_batch(const void* set, const double* queries, const int32_t* cu
                                  out_seg ? out_seg + lo : nullptr, counters, (cudaStream_t)stream);
     if (rc != MREP_OK) return rc;
   }
+  return MREP_OK;
+}
+
+
+int64_t mrep_cells_bytes(const void* table, int64_t S, int d, int grid, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  TableView T;
+  CellGrid g;
+  if (cell_grid(table, S, d, grid, st, T, g) != MREP_OK) return -1;
+  int32_t* cnt = nullptr;
+  if (cudaMallocAsync((void**)&cnt, g.ncell * 4, st) != cudaSuccess) return -1;
+  cells_count_kernel<<<grid_for(g.ncell, 128), 128, 0, st>>>(T, g, cnt);
+  std::vector<int32_t> h(g.ncell);
+  cudaMemcpyAsync(h.data(), cnt, g.ncell * 4, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(cnt, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return -1;
+  int64_t total = 0;
+  for (int32_t v : h) total += v;
+  return (g.ncell + 1 + total) * 4;
+}
+
+int mrep_cells_build(void* table, int64_t S, int d, int grid, void* cells, int64_t bytes,
+                     void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  TableView T;
+  CellGrid g;
+  int rc = cell_grid(table, S, d, grid, st, T, g);
+  if (rc != MREP_OK) return rc;
+  if (!cells || bytes < (g.ncell + 1) * 4) {
+    set_error("mrep_cells_build: cells buffer too small (see mrep_cells_bytes)");
+    return MREP_ERR_ARG;
+  }
+  int32_t* off = (int32_t*)cells;
+  MREP_CUDA_CHECK(cudaMemsetAsync(off + g.ncell, 0, 4, st));
+  cells_count_kernel<<<grid_for(g.ncell, 128), 128, 0, st>>>(T, g, off);
+  MREP_LAUNCH_CHECK();
+  size_t tmp = 0;
+  MREP_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, off, off, (int)(g.ncell + 1), st));
+  void* t = nullptr;
+  MREP_CUDA_CHECK(cudaMallocAsync(&t, tmp + 16, st));
+  MREP_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(t, tmp, off, off, (int)(g.ncell + 1), st));
+  MREP_CUDA_CHECK(cudaFreeAsync(t, st));
+  int32_t total = 0;
+  MREP_CUDA_CHECK(cudaMemcpyAsync(&total, off + g.ncell, 4, cudaMemcpyDeviceToHost, st));
+  MREP_CUDA_CHECK(cudaStreamSynchronize(st));
+  if ((g.ncell + 1 + (int64_t)total) * 4 > bytes) {
+    set_error("mrep_cells_build: cells buffer too small (see mrep_cells_bytes)");
+    return MREP_ERR_ARG;
+  }
+  cells_fill_kernel<<<grid_for(g.ncell, 128), 128, 0, st>>>(T, g, off, off + g.ncell + 1);
+  MREP_LAUNCH_CHECK();
+  // header: cell index pointer, grid, lower corner, inverse cell size, upper corner
+  double h[11];
+  uint64_t bits = (uint64_t)(uintptr_t)cells;
+  memcpy(&h[0], &bits, 8);
+  h[1] = grid;
+  for (int k = 0; k < 3; ++k) {
+    h[2 + k] = g.glo[k];
+    h[5 + k] = 1.0 / g.h[k];
+    h[8 + k] = g.glo[k] + g.h[k] * grid;
+  }
+  MREP_CUDA_CHECK(cudaMemcpyAsync((double*)table + H_CELLS, h, sizeof h, cudaMemcpyHostToDevice, st));
+  MREP_CUDA_CHECK(cudaStreamSynchronize(st));  // h dies here
   return MREP_OK;
 }
 

@@ -23,15 +23,16 @@ import ctypes  # noqa: E402
 from paper_2504_11498_b200 import _lib as L  # noqa: E402
 lib = L.lib()
 p = lambda a: ctypes.c_void_p(a.ctypes.data) if a is not None else ctypes.c_void_p(0)  # noqa
+flags = 1 | wl.tab._cell_flag(n, True)  # what DeviceTable.project_host passes
 for with_seg in (True, False):
     seg = outs[4] if with_seg else None
     for _ in range(3):
-        lib.mrep_project_host(L.ptr(wl.tab.buf), wl.tab.S, 3, p(q), n, 1e-6, 8, 1, p(outs[0]),
+        lib.mrep_project_host(L.ptr(wl.tab.buf), wl.tab.S, 3, p(q), n, 1e-6, 8, flags, p(outs[0]),
                               p(outs[1]), p(outs[2]), p(outs[3]), p(seg), None)
     ts = []
     for _ in range(20):
         t0 = time.perf_counter()
-        lib.mrep_project_host(L.ptr(wl.tab.buf), wl.tab.S, 3, p(q), n, 1e-6, 8, 1, p(outs[0]),
+        lib.mrep_project_host(L.ptr(wl.tab.buf), wl.tab.S, 3, p(q), n, 1e-6, 8, flags, p(outs[0]),
                               p(outs[1]), p(outs[2]), p(outs[3]), p(seg), None)
         ts.append(time.perf_counter() - t0)
     print(f"{cfg} chunk={os.environ.get('MREP_E2E_CHUNK', 'def')} "

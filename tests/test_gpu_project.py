@@ -54,8 +54,10 @@ def test_wavefront_fused_unsorted_agree(gpu, name):
     d = tab.project(z["queries"], extra_flags=L.MREP_PACKET)
     e = tab.project(z["queries"], extra_flags=L.MREP_PER_LANE)
     f = tab.project(z["queries"], extra_flags=L.MREP_GROUP)
+    tab.build_cells()
+    g = tab.project(z["queries"], extra_flags=L.MREP_CELLS)
     for k in (0, 1, 2, 4):
-        for other in (b, c, d, e, f):
+        for other in (b, c, d, e, f, g):
             assert np.array_equal(a[k].cpu().numpy(), other[k].cpu().numpy()), k
 
 
@@ -256,3 +258,20 @@ def test_degenerate_and_far_queries(gpu, oracle_lib):
     assert np.all(np.abs(t - o["t"]) <= 1e-6)
     assert np.all(np.abs(dist - o["dist"]) <= np.maximum(1e-9 * o["dist"], 1e-12))
     assert dist[-2:].max() <= 1e-12  # the clamped ends lie on the curve
+
+
+@pytest.mark.parametrize("grid", [8, 64])
+def test_cell_index_bitwise_equal_to_tree_walk(gpu, grid):
+    """cfg2 curve, 2e5 queries (some outside the grid): the cell-index
+    traversal gives the tree walk's results bit for bit."""
+    from paper_2504_11498_b200 import _lib as L
+    from paper_2504_11498_b200 import _device as D
+    z = load_golden("project_cfg2.npz")
+    tab = D.DeviceTable(z["seg_pts"], z["seg_ta"], z["seg_tb"], z["seam_t"], z["seam_pt"])
+    rng = np.random.default_rng(8)
+    q = np.concatenate([rng.uniform(0, 1, (200000, 3)), rng.uniform(-3, 4, (2000, 3))])
+    a = tab.project(q, extra_flags=L.MREP_PACKET)
+    tab.build_cells(grid)
+    b = tab.project(q, extra_flags=L.MREP_CELLS)
+    for k in (0, 1, 2, 4):
+        assert np.array_equal(a[k].cpu().numpy(), b[k].cpu().numpy()), k
