@@ -111,4 +111,5 @@ def test_table_layout_levels():
                 break
             cnt = (cnt + 7) // 8
             lv += 1
-        assert lib.mrep_table_bytes(S) == (64 + 32 * S + 6 * boxes) * 8
+        # 6 doubles per box + its float copy (6 floats)
+        assert lib.mrep_table_bytes(S) == (64 + 32 * S + 9 * boxes) * 8
