@@ -208,9 +208,15 @@ class SingleCurve:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         self.prep = prepare_curve(BSplineCurve(*self.curve), 1e-4)
+        self.tab = self.prep.table
         torch.cuda.synchronize()
         self.prep_ms = (time.perf_counter() - t0) * 1e3
-        self.tab = self.prep.table
+        # the dense-batch cell index is part of the prepared table (built
+        # lazily by the first large batch; built here so prep_ms includes it)
+        t0 = time.perf_counter()
+        self.tab._cell_flag(max(c["n"], 1 << 20), True)
+        torch.cuda.synchronize()
+        self.cells_ms = (time.perf_counter() - t0) * 1e3
         if n_override:
             self.n = n_override
         elif c["scaling"] == "strong":
@@ -641,6 +647,9 @@ def main():
                              f"_kernels._project_block, bit-exact vs the reference"}
         conf = dict(workload_config(args.config, n), parallelism=f"query-shard x{world}",
                     prep_ms=wl.prep_ms, cubics=wl.num_segments)
+        if getattr(wl, "cells_ms", None) is not None and getattr(wl.tab, "cells", None) is not None:
+            conf["cell_index"] = {"build_ms": wl.cells_ms,
+                                  "bytes": int(wl.tab.cells.numel() * 4)}
         sm_sorted = sorted(step_ms)
         conf["step_ms"] = {"median": statistics.median(step_ms), "min": sm_sorted[0],
                            "max": sm_sorted[-1]}

@@ -167,14 +167,19 @@ class DeviceTable:
     # a cell index pays off for dense batches (queries >> cubics); built once,
     # lazily, on the first such batch (mrep_cells_build)
     CELL_MIN_QUERIES = 1 << 16
-    CELL_MAX_CUBICS = 1 << 14
+    CELL_MAX_CUBICS = 1 << 17
+    CELL_MAX_BYTES = 4 << 30  # skip the index rather than spend more HBM on it
 
     def build_cells(self, grid=None):
         torch = L._torch()
-        grid = grid or (64 if self.d == 3 else 256)
+        if grid is None:
+            big = self.S > (1 << 14)
+            grid = (128 if big else 64) if self.d == 3 else (512 if big else 256)
         nb = L.lib().mrep_cells_bytes(L.ptr(self.buf), self.S, self.d, grid, L.stream_ptr())
         if nb <= 0:
             L.check(1)
+        if nb > self.CELL_MAX_BYTES:
+            return self
         self.cells = torch.empty((nb + 3) // 4, dtype=torch.int32, device=self.buf.device)
         L.check(L.lib().mrep_cells_build(L.ptr(self.buf), self.S, self.d, grid,
                                           L.ptr(self.cells), nb, L.stream_ptr()))

@@ -275,3 +275,21 @@ def test_cell_index_bitwise_equal_to_tree_walk(gpu, grid):
     b = tab.project(q, extra_flags=L.MREP_CELLS)
     for k in (0, 1, 2, 4):
         assert np.array_equal(a[k].cpu().numpy(), b[k].cpu().numpy()), k
+
+
+def test_cell_index_large_table_bvh_build(gpu):
+    """A 2e4-cubic curve (cell lists built by walking the hierarchy, not by
+    brute force): cell traversal == tree walk bit for bit."""
+    from paper_2504_11498_b200 import BSplineCurve, _lib as L, prepare_curve
+    from paper_2504_11498_b200.fixtures import random_clamped_curve
+    cv = random_clamped_curve(np.random.default_rng(17), 3, 20003, 3, uniform_knots=True,
+                              native=True)
+    prep = prepare_curve(cv, 1e-4)
+    assert prep.num_segments == 20000
+    tab = prep.table
+    q = np.random.default_rng(18).uniform(-0.1, 1.1, (150000, 3))
+    a = tab.project(q, extra_flags=L.MREP_PACKET)
+    tab.build_cells(24)
+    b = tab.project(q, extra_flags=L.MREP_CELLS)
+    for k in (0, 1, 2, 4):
+        assert np.array_equal(a[k].cpu().numpy(), b[k].cpu().numpy()), k
