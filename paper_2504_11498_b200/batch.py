@@ -36,17 +36,32 @@ class PreparedCurveSet:
     """
 
     def __init__(self, curves, tolerance, seg_pts, seg_ta, seg_tb, seg_ofs, handle, err=None):
+        # seg_* / err: numpy arrays, or device tensors fetched to the host on
+        # first access (a cfg3 set is ~400 MB of cubics; the device set does
+        # not need the host copy)
         self.curves = list(curves)
         self.tolerance = tolerance
-        self.seg_pts = seg_pts
-        self.seg_ta = seg_ta
-        self.seg_tb = seg_tb
+        self._arrays = {"seg_pts": seg_pts, "seg_ta": seg_ta, "seg_tb": seg_tb,
+                        "measured_error": err}
         self.seg_ofs = np.asarray(seg_ofs, dtype=np.int64)
-        self.measured_error = err
+        self.seg_ofs.flags.writeable = False
         self._handle = handle
-        self.d = int(seg_pts.shape[2]) if seg_pts.ndim == 3 else 3
-        for a in (self.seg_pts, self.seg_ta, self.seg_tb, self.seg_ofs):
+        self.d = int(seg_pts.shape[2]) if len(seg_pts.shape) == 3 else 3
+
+    def _host(self, name):
+        a = self._arrays[name]
+        if a is not None and not isinstance(a, np.ndarray):
+            a = L.to_host(a)
             a.flags.writeable = False
+            self._arrays[name] = a
+        elif isinstance(a, np.ndarray) and a.flags.writeable:
+            a.flags.writeable = False
+        return a
+
+    seg_pts = property(lambda self: self._host("seg_pts"))
+    seg_ta = property(lambda self: self._host("seg_ta"))
+    seg_tb = property(lambda self: self._host("seg_tb"))
+    measured_error = property(lambda self: self._host("measured_error"))
 
     @property
     def handle(self):
@@ -152,7 +167,8 @@ def prepare_curve_set(curves, tolerance: float = 1e-4, batch_cap: int = 4096) ->
         raise DomainError("all curves of a set must have the same dimension")
     for c in curves:
         validate_curve(c)
-        if not c.span_indices():
+        k, p = c.knots.knots, c.degree
+        if not np.any(k[p + 1: len(k) - p] > k[p: len(k) - p - 1]):  # span_indices() empty
             raise EmptyDomain("curve has no nonzero-length span")
     d = dims.pop()
     torch = L._torch()
@@ -171,8 +187,7 @@ def prepare_curve_set(curves, tolerance: float = 1e-4, batch_cap: int = 4096) ->
     L.check(L.lib().mrep_curveset_create_dev(L.ptr(pts), L.ptr(ta), L.ptr(tb),
                                              ctypes.c_void_p(ofs.ctypes.data), len(curves), d,
                                              L.stream_ptr(), ctypes.byref(h)))
-    return PreparedCurveSet(curves, tolerance, L.to_host(pts), L.to_host(ta), L.to_host(tb), ofs,
-                            h, err=L.to_host(err))
+    return PreparedCurveSet(curves, tolerance, pts, ta, tb, ofs, h, err=err)
 
 
 def curve_set_from_prepared(preps) -> PreparedCurveSet:

@@ -359,37 +359,73 @@ __device__ void g1_reduce(const double* Q, int p, int d, double* R, double* d0o,
   if (d1o) *d1o = dd1;
 }
 
+// sum_j bern(p, j, v) Q_j with bern as bernstein_design builds it
+// ((C(p,j) * v**j) * (1-v)**(p-j), basis.py:192-196; FMA accumulation in j
+// order).  The powers come from one double-double chain per base instead of
+// a binary powering per (j, base): the same correctly rounded values (both
+// carry ~2^-100 relative error before the final rounding) at a quarter of
+// the work.
+__device__ __forceinline__ void bern_comb(const double* Q, int p, int d, double v, double* o) {
+  double wp[32];
+  {
+    const double w = 1.0 - v;
+    double h = 1.0, l = 0.0;
+    wp[0] = 1.0;
+    for (int k = 1; k <= p; ++k) {
+      dd_mul(h, l, w, 0.0);
+      wp[k] = (k == 1) ? w : h + l;
+    }
+  }
+  double vh = 1.0, vl = 0.0;
+  for (int j = 0; j <= p; ++j) {
+    double vj;
+    if (j == 0) {
+      vj = 1.0;
+    } else {
+      dd_mul(vh, vl, v, 0.0);
+      vj = (j == 1) ? v : vh + vl;
+    }
+    const double bj = binom(p, j) * vj * wp[p - j];
+    for (int k = 0; k < d; ++k) o[k] = fma(bj, Q[j * 3 + k], o[k]);
+  }
+}
+
 // reduce_approx.py:146-155 for one (cubic, original) pair, warp-cooperative.
-// Writes the argmax mask (err >= mx - 1e-12) and returns mx.
+// Writes the argmax mask (err >= mx - 1e-12) and returns mx.  With `errs`
+// (shared memory, >= ns doubles) the second pass reads the errors back
+// instead of recomputing them (same bits either way).
 __device__ double max_error_warp(const double* P, double pa, double pb, const double* Q, int p,
-                                 int d, double oa, double ob, int ns, uint32_t* mask) {
+                                 int d, double oa, double ob, int ns, uint32_t* mask,
+                                 double* errs = nullptr) {
   int lane = threadIdx.x & 31;
   int nchunks = (ns + 31) / 32;
   double mx = -1.0;
-  // pass 1: the maximum; pass 2: the argmax set (errors recomputed, same bits)
+  // pass 1: the maximum; pass 2: the argmax set
   for (int pass = 0; pass < 2; ++pass) {
     for (int ch = 0; ch < nchunks; ++ch) {
       int i = ch * 32 + lane;
       double err = -1.0;
       if (i < ns) {
-        double u = lin_sample(i, ns);
-        double t = pa + u * (pb - pa);
-        double v = (t - oa) / (ob - oa);
-        double a[3] = {0.0, 0.0, 0.0}, o[3] = {0.0, 0.0, 0.0};
-        for (int j = 0; j < 4; ++j) {
-          double bj = bern(3, j, u);
-          for (int k = 0; k < d; ++k) a[k] = fma(bj, P[j * 3 + k], a[k]);
+        if (pass == 1 && errs) {
+          err = errs[i];
+        } else {
+          double u = lin_sample(i, ns);
+          double t = pa + u * (pb - pa);
+          double v = (t - oa) / (ob - oa);
+          double a[3] = {0.0, 0.0, 0.0}, o[3] = {0.0, 0.0, 0.0};
+          for (int j = 0; j < 4; ++j) {
+            double bj = bern(3, j, u);
+            for (int k = 0; k < d; ++k) a[k] = fma(bj, P[j * 3 + k], a[k]);
+          }
+          bern_comb(Q, p, d, v, o);
+          double s = 0.0;
+          for (int k = 0; k < d; ++k) {
+            double df = a[k] - o[k];
+            s = (k == 0) ? df * df : s + df * df;
+          }
+          err = sqrt(s);
+          if (errs) errs[i] = err;
         }
-        for (int j = 0; j <= p; ++j) {
-          double bj = bern(p, j, v);
-          for (int k = 0; k < d; ++k) o[k] = fma(bj, Q[j * 3 + k], o[k]);
-        }
-        double s = 0.0;
-        for (int k = 0; k < d; ++k) {
-          double df = a[k] - o[k];
-          s = (k == 0) ? df * df : s + df * df;
-        }
-        err = sqrt(s);
       }
       if (pass == 0) {
         mx = fmax(mx, err);
