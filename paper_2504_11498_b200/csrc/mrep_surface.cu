@@ -58,8 +58,17 @@ int ensure_pool();
 //   patch it is far tighter than the axis-aligned box.
 // Boxes: the same 8-ary hierarchy as the curve tables, over the patches in
 // 2-D Morton order of (i, j).
+// Bernstein coefficients of D(u,v) = |S(u,v) - q|^2 at degree (2pu, 2pv)
+// are SS_m - 2 q.E_m + |q|^2 with two query-independent nets stored per
+// patch: E = S elevated to degree (2pu, 2pv) (3 NE doubles) and SS = the
+// coefficients of |S|^2 (NE doubles), NE = (2pu+1)(2pv+1).  min_m D_m is a
+// lower bound on the patch's squared distance (convex hull property).
+__host__ __device__ inline int surf_ne(int pu, int pv) { return (2 * pu + 1) * (2 * pv + 1); }
+__host__ __device__ inline int surf_bern(int pu, int pv) {  // E at +0, SS at +3 NE
+  return 6 * (pu + 1) * (pv + 1) + 5 + 15;
+}
 __host__ __device__ inline int surf_rec(int pu, int pv) {
-  int n = 6 * (pu + 1) * (pv + 1) + 5 + 15;
+  int n = surf_bern(pu, pv) + 4 * surf_ne(pu, pv) + 1;  // + the |SS|,|E| magnitude
   return (n + 7) & ~7;
 }
 __host__ __device__ inline int surf_obb(int pu, int pv) { return 6 * (pu + 1) * (pv + 1) + 5; }
@@ -136,8 +145,16 @@ __device__ __forceinline__ void bern0(double u, double (&B)[P + 1]) {
   for (int a = 0; a <= P; ++a) B[a] = binom_d(P, a) * up[a] * wp[P - a];
 }
 
+// element i of a patch net: global memory (STRIDE 1, read-only path) or a
+// lane's column of the solver's shared-memory staging (STRIDE = block size)
+template <int STRIDE>
+__device__ __forceinline__ double ldp(const double* P, int i) {
+  if (STRIDE == 1) return __ldg(P + i);
+  return P[i * STRIDE];
+}
+
 // S(u, v) only
-template <int PU, int PV>
+template <int PU, int PV, int STRIDE = 1>
 __device__ __forceinline__ void surf_point(const double* P, double u, double v, double (&S)[3]) {
   double Bu[PU + 1], Bv[PV + 1];
   bern0<PU>(u, Bu);
@@ -149,7 +166,7 @@ __device__ __forceinline__ void surf_point(const double* P, double u, double v, 
 #pragma unroll
     for (int c = 0; c <= PV; ++c)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) R[k] += Bv[c] * __ldg(P + (a * (PV + 1) + c) * 3 + k);
+      for (int k = 0; k < 3; ++k) R[k] += Bv[c] * ldp<STRIDE>(P, (a * (PV + 1) + c) * 3 + k);
 #pragma unroll
     for (int k = 0; k < 3; ++k) S[k] += Bu[a] * R[k];
   }
@@ -203,7 +220,7 @@ __device__ __forceinline__ void bern_at(int a, const double (&up)[P + 1], const 
 
 // S and its first / second partials at (u, v).  Register-lean: the u basis
 // is produced one index at a time from the power tables.
-template <int PU, int PV>
+template <int PU, int PV, int STRIDE = 1>
 __device__ __forceinline__ void surf_jet(const double* P, double u, double v, Jet& J) {
   double Bv[PV + 1], dBv[PV + 1], ddBv[PV + 1];
   bern<PV>(v, Bv, dBv, ddBv);
@@ -227,7 +244,7 @@ __device__ __forceinline__ void surf_jet(const double* P, double u, double v, Je
     for (int c = 0; c <= PV; ++c)
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        double p = __ldg(P + (a * (PV + 1) + c) * 3 + k);
+        double p = ldp<STRIDE>(P, (a * (PV + 1) + c) * 3 + k);
         R[k] += Bv[c] * p;
         Rv[k] += dBv[c] * p;
         Rvv[k] += ddBv[c] * p;
@@ -294,11 +311,11 @@ __device__ __forceinline__ void seed_init(const double* P, const double (&q)[3],
 }
 
 // one iteration of the oracle's loop; true when the solve is finished
-template <int PU, int PV>
+template <int PU, int PV, int STRIDE = 1>
 __device__ __forceinline__ bool newton_iter(const double* P, const double (&q)[3], NState& n) {
   const double u = n.u, v = n.v;
   Jet J;
-  surf_jet<PU, PV>(P, u, v, J);
+  surf_jet<PU, PV, STRIDE>(P, u, v, J);
   double rr[3] = {J.S[0] - q[0], J.S[1] - q[1], J.S[2] - q[2]};
   const double f = dot3(rr, rr);
   n.f = f;
@@ -342,7 +359,7 @@ __device__ __forceinline__ bool newton_iter(const double* P, const double (&q)[3
     un = clamp01(u + t * du);
     vn = clamp01(v + t * dv);
     double S[3];
-    surf_point<PU, PV>(P, un, vn, S);
+    surf_point<PU, PV, STRIDE>(P, un, vn, S);
     fn = dist2_to(S, q);
     if (fn < f) {
       ok = true;
@@ -427,6 +444,29 @@ __device__ __forceinline__ void offer_points(const SurfParams& w, int64_t s, con
   }
   ub = fmin(ub, sqrt(m));
   st.points += NP;
+}
+
+// true if the patch's Bernstein lower bound on |S - q|^2 can reach c2
+template <int PU, int PV>
+__device__ __forceinline__ bool bern_patch_may_reach(const double* P, const double (&q)[3],
+                                                     double c2) {
+  constexpr int NE = (2 * PU + 1) * (2 * PV + 1);
+  const double* E = P + surf_bern(PU, PV);
+  const double* SS = E + 3 * NE;
+  const double qq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2];
+  double m = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll 7
+  for (int k = 0; k < NE; ++k) {
+    double d = (__ldg(SS + k) - 2.0 * (q[0] * __ldg(E + 3 * k) + q[1] * __ldg(E + 3 * k + 1) +
+                                       q[2] * __ldg(E + 3 * k + 2))) + qq;
+    m = fmin(m, d);
+  }
+  // rounding: the nets are O(1e-16) relative to their magnitude; the sums
+  // here add a few ulps of (mag + 2|q| mag + |q|^2)
+  const double qa = fabs(q[0]) + fabs(q[1]) + fabs(q[2]);
+  const double mag = __ldg(SS + NE);
+  const double err = 1e-12 * (mag * (1.0 + 2.0 * qa) + qq);
+  return !(m - err > c2);
 }
 
 // S1: per-thread depth-first walk (queries in Morton order)
@@ -573,6 +613,13 @@ __global__ void __launch_bounds__(256) surf_filter(const __grid_constant__ SurfP
 // (its minimum is a tight bound); PASS 1: the compacted survivors.
 template <int PU, int PV, int PASS>
 __global__ void __launch_bounds__(128, (PU + PV <= 6) ? 3 : 1) surf_solve(const __grid_constant__ SurfParams w) {
+  // each lane's current control net, staged column-wise in shared memory
+  // (element k of lane t at [k][t]: conflict-free), so the ~20 surface
+  // evaluations of a solve read shared memory instead of 3(p+1)^2 scattered
+  // global loads each
+  constexpr int NPD = 3 * (PU + 1) * (PV + 1);
+  extern __shared__ double snet[];  // NPD * 128 doubles (dynamic)
+  double* mynet = snet + threadIdx.x;
   const unsigned long long total =
       PASS == 0 ? (unsigned long long)w.n : *(volatile unsigned long long*)&w.cnt[6];
   unsigned long long* queue = &w.cnt[PASS == 0 ? 4 : 5];
@@ -608,12 +655,15 @@ __global__ void __launch_bounds__(128, (PU + PV <= 6) ? 3 : 1) surf_solve(const 
             bool go = true;
             if (PASS == 1) {  // the bound may have tightened since the filter
               double scale = fmax(T.hdr[4], fmax(fabs(q[0]), fmax(fabs(q[1]), fabs(q[2]))));
-              go = obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <=
-                   cut2(smin_of(w, g), scale);
+              const double c2 = cut2(smin_of(w, g), scale);
+              go = obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2 &&
+                   bern_patch_may_reach<PU, PV>(T.rec + s * w.rec, q, c2);
             }
             if (go) {
               P = T.rec + s * w.rec;
               seed_init<PU, PV>(P, q, ns);
+#pragma unroll 4
+              for (int k = 0; k < NPD; ++k) mynet[k * 128] = __ldg(P + k);
               have = true;
             }
           }
@@ -622,7 +672,7 @@ __global__ void __launch_bounds__(128, (PU + PV <= 6) ? 3 : 1) surf_solve(const 
     }
     if (__all_sync(0xffffffffu, done)) break;
     if (!have) continue;
-    if (!newton_iter<PU, PV>(P, q, ns)) continue;
+    if (!newton_iter<PU, PV, 128>(mynet, q, ns)) continue;
     // pair finished: its candidate
     have = false;
     ++npairs;
@@ -845,6 +895,34 @@ __global__ void surf_pack_kernel(const double* pts, const double* iv, const uint
     // non-orthogonality of the rounded axes all err by O(1e-15 |x|)
     for (int i = 0; i < 3; ++i) O[12 + i] = 0.5 * (hi[i] - lo[i]) + 1e-12 * (1.0 + amax);
   }
+  {
+    // elevated net E and |S|^2 coefficients SS (see surf_bern)
+    const int Nu = 2 * pu, Nv = 2 * pv, NE = surf_ne(pu, pv);
+    double* E = r + surf_bern(pu, pv);
+    double* SS = E + 3 * NE;
+    double mag = 0.0;
+    auto C = [](int n, int k) { return binom_d(n, k); };
+    for (int a = 0; a <= Nu; ++a)
+      for (int c = 0; c <= Nv; ++c) {
+        double e[3] = {0.0, 0.0, 0.0}, ss = 0.0;
+        for (int i = (a > pu ? a - pu : 0); i <= (a < pu ? a : pu); ++i)
+          for (int k = (c > pv ? c - pv : 0); k <= (c < pv ? c : pv); ++k) {
+            // elevation: C(pu,i) C(pu,a-i) / C(2pu,a) x the same in v
+            const double wgt = (C(pu, i) * C(pu, a - i) / C(Nu, a)) *
+                               (C(pv, k) * C(pv, c - k) / C(Nv, c));
+            const double* Pik = r + (i * (pv + 1) + k) * 3;
+            const double* Pjl = r + ((a - i) * (pv + 1) + (c - k)) * 3;
+            for (int x = 0; x < 3; ++x) e[x] += wgt * Pik[x];
+            // product of the two degree-p nets (same weights)
+            ss += wgt * (Pik[0] * Pjl[0] + Pik[1] * Pjl[1] + Pik[2] * Pjl[2]);
+          }
+        const int m = a * (Nv + 1) + c;
+        for (int x = 0; x < 3; ++x) E[3 * m + x] = e[x];
+        SS[m] = ss;
+        mag = fmax(mag, fmax(fabs(ss), fmax(fabs(e[0]), fmax(fabs(e[1]), fabs(e[2])))));
+      }
+    SS[NE] = mag;
+  }
   for (int c = 0; c < 3; ++c) {
     box0[k * 6 + c] = lo[c];
     box0[k * 6 + 3 + c] = hi[c];
@@ -985,16 +1063,32 @@ static int launch_surface(SurfParams& w, cudaStream_t st, bool timing) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, block, 0);
     return (unsigned)(sms * (per > 0 ? per : 1));
   };
-  const unsigned g_solve = persist_grid((const void*)surf_solve<PU, PV, 1>, 128);
+  const size_t solve_smem = (size_t)3 * (PU + 1) * (PV + 1) * 128 * sizeof(double);
+  // attribute + grid size once per instantiation and device
+  static int attr_dev = -1;
+  static unsigned g_solve = 0;
+  int cur_dev = 0;
+  MREP_CUDA_CHECK(cudaGetDevice(&cur_dev));
+  if (attr_dev != cur_dev) {
+    for (const void* fn : {(const void*)surf_solve<PU, PV, 0>, (const void*)surf_solve<PU, PV, 1>})
+      MREP_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)solve_smem));
+    int sms = 148, per = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur_dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)surf_solve<PU, PV, 1>, 128,
+                                                  solve_smem);
+    g_solve = (unsigned)(sms * (per > 0 ? per : 1));
+    attr_dev = cur_dev;
+  }
   const unsigned g_sel = persist_grid((const void*)surf_select<PU, PV, 1>, 256);
   StageTimer tm(timing, st);
   tm.mark();
   surf_traverse<PU, PV><<<grid_for(n, 128), 128, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
   tm.mark();
-  surf_solve<PU, PV, 0><<<g_solve, 128, 0, st>>>(w);
+  surf_solve<PU, PV, 0><<<g_solve, 128, solve_smem, st>>>(w);
   surf_filter<PU, PV><<<g_sel, 256, 0, st>>>(w);
-  surf_solve<PU, PV, 1><<<g_solve, 128, 0, st>>>(w);
+  surf_solve<PU, PV, 1><<<g_solve, 128, solve_smem, st>>>(w);
   MREP_LAUNCH_CHECK();
   tm.mark();
   tm.mark();  // (no clip stage for surfaces)
