@@ -412,56 +412,91 @@ struct ClipOut {
 
 // _kernels.py:306-341.  The widths array is tracked only at the two indices
 // the batch kernel reads (i3 and max_iter-1), with the reference's fill rules.
-__device__ __forceinline__ ClipOut clip_root(const double (&b)[6], double tol, int max_iter) {
+// clip_root as an init + one-iteration step, so a solver can interleave
+// many survivors per lane (wave_clip refills a lane when its survivor is
+// done); clip_root below is exactly init + steps until finished.
+struct ClipState {
+  double cur[6];
+  double lo, hi;
+  int it;
   ClipOut r;
+};
+
+__device__ __forceinline__ void clip_init(ClipState& S, const double (&b)[6]) {
+#pragma unroll
+  for (int i = 0; i < 6; ++i) S.cur[i] = b[i];
+  S.lo = 0.0;
+  S.hi = 1.0;
+  S.it = 0;
+  S.r.used = 0;
+  S.r.w3 = 0.0;
+  S.r.wf = 0.0;
+  S.r.ok = false;
+  S.r.root = 0.0;
+}
+
+// one iteration of _kernels.py:305-341; true when S.r is final
+__device__ __forceinline__ bool clip_step(ClipState& S, double tol, int max_iter) {
   const int i3 = max_iter > 2 ? 2 : max_iter - 1;
   const int ilast = max_iter - 1;
-  double lo = 0.0, hi = 1.0, cur[6];
-#pragma unroll
-  for (int i = 0; i < 6; ++i) cur[i] = b[i];
-  r.used = 0;
-  r.w3 = 0.0;
-  r.wf = 0.0;
-  for (int it = 0; it < max_iter; ++it) {
-    double z1, z2;
-    bool found = hull_cross(cur, z1, z2);
-    if (!found) {
-      // widths[k] = hi - lo for k >= it
-      if (it <= i3) r.w3 = hi - lo;
-      r.wf = hi - lo;
-      r.ok = false;
-      r.used = it;
-      r.root = 0.5 * (lo + hi);
-      return r;
-    }
-    r.used = it + 1;
-    double nlo = lo + z1 * (hi - lo);
-    double nhi = lo + z2 * (hi - lo);
-    if (z2 - z1 < 1e-15) {
-      if (it <= i3) r.w3 = 0.0;
-      r.wf = 0.0;
-      r.ok = true;
-      r.root = nlo;
-      return r;
-    }
-    restrict_ordinates(cur, z1, z2, cur);
-    lo = nlo;
-    hi = nhi;
-    double w = hi - lo;
-    if (it == i3) r.w3 = w;
-    if (it == ilast) r.wf = w;
-    if (w <= tol) {
-      // widths[k] = w for k > it
-      if (it < i3) r.w3 = w;
-      if (it < ilast) r.wf = w;
-      r.ok = true;
-      r.root = 0.5 * (lo + hi);
-      return r;
-    }
+  const int it = S.it;
+  ClipOut& r = S.r;
+  if (it >= max_iter) {
+    r.ok = true;
+    r.root = 0.5 * (S.lo + S.hi);
+    return true;
   }
-  r.ok = true;
-  r.root = 0.5 * (lo + hi);
-  return r;
+  double z1, z2;
+  bool found = hull_cross(S.cur, z1, z2);
+  if (!found) {
+    // widths[k] = hi - lo for k >= it
+    if (it <= i3) r.w3 = S.hi - S.lo;
+    r.wf = S.hi - S.lo;
+    r.ok = false;
+    r.used = it;
+    r.root = 0.5 * (S.lo + S.hi);
+    return true;
+  }
+  r.used = it + 1;
+  double nlo = S.lo + z1 * (S.hi - S.lo);
+  double nhi = S.lo + z2 * (S.hi - S.lo);
+  if (z2 - z1 < 1e-15) {
+    if (it <= i3) r.w3 = 0.0;
+    r.wf = 0.0;
+    r.ok = true;
+    r.root = nlo;
+    return true;
+  }
+  restrict_ordinates(S.cur, z1, z2, S.cur);
+  S.lo = nlo;
+  S.hi = nhi;
+  double w = S.hi - S.lo;
+  if (it == i3) r.w3 = w;
+  if (it == ilast) r.wf = w;
+  if (w <= tol) {
+    // widths[k] = w for k > it
+    if (it < i3) r.w3 = w;
+    if (it < ilast) r.wf = w;
+    r.ok = true;
+    r.root = 0.5 * (S.lo + S.hi);
+    return true;
+  }
+  S.it = it + 1;
+  if (S.it >= max_iter) {
+    r.ok = true;
+    r.root = 0.5 * (S.lo + S.hi);
+    return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ ClipOut clip_root(const double (&b)[6], double tol, int max_iter) {
+  ClipState S;
+  clip_init(S, b);
+#pragma unroll 1
+  while (!clip_step(S, tol, max_iter)) {
+  }
+  return S.r;
 }
 
 // The reference's _T5 (power -> degree-5 Bernstein, basis.py:76-92):

@@ -1774,33 +1774,66 @@ __global__ void __launch_bounds__(BLOCK) wave_pairs(const __grid_constant__ Wave
   warp_count(w.counters, MREP_CNT_BOXES, nboxes);
 }
 
+// W3 with lane refill: each lane runs one clipping iteration of its current
+// survivor per loop trip and takes the next survivor from the queue as soon
+// as its own is finished (1..8 iterations per survivor no longer leave
+// lanes idle).  Same arithmetic as clip_root (clip_init + clip_step).
 template <int D, bool MULTI>
 __global__ void __launch_bounds__(BLOCK) wave_clip(const __grid_constant__ WaveParams w) {
-  unsigned long long total = *(volatile unsigned long long*)&w.cnt[1];
-  if (total > w.scap) total = w.scap;
+  const unsigned long long total0 = *(volatile unsigned long long*)&w.cnt[1];
+  const unsigned long long total = total0 > w.scap ? w.scap : total0;
+  unsigned long long* queue = &w.cnt[6];
+  const int lane = threadIdx.x & 31;
   uint64_t nsurv = 0, nit = 0, nmiss = 0;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    int64_t qi = w.sq[i];
-    if (w.flag[qi]) continue;
-    const TableView& T = tab_of<MULTI>(w, qi);
-    const double* o = w.sb + i * 8;
-    double bp[6];
+  bool have = false, done = false;
+  int64_t qi = 0;
+  uint32_t sk = 0;
+  double plo = 0.0, phi = 0.0;
+  ClipState S;
+  for (;;) {
+    const bool want = !have && !done;
+    const unsigned wm = __ballot_sync(0xffffffffu, want);
+    if (wm) {
+      const int leader = __ffs(wm) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(queue, (unsigned long long)__popc(wm));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (want) {
+        const unsigned long long i = base + __popc(wm & ((1u << lane) - 1));
+        if (i >= total) {
+          done = true;
+        } else {
+          qi = w.sq[i];
+          if (!w.flag[qi]) {
+            const double* o = w.sb + i * 8;
+            double bp[6];
 #pragma unroll
-    for (int j = 0; j < 6; ++j) bp[j] = o[j];
-    double lo = o[6], hi = o[7];
-    uint32_t sk = w.ssk[i];
-    int64_t s = sk >> 3;
-    ClipOut co = clip_root(bp, w.clip_tol, w.max_iter);
+            for (int j = 0; j < 6; ++j) bp[j] = o[j];
+            plo = o[6];
+            phi = o[7];
+            sk = w.ssk[i];
+            clip_init(S, bp);
+            have = true;
+          }
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
+    if (!have) continue;
+    if (!clip_step(S, w.clip_tol, w.max_iter)) continue;
+    have = false;
+    const ClipOut& co = S.r;
     ++nsurv;
     nit += (uint64_t)co.used;
     if (!co.ok) {
       ++nmiss;
       continue;
     }
+    const TableView& T = tab_of<MULTI>(w, qi);
+    const int64_t s = sk >> 3;
     const double* r = T.rec + s * REC;
     double ta = __ldg(r + R_TA), tb = __ldg(r + R_TB);
-    double v = lo + co.root * (hi - lo);
+    double v = plo + co.root * (phi - plo);
     double acc = 0.0;
 #pragma unroll
     for (int dim = 0; dim < D; ++dim) {
