@@ -624,6 +624,40 @@ __device__ __forceinline__ bool bern_may_reach(const TableView& T, int64_t s, co
   return !(dmin_b - 1e-9 * mag > cut_sq);
 }
 
+// the early-exit tests of prep_pair_cut alone (same arithmetic): true if the
+// pair can contribute a survivor within cut_sq
+template <int D>
+__device__ __forceinline__ bool pair_may_survive(const TableView& T, int64_t s, const double (&q)[D],
+                                                 double cut_sq) {
+  const double* r = T.rec + s * REC;
+  double w[4][D];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int dim = 0; dim < D; ++dim) w[k][dim] = __ldg(r + k * 3 + dim);
+  double e[6], b[6];
+  distance_poly_w<D>(w, q, e);
+  rebase5(e, b);
+  double d0 = 0.0;
+#pragma unroll
+  for (int dim = 0; dim < D; ++dim) {
+    double df = w[0][dim] - q[dim];
+    d0 += df * df;
+  }
+  double di = d0, dmin_b = d0, mag = fabs(d0);
+  bool pos = true, neg = true;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    di += b[i] * (1.0 / 6.0);
+    dmin_b = fmin(dmin_b, di);
+    mag += fabs(b[i]);
+    pos = pos && b[i] > 1e-290;
+    neg = neg && b[i] < -1e-290;
+  }
+  if (dmin_b - 1e-9 * mag > cut_sq) return false;
+  return !(pos || neg);
+}
+
 // prep_pair with a rigorous early exit: the degree-6 Bernstein coefficients
 // of D(u) = |C(u) - q|^2 follow from E = D' by d_0 = D(0), d_{i+1} = d_i + b_i/6
 // (b = Bernstein ordinates of E); min_i d_i <= min_u D(u).  If that bound
@@ -1020,6 +1054,8 @@ struct WaveParams {
   unsigned long long* cnt;   // [0] pairs, [1] survivors, [2] candidates, [3] fallbacks
   uint32_t* pq;
   uint32_t* ps;
+  uint32_t* pq2;  // pairs that pass W2a (compacted)
+  uint32_t* ps2;
   unsigned long long pcap;
   double* sb;  // survivors: b0..b5, lo, hi
   uint32_t* sq;
@@ -1721,11 +1757,15 @@ __global__ void __launch_bounds__(BLOCK) wave_traverse_group(const __grid_consta
   }
 }
 
+// W2a: the cheap tests of every traversal pair (box re-test with the final
+// seam bound, Bernstein distance bound, one-signed E) -- about half the pairs
+// stop here; the rest are compacted so W2b's quartic + pieces run on
+// uniformly hard work (less divergence).
 template <int D, bool MULTI>
-__global__ void __launch_bounds__(BLOCK) wave_pairs(const __grid_constant__ WaveParams w) {
+__global__ void __launch_bounds__(BLOCK) wave_pairs_filter(const __grid_constant__ WaveParams w) {
   unsigned long long total = *(volatile unsigned long long*)&w.cnt[0];
   if (total > w.pcap) total = w.pcap;
-  uint64_t npairs = 0, nboxes = 0;
+  uint64_t nboxes = 0;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     int64_t qi = w.pq[i];  // sorted position
@@ -1741,9 +1781,40 @@ __global__ void __launch_bounds__(BLOCK) wave_pairs(const __grid_constant__ Wave
     for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
     const double c2 = cut2(rec.w, scale);  // the query's final seam bound
     ++nboxes;
-    if (!((fbox_ok(scale) ? box_lb2f<D>(T, T.lvl_off[0] + s, make_fq<D>(q, scale)) : box_lb2<D>(T, T.lvl_off[0] + s, q)) <= c2)) continue;
+    bool keep = (fbox_ok(scale) ? box_lb2f<D>(T, T.lvl_off[0] + s, make_fq<D>(q, scale))
+                                : box_lb2<D>(T, T.lvl_off[0] + s, q)) <= c2;
+    if (keep) keep = pair_may_survive<D>(T, s, q, c2);
+    unsigned long long slot = wave_append(&w.cnt[7], keep);
+    if (keep) {  // slot < pcap: never longer than the input list
+      w.pq2[slot] = (uint32_t)qi;
+      w.ps2[slot] = (uint32_t)s;
+    }
+  }
+  warp_count(w.counters, MREP_CNT_BOXES, nboxes);
+}
+
+// W2b: E' roots, monotone pieces, elimination for the filtered pairs
+template <int D, bool MULTI>
+__global__ void __launch_bounds__(BLOCK) wave_pairs(const __grid_constant__ WaveParams w) {
+  unsigned long long total = *(volatile unsigned long long*)&w.cnt[7];
+  if (total > w.pcap) total = w.pcap;
+  uint64_t npairs = 0;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    int64_t qi = w.pq2[i];  // sorted position
+    int64_t s = w.ps2[i];
+    const TableView& T = tab_of<MULTI>(w, qi);
+    double4 rec = *(const double4*)(w.qs + qi * 4);
+    double q[D];
+    q[0] = rec.x;
+    q[1] = rec.y;
+    if (D == 3) q[D - 1] = rec.z;
+    double scale = T.hdr[4];
+#pragma unroll
+    for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
+    const double c2 = cut2(rec.w, scale);  // the query's final seam bound
     PairPrep P;
-    if (!prep_pair_cut<D>(T, s, q, c2, P)) continue;
+    if (!prep_pair_cut<D>(T, s, q, c2, P)) continue;  // (W2a already passed it)
     ++npairs;
     double lo = 0.0;
 #pragma unroll 1
@@ -1771,7 +1842,6 @@ __global__ void __launch_bounds__(BLOCK) wave_pairs(const __grid_constant__ Wave
     }
   }
   warp_count(w.counters, MREP_CNT_PAIRS, npairs);
-  warp_count(w.counters, MREP_CNT_BOXES, nboxes);
 }
 
 // W3 with lane refill: each lane runs one clipping iteration of its current
@@ -2297,7 +2367,8 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   };
   size_t o_cnt = take(8 * sizeof(unsigned long long));
   size_t o_dmin = take(n * 8), o_tkey = take(n * 8), o_okey = take(n * 8), o_flag = take(n * 4);
-  size_t o_pq = take(pcap * 4), o_ps = take(pcap * 4);
+  size_t o_pq = take(pcap * 4), o_ps = take(pcap * 4), o_pq2 = take(pcap * 4),
+         o_ps2 = take(pcap * 4);
   size_t o_sb = take(scap * 64), o_sq = take(scap * 4), o_ssk = take(scap * 4);
   size_t o_cq = take(ccap * 4), o_ct = take(ccap * 8), o_cd = take(ccap * 8), o_cv = take(ccap * 8),
          o_cord = take(ccap * 8);
@@ -2327,6 +2398,8 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   w.flag = (int32_t*)(base + o_flag);
   w.pq = (uint32_t*)(base + o_pq);
   w.ps = (uint32_t*)(base + o_ps);
+  w.pq2 = (uint32_t*)(base + o_pq2);
+  w.ps2 = (uint32_t*)(base + o_ps2);
   w.pcap = pcap;
   w.sb = (double*)(base + o_sb);
   w.sq = (uint32_t*)(base + o_sq);
@@ -2404,6 +2477,7 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   }
   MREP_LAUNCH_CHECK();
   tm.mark();
+  wave_pairs_filter<D, MULTI><<<g_pairs, BLOCK, 0, st>>>(w);
   wave_pairs<D, MULTI><<<g_pairs, BLOCK, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
   tm.mark();
