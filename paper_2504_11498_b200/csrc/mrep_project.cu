@@ -1043,8 +1043,6 @@ struct WaveParams {
   int32_t* out_seg;
   uint64_t* counters;
   unsigned long long* dmin;  // bits of the running min distance (non-negative double)
-  unsigned long long* tkey;  // order key of the min t inside the band
-  unsigned long long* okey;  // min reference order among band members with that t
   int32_t* flag;             // 1 = finish in the fallback kernel
   double* qs;                // per sorted query: 4 doubles = coords (D) + running min (slot 3)
   double* win_t;             // winner record per sorted position
@@ -1061,6 +1059,8 @@ struct WaveParams {
   uint32_t* sq;
   uint32_t* ssk;  // cubic << 3 | piece
   unsigned long long scap;
+  uint32_t* chead;  // per sorted query: last candidate appended (linked list), ~0 = none
+  uint32_t* cnext;  // per candidate: the query's previous candidate
   uint32_t* cq;
   double* ct;
   double* cd;
@@ -1137,8 +1137,6 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
     if (cid < 0 || cid >= w.ncurves) cid = -1;
     w.gcur[gi] = cid;
     if (cid < 0) {  // out-of-range curve id (sorted last): NaN result, no work
-      w.tkey[gi] = ~0ull;
-      w.okey[gi] = ~0ull;
       w.scnt[gi] = 0;
       w.flag[gi] = 0;
       active = false;
@@ -1156,10 +1154,6 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
   for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
   const bool fb = fbox_ok(scale);  // float box tests (see box_lb2f)
   const FQ<D> fq = make_fq<D>(q, scale);
-  if (active) {
-    w.tkey[gi] = ~0ull;
-    w.okey[gi] = ~0ull;
-  }
   // cell mode: the query's cell in the uniform grid over the table box lists
   // every cubic that can hold a candidate for ANY query of the cell
   // (mrep_cells_build), nearest first; queries outside the grid walk the tree
@@ -1432,6 +1426,7 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
         w.cd[slot] = B.d[j];
         w.cv[slot] = -1.0;
         w.cord[slot] = B.ord[j];
+        w.cnext[slot] = atomicExch(&w.chead[gi], (uint32_t)slot);
       } else {
         fall = true;
       }
@@ -1555,8 +1550,6 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
     if (sub == 0) w.gcur[g] = cid;
     if (cid < 0) {  // out-of-range curve id (sorted last): NaN result, no work
       if (sub == 0) {
-        w.tkey[g] = ~0ull;
-        w.okey[g] = ~0ull;
         w.scnt[g] = 0;
         w.flag[g] = 0;
       }
@@ -1578,8 +1571,6 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
   int sp = 0, npark = 0;
   if (active) {
     if (sub == 0) {
-      w.tkey[g] = ~0ull;
-      w.okey[g] = ~0ull;
       SK[0] = ((unsigned long long)T.top << 40);
       SL[0] = 0.0;
     }
@@ -1696,6 +1687,7 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
         w.cd[slot] = d;
         w.cv[slot] = -1.0;
         w.cord[slot] = (unsigned long long)(j == 0 ? sb.s1 : sb.s2);
+        w.cnext[slot] = atomicExch(&w.chead[g], (uint32_t)slot);
       } else {
         fall = true;
       }
@@ -1926,6 +1918,7 @@ __global__ void __launch_bounds__(BLOCK) wave_clip(const __grid_constant__ WaveP
         w.cd[slot] = d;
         w.cv[slot] = v;
         w.cord[slot] = SURV_BIT | sk;
+        w.cnext[slot] = atomicExch(&w.chead[qi], (uint32_t)slot);
       } else if (atomicExch(&w.flag[qi], 1) == 0) {
         unsigned long long fs = atomicAdd(&w.cnt[3], 1ull);
         w.fb[fs] = qi;
@@ -1937,47 +1930,32 @@ __global__ void __launch_bounds__(BLOCK) wave_clip(const __grid_constant__ WaveP
   warp_count(w.counters, MREP_CNT_HULL_MISS, nmiss);
 }
 
-// W4..W6: the reference's selection as three atomic passes over candidates
-template <int D, int PASS>
-__global__ void __launch_bounds__(256) wave_select(const __grid_constant__ WaveParams w) {
-  unsigned long long total = *(volatile unsigned long long*)&w.cnt[2];
-  if (total > w.ccap) total = w.ccap;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    int64_t qi = w.cq[i];
-    if (w.flag[qi]) continue;
-    double d = w.cd[i];
-    if (!(d <= dmin_of(w, qi) + 1e-12)) continue;
-    unsigned long long tk = tkey_of(w.ct[i]);
-    if (PASS == 0) {
-      atomicMin(&w.tkey[qi], tk);
-      continue;
-    }
-    if (tk != w.tkey[qi]) continue;
-    unsigned long long ord = w.cord[i];
-    if (PASS == 1) {
-      atomicMin(&w.okey[qi], ord);
-      continue;
-    }
-    if (ord != w.okey[qi]) continue;
-    // winner record (identical duplicates write identical values)
-    w.win_t[qi] = w.ct[i];
-    w.win_d[qi] = d;
-    w.win_v[qi] = w.cv[i];
-  }
-}
-
-// Final pass in sorted order: foot point of each winner (recomputed exactly
-// as the reference stored it) and one scattered write of the outputs.
+// W4: selection + emit, one thread per sorted query walking its candidate
+// list: the reference's rule (_kernels.py:480-490) -- minimum distance, then
+// inside dmin + 1e-12 the smallest t (-0.0 == +0.0), then the smallest
+// reference order -- then the winner's foot point (recomputed exactly as the
+// reference stores it) and one scattered write of the outputs.
 template <int D, bool MULTI>
 __global__ void __launch_bounds__(256) wave_emit(const __grid_constant__ WaveParams w) {
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= w.n) return;
   if (w.flag[g]) return;  // written by the fallback kernel
   int64_t qi = w.perm ? (int64_t)w.perm[g] : g;
-  unsigned long long ord = w.okey[g];
   if (w.out_cand) w.out_cand[qi] = w.scnt[g];
-  if (ord == ~0ull) {
+  const double lim = dmin_of(w, g) + 1e-12;
+  unsigned long long bt = ~0ull, bo = ~0ull;
+  uint32_t bc = ~0u;
+  for (uint32_t c = w.chead[g]; c != ~0u; c = w.cnext[c]) {
+    if (!(w.cd[c] <= lim)) continue;
+    const unsigned long long tk = tkey_of(w.ct[c]);
+    const unsigned long long ok = w.cord[c];
+    if (tk < bt || (tk == bt && ok < bo)) {
+      bt = tk;
+      bo = ok;
+      bc = c;
+    }
+  }
+  if (bc == ~0u) {
     const double NaN = __longlong_as_double(0x7ff8000000000000LL);
     w.out_t[qi] = NaN;
     w.out_dist[qi] = NaN;
@@ -1989,22 +1967,22 @@ __global__ void __launch_bounds__(256) wave_emit(const __grid_constant__ WavePar
   const TableView& T = tab_of<MULTI>(w, g);
   double foot[D];
   int32_t seg;
-  if (ord & SURV_BIT) {
-    int64_t s = (int64_t)((ord & ~SURV_BIT) >> 3);
+  if (bo & SURV_BIT) {
+    int64_t s = (int64_t)((bo & ~SURV_BIT) >> 3);
     const double* r = T.rec + s * REC;
-    double v = w.win_v[g];
+    double v = w.cv[bc];
 #pragma unroll
     for (int dim = 0; dim < D; ++dim)
       foot[dim] = decasteljau1(r[R_P + dim], r[R_P + 3 + dim], r[R_P + 6 + dim], r[R_P + 9 + dim], v);
     seg = (int32_t)s;
   } else {
-    int64_t s = (int64_t)ord;
+    int64_t s = (int64_t)bo;
     double stt;
     seam_point<D>(T, s, foot, stt);
     seg = (int32_t)(s > 0 ? s - 1 : 0);
   }
-  w.out_t[qi] = w.win_t[g];
-  w.out_dist[qi] = w.win_d[g];
+  w.out_t[qi] = w.ct[bc];
+  w.out_dist[qi] = w.cd[bc];
 #pragma unroll
   for (int k = 0; k < D; ++k) w.out_foot[qi * D + k] = foot[k];
   if (w.out_seg) w.out_seg[qi] = seg;
@@ -2366,12 +2344,12 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
     return o;
   };
   size_t o_cnt = take(8 * sizeof(unsigned long long));
-  size_t o_dmin = take(n * 8), o_tkey = take(n * 8), o_okey = take(n * 8), o_flag = take(n * 4);
+  size_t o_dmin = take(n * 8), o_flag = take(n * 4);
   size_t o_pq = take(pcap * 4), o_ps = take(pcap * 4), o_pq2 = take(pcap * 4),
          o_ps2 = take(pcap * 4);
   size_t o_sb = take(scap * 64), o_sq = take(scap * 4), o_ssk = take(scap * 4);
   size_t o_cq = take(ccap * 4), o_ct = take(ccap * 8), o_cd = take(ccap * 8), o_cv = take(ccap * 8),
-         o_cord = take(ccap * 8);
+         o_cord = take(ccap * 8), o_cnext = take(ccap * 4), o_chead = take(n * 4);
   size_t o_fb = take(n * 8);
   size_t o_qs = take(n * 4 * 8), o_wt = take(n * 8), o_wd = take(n * 8), o_wv = take(n * 8),
          o_sc = take(n * 8);
@@ -2393,8 +2371,6 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   w.counters = p.counters;
   w.cnt = (unsigned long long*)(base + o_cnt);
   w.dmin = (unsigned long long*)(base + o_dmin);
-  w.tkey = (unsigned long long*)(base + o_tkey);
-  w.okey = (unsigned long long*)(base + o_okey);
   w.flag = (int32_t*)(base + o_flag);
   w.pq = (uint32_t*)(base + o_pq);
   w.ps = (uint32_t*)(base + o_ps);
@@ -2410,6 +2386,9 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   w.cd = (double*)(base + o_cd);
   w.cv = (double*)(base + o_cv);
   w.cord = (unsigned long long*)(base + o_cord);
+  w.cnext = (uint32_t*)(base + o_cnext);
+  w.chead = (uint32_t*)(base + o_chead);
+  MREP_CUDA_CHECK(cudaMemsetAsync(w.chead, 0xff, n * 4, st));
   w.ccap = ccap;
   w.fb = (int64_t*)(base + o_fb);
   w.qs = (double*)(base + o_qs);
@@ -2447,7 +2426,6 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   };
   const unsigned g_pairs = persist_grid((const void*)wave_pairs<D, MULTI>, BLOCK);
   const unsigned g_clip = persist_grid((const void*)wave_clip<D, MULTI>, BLOCK);
-  const unsigned persist = persist_grid((const void*)wave_select<D, 2>, 256);
   StageTimer tm(timing, st);
   tm.mark();
   if (tmode == TRAV_GROUP) {
@@ -2484,10 +2462,6 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   wave_clip<D, MULTI><<<g_clip, BLOCK, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
   tm.mark();
-  wave_select<D, 0><<<persist, 256, 0, st>>>(w);
-  wave_select<D, 1><<<persist, 256, 0, st>>>(w);
-  wave_select<D, 2><<<persist, 256, 0, st>>>(w);
-  MREP_LAUNCH_CHECK();
   wave_emit<D, MULTI><<<grid_for(n, 256), 256, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
   tm.mark();
