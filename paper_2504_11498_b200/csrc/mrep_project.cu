@@ -1013,19 +1013,22 @@ __global__ void __launch_bounds__(BLOCK) project_pass2_kernel(ProjParams p) {
 //
 // Small single-purpose kernels, each with a compact instruction footprint
 // and uniform work items, connected by device-side append buffers:
-//   W1 traverse  (thread / query, Morton order): BVH walk with the seam upper
-//                bound; emits (query, cubic) pairs and the seam candidates
-//                inside the seam tie band;
-//   W2 pairs     (thread / pair): E, E' roots, monotone pieces, elimination;
+//   W1 traverse  (thread / query, Morton order; or an 8-lane group per query
+//                for sparse batches): cell-list scan or BVH walk with the seam
+//                upper bound; emits (query, cubic) pairs and the seam
+//                candidates inside the seam tie band;
+//   W2a filter   (thread / pair): box, Bernstein and one-signed-E tests with
+//                the final seam bound; compacts the pairs that can survive;
+//   W2b pairs    (thread / pair): E, E' roots, monotone pieces, elimination;
 //                emits surviving pieces;
-//   W3 clip      (thread / survivor): Bezier clipping, foot point, distance;
+//   W3 clip      (lane refill): Bezier clipping, foot point, distance;
 //                emits candidates that can still reach the tie band and
 //                lowers the query's running minimum (atomicMin on the bits of
 //                a non-negative double);
-//   W4/W5/W6     exact tie-band selection over the candidate list, the
-//                reference's two-pass rule (_kernels.py:480-490) as three
-//                atomic passes: min distance -> min t inside dmin + 1e-12 ->
-//                min reference order -> the winner writes its outputs.
+//   W4 emit      (thread / query): walks the query's candidate list (atomic
+//                head + next links) applying the reference's two-pass rule
+//                (_kernels.py:480-490): min distance -> min t inside
+//                dmin + 1e-12 -> min reference order; writes the winner.
 // Queries whose buffers would overflow (or whose seam band exceeds BAND_K)
 // are finished by a per-thread exact fallback kernel.
 // =================================================================
