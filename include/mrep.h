@@ -229,10 +229,19 @@ MREP_API int mrep_synth_walk(const double* v0, const double* g, int64_t n, int d
  * for in-grid queries (results bit-identical).  mrep_cells_bytes sizes the
  * caller-owned buffer (synchronous); mrep_cells_build fills it and records
  * it in the table header (the buffer must outlive the table's use).
- * S <= 16384, grid <= 256. */
+ * grid <= 512; the Python layer builds it for S <= 2^17. */
 MREP_API int64_t mrep_cells_bytes(const void* table_dev, int64_t S, int d, int grid, void* stream);
 MREP_API int mrep_cells_build(void* table_dev, int64_t S, int d, int grid, void* cells_dev,
                               int64_t bytes, void* stream);
+
+/* The same cell index for a surface table (mrep_surface_table_pack): the
+ * exact points are each patch's seed grid; mrep_project_surface with
+ * MREP_CELLS scans the query's cell list instead of walking the patch
+ * hierarchy (results bit-identical).  Re-packing the table drops it. */
+MREP_API int64_t mrep_surface_cells_bytes(const void* table_dev, int64_t npatch, int pu, int pv,
+                                          int grid, void* stream);
+MREP_API int mrep_surface_cells_build(void* table_dev, int64_t npatch, int pu, int pv, int grid,
+                                      void* cells_dev, int64_t bytes, void* stream);
 
 /* Knot span of each parameter: searchsorted(knots, t, 'right') - 1 clipped
  * to [p, m - p - 2] (the span convention of core.py:108-112). */

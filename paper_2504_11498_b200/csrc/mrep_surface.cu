@@ -37,6 +37,7 @@
 
 #include "mrep_common.cuh"
 #include "mrep_screen.cuh"
+#include "mrep_cells.cuh"
 
 namespace mrep {
 
@@ -421,6 +422,7 @@ struct SurfParams {
   double* cd;
   unsigned long long ccap;
   int64_t* fb;
+  int cells;  // MREP_CELLS: scan the query's cell list instead of the tree
 };
 
 __device__ __forceinline__ unsigned long long* smin_ptr(const SurfParams& w, int64_t g) {
@@ -485,7 +487,33 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
   for (int k = 0; k < 3; ++k) scale = fmax(scale, fabs(q[k]));
   double ub = __longlong_as_double(0x7ff0000000000000LL);
   bool fall = false;
-  if (active) {
+  int64_t cell = 0;
+  if (active && w.cells && cell_of<3>(T, q, cell)) {
+    // cell index: the list holds every patch that can come within the cut of
+    // any query in the cell, nearest first; the first one seeds the bound
+    int32_t a, b;
+    const int32_t* ids = cell_list(T, 3, cell, a, b);
+    const int64_t p0 = __ldg(ids + a);
+    offer_points<PU, PV>(w, p0, q, ub, st);
+    w.prim[g] = (int32_t)p0;
+#pragma unroll 1
+    for (int32_t i = a; i < b; ++i) {
+      const int64_t s = __ldg(ids + i);
+      const double c2 = cut2(ub, scale);
+      st.boxes++;
+      if (box_lb2<3>(T, T.lvl_off[0] + s, q) <= c2 &&
+          obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2) {
+        if (s != p0) offer_points<PU, PV>(w, s, q, ub, st);
+        unsigned long long slot = wave_append(&w.cnt[0], true);
+        if (slot < w.pcap) {
+          w.pq[slot] = (uint32_t)g;
+          w.ps[slot] = (uint32_t)s;
+        } else {
+          fall = true;
+        }
+      }
+    }
+  } else if (active) {
     // greedy descent to a nearby patch: its points give the first bound
     int level = T.top;
     int64_t idx = 0;
@@ -559,6 +587,8 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
         masks |= (uint64_t)m << (8 * lv);
       }
     }
+  }
+  if (active) {
     double4 rec;
     rec.x = q[0];
     rec.y = q[1];
@@ -1123,6 +1153,7 @@ static int surface_chunk(const void* table, int64_t np, int pu, int pv, const do
   w.out_dist = out_dist;
   w.out_patch = out_patch;
   w.counters = counters;
+  w.cells = (flags & MREP_CELLS) ? 1 : 0;
   size_t sort_tmp = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                   (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 30, st);
@@ -1162,11 +1193,44 @@ static int surface_chunk(const void* table, int64_t np, int pu, int pv, const do
   return rc;
 }
 
+// cell-index leaf points of a patch: its (pu+1)(pv+1) seed-grid points
+struct SurfaceLeaves {
+  int pu, pv, rec;
+  __device__ int npts(const TableView&) const { return (pu + 1) * (pv + 1); }
+  __device__ void pt(const TableView& T, int, int64_t s, int k, double* p) const {
+    const double* G = T.rec + s * rec + surf_seed(pu, pv) + 3 * k;
+    p[0] = G[0];
+    p[1] = G[1];
+    p[2] = G[2];
+  }
+};
+
 }  // namespace mrep
 
 using namespace mrep;
 
 extern "C" {
+
+int64_t mrep_surface_cells_bytes(const void* table, int64_t npatch, int pu, int pv, int grid,
+                                 void* stream) {
+  if (!degree_supported(pu, pv)) {
+    set_error("mrep_surface_cells_bytes: unsupported degrees");
+    return -1;
+  }
+  const int R = surf_rec(pu, pv);
+  return cells_bytes(table, npatch, 3, grid, R, SurfaceLeaves{pu, pv, R}, (cudaStream_t)stream);
+}
+
+int mrep_surface_cells_build(void* table, int64_t npatch, int pu, int pv, int grid, void* cells,
+                             int64_t bytes, void* stream) {
+  if (!degree_supported(pu, pv)) {
+    set_error("mrep_surface_cells_build: unsupported degrees");
+    return MREP_ERR_ARG;
+  }
+  const int R = surf_rec(pu, pv);
+  return cells_build(table, npatch, 3, grid, R, SurfaceLeaves{pu, pv, R}, cells, bytes,
+                     (cudaStream_t)stream);
+}
 
 int64_t mrep_surface_table_bytes(int64_t npatch, int pu, int pv) {
   if (npatch < 1 || pu < 1 || pv < 1) return -1;

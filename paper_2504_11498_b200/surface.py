@@ -175,6 +175,39 @@ class DeviceSurfaceTable:
         I = L.to_dev(np.ascontiguousarray(patch_iv).reshape(-1))
         L.check(L.lib().mrep_surface_table_pack(L.ptr(P), L.ptr(I), nus, nvs, pu, pv,
                                                 L.ptr(self.buf), L.stream_ptr()))
+        self.cells = None
+        self.cells_tried = False
+        self.use_cells = True  # False: always walk the hierarchy
+
+    # cell index (mrep_surface_cells_build): built once, lazily, on the first
+    # dense batch (queries >> patches), as for curve tables
+    CELL_MIN_QUERIES = 1 << 16
+    CELL_MAX_PATCHES = 1 << 17
+    CELL_MAX_BYTES = 4 << 30
+
+    def build_cells(self, grid=None):
+        torch = L._torch()
+        if grid is None:
+            grid = 128 if self.npatch > (1 << 14) else 64
+        nb = L.lib().mrep_surface_cells_bytes(L.ptr(self.buf), self.npatch, self.pu, self.pv,
+                                              grid, L.stream_ptr())
+        if nb <= 0:
+            L.check(1)
+        if nb > self.CELL_MAX_BYTES:
+            return self
+        self.cells = torch.empty((nb + 3) // 4, dtype=torch.int32, device=self.buf.device)
+        L.check(L.lib().mrep_surface_cells_build(L.ptr(self.buf), self.npatch, self.pu, self.pv,
+                                                  grid, L.ptr(self.cells), nb, L.stream_ptr()))
+        return self
+
+    def _cell_flag(self, n):
+        if not self.use_cells or self.npatch > self.CELL_MAX_PATCHES:
+            return 0
+        if (self.cells is None and not self.cells_tried
+                and n >= max(self.CELL_MIN_QUERIES, 8 * self.npatch)):
+            self.cells_tried = True
+            self.build_cells()
+        return L.MREP_CELLS if (self.cells is not None and n >= 8 * self.npatch) else 0
 
     def project(self, queries, counters=None, extra_flags=0):
         """Device queries (n, 3) -> device (u, v, foot, dist, patch)."""
@@ -189,8 +222,8 @@ class DeviceSurfaceTable:
         dist = torch.empty((n,), dtype=torch.float64, device=dev)
         patch = torch.empty((n,), dtype=torch.int32, device=dev)
         L.check(L.lib().mrep_project_surface(
-            L.ptr(self.buf), self.npatch, self.pu, self.pv, L.ptr(q), n, int(extra_flags),
-            L.ptr(u), L.ptr(v), L.ptr(foot), L.ptr(dist), L.ptr(patch), L.ptr(counters),
+            L.ptr(self.buf), self.npatch, self.pu, self.pv, L.ptr(q), n,
+            int(extra_flags) | self._cell_flag(n), L.ptr(u), L.ptr(v), L.ptr(foot), L.ptr(dist), L.ptr(patch), L.ptr(counters),
             L.stream_ptr()))
         return u, v, foot, dist, patch
 
@@ -203,7 +236,8 @@ class DeviceSurfaceTable:
         u, v, foot, dist, patch = out
         p = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
         L.check(L.lib().mrep_project_surface_host(
-            L.ptr(self.buf), self.npatch, self.pu, self.pv, p(q), n, int(extra_flags), p(u),
+            L.ptr(self.buf), self.npatch, self.pu, self.pv, p(q), n,
+            int(extra_flags) | self._cell_flag(n), p(u),
             p(v), p(foot), p(dist), p(patch),
             p(counters) if counters is not None else ctypes.c_void_p(0)))
         return out

@@ -124,3 +124,25 @@ def test_large_surface_screened_vs_oracle_subsample(gpu, oracle_lib):
     o = oracle_lib.surface_project(prep.patch_pts.reshape(-1, 4, 4, 3),
                                    prep.patch_iv.reshape(-1, 4), 3, 3, q[idx], workers=16)
     _check(tuple(a[idx] for a in g), o)
+
+
+@pytest.mark.parametrize("pu,pv,n,grid", [(3, 3, 24, 16), (3, 3, 24, 64), (5, 5, 14, 32),
+                                          (3, 5, 12, 8), (1, 1, 30, 40), (3, 3, 82, 48)])
+def test_cell_index_matches_tree_walk(gpu, pu, pv, n, grid):
+    """mrep_surface_cells_build + MREP_CELLS: bit-identical to the hierarchy
+    walk, for queries inside the grid, outside it and on the surface (the
+    82 x 82 net has 6241 patches: the branch-and-bound cell bound)."""
+    from paper_2504_11498_b200 import _lib as L, eval_surface, prepare_surface
+    s = _surf(pu, pv, n, seed=3 * pu + pv)
+    prep = prepare_surface(s)
+    tab = prep.table
+    rng = np.random.default_rng(grid)
+    q = np.concatenate([rng.uniform(0, 1, (30000, 3)), rng.uniform(-0.5, 1.5, (5000, 3)),
+                        eval_surface(s, rng.uniform(0, 1, (3000, 2))),
+                        s.control_points[[0, -1], [0, -1]]])
+    tab.use_cells = False
+    a = [x.cpu().numpy() for x in tab.project(q)]
+    tab.build_cells(grid)
+    b = [x.cpu().numpy() for x in tab.project(q, extra_flags=L.MREP_CELLS)]
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
