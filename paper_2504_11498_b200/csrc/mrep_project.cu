@@ -36,6 +36,7 @@
 #include "mrep_math.cuh"
 #include "mrep_screen.cuh"
 #include "mrep_cells.cuh"
+#include "mrep_sort.cuh"
 
 namespace mrep {
 
@@ -2875,6 +2876,10 @@ static int project_chunk(const void* table, int64_t S, int d, const double* quer
   size_t sort_tmp = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                   (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 30, st);
+  // MREP_RADIX_SORT=1: the full 24-bit Morton radix sort instead of the
+  // bucket sort (mrep_sort.cuh), for comparison
+  static const bool radix = getenv("MREP_RADIX_SORT") != nullptr;
+  if (!radix) sort_tmp = bucket_sort_bytes(n, d);
   size_t off_list = 16, off_keys = off_list + sizeof(int64_t) * (size_t)n;
   size_t off_tmp = off_keys + 4 * sizeof(uint32_t) * (size_t)n;
   size_t wsb = off_tmp + sort_tmp + 256;
@@ -2894,6 +2899,13 @@ static int project_chunk(const void* table, int64_t S, int d, const double* quer
     uint32_t* i_in = k_out + n;
     uint32_t* i_out = i_in + n;
     const double* root = p.tab.box + p.tab.lvl_off[p.tab.top] * 6;
+    if (!radix) {
+      const int rc = bucket_sort(queries, n, d, root, wc + off_tmp, sort_tmp, i_out, st);
+      if (rc != MREP_OK) {
+        cudaFreeAsync(ws, st);
+        return rc;
+      }
+    } else {
     if (d == 3) morton_kernel<3><<<grid_for(n, 256), 256, 0, st>>>(queries, n, root, k_in, i_in);
     else morton_kernel<2><<<grid_for(n, 256), 256, 0, st>>>(queries, n, root, k_in, i_in);
     MREP_LAUNCH_CHECK();
@@ -2907,6 +2919,7 @@ static int project_chunk(const void* table, int64_t S, int d, const double* quer
     const int begin_bit = (sort_bits > 0 && sort_bits < end_bit) ? end_bit - sort_bits : 0;
     MREP_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(wc + off_tmp, sort_tmp, k_in, k_out, i_in, i_out,
                                                     (int)n, begin_bit, end_bit, st));
+    }
     p.perm = i_out;
   }
   sort_tm.mark();

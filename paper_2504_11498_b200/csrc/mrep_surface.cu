@@ -38,6 +38,7 @@
 #include "mrep_common.cuh"
 #include "mrep_screen.cuh"
 #include "mrep_cells.cuh"
+#include "mrep_sort.cuh"
 
 namespace mrep {
 
@@ -1157,6 +1158,8 @@ static int surface_chunk(const void* table, int64_t np, int pu, int pv, const do
   size_t sort_tmp = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                   (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 30, st);
+  static const bool radix = getenv("MREP_RADIX_SORT") != nullptr;
+  if (!radix) sort_tmp = bucket_sort_bytes(n, 3);
   char* ws = nullptr;
   const size_t o_tmp = 16 * (size_t)n + 256;
   MREP_CUDA_CHECK(cudaMallocAsync((void**)&ws, o_tmp + sort_tmp + 256, st));
@@ -1170,10 +1173,18 @@ static int surface_chunk(const void* table, int64_t np, int pu, int pv, const do
   w.perm = nullptr;
   if (!(flags & MREP_NO_SORT) && n > 64) {
     const double* root = w.tab.box + w.tab.lvl_off[w.tab.top] * 6;
-    surf_morton_kernel<<<grid_for(n, 256), 256, 0, st>>>(queries, n, root, k_in, i_in);
-    MREP_LAUNCH_CHECK();
-    MREP_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(ws + o_tmp, sort_tmp, k_in, k_out, i_in, i_out,
-                                                    (int)n, 0, 30, st));
+    if (!radix) {
+      const int rc = bucket_sort(queries, n, 3, root, ws + o_tmp, sort_tmp, i_out, st);
+      if (rc != MREP_OK) {
+        cudaFreeAsync(ws, st);
+        return rc;
+      }
+    } else {
+      surf_morton_kernel<<<grid_for(n, 256), 256, 0, st>>>(queries, n, root, k_in, i_in);
+      MREP_LAUNCH_CHECK();
+      MREP_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(ws + o_tmp, sort_tmp, k_in, k_out, i_in,
+                                                      i_out, (int)n, 0, 30, st));
+    }
     w.perm = i_out;
   }
   sort_tm.mark();

@@ -7,7 +7,7 @@ sys.path.insert(0, ".")
 import bench  # noqa: E402
 
 wl = bench.SingleCurve("cfg2", 0, 1, 0)
-for m in (65536, 131072, 262144, 458752, 1000000):
+for m in [int(x) for x in sys.argv[1:]] or (65536, 131072, 262144, 458752, 1000000):
     q = wl.q[:m].contiguous()
     for _ in range(3):
         wl.tab.project(q)

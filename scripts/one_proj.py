@@ -1,0 +1,18 @@
+"""One screened cfg2 projection of n queries (for ncu launch lists)."""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 125000
+wl = bench.SingleCurve("cfg2", 0, 1, 0)
+flags = wl.tab._cell_flag(1 << 20, True)
+q = wl.q[:n].contiguous()
+for _ in range(3):
+    wl.tab.project(q, extra_flags=flags)
+torch.cuda.synchronize()
+torch.cuda.nvtx.range_push("timed")
+wl.tab.project(q, extra_flags=flags)
+torch.cuda.synchronize()
