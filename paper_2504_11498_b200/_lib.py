@@ -17,7 +17,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmrep.so")
+# MREP_LIB: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("MREP_LIB") or os.path.join(_HERE, "libmrep.so")
 
 MREP_SCREEN = 1
 MREP_STATS = 2

@@ -75,6 +75,11 @@ struct HostCtx {
   Slot slot[NSLOT_MAX];
   BigBuf big;
   cudaStream_t cin = nullptr, cout = nullptr;  // copy-in / copy-out streams (fast path)
+  // fast-path compute streams by chunk index, in descending priority: the
+  // earliest chunk's kernels win the SMs, so its download starts first and
+  // later chunks fill the gaps
+  static constexpr int NPRIO = 8;
+  cudaStream_t prio[NPRIO] = {};
   std::vector<cudaEvent_t> ev_in, ev_comp;     // per-chunk hand-off events (cached)
   bool ready = false;
 };
@@ -114,6 +119,14 @@ int ensure_ctx() {
     MREP_CUDA_CHECK(cudaMallocHost(&s.hseg, CHUNK_MAX * sizeof(int32_t)));
     MREP_CUDA_CHECK(cudaMallocHost(&s.hcur, CHUNK_MAX * sizeof(int32_t)));
   }
+  {
+    int least = 0, greatest = 0;
+    MREP_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    for (int k = 0; k < HostCtx::NPRIO; ++k) {
+      const int pr = greatest + k < least ? greatest + k : least;
+      MREP_CUDA_CHECK(cudaStreamCreateWithPriority(&g_ctx.prio[k], cudaStreamDefault, pr));
+    }
+  }
   MREP_CUDA_CHECK(cudaStreamCreateWithFlags(&g_ctx.cin, cudaStreamDefault));
   MREP_CUDA_CHECK(cudaStreamCreateWithFlags(&g_ctx.cout, cudaStreamDefault));
   g_ctx.device = dev;
@@ -135,6 +148,7 @@ template <class Launch>
 int host_pipeline(int d, const double* queries, const int32_t* curve_ids, int64_t n,
                   double* out_t, double* out_foot, double* out_dist, int64_t* out_cand,
                   int32_t* out_seg, uint64_t* counters_host, Launch launch) {
+  const auto t_entry = std::chrono::steady_clock::now();
   int rc = ensure_ctx();
   if (rc != MREP_OK) return rc;
   const bool pin_in = is_pinned(queries) && (!curve_ids || is_pinned(curve_ids));
@@ -142,9 +156,12 @@ int host_pipeline(int d, const double* queries, const int32_t* curve_ids, int64_
                        is_pinned(out_cand) && (!out_seg || is_pinned(out_seg));
 
   const int NS = num_slots();
+  const bool fast = pin_in && pin_out && !getenv("MREP_E2E_SLOTTED");
   for (auto& s : g_ctx.slot)
-    MREP_CUDA_CHECK(cudaMemsetAsync(s.dcnt, 0, MREP_NUM_COUNTERS * sizeof(uint64_t), s.st));
-  if (pin_in && pin_out && !getenv("MREP_E2E_SLOTTED")) {
+    MREP_CUDA_CHECK(cudaMemsetAsync(s.dcnt, 0, MREP_NUM_COUNTERS * sizeof(uint64_t),
+                                    fast ? g_ctx.cin : s.st));
+  if (fast) {
+    static const bool use_prio = !getenv("MREP_E2E_PRIO") || atoi(getenv("MREP_E2E_PRIO")) != 0;
     const int NS = getenv("MREP_E2E_SLOTS") ? num_slots() : 2;
     // Pinned fast path: device buffers for the whole batch, every chunk
     // enqueued at once round-robin over NS streams (H2D -> kernels -> D2H
@@ -228,6 +245,7 @@ int host_pipeline(int d, const double* queries, const int32_t* curve_ids, int64_
     for (int64_t c = 0; c < nch; ++c) {
       const int64_t lo = cl[c].first;
       Slot v = g_ctx.slot[c % NS];  // stream + counters of the slot, big-buffer views
+      if (use_prio) v.st = g_ctx.prio[c < HostCtx::NPRIO ? c : HostCtx::NPRIO - 1];
       v.lo = lo;
       v.cnt = cl[c].second;
       v.dq = B.dq + lo * d;
@@ -246,7 +264,13 @@ int host_pipeline(int d, const double* queries, const int32_t* curve_ids, int64_
       MREP_CUDA_CHECK(cudaEventRecord(g_ctx.ev_in[c], ci));
       tmark(ci);
       MREP_CUDA_CHECK(cudaStreamWaitEvent(v.st, g_ctx.ev_in[c], 0));
+      const auto t_l0 = std::chrono::steady_clock::now();
       if ((rc = launch(v)) != MREP_OK) return rc;
+      if (dtrace)
+        fprintf(stderr, "chunk %lld: host launch %.3f ms (at %.3f)\n", (long long)c,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_l0)
+                    .count(),
+                std::chrono::duration<double, std::milli>(t_l0 - t_entry).count());
       MREP_CUDA_CHECK(cudaEventRecord(g_ctx.ev_comp[c], v.st));
       tmark(v.st);
       MREP_CUDA_CHECK(cudaStreamWaitEvent(co, g_ctx.ev_comp[c], 0));
@@ -263,8 +287,13 @@ int host_pipeline(int d, const double* queries, const int32_t* curve_ids, int64_
                                         cudaMemcpyDeviceToHost, co));
       tmark(co);
     }
+    const auto t_enq = std::chrono::steady_clock::now();
     MREP_CUDA_CHECK(cudaStreamSynchronize(g_ctx.cout));
     if (dtrace) {
+      const auto t_sync = std::chrono::steady_clock::now();
+      fprintf(stderr, "host: enqueue %.3f ms, wait %.3f ms\n",
+              std::chrono::duration<double, std::milli>(t_enq - t_entry).count(),
+              std::chrono::duration<double, std::milli>(t_sync - t_enq).count());
       cudaDeviceSynchronize();
       for (size_t k = 0; k + 2 < te.size(); k += 3) {
         float a = 0, b = 0, e = 0;
@@ -276,7 +305,7 @@ int host_pipeline(int d, const double* queries, const int32_t* curve_ids, int64_
       for (auto ev : te) cudaEventDestroy(ev);
       cudaEventDestroy(te0);
     }
-    for (int i = 0; i < NS; ++i) MREP_CUDA_CHECK(cudaStreamSynchronize(g_ctx.slot[i].st));
+    // (every chunk's kernels precede its download on the copy-out stream)
     if (counters_host) {
       for (auto& s : g_ctx.slot) {
         uint64_t cc[MREP_NUM_COUNTERS];

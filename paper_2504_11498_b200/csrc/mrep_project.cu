@@ -67,6 +67,18 @@ constexpr uint64_t SURV_BIT = 1ull << 62;
 constexpr int BAND_K = 4;
 constexpr int LIST_CAP = 32;
 constexpr int BLOCK = 128;
+// resident blocks per SM the wave kernels are compiled for (register caps:
+// 65536 / (128 x minb) per thread; measured on cfg2: 0.865 vs 0.958 ms for
+// the uncapped 80-96 registers, despite small spills)
+#ifndef MREP_TRAV_MINB
+#define MREP_TRAV_MINB 6
+#endif
+#ifndef MREP_PAIRS_MINB
+#define MREP_PAIRS_MINB 6
+#endif
+#ifndef MREP_CLIP_MINB
+#define MREP_CLIP_MINB 8
+#endif
 
 struct ProjParams {
   TableView tab;
@@ -1447,7 +1459,7 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
 // persistent warps pull 32-position tasks from an atomic work queue, so the
 // long tasks start first and the short ones fill the tail (LPT order).
 template <int D, bool MULTI, int TM>
-__global__ void __launch_bounds__(BLOCK) wave_traverse(const __grid_constant__ WaveParams w) {
+__global__ void __launch_bounds__(BLOCK, MREP_TRAV_MINB) wave_traverse(const __grid_constant__ WaveParams w) {
   __shared__ unsigned long long stk[BLOCK / 32][PSTACK];
   const int lane = threadIdx.x & 31;
   unsigned long long* S = stk[threadIdx.x >> 5];
@@ -1784,7 +1796,7 @@ __global__ void __launch_bounds__(BLOCK) wave_pairs_filter(const __grid_constant
 
 // W2b: E' roots, monotone pieces, elimination for the filtered pairs
 template <int D, bool MULTI>
-__global__ void __launch_bounds__(BLOCK) wave_pairs(const __grid_constant__ WaveParams w) {
+__global__ void __launch_bounds__(BLOCK, MREP_PAIRS_MINB) wave_pairs(const __grid_constant__ WaveParams w) {
   unsigned long long total = *(volatile unsigned long long*)&w.cnt[7];
   if (total > w.pcap) total = w.pcap;
   uint64_t npairs = 0;
@@ -1838,7 +1850,7 @@ __global__ void __launch_bounds__(BLOCK) wave_pairs(const __grid_constant__ Wave
 // as its own is finished (1..8 iterations per survivor no longer leave
 // lanes idle).  Same arithmetic as clip_root (clip_init + clip_step).
 template <int D, bool MULTI>
-__global__ void __launch_bounds__(BLOCK) wave_clip(const __grid_constant__ WaveParams w) {
+__global__ void __launch_bounds__(BLOCK, MREP_CLIP_MINB) wave_clip(const __grid_constant__ WaveParams w) {
   const unsigned long long total0 = *(volatile unsigned long long*)&w.cnt[1];
   const unsigned long long total = total0 > w.scap ? w.scap : total0;
   unsigned long long* queue = &w.cnt[6];

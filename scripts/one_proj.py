@@ -7,10 +7,11 @@ sys.path.insert(0, ".")
 import bench  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 125000
+warm = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 wl = bench.SingleCurve("cfg2", 0, 1, 0)
 flags = wl.tab._cell_flag(1 << 20, True)
 q = wl.q[:n].contiguous()
-for _ in range(3):
+for _ in range(warm):
     wl.tab.project(q, extra_flags=flags)
 torch.cuda.synchronize()
 torch.cuda.nvtx.range_push("timed")
