@@ -1046,6 +1046,22 @@ __global__ void __launch_bounds__(BLOCK) project_pass2_kernel(ProjParams p) {
 // Queries whose buffers would overflow (or whose seam band exceeds BAND_K)
 // are finished by a per-thread exact fallback kernel.
 // =================================================================
+// a candidate of a query's final selection: parameter, distance, local
+// parameter of a clipped survivor (-1 for seams), tie order (seam index, or
+// CAND_SURV | cubic << 3 | piece for survivors) and the query's previous
+// candidate (a per-query linked list headed by chead): one sector per record
+constexpr uint32_t CAND_SURV = 1u << 31;
+struct alignas(32) Cand {
+  double t, d, v;
+  uint32_t ord, next;
+};
+
+__device__ __forceinline__ void put_cand(Cand* c, double t, double d, double v, uint32_t ord,
+                                         uint32_t next) {
+  double4* p = reinterpret_cast<double4*>(c);
+  *p = make_double4(t, d, v, __longlong_as_double((long long)(((uint64_t)next << 32) | ord)));
+}
+
 struct WaveParams {
   TableView tab;
   const double* q;
@@ -1077,12 +1093,7 @@ struct WaveParams {
   uint32_t* ssk;  // cubic << 3 | piece
   unsigned long long scap;
   uint32_t* chead;  // per sorted query: last candidate appended (linked list), ~0 = none
-  uint32_t* cnext;  // per candidate: the query's previous candidate
-  uint32_t* cq;
-  double* ct;
-  double* cd;
-  double* cv;
-  unsigned long long* cord;
+  Cand* cand;       // candidate records (one 32-B sector each)
   unsigned long long ccap;
   int64_t* fb;
   // multi-curve batch (mrep_project_batch): per-curve table descriptors, the
@@ -1224,6 +1235,7 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
         for (int e = 0; e < 2; ++e) offer_seam<D>(T, ch + e, q, B, st);
       }
       unsigned long long slot = wave_append(&w.cnt[0], need);
+      st.pairs += need ? 1 : 0;
       if (need) {
         if (slot < w.pcap) {
           w.pq[slot] = (uint32_t)gi;
@@ -1266,6 +1278,7 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
           need = bern_may_reach<D>(T, ch, q, cut2(B.dmin, scale));
         }
         unsigned long long slot = wave_append(&w.cnt[0], need);
+        st.pairs += need ? 1 : 0;
         if (need) {
           if (slot < w.pcap) {
             w.pq[slot] = (uint32_t)gi;
@@ -1316,6 +1329,7 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
           }
         }
         unsigned long long slot = wave_append(&w.cnt[0], need);
+        st.pairs += need ? 1 : 0;
         if (need) {
           if (slot < w.pcap) {
             w.pq[slot] = (uint32_t)gi;
@@ -1430,19 +1444,17 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
     unsigned long long slot = wave_append(&w.cnt[2], want);
     if (want) {
       if (slot < w.ccap) {
-        w.cq[slot] = (uint32_t)gi;
-        w.ct[slot] = B.t[j];
-        w.cd[slot] = B.d[j];
-        w.cv[slot] = -1.0;
-        w.cord[slot] = B.ord[j];
-        w.cnext[slot] = atomicExch(&w.chead[gi], (uint32_t)slot);
+        put_cand(w.cand + slot, B.t[j], B.d[j], -1.0, (uint32_t)B.ord[j],
+                 atomicExch(&w.chead[gi], (uint32_t)slot));
       } else {
         fall = true;
       }
     }
   }
   if (active) {
-    w.scnt[gi] = (int64_t)st.offers;
+    // cand (screened): seams offered + cubics queued for the exact solve by
+    // this query's traversal -- independent of the other queries' timing
+    w.scnt[gi] = (int64_t)(st.offers + st.pairs);
     w.flag[gi] = fall ? 1 : 0;
     if (fall) {
       unsigned long long slot = atomicAdd(&w.cnt[3], 1ull);
@@ -1522,7 +1534,7 @@ template <int D>
 __device__ __forceinline__ void flush_pairs(const WaveParams& w, const TableView& T, int64_t g,
                                             const double (&q)[D], double c2, const uint32_t* PC,
                                             const double* PL, int cnt, int rounds, int sub,
-                                            bool& fall) {
+                                            bool& fall, uint64_t& npairs) {
   for (int r = 0; r < rounds; ++r) {
     const int i = r * 8 + sub;
     bool need = false;
@@ -1532,6 +1544,7 @@ __device__ __forceinline__ void flush_pairs(const WaveParams& w, const TableView
       need = PL[i] <= c2 && bern_may_reach<D>(T, ch, q, c2);
     }
     unsigned long long slot = wave_append(&w.cnt[0], need);
+    npairs += need ? 1 : 0;
     if (need) {
       if (slot < w.pcap) {
         w.pq[slot] = (uint32_t)g;
@@ -1644,7 +1657,7 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
       const bool park = keep && lb <= c2;
       const unsigned pm = (__ballot_sync(gmask, park) >> (lane & 24)) & 0xffu;
       if (npark + __popc(pm) > GPAIRS) {  // list full: flush with the current bound
-        flush_pairs<D>(w, T, g, q, c2, PC, PL, npark, (npark + 7) >> 3, sub, fall);
+        flush_pairs<D>(w, T, g, q, c2, PC, PL, npark, (npark + 7) >> 3, sub, fall, st.pairs);
         __syncwarp(gmask);
         npark = 0;
       }
@@ -1691,12 +1704,8 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
       if (slot < w.ccap) {
         double pt[D], ts;
         seam_point<D>(T, j == 0 ? sb.s1 : sb.s2, pt, ts);
-        w.cq[slot] = (uint32_t)g;
-        w.ct[slot] = ts;
-        w.cd[slot] = d;
-        w.cv[slot] = -1.0;
-        w.cord[slot] = (unsigned long long)(j == 0 ? sb.s1 : sb.s2);
-        w.cnext[slot] = atomicExch(&w.chead[g], (uint32_t)slot);
+        put_cand(w.cand + slot, ts, d, -1.0, (uint32_t)(j == 0 ? sb.s1 : sb.s2),
+                 atomicExch(&w.chead[g], (uint32_t)slot));
       } else {
         fall = true;
       }
@@ -1704,9 +1713,9 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
   }
   // parked leaves that still pass the final bound become pairs
   const int rounds = (__reduce_max_sync(0xffffffffu, (unsigned)npark) + 7) >> 3;
-  flush_pairs<D>(w, T, g, q, c2f, PC, PL, npark, rounds, sub, fall);
+  flush_pairs<D>(w, T, g, q, c2f, PC, PL, npark, rounds, sub, fall, st.pairs);
   // group totals to the leader lane
-  unsigned long long offers = st.offers;
+  unsigned long long offers = st.offers + st.pairs;
   offers += __shfl_xor_sync(0xffffffffu, offers, 4);
   offers += __shfl_xor_sync(0xffffffffu, offers, 2);
   offers += __shfl_xor_sync(0xffffffffu, offers, 1);
@@ -1915,19 +1924,14 @@ __global__ void __launch_bounds__(BLOCK, MREP_CLIP_MINB) wave_clip(const __grid_
     }
     double d = sqrt(acc);
     double t = ta + v * (tb - ta);
-    atomicAdd((unsigned long long*)&w.scnt[qi], 1ull);
     double cur = dmin_of(w, qi);
     bool keep = d <= cur + 1e-12;
     unsigned long long slot = wave_append(&w.cnt[2], keep);
     if (keep) {
       atomicMin(dmin_ptr(w, qi), (unsigned long long)__double_as_longlong(d));
       if (slot < w.ccap) {
-        w.cq[slot] = (uint32_t)qi;
-        w.ct[slot] = t;
-        w.cd[slot] = d;
-        w.cv[slot] = v;
-        w.cord[slot] = SURV_BIT | sk;
-        w.cnext[slot] = atomicExch(&w.chead[qi], (uint32_t)slot);
+        put_cand(w.cand + slot, t, d, v, CAND_SURV | (uint32_t)sk,
+                 atomicExch(&w.chead[qi], (uint32_t)slot));
       } else if (atomicExch(&w.flag[qi], 1) == 0) {
         unsigned long long fs = atomicAdd(&w.cnt[3], 1ull);
         w.fb[fs] = qi;
@@ -1952,19 +1956,27 @@ __global__ void __launch_bounds__(256) wave_emit(const __grid_constant__ WavePar
   int64_t qi = w.perm ? (int64_t)w.perm[g] : g;
   if (w.out_cand) w.out_cand[qi] = w.scnt[g];
   const double lim = dmin_of(w, g) + 1e-12;
-  unsigned long long bt = ~0ull, bo = ~0ull;
-  uint32_t bc = ~0u;
-  for (uint32_t c = w.chead[g]; c != ~0u; c = w.cnext[c]) {
-    if (!(w.cd[c] <= lim)) continue;
-    const unsigned long long tk = tkey_of(w.ct[c]);
-    const unsigned long long ok = w.cord[c];
+  unsigned long long bt = ~0ull;
+  uint32_t bo = ~0u;
+  bool found = false;
+  double best_t = 0.0, best_d = 0.0, best_v = 0.0;
+  for (uint32_t c = w.chead[g]; c != ~0u;) {
+    const double4 r = *reinterpret_cast<const double4*>(w.cand + c);
+    const uint64_t on = (uint64_t)__double_as_longlong(r.w);
+    c = (uint32_t)(on >> 32);
+    if (!(r.y <= lim)) continue;
+    const unsigned long long tk = tkey_of(r.x);
+    const uint32_t ok = (uint32_t)on;
     if (tk < bt || (tk == bt && ok < bo)) {
       bt = tk;
       bo = ok;
-      bc = c;
+      best_t = r.x;
+      best_d = r.y;
+      best_v = r.z;
+      found = true;
     }
   }
-  if (bc == ~0u) {
+  if (!found) {
     const double NaN = __longlong_as_double(0x7ff8000000000000LL);
     w.out_t[qi] = NaN;
     w.out_dist[qi] = NaN;
@@ -1976,10 +1988,10 @@ __global__ void __launch_bounds__(256) wave_emit(const __grid_constant__ WavePar
   const TableView& T = tab_of<MULTI>(w, g);
   double foot[D];
   int32_t seg;
-  if (bo & SURV_BIT) {
-    int64_t s = (int64_t)((bo & ~SURV_BIT) >> 3);
+  if (bo & CAND_SURV) {
+    int64_t s = (int64_t)((bo & ~CAND_SURV) >> 3);
     const double* r = T.rec + s * REC;
-    double v = w.cv[bc];
+    double v = best_v;
 #pragma unroll
     for (int dim = 0; dim < D; ++dim)
       foot[dim] = decasteljau1(r[R_P + dim], r[R_P + 3 + dim], r[R_P + 6 + dim], r[R_P + 9 + dim], v);
@@ -1990,8 +2002,8 @@ __global__ void __launch_bounds__(256) wave_emit(const __grid_constant__ WavePar
     seam_point<D>(T, s, foot, stt);
     seg = (int32_t)(s > 0 ? s - 1 : 0);
   }
-  w.out_t[qi] = w.ct[bc];
-  w.out_dist[qi] = w.cd[bc];
+  w.out_t[qi] = best_t;
+  w.out_dist[qi] = best_d;
 #pragma unroll
   for (int k = 0; k < D; ++k) w.out_foot[qi * D + k] = foot[k];
   if (w.out_seg) w.out_seg[qi] = seg;
@@ -2357,8 +2369,7 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   size_t o_pq = take(pcap * 4), o_ps = take(pcap * 4), o_pq2 = take(pcap * 4),
          o_ps2 = take(pcap * 4);
   size_t o_sb = take(scap * 64), o_sq = take(scap * 4), o_ssk = take(scap * 4);
-  size_t o_cq = take(ccap * 4), o_ct = take(ccap * 8), o_cd = take(ccap * 8), o_cv = take(ccap * 8),
-         o_cord = take(ccap * 8), o_cnext = take(ccap * 4), o_chead = take(n * 4);
+  size_t o_cand = take(ccap * sizeof(Cand)), o_chead = take(n * 4);
   size_t o_fb = take(n * 8);
   size_t o_qs = take(n * 4 * 8), o_wt = take(n * 8), o_wd = take(n * 8), o_wv = take(n * 8),
          o_sc = take(n * 8);
@@ -2390,12 +2401,7 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   w.sq = (uint32_t*)(base + o_sq);
   w.ssk = (uint32_t*)(base + o_ssk);
   w.scap = scap;
-  w.cq = (uint32_t*)(base + o_cq);
-  w.ct = (double*)(base + o_ct);
-  w.cd = (double*)(base + o_cd);
-  w.cv = (double*)(base + o_cv);
-  w.cord = (unsigned long long*)(base + o_cord);
-  w.cnext = (uint32_t*)(base + o_cnext);
+  w.cand = (Cand*)(base + o_cand);
   w.chead = (uint32_t*)(base + o_chead);
   MREP_CUDA_CHECK(cudaMemsetAsync(w.chead, 0xff, n * 4, st));
   w.ccap = ccap;
@@ -2890,7 +2896,11 @@ static int project_chunk(const void* table, int64_t S, int d, const double* quer
                                   (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 30, st);
   // MREP_RADIX_SORT=1: the full 24-bit Morton radix sort instead of the
   // bucket sort (mrep_sort.cuh), for comparison
-  static const bool radix = getenv("MREP_RADIX_SORT") != nullptr;
+  // packet walks depend on which queries share a warp, so they keep the
+  // stable radix order (deterministic warps, hence deterministic `cand`);
+  // per-query walks (cells, lanes, groups) take the bucket order
+  const int tmode = trav_mode(flags, n, S, table_view(table, S).top);
+  const bool radix = getenv("MREP_RADIX_SORT") != nullptr || tmode == TRAV_PACKET;
   if (!radix) sort_tmp = bucket_sort_bytes(n, d);
   size_t off_list = 16, off_keys = off_list + sizeof(int64_t) * (size_t)n;
   size_t off_tmp = off_keys + 4 * sizeof(uint32_t) * (size_t)n;
@@ -2938,7 +2948,6 @@ static int project_chunk(const void* table, int64_t S, int d, const double* quer
   sort_tm.finish(0);
   int rc;
   bool wave = (flags & MREP_SCREEN) && !(flags & MREP_STATS) && !(flags & MREP_FUSED);
-  const int tmode = trav_mode(flags, n, S, p.tab.top);
   if (wave)
     rc = d == 3 ? launch_wave<3, false>(p, st, timing, tmode)
                 : launch_wave<2, false>(p, st, timing, tmode);

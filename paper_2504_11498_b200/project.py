@@ -11,7 +11,8 @@ like the reference's numba batch driver.
 Modes of project_prepared:
 * default (screen=True): BVH-screened exact solve.  t, foot, distance (and the
   winning segment) are those of the brute-force reference kernel; `cand`
-  counts the candidates the screened kernel examined (the reference counts
+  counts what the query's screened traversal examined: seams offered plus
+  cubics queued for the exact solve (the reference counts
   every seam plus every survivor of every cubic, a brute-force quantity).
 * screen=False, or with_stats / soundness_samples: brute force over all
   cubics with the reference's exact cand, ProjectionStats and soundness.

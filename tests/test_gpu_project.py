@@ -293,3 +293,22 @@ def test_cell_index_large_table_bvh_build(gpu):
     b = tab.project(q, extra_flags=L.MREP_CELLS)
     for k in (0, 1, 2, 4):
         assert np.array_equal(a[k].cpu().numpy(), b[k].cpu().numpy()), k
+
+
+def test_cand_deterministic_with_bucket_order(gpu):
+    """Cell / per-lane walks take the bucket-sorted order (queries of one
+    bucket in no fixed order); every output, `cand` included, is a function of
+    the query alone: repeated calls and a sub-batch agree bit for bit."""
+    from paper_2504_11498_b200 import _lib as L
+    from paper_2504_11498_b200 import _device as D
+    z = load_golden("project_cfg2.npz")
+    tab = D.DeviceTable(z["seg_pts"], z["seg_ta"], z["seg_tb"], z["seam_t"], z["seam_pt"])
+    tab.build_cells(32)
+    q = np.random.default_rng(21).uniform(-0.2, 1.2, (100000, 3))
+    for flags in (L.MREP_CELLS, L.MREP_PER_LANE, L.MREP_GROUP):
+        a = [x.cpu().numpy() for x in tab.project(q, extra_flags=flags)[:5]]
+        b = [x.cpu().numpy() for x in tab.project(q, extra_flags=flags)[:5]]
+        c = [x.cpu().numpy() for x in tab.project(q[:7777], extra_flags=flags)[:5]]
+        for x, y, zz in zip(a, b, c):
+            assert np.array_equal(x, y)
+            assert np.array_equal(x[:7777], zz)
