@@ -360,6 +360,10 @@ __device__ __forceinline__ bool newton_iter(const double* P, const double (&q)[3
   for (int ls = 0; ls < LS_MAX; ++ls) {
     un = clamp01(u + t * du);
     vn = clamp01(v + t * dv);
+    // the step rounds away: every further (halved) trial is this same point,
+    // whose value f cannot beat -- the search fails exactly as it would after
+    // LS_MAX evaluations (same state, no wasted evaluations)
+    if (un == u && vn == v) break;
     double S[3];
     surf_point<PU, PV, STRIDE>(P, un, vn, S);
     fn = dist2_to(S, q);
