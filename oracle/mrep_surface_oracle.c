@@ -30,6 +30,7 @@
 
 #define NEWTON_MAX 30
 #define LS_MAX 12
+#define LS_STEP_MIN 1e-11
 
 static double binom_d(int n, int k) {
   double r = 1.0;
@@ -170,8 +171,13 @@ void oracle_surf_patch_min(const double* P, int pu, int pv, const double* q, dou
     double t = 1.0, un = u, vn = v, fn = f;
     int ok = 0;
     for (int ls = 0; ls < LS_MAX; ++ls) {
+      /* the full step is always tried; no decrease down to a halved step of
+       * LS_STEP_MIN: stationary to that resolution (further halvings only
+       * chase rounding noise in f) */
+      if (ls > 0 && t * fmax(fabs(du), fabs(dv)) < LS_STEP_MIN) break;
       un = clamp01(u + t * du);
       vn = clamp01(v + t * dv);
+      if (un == u && vn == v) break; /* the step rounds away: no decrease possible */
       double S[3];
       surf_point(P, pu, pv, un, vn, S);
       fn = dist2(S, q);

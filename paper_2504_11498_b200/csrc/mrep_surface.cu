@@ -282,6 +282,7 @@ struct QStatsLite {
 
 constexpr int NEWTON_MAX = 30;
 constexpr int LS_MAX = 12;
+constexpr double LS_STEP_MIN = 1e-11;
 
 // Minimum of |S(u,v) - q|^2 on one patch: best Bernstein seed, then
 // projected Newton (oracle: surf_patch_min in mrep_surface_oracle.c).  Split
@@ -358,6 +359,10 @@ __device__ __forceinline__ bool newton_iter(const double* P, const double (&q)[3
   bool ok = false;
 #pragma unroll 1
   for (int ls = 0; ls < LS_MAX; ++ls) {
+    // the full step is always tried; no decrease down to a halved step of
+    // LS_STEP_MIN: the iterate is stationary to that resolution (the
+    // remaining halvings would only chase rounding noise in f)
+    if (ls > 0 && t * fmax(fabs(du), fabs(dv)) < LS_STEP_MIN) break;
     un = clamp01(u + t * du);
     vn = clamp01(v + t * dv);
     // the step rounds away: every further (halved) trial is this same point,
