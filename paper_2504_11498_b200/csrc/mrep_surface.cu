@@ -635,7 +635,8 @@ __global__ void __launch_bounds__(256) surf_filter(const __grid_constant__ SurfP
       double scale = fmax(T.hdr[4], fmax(fabs(q[0]), fmax(fabs(q[1]), fabs(q[2]))));
       const double c2 = cut2(rec.w, scale);
       keep = box_lb2<3>(T, T.lvl_off[0] + s, q) <= c2 &&
-             obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2;
+             obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2 &&
+             bern_patch_may_reach<PU, PV>(T.rec + s * w.rec, q, c2);
     }
     unsigned long long slot = wave_append(&w.cnt[6], keep);
     if (keep) {  // slot < pcap: the compact list is never longer than the input
@@ -696,8 +697,7 @@ __global__ void __launch_bounds__(128, (PU + PV <= 6) ? 3 : 1) surf_solve(const 
             if (PASS == 1) {  // the bound may have tightened since the filter
               double scale = fmax(T.hdr[4], fmax(fabs(q[0]), fmax(fabs(q[1]), fabs(q[2]))));
               const double c2 = cut2(smin_of(w, g), scale);
-              go = obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2 &&
-                   bern_patch_may_reach<PU, PV>(T.rec + s * w.rec, q, c2);
+              go = obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2;
             }
             if (go) {
               P = T.rec + s * w.rec;
