@@ -1221,27 +1221,68 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
 #pragma unroll 1
     for (int e = 0; e < 2; ++e) offer_seam<D>(T, idx + e, q, B, st);
   }
+  // cell mode buffers a lane's pairs in registers and appends them once per
+  // query (one warp-aggregated reservation) instead of one warp-wide atomic
+  // round trip per list entry that any lane needs
+  constexpr int PEND = 8;
+  uint32_t pend[PEND];
+  int np = 0;
   if (TM == TM_CELLS && incell) {
     int32_t a, b;
     const int32_t* ids = cell_list(T, D, cell, a, b);
+    int32_t nxt = a < b ? __ldg(ids + a) : 0;
 #pragma unroll 1
     for (int32_t k = a; k < b; ++k) {
-      const int64_t ch = __ldg(ids + k);
+      const int64_t ch = nxt;
+      if (k + 1 < b) nxt = __ldg(ids + k + 1);  // next id in flight during this entry
       st.boxes++;
       bool need = (fb ? box_lb2f<D>(T, T.lvl_off[0] + ch, fq) : box_lb2<D>(T, T.lvl_off[0] + ch, q)) <=
                   cut2(B.dmin, scale);
       if (need) {
 #pragma unroll 1
         for (int e = 0; e < 2; ++e) offer_seam<D>(T, ch + e, q, B, st);
+        st.pairs++;
+        if (np == PEND) {  // buffer full (rare): this lane appends alone
+          const unsigned long long base = atomicAdd(&w.cnt[0], (unsigned long long)PEND);
+#pragma unroll
+          for (int e = 0; e < PEND; ++e) {
+            if (base + e < w.pcap) {
+              w.pq[base + e] = (uint32_t)gi;
+              w.ps[base + e] = pend[e];
+            } else {
+              fall = true;
+            }
+          }
+          np = 0;
+        }
+#pragma unroll
+        for (int e = 0; e < PEND; ++e)
+          if (e == np) pend[e] = (uint32_t)ch;
+        ++np;
       }
-      unsigned long long slot = wave_append(&w.cnt[0], need);
-      st.pairs += need ? 1 : 0;
-      if (need) {
-        if (slot < w.pcap) {
-          w.pq[slot] = (uint32_t)gi;
-          w.ps[slot] = (uint32_t)ch;
-        } else {
-          fall = true;
+    }
+  }
+  if (TM == TM_CELLS) {  // warp-uniform: all lanes reconverge here
+    int incl = np;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total) {
+      unsigned long long base = 0;
+      if (lane == 31) base = atomicAdd(&w.cnt[0], (unsigned long long)total);
+      base = __shfl_sync(0xffffffffu, base, 31) + (unsigned long long)(incl - np);
+#pragma unroll
+      for (int e = 0; e < PEND; ++e) {
+        if (e < np) {
+          if (base + e < w.pcap) {
+            w.pq[base + e] = (uint32_t)gi;
+            w.ps[base + e] = pend[e];
+          } else {
+            fall = true;
+          }
         }
       }
     }
