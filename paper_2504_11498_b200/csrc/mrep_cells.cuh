@@ -27,7 +27,7 @@
 namespace mrep {
 
 // header slots of a table holding a cell index
-constexpr int H_CELLS = 8, H_GRID = 9, H_GLO = 10, H_GINV = 13, H_GHI = 16;
+constexpr int H_CELLS = 8, H_GRID = 9, H_GLO = 10, H_GINV = 13, H_GHI = 16, H_CTOT = 19;
 
 struct CellGrid {
   int G, d;
@@ -222,43 +222,47 @@ __global__ void cells_count_kernel(const __grid_constant__ TableView T, const LP
 template <class LP>
 __global__ void cells_fill_kernel(const __grid_constant__ TableView T, const LP lp,
                                   const __grid_constant__ CellGrid g, const int32_t* off,
-                                  int32_t* ids) {
+                                  int32_t* ids, float* keys) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= g.ncell) return;
   double lo[3], hi[3];
   cell_box(g, c, lo, hi);
   const double c2 = cell_cut2(T, lp, g, lo, hi);
   int32_t* out = ids + off[c];
+  float* key = keys + off[c];
   int32_t n = 0;
   cell_leaves(T, g, lo, hi, c2, [&](int64_t s) { out[n++] = (int32_t)s; });
+  // key = distance^2 from the (grown) cell to the leaf box, rounded down: a
+  // lower bound of box_lb2(q, box) for every query q of the cell.  Sorted
+  // ascending (ties by leaf id), the scan of a query can stop at the first
+  // key above its cut: every later leaf fails the box test too.
+  for (int32_t i = 0; i < n; ++i)
+    key[i] = __double2float_rd(cellbox_lb2(T, g.d, T.lvl_off[0] + out[i], lo, hi));
+  // equal keys (typically 0: boxes meeting the cell) go nearest to the cell
+  // centre first, so the running bound tightens early; then by leaf id
   double ctr[3];
   for (int k = 0; k < 3; ++k) ctr[k] = 0.5 * (lo[k] + hi[k]);
-  if (n <= 64) {
-    // nearest first (from the cell centre): the running bound tightens early
-    for (int32_t i = 1; i < n; ++i) {
-      int32_t v = out[i];
-      double kv = cellbox_lb2(T, g.d, T.lvl_off[0] + v, ctr, ctr);
-      int32_t j = i - 1;
-      while (j >= 0 && cellbox_lb2(T, g.d, T.lvl_off[0] + out[j], ctr, ctr) > kv) {
-        out[j + 1] = out[j];
-        --j;
+  auto after = [&](float ka, int32_t va, float kb, int32_t vb) {  // (ka, va) sorts after (kb, vb)
+    if (ka != kb) return ka > kb;
+    const double da = cellbox_lb2(T, g.d, T.lvl_off[0] + va, ctr, ctr);
+    const double db = cellbox_lb2(T, g.d, T.lvl_off[0] + vb, ctr, ctr);
+    return da != db ? da > db : va > vb;
+  };
+  int32_t gap = 1;
+  while (gap < n / 3) gap = 3 * gap + 1;
+  for (; gap > 0; gap /= 3) {  // shell sort
+    for (int32_t i = gap; i < n; ++i) {
+      const float kv = key[i];
+      const int32_t v = out[i];
+      int32_t j = i;
+      while (j >= gap && after(key[j - gap], out[j - gap], kv, v)) {
+        key[j] = key[j - gap];
+        out[j] = out[j - gap];
+        j -= gap;
       }
-      out[j + 1] = v;
+      key[j] = kv;
+      out[j] = v;
     }
-  } else {
-    // long lists: only the nearest leaf (by box, from the centre) moves first
-    int32_t bi = 0;
-    double bk = cellbox_lb2(T, g.d, T.lvl_off[0] + out[0], ctr, ctr);
-    for (int32_t i = 1; i < n; ++i) {
-      double k = cellbox_lb2(T, g.d, T.lvl_off[0] + out[i], ctr, ctr);
-      if (k < bk) {
-        bk = k;
-        bi = i;
-      }
-    }
-    int32_t t = out[0];
-    out[0] = out[bi];
-    out[bi] = t;
   }
 }
 
@@ -311,7 +315,7 @@ int64_t cells_bytes(const void* table, int64_t S, int d, int grid, int rec, cons
   if (cudaStreamSynchronize(st) != cudaSuccess) return -1;
   int64_t total = 0;
   for (int32_t v : h) total += v;
-  return (g.ncell + 1 + total) * 4;
+  return (g.ncell + 1 + 2 * total) * 4;  // offsets, leaf ids, keys
 }
 
 template <class LP>
@@ -338,14 +342,16 @@ int cells_build(void* table, int64_t S, int d, int grid, int rec, const LP& lp, 
   int32_t total = 0;
   MREP_CUDA_CHECK(cudaMemcpyAsync(&total, off + g.ncell, 4, cudaMemcpyDeviceToHost, st));
   MREP_CUDA_CHECK(cudaStreamSynchronize(st));
-  if ((g.ncell + 1 + (int64_t)total) * 4 > bytes) {
+  if ((g.ncell + 1 + 2 * (int64_t)total) * 4 > bytes) {
     set_error("mrep_cells_build: cells buffer too small (see mrep_cells_bytes)");
     return MREP_ERR_ARG;
   }
-  cells_fill_kernel<LP><<<grid_for(g.ncell, 128), 128, 0, st>>>(T, lp, g, off, off + g.ncell + 1);
+  cells_fill_kernel<LP><<<grid_for(g.ncell, 128), 128, 0, st>>>(
+      T, lp, g, off, off + g.ncell + 1, reinterpret_cast<float*>(off + g.ncell + 1 + total));
   MREP_LAUNCH_CHECK();
-  // header: cell index pointer, grid, lower corner, inverse cell size, upper corner
-  double h[11];
+  // header: cell index pointer, grid, lower corner, inverse cell size, upper
+  // corner, number of list entries
+  double h[12];
   uint64_t bits = (uint64_t)(uintptr_t)cells;
   memcpy(&h[0], &bits, 8);
   h[1] = grid;
@@ -354,6 +360,7 @@ int cells_build(void* table, int64_t S, int d, int grid, int rec, const LP& lp, 
     h[5 + k] = 1.0 / g.h[k];
     h[8 + k] = g.glo[k] + g.h[k] * grid;
   }
+  h[11] = (double)total;
   MREP_CUDA_CHECK(cudaMemcpyAsync((double*)table + H_CELLS, h, sizeof h, cudaMemcpyHostToDevice, st));
   MREP_CUDA_CHECK(cudaStreamSynchronize(st));  // h dies here
   return MREP_OK;
@@ -385,6 +392,11 @@ __device__ __forceinline__ const int32_t* cell_list(const TableView& T, int d, i
   a = __ldg(off + cell);
   b = __ldg(off + cell + 1);
   return off + ncell + 1;
+}
+
+// the lists' sort keys (parallel to the ids cell_list returns)
+__device__ __forceinline__ const float* cell_keys(const TableView& T, const int32_t* ids) {
+  return reinterpret_cast<const float*>(ids + (int64_t)T.hdr[H_CTOT]);
 }
 
 }  // namespace mrep

@@ -1230,9 +1230,13 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
   if (TM == TM_CELLS && incell) {
     int32_t a, b;
     const int32_t* ids = cell_list(T, D, cell, a, b);
+    const float* keys = cell_keys(T, ids);
     int32_t nxt = a < b ? __ldg(ids + a) : 0;
 #pragma unroll 1
     for (int32_t k = a; k < b; ++k) {
+      // keys ascend and bound the box distance of every query of the cell:
+      // past the cut, no later cubic can hold a band candidate
+      if ((double)__ldg(keys + k) > cut2(B.dmin, scale)) break;
       const int64_t ch = nxt;
       if (k + 1 < b) nxt = __ldg(ids + k + 1);  // next id in flight during this entry
       st.boxes++;

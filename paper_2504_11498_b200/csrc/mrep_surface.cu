@@ -503,13 +503,15 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
     // any query in the cell, nearest first; the first one seeds the bound
     int32_t a, b;
     const int32_t* ids = cell_list(T, 3, cell, a, b);
+    const float* keys = cell_keys(T, ids);
     const int64_t p0 = __ldg(ids + a);
     offer_points<PU, PV>(w, p0, q, ub, st);
     w.prim[g] = (int32_t)p0;
 #pragma unroll 1
     for (int32_t i = a; i < b; ++i) {
-      const int64_t s = __ldg(ids + i);
       const double c2 = cut2(ub, scale);
+      if ((double)__ldg(keys + i) > c2) break;  // keys ascend: the rest lie beyond the cut
+      const int64_t s = __ldg(ids + i);
       st.boxes++;
       if (box_lb2<3>(T, T.lvl_off[0] + s, q) <= c2 &&
           obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2) {
