@@ -510,6 +510,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push("bench_timed")  # ncu --nvtx-include bench_timed/
     for i in range(args.steps):
         flush.fill_(float(i))
         starts[i].record(stream)
@@ -519,6 +520,7 @@ def main():
         gather(out)
         ends[i].record(stream)
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     if world > 1:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]

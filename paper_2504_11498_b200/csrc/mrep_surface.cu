@@ -458,28 +458,6 @@ __device__ __forceinline__ void offer_points(const SurfParams& w, int64_t s, con
   st.points += NP;
 }
 
-// true if the patch's Bernstein lower bound on |S - q|^2 can reach c2
-template <int PU, int PV>
-__device__ __forceinline__ bool bern_patch_may_reach(const double* P, const double (&q)[3],
-                                                     double c2) {
-  constexpr int NE = (2 * PU + 1) * (2 * PV + 1);
-  const double* E = P + surf_bern(PU, PV);
-  const double* SS = E + 3 * NE;
-  const double qq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2];
-  double m = __longlong_as_double(0x7ff0000000000000LL);
-#pragma unroll 7
-  for (int k = 0; k < NE; ++k) {
-    double d = (__ldg(SS + k) - 2.0 * (q[0] * __ldg(E + 3 * k) + q[1] * __ldg(E + 3 * k + 1) +
-                                       q[2] * __ldg(E + 3 * k + 2))) + qq;
-    m = fmin(m, d);
-  }
-  // rounding: the nets are O(1e-16) relative to their magnitude; the sums
-  // here add a few ulps of (mag + 2|q| mag + |q|^2)
-  const double qa = fabs(q[0]) + fabs(q[1]) + fabs(q[2]);
-  const double mag = __ldg(SS + NE);
-  const double err = 1e-12 * (mag * (1.0 + 2.0 * qa) + qq);
-  return !(m - err > c2);
-}
 
 // S1: per-thread depth-first walk (queries in Morton order)
 template <int PU, int PV>
@@ -623,27 +601,60 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
 // lanes only ever hold real work.
 template <int PU, int PV>
 __global__ void __launch_bounds__(256) surf_filter(const __grid_constant__ SurfParams w) {
+  // one 8-lane group per pair.  Bernstein test: |S - q|^2 over the patch is
+  // a degree-(2pu, 2pv) polynomial whose Bernstein coefficients are
+  // SS_k - 2 q.E_k + |q|^2 (surf_bern nets); their minimum bounds it from
+  // below.  The group splits the (2pu+1)(2pv+1) coefficients and
+  // min-reduces by shuffles (min is exact: the order does not matter).
+  // Rounding: the nets are O(1e-16) relative to their magnitude; the sums
+  // add a few ulps of (mag + 2|q| mag + |q|^2).
+  constexpr int NE = (2 * PU + 1) * (2 * PV + 1);
   unsigned long long total = *(volatile unsigned long long*)&w.cnt[0];
   if (total > w.pcap) total = w.pcap;
   const TableView& T = w.tab;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31, sub = lane & 7;
+  const unsigned gmask = 0xffu << (lane & 24);
+  const unsigned long long ng = ((unsigned long long)gridDim.x * blockDim.x) >> 3;
+  for (unsigned long long i = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+       i < total; i += ng) {
     const int64_t g = w.pq[i];
     const int64_t s = w.ps[i];
     bool keep = !w.flag[g] && s != w.prim[g];
+    double q[3] = {0.0, 0.0, 0.0}, c2 = 0.0;
     if (keep) {
       double4 rec = *(const double4*)(w.qs + g * 4);
-      double q[3] = {rec.x, rec.y, rec.z};
+      q[0] = rec.x;
+      q[1] = rec.y;
+      q[2] = rec.z;
       double scale = fmax(T.hdr[4], fmax(fabs(q[0]), fmax(fabs(q[1]), fabs(q[2]))));
-      const double c2 = cut2(rec.w, scale);
+      c2 = cut2(rec.w, scale);
       keep = box_lb2<3>(T, T.lvl_off[0] + s, q) <= c2 &&
-             obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2 &&
-             bern_patch_may_reach<PU, PV>(T.rec + s * w.rec, q, c2);
+             obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2;
     }
-    unsigned long long slot = wave_append(&w.cnt[6], keep);
-    if (keep) {  // slot < pcap: the compact list is never longer than the input
-      w.fq[slot] = (uint32_t)g;
-      w.fs[slot] = (uint32_t)s;
+    if (keep) {  // group-uniform (same pair in all 8 lanes)
+      const double* E = T.rec + s * w.rec + surf_bern(PU, PV);
+      const double* SS = E + 3 * NE;
+      const double qq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2];
+      double m = __longlong_as_double(0x7ff0000000000000LL);
+      for (int k = sub; k < NE; k += 8) {
+        double d = (__ldg(SS + k) - 2.0 * (q[0] * __ldg(E + 3 * k) + q[1] * __ldg(E + 3 * k + 1) +
+                                           q[2] * __ldg(E + 3 * k + 2))) + qq;
+        m = fmin(m, d);
+      }
+      m = fmin(m, __shfl_xor_sync(gmask, m, 4));
+      m = fmin(m, __shfl_xor_sync(gmask, m, 2));
+      m = fmin(m, __shfl_xor_sync(gmask, m, 1));
+      const double qa = fabs(q[0]) + fabs(q[1]) + fabs(q[2]);
+      const double mag = __ldg(SS + NE);
+      const double err = 1e-12 * (mag * (1.0 + 2.0 * qa) + qq);
+      keep = !(m - err > c2);
+    }
+    if (sub == 0) {
+      unsigned long long slot = wave_append(&w.cnt[6], keep);
+      if (keep) {  // slot < pcap: the compact list is never longer than the input
+        w.fq[slot] = (uint32_t)g;
+        w.fs[slot] = (uint32_t)s;
+      }
     }
   }
 }
