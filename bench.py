@@ -587,8 +587,11 @@ def main():
     if os.path.exists(prof) and dom:
         try:
             pj = json.load(open(prof))
-            traffic = (pj.get("dram_bytes_per_launch_by_config", {}).get(args.config, {})
-                       .get(f"wave_{dom}"))
+            per = pj.get("dram_bytes_per_launch_by_config", {}).get(args.config, {})
+            base = f"surf_{dom}" if surf else f"wave_{dom}"
+            traffic = per.get(base)
+            if traffic is None:  # e.g. wave_traverse_group for a traverse stage
+                traffic = next((v for k, v in sorted(per.items()) if k.startswith(base)), None)
             if traffic is None and args.config == pj.get("config", "cfg2"):
                 traffic = pj.get("dram_bytes_per_launch", {}).get(f"wave_{dom}")
         except Exception:

@@ -1,6 +1,6 @@
 """Summarise ncu captures into profiles/ (JSON + text), run here (no GPU).
 
-    python scripts/ncu_summarize.py <full.ncu-rep> <launches.csv> <tag> [config]
+    python scripts/ncu_summarize.py <full.ncu-rep> <launches.csv|-> <tag> [config]
 
 The per-kernel DRAM traffic goes into profiles/ncu_summary.json under
 dram_bytes_per_launch_by_config[config] (bench.py reads it as `traffic`).
@@ -57,7 +57,7 @@ def main():
     rep, ll, tag = sys.argv[1], sys.argv[2], sys.argv[3]
     config = sys.argv[4] if len(sys.argv) > 4 else "cfg2"
     kern = full(rep)
-    lst = launches(ll)
+    lst = launches(ll) if ll != "-" else []
     prof = os.path.join(ROOT, "profiles")
     per = {}
     for k in kern:
@@ -65,7 +65,10 @@ def main():
         mult = 1e6 if k.get("dram__bytes_read.sum.unit") == "Mbyte" else (
             1e9 if k.get("dram__bytes_read.sum.unit") == "Gbyte" else 1e3
             if k.get("dram__bytes_read.sum.unit") == "Kbyte" else 1.0)
-        per.setdefault(name, (k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"]) * mult)
+        # summed over the capture's launches of that kernel (one projection
+        # call: per call, e.g. both surf_solve passes)
+        per[name] = per.get(name, 0.0) + (k["dram__bytes_read.sum"] +
+                                          k["dram__bytes_write.sum"]) * mult
     path = os.path.join(prof, "ncu_summary.json")
     summary = json.load(open(path)) if os.path.exists(path) else {}
     summary.setdefault("dram_bytes_per_launch_by_config", {})[config] = per
@@ -81,6 +84,8 @@ def main():
             for m in METRICS:
                 if m in k:
                     f.write(f"    {m:62s} {k[m]} {k.get(m + '.unit', '')}\n")
+    if not lst:
+        return
     # launch list: share of device time per kernel name over the whole command
     tot = {}
     for name, ns in lst:
