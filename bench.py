@@ -497,9 +497,15 @@ def main():
     # start-up never lands inside a timed step
     clocks = ClockSampler(local)
     clocks.__enter__()
+    # warm-up mirrors the timed loop exactly: the L2-flush fills (zero and
+    # non-zero values take different paths) and the previous step's outputs
+    # alive while the next step allocates (otherwise the allocator's first
+    # second-buffer cudaMalloc lands in timed step 1 and stalls it)
+    out = None
     for i in range(args.warmup):
-        flush.fill_(float(i + 1))  # the timed loop's L2 flush, warmed too
-        gather(wl.step(dense=dense))
+        flush.fill_(float(i % 2))
+        out = wl.step(dense=dense)
+        gather(out)
     torch.cuda.synchronize()
 
     # ---- timed device steps (inputs resident in HBM) ----
