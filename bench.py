@@ -657,7 +657,7 @@ def main():
            "d2h_bytes_per_step": n * ((8 + 8 + 24 + 8 + 4) if surf else (8 + 24 + 8 + 8)),
            "path": ("mrep_project_batch_host" if args.config == "cfg3" else
                     "mrep_project_surface_host" if surf else "mrep_project_host")
-           + " (C ABI, pinned host buffers, 2-stream chunked pipeline)"}
+           + " (C ABI, pinned host buffers, five-chunk pipeline on priority streams)"}
 
     if rank == 0:
         cpu = None
