@@ -73,6 +73,9 @@ constexpr int BLOCK = 128;
 #ifndef MREP_TRAV_MINB
 #define MREP_TRAV_MINB 6
 #endif
+#ifndef MREP_GROUP_MINB
+#define MREP_GROUP_MINB 6
+#endif
 #ifndef MREP_PAIRS_MINB
 #define MREP_PAIRS_MINB 6
 #endif
@@ -1784,7 +1787,7 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
 }
 
 template <int D, bool MULTI>
-__global__ void __launch_bounds__(BLOCK) wave_traverse_group(const __grid_constant__ WaveParams w) {
+__global__ void __launch_bounds__(BLOCK, MREP_GROUP_MINB) wave_traverse_group(const __grid_constant__ WaveParams w) {
   __shared__ unsigned long long sk[BLOCK / 8][GSTACK];
   __shared__ double sl[BLOCK / 8][GSTACK];
   __shared__ uint32_t pc[BLOCK / 8][GPAIRS];
