@@ -69,8 +69,13 @@ __host__ __device__ inline int surf_ne(int pu, int pv) { return (2 * pu + 1) * (
 __host__ __device__ inline int surf_bern(int pu, int pv) {  // E at +0, SS at +3 NE
   return 6 * (pu + 1) * (pv + 1) + 5 + 15;
 }
+// float copy of the nets for the filter's test: per coefficient m a float4
+// (E_m xyz, SS_m), rounded to nearest; 16-B aligned (even double offset)
+__host__ __device__ inline int surf_bernf(int pu, int pv) {
+  return (surf_bern(pu, pv) + 4 * surf_ne(pu, pv) + 1 + 1) & ~1;  // after the magnitude
+}
 __host__ __device__ inline int surf_rec(int pu, int pv) {
-  int n = surf_bern(pu, pv) + 4 * surf_ne(pu, pv) + 1;  // + the |SS|,|E| magnitude
+  int n = surf_bernf(pu, pv) + 2 * surf_ne(pu, pv);
   return (n + 7) & ~7;
 }
 __host__ __device__ inline int surf_obb(int pu, int pv) { return 6 * (pu + 1) * (pv + 1) + 5; }
@@ -635,22 +640,28 @@ __global__ void __launch_bounds__(256) surf_filter(const __grid_constant__ SurfP
              obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2;
     }
     if (keep) {  // group-uniform (same pair in all 8 lanes)
-      const double* E = T.rec + s * w.rec + surf_bern(PU, PV);
-      const double* SS = E + 3 * NE;
-      const double qq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2];
-      double m = __longlong_as_double(0x7ff0000000000000LL);
+      // on the float copy of the nets (half the bytes; the filter is
+      // L2-bandwidth bound): every coefficient, the query and each of the
+      // ~6 operations err by <= 2^-24 relative, so the float minimum is
+      // within 8 * 2^-24 (mag (1 + 2|q|_1) + |q|^2) of the exact one (mag
+      // bounds |E|, |SS|); 4e-6 covers it with an 8x margin
+      const float4* F = reinterpret_cast<const float4*>(T.rec + s * w.rec + surf_bernf(PU, PV));
+      const float q0 = __double2float_rn(q[0]), q1 = __double2float_rn(q[1]),
+                  q2 = __double2float_rn(q[2]);
+      const float qqf = q0 * q0 + q1 * q1 + q2 * q2;
+      float m = __int_as_float(0x7f800000);
       for (int k = sub; k < NE; k += 8) {
-        double d = (__ldg(SS + k) - 2.0 * (q[0] * __ldg(E + 3 * k) + q[1] * __ldg(E + 3 * k + 1) +
-                                           q[2] * __ldg(E + 3 * k + 2))) + qq;
-        m = fmin(m, d);
+        const float4 e = __ldg(F + k);
+        m = fminf(m, (e.w - 2.0f * (q0 * e.x + q1 * e.y + q2 * e.z)) + qqf);
       }
-      m = fmin(m, __shfl_xor_sync(gmask, m, 4));
-      m = fmin(m, __shfl_xor_sync(gmask, m, 2));
-      m = fmin(m, __shfl_xor_sync(gmask, m, 1));
+      m = fminf(m, __shfl_xor_sync(gmask, m, 4));
+      m = fminf(m, __shfl_xor_sync(gmask, m, 2));
+      m = fminf(m, __shfl_xor_sync(gmask, m, 1));
+      const double qq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2];
       const double qa = fabs(q[0]) + fabs(q[1]) + fabs(q[2]);
-      const double mag = __ldg(SS + NE);
-      const double err = 1e-12 * (mag * (1.0 + 2.0 * qa) + qq);
-      keep = !(m - err > c2);
+      const double mag = __ldg(T.rec + s * w.rec + surf_bern(PU, PV) + 4 * NE);
+      const double err = 4e-6 * (mag * (1.0 + 2.0 * qa) + qq);
+      keep = !((double)m - err > c2);
     }
     if (sub == 0) {
       unsigned long long slot = wave_append(&w.cnt[6], keep);
@@ -980,6 +991,9 @@ __global__ void surf_pack_kernel(const double* pts, const double* iv, const uint
         const int m = a * (Nv + 1) + c;
         for (int x = 0; x < 3; ++x) E[3 * m + x] = e[x];
         SS[m] = ss;
+        float* F = reinterpret_cast<float*>(r + surf_bernf(pu, pv)) + 4 * m;
+        for (int x = 0; x < 3; ++x) F[x] = __double2float_rn(e[x]);
+        F[3] = __double2float_rn(ss);
         mag = fmax(mag, fmax(fabs(ss), fmax(fabs(e[0]), fmax(fabs(e[1]), fabs(e[2])))));
       }
     SS[NE] = mag;
