@@ -69,7 +69,10 @@ MREP_API int mrep_device_count(void);
  * Segment table: the device-resident form of a PreparedCurve
  * (project.py:110-121, 220-242).  Packed 256-B records per cubic (power
  * coefficients, control points, interval, end seam) plus an 8-ary AABB
- * hierarchy over the cubics for screening.
+ * hierarchy over the cubics for screening.  A record whose seg_ta is NaN is
+ * a separator (empty box, never tested in range; its seams stay real
+ * points): several curves packed into one table, separated by one such
+ * record each, project onto the nearest of them (nearest.py).
  * ------------------------------------------------------------------- */
 MREP_API int64_t mrep_table_bytes(int64_t S);
 MREP_API int mrep_table_pack(const double* seg_pts_dev, /* [S][4][d] */

@@ -221,7 +221,7 @@ class DeviceTable:
         return t, foot, dist, cand, seg, st, sound
 
     def project_host(self, queries, out=None, clip_tol=1e-6, max_iter=8, screen=True,
-                     counters=None):
+                     counters=None, extra_flags=0):
         """End-to-end call on HOST arrays through mrep_project_host."""
         q = np.ascontiguousarray(queries, dtype=np.float64)
         n = q.shape[0]
@@ -232,6 +232,7 @@ class DeviceTable:
         import ctypes
         p = lambda a: ctypes.c_void_p(a.ctypes.data if a is not None else 0)  # noqa: E731
         flags = (L.MREP_SCREEN | self._cell_flag(n, True)) if screen else 0
+        flags |= int(extra_flags)
         L.check(L.lib().mrep_project_host(
             L.ptr(self.buf), self.S, self.d, p(q), n, float(clip_tol), int(max_iter),
             flags, p(t), p(foot), p(dist), p(cand), p(seg),

@@ -2115,6 +2115,9 @@ __global__ void pack_records_kernel(const double* seg_pts, const double* seg_ta,
   double P[4][3];
   for (int j = 0; j < 4; ++j)
     for (int k = 0; k < 3; ++k) P[j][k] = k < d ? seg_pts[(s * 4 + j) * d + k] : 0.0;
+  // a separator record (NaN interval) between the curves of a nearest-over-set
+  // table: an empty box (never tested in range), seams still real points
+  const bool sep = isnan(seg_ta[s]);
   double amax = 0.0;
   for (int k = 0; k < 3; ++k) {
     double w0, w1, w2, w3;
@@ -2130,8 +2133,8 @@ __global__ void pack_records_kernel(const double* seg_pts, const double* seg_ta,
       hi = fmax(hi, P[j][k]);
       amax = fmax(amax, fabs(P[j][k]));
     }
-    box0[s * 6 + k] = lo;
-    box0[s * 6 + 3 + k] = hi;
+    box0[s * 6 + k] = sep ? INFINITY : lo;
+    box0[s * 6 + 3 + k] = sep ? -INFINITY : hi;
   }
   r[R_TA] = seg_ta[s];
   r[R_TB] = seg_tb[s];

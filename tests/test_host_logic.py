@@ -113,3 +113,15 @@ def test_table_layout_levels():
             lv += 1
         # 6 doubles per box + its float copy (6 floats)
         assert lib.mrep_table_bytes(S) == (64 + 32 * S + 9 * boxes) * 8
+
+
+def test_nearest_set_locate():
+    """Global winning index -> (curve, local cubic); the separator before a
+    curve maps to that curve's cubic 0 (a seam candidate at its start)."""
+    from paper_2504_11498_b200.nearest import PreparedNearestSet
+    ns = object.__new__(PreparedNearestSet)
+    ns.counts = np.array([3, 1, 4])
+    ns.starts = np.array([0, 4, 6])  # cubics 0-2, sep 3, cubic 4, sep 5, cubics 6-9
+    cid, local = ns.locate([0, 2, 3, 4, 5, 6, 9])
+    assert cid.tolist() == [0, 0, 1, 1, 2, 2, 2]
+    assert local.tolist() == [0, 2, 0, 0, 0, 0, 3]
