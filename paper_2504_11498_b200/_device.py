@@ -168,13 +168,15 @@ class DeviceTable:
     # lazily, on the first such batch (mrep_cells_build)
     CELL_MIN_QUERIES = 1 << 16
     CELL_MAX_CUBICS = 1 << 17
-    CELL_MAX_BYTES = 4 << 30  # skip the index rather than spend more HBM on it
+    CELL_MAX_BYTES = 16 << 30  # skip the index rather than spend more HBM on it
 
     def build_cells(self, grid=None):
         torch = L._torch()
         if grid is None:
             big = self.S > (1 << 14)
-            grid = (128 if big else 64) if self.d == 3 else (512 if big else 256)
+            # big tables: 256^3 (cfg5, 10^5 cubics: 5.7 GB, built in 1.5 s;
+            # 22% faster projection than 128^3, 384^3 only 8% more)
+            grid = (256 if big else 64) if self.d == 3 else (512 if big else 256)
         nb = L.lib().mrep_cells_bytes(L.ptr(self.buf), self.S, self.d, grid, L.stream_ptr())
         if nb <= 0:
             L.check(1)
