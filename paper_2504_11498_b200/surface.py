@@ -195,7 +195,10 @@ class DeviceSurfaceTable:
             L.check(1)
         if nb > self.CELL_MAX_BYTES:
             return self
-        self.cells = torch.empty((nb + 3) // 4, dtype=torch.int32, device=self.buf.device)
+        try:
+            self.cells = torch.empty((nb + 3) // 4, dtype=torch.int32, device=self.buf.device)
+        except torch.cuda.OutOfMemoryError:
+            return self  # no room: the hierarchy walk is exact without the index
         L.check(L.lib().mrep_surface_cells_build(L.ptr(self.buf), self.npatch, self.pu, self.pv,
                                                   grid, L.ptr(self.cells), nb, L.stream_ptr()))
         return self
