@@ -2966,7 +2966,10 @@ static int project_chunk(const void* table, int64_t S, int d, const double* quer
   const bool timing = (flags & MREP_TIMING) != 0;
   StageTimer sort_tm(timing, st);
   sort_tm.mark();
-  if (!(flags & MREP_NO_SORT) && n > 64) {
+  // small batches skip the ordering: below 2^16 queries the sort's fixed
+  // cost (~28 us) exceeds what coherence saves (measured 5-10% faster
+  // unsorted at 2e3..3e4 queries, even with packet walks)
+  if (!(flags & MREP_NO_SORT) && n >= ((int64_t)1 << 16)) {
     uint32_t* k_in = (uint32_t*)(wc + off_keys);
     uint32_t* k_out = k_in + n;
     uint32_t* i_in = k_out + n;

@@ -312,3 +312,19 @@ def test_cand_deterministic_with_bucket_order(gpu):
         for x, y, zz in zip(a, b, c):
             assert np.array_equal(x, y)
             assert np.array_equal(x[:7777], zz)
+
+
+@pytest.mark.parametrize("flags", ["default", "packet", "lane"])
+def test_sorted_and_unsorted_agree(gpu, flags):
+    """Batches of >= 2^16 queries are bucket- or radix-sorted, smaller ones
+    are not: the outputs never depend on the order (bit for bit)."""
+    from paper_2504_11498_b200 import _lib as L
+    from paper_2504_11498_b200 import _device as D
+    z = load_golden("project_cfg2.npz")
+    tab = D.DeviceTable(z["seg_pts"], z["seg_ta"], z["seg_tb"], z["seam_t"], z["seam_pt"])
+    q = np.random.default_rng(31).uniform(-0.1, 1.1, (70000, 3))
+    f = {"default": 0, "packet": L.MREP_PACKET, "lane": L.MREP_PER_LANE}[flags]
+    a = [x.cpu().numpy() for x in tab.project(q, extra_flags=f)[:5]]
+    b = [x.cpu().numpy() for x in tab.project(q, extra_flags=f | L.MREP_NO_SORT)[:5]]
+    for k in (0, 1, 2, 4):
+        assert np.array_equal(a[k], b[k]), k
