@@ -31,15 +31,13 @@ __device__ __forceinline__ double sel6(const double (&b)[6], int i) {
   return r;
 }
 
-// xs[i] = i / 5 (_kernels.py:249-251); literals are the correctly rounded quotients
+// xs[i] = i / 5 (_kernels.py:249-251), the correctly rounded quotients:
+// i * 0.2 rounds to them for every i in [0, 5] except 3 (3 * 0.2 is a tie
+// that rounds up to 0.6000000000000001), so one multiply and one select
+// replace a five-way select chain
 __device__ __forceinline__ double xs5(int i) {
-  double r = 0.0;
-  r = (i == 1) ? 0.2 : r;
-  r = (i == 2) ? 0.4 : r;
-  r = (i == 3) ? 0.6 : r;
-  r = (i == 4) ? 0.8 : r;
-  r = (i == 5) ? 1.0 : r;
-  return r;
+  const double r = (double)i * 0.2;
+  return i == 3 ? 0.6 : r;
 }
 
 // numba lowers np.cbrt to sign(x)*pow(|x|, 1/3) (numba/np/npyfuncs.py); on the
@@ -342,9 +340,9 @@ __device__ __forceinline__ double eval_ordinates(const double (&b)[6], double u)
 __device__ __forceinline__ bool hull_cross(const double (&b)[6], double& z1o, double& z2o) {
   uint32_t lo_st = 0, hi_st = 0;
   int nl = 0, nh = 0;
-#pragma unroll 1
-  for (int i = 0; i < 6; ++i) {
-    double x = xs5(i), y = sel6(b, i);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {  // unrolled: the new point is b[i] at x = i/5
+    double x = xs5(i), y = b[i];
     while (nl > 1) {
       int a = (lo_st >> (3 * (nl - 1))) & 7, c = (lo_st >> (3 * (nl - 2))) & 7;
       double xa = xs5(a), ya = sel6(b, a), xc = xs5(c), yc = sel6(b, c);
