@@ -340,25 +340,54 @@ __device__ __forceinline__ double eval_ordinates(const double (&b)[6], double u)
 __device__ __forceinline__ bool hull_cross(const double (&b)[6], double& z1o, double& z2o) {
   uint32_t lo_st = 0, hi_st = 0;
   int nl = 0, nh = 0;
+  // the top two points of each chain are kept as values (a = top, c = the
+  // one below); a pop fetches only the new second point.  Same tests on the
+  // same operands as the reference, so the same chains.
+  double lax = 0.0, lay = 0.0, lcx = 0.0, lcy = 0.0;
+  double hax = 0.0, hay = 0.0, hcx = 0.0, hcy = 0.0;
 #pragma unroll
   for (int i = 0; i < 6; ++i) {  // unrolled: the new point is b[i] at x = i/5
-    double x = xs5(i), y = b[i];
+    const double x = xs5(i), y = b[i];
     while (nl > 1) {
-      int a = (lo_st >> (3 * (nl - 1))) & 7, c = (lo_st >> (3 * (nl - 2))) & 7;
-      double xa = xs5(a), ya = sel6(b, a), xc = xs5(c), yc = sel6(b, c);
-      if (((xa - xc) * (y - yc) - (x - xc) * (ya - yc)) <= 0.0) --nl;
-      else break;
+      if (((lax - lcx) * (y - lcy) - (x - lcx) * (lay - lcy)) <= 0.0) {
+        --nl;
+        lax = lcx;
+        lay = lcy;
+        if (nl > 1) {
+          const int c = (lo_st >> (3 * (nl - 2))) & 7;
+          lcx = xs5(c);
+          lcy = sel6(b, c);
+        }
+      } else {
+        break;
+      }
     }
     lo_st = (lo_st & ~(7u << (3 * nl))) | ((uint32_t)i << (3 * nl));
     ++nl;
+    lcx = lax;
+    lcy = lay;
+    lax = x;
+    lay = y;
     while (nh > 1) {
-      int a = (hi_st >> (3 * (nh - 1))) & 7, c = (hi_st >> (3 * (nh - 2))) & 7;
-      double xa = xs5(a), ya = sel6(b, a), xc = xs5(c), yc = sel6(b, c);
-      if (((xa - xc) * (y - yc) - (x - xc) * (ya - yc)) >= 0.0) --nh;
-      else break;
+      if (((hax - hcx) * (y - hcy) - (x - hcx) * (hay - hcy)) >= 0.0) {
+        --nh;
+        hax = hcx;
+        hay = hcy;
+        if (nh > 1) {
+          const int c = (hi_st >> (3 * (nh - 2))) & 7;
+          hcx = xs5(c);
+          hcy = sel6(b, c);
+        }
+      } else {
+        break;
+      }
     }
     hi_st = (hi_st & ~(7u << (3 * nh))) | ((uint32_t)i << (3 * nh));
     ++nh;
+    hcx = hax;
+    hcy = hay;
+    hax = x;
+    hay = y;
   }
   double z1 = 2.0, z2 = -1.0;
 #pragma unroll 1
