@@ -1931,18 +1931,19 @@ __global__ void __launch_bounds__(BLOCK, MREP_CLIP_MINB) wave_clip(const __grid_
         if (i >= total) {
           done = true;
         } else {
+          // no flag test here: a survivor of a query already handed to the
+          // fallback is clipped anyway (harmless: emit skips the query and the
+          // fallback recomputes it), which keeps the refill's loads independent
           qi = w.sq[i];
-          if (!w.flag[qi]) {
-            const double* o = w.sb + i * 8;
-            double bp[6];
+          const double* o = w.sb + i * 8;
+          double bp[6];
 #pragma unroll
-            for (int j = 0; j < 6; ++j) bp[j] = o[j];
-            plo = o[6];
-            phi = o[7];
-            sk = w.ssk[i];
-            clip_init(S, bp);
-            have = true;
-          }
+          for (int j = 0; j < 6; ++j) bp[j] = o[j];
+          plo = o[6];
+          phi = o[7];
+          sk = w.ssk[i];
+          clip_init(S, bp);
+          have = true;
         }
       }
     }
