@@ -720,24 +720,24 @@ __global__ void __launch_bounds__(128, (PU + PV <= 6) ? 3 : 1) surf_solve(const 
         } else {
           g = PASS == 0 ? (int64_t)i : (int64_t)w.fq[i];
           s = PASS == 0 ? (int64_t)w.prim[g] : (int64_t)w.fs[i];
-          if (!w.flag[g]) {
-            double4 rec = *(const double4*)(w.qs + g * 4);
-            q[0] = rec.x;
-            q[1] = rec.y;
-            q[2] = rec.z;
-            bool go = true;
-            if (PASS == 1) {  // the bound may have tightened since the filter
-              double scale = fmax(T.hdr[4], fmax(fabs(q[0]), fmax(fabs(q[1]), fabs(q[2]))));
-              const double c2 = cut2(smin_of(w, g), scale);
-              go = obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2;
-            }
-            if (go) {
-              P = T.rec + s * w.rec;
-              seed_init<PU, PV>(P, q, ns);
+          // (no fallback-flag test: a flagged query's pair is solved anyway,
+          // harmlessly -- select skips the query, the fallback recomputes it)
+          double4 rec = *(const double4*)(w.qs + g * 4);
+          q[0] = rec.x;
+          q[1] = rec.y;
+          q[2] = rec.z;
+          bool go = true;
+          if (PASS == 1) {  // the bound may have tightened since the filter
+            double scale = fmax(T.hdr[4], fmax(fabs(q[0]), fmax(fabs(q[1]), fabs(q[2]))));
+            const double c2 = cut2(smin_of(w, g), scale);
+            go = obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2;
+          }
+          if (go) {
+            P = T.rec + s * w.rec;
+            seed_init<PU, PV>(P, q, ns);
 #pragma unroll 4
-              for (int k = 0; k < NPD; ++k) mynet[k * 128] = __ldg(P + k);
-              have = true;
-            }
+            for (int k = 0; k < NPD; ++k) mynet[k * 128] = __ldg(P + k);
+            have = true;
           }
         }
       }
