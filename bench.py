@@ -553,14 +553,15 @@ def main():
     wl.step(counters, dense=dense)
     c = counters.cpu().numpy().astype(np.float64)
     import ctypes
-    stage = np.zeros(8)
-    reps = 5
+    reps = 7
+    per_rep = []
     for _ in range(reps):
         flush.fill_(2.0)
         wl.step(extra_flags=L.MREP_TIMING, dense=dense)
         buf = (ctypes.c_double * 8)()
         L.lib().mrep_last_stage_times(buf, 8)
-        stage += np.array(buf[:8]) / reps
+        per_rep.append(np.array(buf[:8]))
+    stage = np.median(np.stack(per_rep), axis=0)  # robust to a one-off slow rep
     peak = ctypes.c_double()
     L.check(L.lib().mrep_fp64_peak(ctypes.byref(peak)))
     kms = statistics.mean(kern_ms)
