@@ -9,14 +9,14 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _curves(seed, m=5):
+def _curves(seed, m=5, dim=3):
     from paper_2504_11498_b200 import prepare_curve
     from paper_2504_11498_b200.fixtures import random_clamped_curve
     rng = np.random.default_rng(seed)
     preps = []
     for i in range(m):
         p = int(rng.integers(3, 8))
-        c = random_clamped_curve(rng, p, int(rng.integers(p + 2, 40)), 3, uniform_knots=True)
+        c = random_clamped_curve(rng, p, int(rng.integers(p + 2, 40)), dim, uniform_knots=True)
         preps.append(prepare_curve(c, 1e-4))
     return preps
 
@@ -75,3 +75,11 @@ def test_nearest_edge_cases(gpu):
         project_nearest(nset, np.zeros((3, 2)))
     with pytest.raises(DomainError):
         prepare_nearest_set([])
+
+
+def test_nearest_planar_curves(gpu):
+    """d = 2 tables (separators and seams in the plane)."""
+    from paper_2504_11498_b200 import prepare_nearest_set, project_nearest
+    preps = _curves(13, m=4, dim=2)
+    q = np.random.default_rng(2).uniform(-0.2, 1.2, (5000, 2))
+    _check(preps, q, project_nearest(prepare_nearest_set(preps), q))
