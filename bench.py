@@ -76,6 +76,12 @@ CONFIGS = {
     "cfg5": dict(degree=3, ctrl=100_003, n=100_000_000, queries="uniform", scaling="strong",
                  desc="cfg5: 1e8 random points onto a degree-3 B-spline with 100003 ctrl pts "
                       "(1e5 cubics), sharded across GPUs"),
+    # SURVEY.md 8(f) item 4 (not a BASELINE config): nearest-over-set
+    "cfg6": dict(degree="3-9", ctrl="8-2048", curves=100, n=1_000_000, queries="uniform",
+                 scaling="weak", nearest=True,
+                 desc="cfg6 (8(f) nearest-over-set): 1e6 random points/GPU, each projected "
+                      "onto the NEAREST of 100 mixed curves (degree 3-9, 8-2048 ctrl pts) "
+                      "merged into one table"),
 }
 
 
@@ -302,6 +308,55 @@ class CurveSetWorkload:
         return jobs, desc
 
 
+class NearestWorkload:
+    """cfg6: the first 100 curves of the cfg3 generator merged into one
+    nearest-over-set table (nearest.py); every query against all of them."""
+
+    def __init__(self, cfg, rank, world, n_override):
+        import torch
+        from paper_2504_11498_b200 import _lib as L, prepare_curve_set, prepare_nearest_set
+        from paper_2504_11498_b200.fixtures import mixed_curve_batch
+        c = CONFIGS[cfg]
+        self.curves = mixed_curve_batch(c["curves"])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cset = prepare_curve_set(self.curves, 1e-4)
+        self.preps = [cset[i] for i in range(len(self.curves))]
+        self.nset = prepare_nearest_set(self.preps)
+        self.tab = self.nset.table
+        torch.cuda.synchronize()
+        self.prep_ms = (time.perf_counter() - t0) * 1e3
+        t0 = time.perf_counter()
+        self.tab._cell_flag(max(c["n"], 1 << 20), True)
+        torch.cuda.synchronize()
+        self.cells_ms = (time.perf_counter() - t0) * 1e3
+        self.n = n_override or c["n"]
+        self.n_total = world * self.n
+        self.q_host = np.random.default_rng(1 + rank).uniform(0.0, 1.0, (self.n, 3))
+        self.q = torch.from_numpy(self.q_host).cuda()
+        self.num_segments = int(self.nset.counts.sum())
+        self.h2d = self.n * 24
+        # per-query walks offer both seams of a cubic (nearest.py)
+        self.mode = 0 if self.n >= 8 * self.tab.S else L.MREP_PER_LANE
+        self.cpu_div = len(self.preps)  # the CPU sample runs every curve per query
+
+    def step(self, counters=None, extra_flags=0, dense=False):
+        return self.tab.project(self.q, counters=counters, extra_flags=extra_flags | self.mode)
+
+    def pinned(self):
+        import torch
+        self.q_pin = torch.from_numpy(self.q_host).pin_memory().numpy()
+
+    def host(self, out, dense=False):
+        self.tab.project_host(self.q_pin, out=out[:4] + (None,), extra_flags=self.mode)
+
+    def cpu_jobs(self, sample):
+        sample = max(64, min(sample, 2048))
+        desc = (f"first {sample} of the {self.n} queries, brute force over all "
+                f"{self.num_segments} cubics of the {len(self.preps)} curves (per curve, min kept)")
+        return [(_seg(p), self.q_host[:sample]) for p in self.preps], desc
+
+
 class SurfaceWorkload:
     """cfg4: one prepared surface (64 x 64 net), the rank's 1e6 queries."""
 
@@ -352,6 +407,11 @@ class SurfaceWorkload:
 
 def run_reference(args, rank):
     if rank != 0:
+        return
+    if CONFIGS[args.config].get("nearest"):
+        print(json.dumps({"impl": "reference", "unavailable": "the reference has no "
+                          "nearest-over-set call (SPEC.md:497 non-goal); the mrep line's "
+                          "cpu_baseline times the per-curve oracle instead"}), flush=True)
         return
     import oracle
     from oracle import prep as P
@@ -475,7 +535,8 @@ def main():
     cfg = CONFIGS[args.config]
     surf = CONFIGS[args.config].get("surface", False)
     wl = (CurveSetWorkload if args.config == "cfg3" else SurfaceWorkload if surf
-          else SingleCurve)(args.config, rank, world, args.n)
+          else NearestWorkload if cfg.get("nearest") else SingleCurve)(args.config, rank, world,
+                                                                         args.n)
     n, n_total = wl.n, wl.n_total
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -671,6 +732,7 @@ def main():
             cores = len(os.sched_getaffinity(0))
             jobs, desc = wl.cpu_jobs(args.cpu_sample)
             nq, dt = cpu_time(jobs, cores)
+            nq /= getattr(wl, "cpu_div", 1)  # queries, not (query, curve) projections
             cpu = {"value": nq / dt, "unit": UNIT, "cores": cores, "kind": "port",
                    "sample": f"{desc} ({dt:.1f} s wall on {cores} threads); C restatement of "
                              f"_kernels._project_block, bit-exact vs the reference"}

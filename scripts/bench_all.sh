@@ -1,6 +1,6 @@
 # every bench line of the round into gpurun_out/bench_<cfg>.json (+ logs)
 mkdir -p gpurun_out
-for c in cfg2 cfg1 cfg3 cfg4 cfg4q; do
+for c in cfg2 cfg1 cfg3 cfg4 cfg4q cfg6; do
   timeout 600 python bench.py --config $c --steps 50 --warmup 5 > gpurun_out/bench_$c.log 2>&1
   tail -1 gpurun_out/bench_$c.log > gpurun_out/bench_$c.json
 done

@@ -8,7 +8,8 @@ rows = [("cfg1", "cfg1 (10⁴ on-curve, 61 cubics)"),
         ("cfg3", "cfg3 (10⁴ curves, 10⁶ queries)"),
         ("cfg4", "cfg4 (bicubic surface, 3721 patches)"),
         ("cfg4q", "cfg4q (biquintic surface, 3481 patches)"),
-        ("cfg5", "cfg5 (10⁸ onto 10⁵ cubics)")]
+        ("cfg5", "cfg5 (10⁸ onto 10⁵ cubics)"),
+        ("cfg6", "cfg6 (§8(f) nearest of 100 curves, 41k cubics)")]
 ref = json.load(open(os.path.join(ROOT, "gpurun_out", "bench_ref.json")))
 print("| Config | device pts/s | e2e pts/s | CPU port (16 thr) | e2e / CPU | dominant kernel, FP64 frac |")
 print("|---|---|---|---|---|---|")
