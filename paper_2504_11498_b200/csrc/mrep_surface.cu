@@ -451,7 +451,7 @@ __device__ __forceinline__ double smin_of(const SurfParams& w, int64_t g) {
 }
 
 template <int PU, int PV>
-__device__ __forceinline__ void offer_points(const SurfParams& w, int64_t s, const double (&q)[3],
+__device__ __forceinline__ bool offer_points(const SurfParams& w, int64_t s, const double (&q)[3],
                                              double& ub, QStatsLite& st) {
   // the patch's seed grid: (pu+1)(pv+1) exact surface points
   const double* G = w.tab.rec + s * w.rec + surf_seed(PU, PV);
@@ -462,8 +462,11 @@ __device__ __forceinline__ void offer_points(const SurfParams& w, int64_t s, con
     double S[3] = {__ldg(G + 3 * k), __ldg(G + 3 * k + 1), __ldg(G + 3 * k + 2)};
     m = fmin(m, dist2_to(S, q));
   }
-  ub = fmin(ub, sqrt(m));
   st.points += NP;
+  const double d = sqrt(m);
+  if (!(d < ub)) return false;
+  ub = d;
+  return true;  // this patch now holds the nearest seed point seen
 }
 
 
@@ -492,7 +495,7 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
     const float* keys = cell_keys(T, ids);
     const int64_t p0 = __ldg(ids + a);
     offer_points<PU, PV>(w, p0, q, ub, st);
-    w.prim[g] = (int32_t)p0;
+    int64_t prim = p0;  // the patch holding the nearest seed point: solved first
 #pragma unroll 1
     for (int32_t i = a; i < b; ++i) {
       const double c2 = cut2(ub, scale);
@@ -501,7 +504,7 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
       st.boxes++;
       if (box_lb2<3>(T, T.lvl_off[0] + s, q) <= c2 &&
           obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2) {
-        if (s != p0) offer_points<PU, PV>(w, s, q, ub, st);
+        if (s != p0 && offer_points<PU, PV>(w, s, q, ub, st)) prim = s;
         unsigned long long slot = wave_append(&w.cnt[0], true);
         if (slot < w.pcap) {
           w.pq[slot] = (uint32_t)g;
@@ -511,6 +514,7 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
         }
       }
     }
+    w.prim[g] = (int32_t)prim;
   } else if (active) {
     // greedy descent to a nearby patch: its points give the first bound
     int level = T.top;
@@ -535,7 +539,7 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
       --level;
     }
     offer_points<PU, PV>(w, idx, q, ub, st);
-    w.prim[g] = (int32_t)idx;
+    int64_t prim = idx;  // the patch holding the nearest seed point: solved first
     int lv = T.top;
     int64_t node = 0;
     uint64_t masks = 0;
@@ -563,7 +567,7 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
       if (lv == 1) {
         if (box_lb2<3>(T, T.lvl_off[0] + ch, q) <= c2 &&
             obb_lb2(T.rec + ch * w.rec + surf_obb(PU, PV), q) <= c2) {
-          offer_points<PU, PV>(w, ch, q, ub, st);
+          if (offer_points<PU, PV>(w, ch, q, ub, st)) prim = ch;
           unsigned long long slot = wave_append(&w.cnt[0], true);
           if (slot < w.pcap) {
             w.pq[slot] = (uint32_t)g;
@@ -585,6 +589,7 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
         masks |= (uint64_t)m << (8 * lv);
       }
     }
+    w.prim[g] = (int32_t)prim;
   }
   if (active) {
     double4 rec;
