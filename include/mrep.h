@@ -250,6 +250,12 @@ MREP_API int mrep_surface_cells_build(void* table_dev, int64_t npatch, int pu, i
  * to [p, m - p - 2] (the span convention of core.py:108-112). */
 MREP_API int mrep_knot_span(const double* knots_dev, int64_t m, int p, const double* t_dev, int64_t n,
                    int32_t* span_dev, void* stream);
+/* The same for a curve set: query i uses curve curve_ids[i]'s knots
+ * knots_dev[knot_ofs[c] .. knot_ofs[c+1]) and degree[c] (all device arrays;
+ * the CSR layout of mrep_decompose). */
+MREP_API int mrep_knot_span_batch(const double* knots_dev, const int64_t* knot_ofs_dev,
+                                  const int32_t* degree_dev, const int32_t* curve_ids_dev,
+                                  const double* t_dev, int64_t n, int32_t* span_dev, void* stream);
 
 /* ---------------------------------------------------------------------
  * Per-operation batch kernels (the public single-pair ops of project.py

@@ -63,7 +63,7 @@ def lib():
         L.oracle_project_block.argtypes = [
             _dp, _dp, _dp, _dp, _dp, ctypes.c_int64, ctypes.c_int, _dp, ctypes.c_int64,
             ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-            _dp, _dp, _dp, _i64p, _i64p, _dp, _i64p, _i32p]
+            _dp, _dp, _dp, _i64p, _i64p, _dp, _i64p, _i32p, _i32p]
         L.oracle_quartic_block.argtypes = [_dp, ctypes.c_int64, _dp, _i64p]
         L.oracle_newton_quartic_block.argtypes = [_dp, ctypes.c_int64, _dp, _i64p]
         L.oracle_surf_patch_min.argtypes = [_dp, ctypes.c_int, ctypes.c_int, _dp, _dp, _dp, _dp,
@@ -157,7 +157,9 @@ def project_block(seg_pts, seg_ta, seg_tb, seam_t, seam_pt, queries, clip_tol=1e
                   max_iter=8, soundness_samples=0, workers=1):
     """The reference's _project_block over a query batch (workers = OpenMP threads).
 
-    Returns dict(t, foot, dist, cand, stats[n,6], sound, win, seg)."""
+    Returns dict(t, foot, dist, cand, stats[n,6], sound, win, seg, tie); tie[i]
+    counts candidates of another segment within dmin + 2e-12 (query i's
+    winning segment is ambiguous at the ulp level iff tie[i] > 0)."""
     seg_pts, seg_ta, seg_tb = _f64(seg_pts), _f64(seg_ta), _f64(seg_tb)
     seam_t, seam_pt, queries = _f64(seam_t), _f64(seam_pt), _f64(np.atleast_2d(queries))
     S, _, d = seg_pts.shape
@@ -165,13 +167,13 @@ def project_block(seg_pts, seg_ta, seg_tb, seam_t, seam_pt, queries, clip_tol=1e
     out = dict(t=np.empty(n), foot=np.empty((n, d)), dist=np.empty(n),
                cand=np.empty(n, dtype=np.int64), stats=np.zeros((n, 6), dtype=np.int64),
                sound=np.empty(n), win=np.empty(n, dtype=np.int64),
-               seg=np.empty(n, dtype=np.int32))
+               seg=np.empty(n, dtype=np.int32), tie=np.empty(n, dtype=np.int32))
     lib().oracle_project_block(
         _p(seg_pts), _p(seg_ta), _p(seg_tb), _p(seam_t), _p(seam_pt), S, d, _p(queries), n,
         float(clip_tol), int(max_iter), int(soundness_samples), int(workers),
         _p(out["t"]), _p(out["foot"]), _p(out["dist"]), _p(out["cand"], _i64p),
         _p(out["stats"], _i64p), _p(out["sound"]), _p(out["win"], _i64p),
-        _p(out["seg"], _i32p))
+        _p(out["seg"], _i32p), _p(out["tie"], _i32p))
     return out
 
 

@@ -83,6 +83,7 @@ _SIGS = {
     "mrep_surface_cells_bytes": ([_vp, _i64, _i32, _i32, _i32, _vp], _i64),
     "mrep_surface_cells_build": ([_vp, _i64, _i32, _i32, _i32, _vp, _i64, _vp], _i32),
     "mrep_knot_span": ([_vp, _i64, _i32, _vp, _i64, _vp, _vp], _i32),
+    "mrep_knot_span_batch": ([_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp], _i32),
     "mrep_quartic_roots": ([_vp, _i64, _vp, _vp, _vp], _i32),
     "mrep_newton_quartic_roots": ([_vp, _i64, _vp, _vp, _vp], _i32),
     "mrep_distance_poly": ([_vp, _vp, _i64, _i32, _vp, _vp], _i32),

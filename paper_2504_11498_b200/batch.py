@@ -35,7 +35,8 @@ class PreparedCurveSet:
     prepare_curve(curves[c])).
     """
 
-    def __init__(self, curves, tolerance, seg_pts, seg_ta, seg_tb, seg_ofs, handle, err=None):
+    def __init__(self, curves, tolerance, seg_pts, seg_ta, seg_tb, seg_ofs, handle, err=None,
+                 dev_curves=None):
         # seg_* / err: numpy arrays, or device tensors fetched to the host on
         # first access (a cfg3 set is ~400 MB of cubics; the device set does
         # not need the host copy)
@@ -46,6 +47,7 @@ class PreparedCurveSet:
         self.seg_ofs = np.asarray(seg_ofs, dtype=np.int64)
         self.seg_ofs.flags.writeable = False
         self._handle = handle
+        self._dev_curves = dev_curves  # CSR device knots for knot_spans
         self.d = int(seg_pts.shape[2]) if len(seg_pts.shape) == 3 else 3
 
     def _host(self, name):
@@ -87,6 +89,24 @@ class PreparedCurveSet:
         err = None if self.measured_error is None else self.measured_error[a:b]
         return PreparedCurve(self.curves[c], self.tolerance, pts, ta, tb, seam_t, seam_pt,
                              measured_error=err)
+
+    def knot_spans(self, t, curve_ids):
+        """Knot span of t[i] in curve curve_ids[i] (mrep_knot_span_batch; the
+        span convention of core.py:108-112).  Host arrays or device tensors."""
+        torch = L._torch()
+        if self._dev_curves is None:
+            if any(c is None for c in self.curves):
+                raise DomainError("knot spans need every curve's knot vector")
+            self._dev_curves = DeviceCurves(self.curves)
+        dc = self._dev_curves
+        td = L.to_dev(t)
+        cid = L.to_dev(curve_ids, torch.int32)
+        n = int(td.shape[0])
+        span = torch.empty((n,), dtype=torch.int32, device=td.device)
+        L.check(L.lib().mrep_knot_span_batch(L.ptr(dc.knots), L.ptr(dc.knot_ofs),
+                                             L.ptr(dc.degree), L.ptr(cid), L.ptr(td), n,
+                                             L.ptr(span), L.stream_ptr()))
+        return L.to_host(span)
 
     def device_bytes(self):
         nb = ctypes.c_int64()
@@ -172,7 +192,9 @@ def prepare_curve_set(curves, tolerance: float = 1e-4, batch_cap: int = 4096) ->
             raise EmptyDomain("curve has no nonzero-length span")
     d = dims.pop()
     torch = L._torch()
-    dec = decompose_device(DeviceCurves(curves))
+    dcurves = DeviceCurves(curves)
+    dec = decompose_device(dcurves)
+    dcurves.ctrl = dcurves.ctrl_ofs = None  # knots stay for knot_spans
     cap = int(min(max(batch_cap, 1) * len(curves), 1 << 22))
     res = approximate_device(dec["rows"], dec["row_ofs"], dec["iv"], dec["curve"], dec["nseg"], d,
                              tolerance, cap)
@@ -187,7 +209,7 @@ def prepare_curve_set(curves, tolerance: float = 1e-4, batch_cap: int = 4096) ->
     L.check(L.lib().mrep_curveset_create_dev(L.ptr(pts), L.ptr(ta), L.ptr(tb),
                                              ctypes.c_void_p(ofs.ctypes.data), len(curves), d,
                                              L.stream_ptr(), ctypes.byref(h)))
-    return PreparedCurveSet(curves, tolerance, pts, ta, tb, ofs, h, err=err)
+    return PreparedCurveSet(curves, tolerance, pts, ta, tb, ofs, h, err=err, dev_curves=dcurves)
 
 
 def curve_set_from_prepared(preps) -> PreparedCurveSet:
@@ -215,10 +237,11 @@ def curve_set_from_prepared(preps) -> PreparedCurveSet:
 
 def project_batch(cset: PreparedCurveSet, queries, curve_ids, workers: int | None = None,
                   clip_tol: float = 1e-6, max_iterations: int = 8, *,
-                  return_segments: bool = False):
+                  return_segments: bool = False, return_spans: bool = False):
     """Project query i onto curve curve_ids[i]; returns host arrays
-    (t, foot, dist, cand[, seg]) -- per query what project_prepared(cset[c], q)
-    returns (cand: candidates the screened kernel examined)."""
+    (t, foot, dist, cand[, seg][, span]) -- per query what
+    project_prepared(cset[c], q) returns (cand: candidates the screened kernel
+    examined; span: knot span of t* in curve c, core.py:108-112)."""
     if max_iterations < 1:
         raise DomainError("max_iterations must be >= 1")
     q = np.ascontiguousarray(np.atleast_2d(np.asarray(queries, dtype=np.float64)))
@@ -234,11 +257,13 @@ def project_batch(cset: PreparedCurveSet, queries, curve_ids, workers: int | Non
     n = q.shape[0]
     if n == 0:
         out = (np.empty(0), np.empty((0, cset.d)), np.empty(0), np.empty(0, np.int64))
-        return out + ((np.empty(0, np.int32),) if return_segments else ())
+        return (out + ((np.empty(0, np.int32),) if return_segments else ())
+                + ((np.empty(0, np.int32),) if return_spans else ()))
     cnt = np.zeros(L.NUM_COUNTERS, dtype=np.uint64)
     t, foot, dist, cand, seg = cset.project_host(q, cid, clip_tol=clip_tol,
                                                  max_iter=max_iterations, counters=cnt)
     if int(cnt[L.CNT_HULL_MISS]) > 0:
         raise NoRoot("hull never crossed on a surviving piece; elimination bug")
     out = (t, foot, dist, cand)
-    return out + ((seg,) if return_segments else ())
+    return (out + ((seg,) if return_segments else ())
+            + ((cset.knot_spans(t, cid),) if return_spans else ()))

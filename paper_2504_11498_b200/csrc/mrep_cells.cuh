@@ -315,6 +315,11 @@ int64_t cells_bytes(const void* table, int64_t S, int d, int grid, int rec, cons
   if (cudaStreamSynchronize(st) != cudaSuccess) return -1;
   int64_t total = 0;
   for (int32_t v : h) total += v;
+  if (total > INT32_MAX || g.ncell + 1 > INT32_MAX) {
+    // offsets and the prefix sum are int32: refuse instead of overflowing
+    set_error("mrep_cells_bytes: cell lists exceed 2^31 entries; use a smaller grid");
+    return -1;
+  }
   return (g.ncell + 1 + 2 * total) * 4;  // offsets, leaf ids, keys
 }
 
@@ -333,6 +338,18 @@ int cells_build(void* table, int64_t S, int d, int grid, int rec, const LP& lp, 
   MREP_CUDA_CHECK(cudaMemsetAsync(off + g.ncell, 0, 4, st));
   cells_count_kernel<LP><<<grid_for(g.ncell, 128), 128, 0, st>>>(T, lp, g, off);
   MREP_LAUNCH_CHECK();
+  {
+    // the int32 prefix sum below must not overflow: total the counts in int64
+    std::vector<int32_t> hc(g.ncell);
+    MREP_CUDA_CHECK(cudaMemcpyAsync(hc.data(), off, g.ncell * 4, cudaMemcpyDeviceToHost, st));
+    MREP_CUDA_CHECK(cudaStreamSynchronize(st));
+    int64_t tot64 = 0;
+    for (int32_t v : hc) tot64 += v;
+    if (tot64 > INT32_MAX || g.ncell + 1 > INT32_MAX) {
+      set_error("mrep_cells_build: cell lists exceed 2^31 entries; use a smaller grid");
+      return MREP_ERR_ARG;
+    }
+  }
   size_t tmp = 0;
   MREP_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, off, off, (int)(g.ncell + 1), st));
   void* t = nullptr;

@@ -84,7 +84,27 @@ struct HostCtx {
   bool ready = false;
 };
 
-HostCtx g_ctx;
+// One pipeline context per device (slots, streams, events and whole-batch
+// buffers all belong to the device they were created on); created on the
+// first host-buffer call made with that device current, never torn down.
+constexpr int MAX_DEVICES = 64;
+HostCtx* g_ctxs[MAX_DEVICES] = {};
+std::mutex g_ctxs_mu;
+
+HostCtx* current_ctx() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= MAX_DEVICES) {
+    cudaGetLastError();
+    set_error("no current CUDA device");
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_ctxs_mu);
+  if (!g_ctxs[dev]) {
+    g_ctxs[dev] = new HostCtx;
+    g_ctxs[dev]->device = dev;
+  }
+  return g_ctxs[dev];
+}
 
 bool is_pinned(const void* p) {
   cudaPointerAttributes a;
@@ -95,10 +115,8 @@ bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-int ensure_ctx() {
-  int dev = 0;
-  MREP_CUDA_CHECK(cudaGetDevice(&dev));
-  if (g_ctx.ready && g_ctx.device == dev) return MREP_OK;
+int ensure_ctx(HostCtx& g_ctx) {
+  if (g_ctx.ready) return MREP_OK;
   for (auto& s : g_ctx.slot) {
     // blocking streams: ordered after work on the legacy default stream (torch)
     MREP_CUDA_CHECK(cudaStreamCreateWithFlags(&s.st, cudaStreamDefault));
@@ -129,7 +147,6 @@ int ensure_ctx() {
   }
   MREP_CUDA_CHECK(cudaStreamCreateWithFlags(&g_ctx.cin, cudaStreamDefault));
   MREP_CUDA_CHECK(cudaStreamCreateWithFlags(&g_ctx.cout, cudaStreamDefault));
-  g_ctx.device = dev;
   g_ctx.ready = true;
   return MREP_OK;
 }
@@ -145,11 +162,11 @@ namespace {
 // Chunked H2D -> kernel -> D2H pipeline over the two slots.  `launch` runs the
 // projection of one chunk already resident in the slot's device buffers.
 template <class Launch>
-int host_pipeline(int d, const double* queries, const int32_t* curve_ids, int64_t n,
+int host_pipeline(HostCtx& g_ctx, int d, const double* queries, const int32_t* curve_ids, int64_t n,
                   double* out_t, double* out_foot, double* out_dist, int64_t* out_cand,
                   int32_t* out_seg, uint64_t* counters_host, Launch launch) {
   const auto t_entry = std::chrono::steady_clock::now();
-  int rc = ensure_ctx();
+  int rc = ensure_ctx(g_ctx);
   if (rc != MREP_OK) return rc;
   const bool pin_in = is_pinned(queries) && (!curve_ids || is_pinned(curve_ids));
   const bool pin_out = is_pinned(out_t) && is_pinned(out_foot) && is_pinned(out_dist) &&
@@ -444,9 +461,11 @@ extern "C" int mrep_project_host(const void* table, int64_t S, int d, const doub
     return MREP_ERR_ARG;
   }
   if (n == 0) return MREP_OK;
-  std::lock_guard<std::mutex> lock(g_ctx.mu);
+  HostCtx* C = current_ctx();
+  if (!C) return MREP_ERR_CUDA;
+  std::lock_guard<std::mutex> lock(C->mu);
   flags &= ~MREP_STATS;
-  return host_pipeline(d, queries, nullptr, n, out_t, out_foot, out_dist, out_cand, out_seg,
+  return host_pipeline(*C, d, queries, nullptr, n, out_t, out_foot, out_dist, out_cand, out_seg,
                        counters_host, [&](Slot& s) {
                          return mrep_project(table, S, d, s.dq, s.cnt, clip_tol, max_iter, 0,
                                              flags, s.dt, s.dfoot, s.ddist, s.dcand, s.dseg,
@@ -465,8 +484,10 @@ extern "C" int mrep_project_batch_host(const void* set, const double* queries,
     return MREP_ERR_ARG;
   }
   if (n == 0) return MREP_OK;
-  std::lock_guard<std::mutex> lock(g_ctx.mu);
-  return host_pipeline(d, queries, curve_ids, n, out_t, out_foot, out_dist, out_cand, out_seg,
+  HostCtx* C = current_ctx();
+  if (!C) return MREP_ERR_CUDA;
+  std::lock_guard<std::mutex> lock(C->mu);
+  return host_pipeline(*C, d, queries, curve_ids, n, out_t, out_foot, out_dist, out_cand, out_seg,
                        counters_host, [&](Slot& s) {
                          return mrep_project_batch(set, s.dq, s.dcur, s.cnt, clip_tol, max_iter,
                                                    flags, s.dt, s.dfoot, s.ddist, s.dcand, s.dseg,
@@ -486,8 +507,10 @@ extern "C" int mrep_project_surface_host(const void* table, int64_t npatch, int 
     return MREP_ERR_ARG;
   }
   if (n == 0) return MREP_OK;
-  std::lock_guard<std::mutex> lock(g_ctx.mu);
-  return host_pipeline(3, queries, nullptr, n, out_u, out_foot, out_dist, (int64_t*)out_v,
+  HostCtx* C = current_ctx();
+  if (!C) return MREP_ERR_CUDA;
+  std::lock_guard<std::mutex> lock(C->mu);
+  return host_pipeline(*C, 3, queries, nullptr, n, out_u, out_foot, out_dist, (int64_t*)out_v,
                        out_patch, counters_host, [&](Slot& s) {
                          return mrep_project_surface(table, npatch, pu, pv, s.dq, s.cnt, flags,
                                                      s.dt, (double*)s.dcand, s.dfoot, s.ddist,

@@ -2170,12 +2170,10 @@ __global__ void reduce_boxes_kernel(const double* child, int64_t nchild, double*
   }
 }
 
-__global__ void knot_span_kernel(const double* knots, int64_t m, int p, const double* t, int64_t n,
-                                 int32_t* span) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double x = t[i];
-  // searchsorted(knots, x, 'right'): first index with knots[idx] > x
+// searchsorted(knots, x, 'right') - 1 clipped to [p, m - p - 2]: the span
+// index q of core.py:108-112 whose [t_q, t_{q+1}) holds x (the last nonzero
+// span for x at the domain end).  Pure comparisons: bit-exact by construction.
+__device__ __forceinline__ int32_t knot_span_of(const double* knots, int64_t m, int p, double x) {
   int64_t lo = 0, hi = m;
   while (lo < hi) {
     int64_t mid = (lo + hi) >> 1;
@@ -2186,7 +2184,26 @@ __global__ void knot_span_kernel(const double* knots, int64_t m, int p, const do
   int64_t last = m - p - 2;
   if (s < p) s = p;
   if (s > last) s = last;
-  span[i] = (int32_t)s;
+  return (int32_t)s;
+}
+
+__global__ void knot_span_kernel(const double* knots, int64_t m, int p, const double* t, int64_t n,
+                                 int32_t* span) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  span[i] = knot_span_of(knots, m, p, t[i]);
+}
+
+// curve-set variant: query i searches the knot vector of curve curve_ids[i]
+// (CSR knots[knot_ofs[c] .. knot_ofs[c+1]))
+__global__ void knot_span_batch_kernel(const double* knots, const int64_t* knot_ofs,
+                                       const int32_t* degree, const int32_t* curve_ids,
+                                       const double* t, int64_t n, int32_t* span) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int c = curve_ids[i];
+  int64_t a = knot_ofs[c];
+  span[i] = knot_span_of(knots + a, knot_ofs[c + 1] - a, degree[c], t[i]);
 }
 
 // ------------------------------------------------------------ per-op kernels
@@ -3147,6 +3164,16 @@ int mrep_knot_span(const double* knots, int64_t m, int p, const double* t, int64
                    int32_t* span, void* stream) {
   if (n <= 0) return MREP_OK;
   knot_span_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(knots, m, p, t, n, span);
+  MREP_LAUNCH_CHECK();
+  return MREP_OK;
+}
+
+int mrep_knot_span_batch(const double* knots, const int64_t* knot_ofs, const int32_t* degree,
+                         const int32_t* curve_ids, const double* t, int64_t n, int32_t* span,
+                         void* stream) {
+  if (n <= 0) return MREP_OK;
+  knot_span_batch_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      knots, knot_ofs, degree, curve_ids, t, n, span);
   MREP_LAUNCH_CHECK();
   return MREP_OK;
 }

@@ -645,28 +645,50 @@ __global__ void __launch_bounds__(256) surf_filter(const __grid_constant__ SurfP
              obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2;
     }
     if (keep) {  // group-uniform (same pair in all 8 lanes)
-      // on the float copy of the nets (half the bytes; the filter is
-      // L2-bandwidth bound): every coefficient, the query and each of the
-      // ~6 operations err by <= 2^-24 relative, so the float minimum is
-      // within 8 * 2^-24 (mag (1 + 2|q|_1) + |q|^2) of the exact one (mag
-      // bounds |E|, |SS|); 4e-6 covers it with an 8x margin
-      const float4* F = reinterpret_cast<const float4*>(T.rec + s * w.rec + surf_bernf(PU, PV));
-      const float q0 = __double2float_rn(q[0]), q1 = __double2float_rn(q[1]),
-                  q2 = __double2float_rn(q[2]);
-      const float qqf = q0 * q0 + q1 * q1 + q2 * q2;
-      float m = __int_as_float(0x7f800000);
-      for (int k = sub; k < NE; k += 8) {
-        const float4 e = __ldg(F + k);
-        m = fminf(m, (e.w - 2.0f * (q0 * e.x + q1 * e.y + q2 * e.z)) + qqf);
-      }
-      m = fminf(m, __shfl_xor_sync(gmask, m, 4));
-      m = fminf(m, __shfl_xor_sync(gmask, m, 2));
-      m = fminf(m, __shfl_xor_sync(gmask, m, 1));
       const double qq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2];
       const double qa = fabs(q[0]) + fabs(q[1]) + fabs(q[2]);
       const double mag = __ldg(T.rec + s * w.rec + surf_bern(PU, PV) + 4 * NE);
-      const double err = 4e-6 * (mag * (1.0 + 2.0 * qa) + qq);
-      keep = !((double)m - err > c2);
+      // the float test needs every term inside float's normal range: mag
+      // (~length^2) and |q|^2 below ~1e30, and mag large enough that float
+      // underflow (absolute error < 1e-37) is far below the allowance
+      bool fnet = mag > 1e-25 && mag < 1e30 && qa < 1e15;
+      double lb = 0.0, err = 0.0;
+      if (fnet) {
+        // on the float copy of the nets (half the bytes; the filter is
+        // L2-bandwidth bound): every coefficient, the query and each of the
+        // ~6 operations err by <= 2^-24 relative, so the float minimum is
+        // within 8 * 2^-24 (mag (1 + 2|q|_1) + |q|^2) of the exact one (mag
+        // bounds |E|, |SS|); 4e-6 covers it with an 8x margin
+        const float4* F = reinterpret_cast<const float4*>(T.rec + s * w.rec + surf_bernf(PU, PV));
+        const float q0 = __double2float_rn(q[0]), q1 = __double2float_rn(q[1]),
+                    q2 = __double2float_rn(q[2]);
+        const float qqf = q0 * q0 + q1 * q1 + q2 * q2;
+        float m = __int_as_float(0x7f800000);
+        for (int k = sub; k < NE; k += 8) {
+          const float4 e = __ldg(F + k);
+          m = fminf(m, (e.w - 2.0f * (q0 * e.x + q1 * e.y + q2 * e.z)) + qqf);
+        }
+        m = fminf(m, __shfl_xor_sync(gmask, m, 4));
+        m = fminf(m, __shfl_xor_sync(gmask, m, 2));
+        m = fminf(m, __shfl_xor_sync(gmask, m, 1));
+        lb = (double)m;
+        err = 4e-6 * (mag * (1.0 + 2.0 * qa) + qq);
+        fnet = isfinite(lb);
+      }
+      if (!fnet) {
+        // the double nets: a few ulps of the same magnitudes
+        const double* E = T.rec + s * w.rec + surf_bern(PU, PV);
+        double m = INFINITY;
+        for (int k = sub; k < NE; k += 8)
+          m = fmin(m, (E[3 * NE + k] - 2.0 * (q[0] * E[3 * k] + q[1] * E[3 * k + 1] +
+                                               q[2] * E[3 * k + 2])) + qq);
+        m = fmin(m, __shfl_xor_sync(gmask, m, 4));
+        m = fmin(m, __shfl_xor_sync(gmask, m, 2));
+        m = fmin(m, __shfl_xor_sync(gmask, m, 1));
+        lb = m;
+        err = 1e-13 * (mag * (1.0 + 2.0 * qa) + qq);
+      }
+      keep = !(lb - err > c2);
     }
     if (sub == 0) {
       unsigned long long slot = wave_append(&w.cnt[6], keep);

@@ -157,6 +157,23 @@ class PreparedCurve:
     def num_segments(self) -> int:
         return len(self.seg_ta)
 
+    def knot_spans(self, t):
+        """Knot span of each parameter on the GPU (mrep_knot_span):
+        searchsorted(knots, t, 'right') - 1 clipped to [p, n - 1], the span
+        convention of core.py:108-112.  t: host array or device tensor."""
+        torch = L._torch()
+        if self.curve is None:
+            raise DomainError("knot spans need the prepared curve's knot vector")
+        if getattr(self, "_knots_dev", None) is None:
+            self._knots_dev = L.to_dev(np.asarray(self.curve.knots.knots, dtype=np.float64))
+        td = L.to_dev(t)
+        n = int(td.shape[0])
+        span = torch.empty((n,), dtype=torch.int32, device=td.device)
+        L.check(L.lib().mrep_knot_span(L.ptr(self._knots_dev), int(self._knots_dev.shape[0]),
+                                       int(self.curve.degree), L.ptr(td), n, L.ptr(span),
+                                       L.stream_ptr()))
+        return L.to_host(span)
+
 
 # ------------------------------------------------------------ single-pair ops
 def rebase(e) -> NonParametricBezier:
@@ -291,10 +308,12 @@ def _as_queries(prep, queries):
 def project_prepared(prep: PreparedCurve, queries, workers: int | None = None,
                      clip_tol: float = 1e-6, max_iterations: int = 8,
                      with_stats: bool = False, soundness_samples: int = 0, *,
-                     screen: bool = True, return_segments: bool = False):
+                     screen: bool = True, return_segments: bool = False,
+                     return_spans: bool = False):
     """Project every query; returns (t, foot, distance, candidates) host arrays,
     plus (ProjectionStats, sound) when with_stats, plus the winning cubic index
-    per query when return_segments."""
+    per query when return_segments, plus the knot span of t* in the original
+    B-spline (core.py:108-112) when return_spans."""
     q = _as_queries(prep, queries)
     plan_work(len(q), 1 if workers is None else workers)
     if max_iterations < 1:
@@ -306,7 +325,8 @@ def project_prepared(prep: PreparedCurve, queries, workers: int | None = None,
         empty = (np.empty(0), np.empty((0, q.shape[1])), np.empty(0), np.empty(0, np.int64))
         if with_stats:
             empty = empty + (ProjectionStats(0, 0, 0, 0, 0, 0), np.empty(0))
-        return empty + ((np.empty(0, np.int32),) if return_segments else ())
+        return (empty + ((np.empty(0, np.int32),) if return_segments else ())
+                + ((np.empty(0, np.int32),) if return_spans else ()))
     if not dense:
         cnt = np.zeros(L.NUM_COUNTERS, dtype=np.uint64)
         t, foot, dist, cand, seg = tab.project_host(q, clip_tol=clip_tol, max_iter=max_iterations,
@@ -314,7 +334,8 @@ def project_prepared(prep: PreparedCurve, queries, workers: int | None = None,
         if int(cnt[L.CNT_HULL_MISS]) > 0:
             raise NoRoot("hull never crossed on a surviving piece; elimination bug")
         out = (t, foot, dist, cand)
-        return out + ((seg,) if return_segments else ())
+        return (out + ((seg,) if return_segments else ())
+                + ((prep.knot_spans(t),) if return_spans else ()))
     td, fd, dd, cd, sd, std, snd = tab.project(L.to_dev(q), clip_tol, max_iterations,
                                                soundness_samples, screen=False, stats=True)
     t, foot, dist, cand = L.to_host(td), L.to_host(fd), L.to_host(dd), L.to_host(cd)
@@ -325,7 +346,8 @@ def project_prepared(prep: PreparedCurve, queries, workers: int | None = None,
     if with_stats:
         tot = stats_arr.sum(axis=0)
         out = out + (ProjectionStats(*(int(x) for x in tot)), sound)
-    return out + ((seg,) if return_segments else ())
+    return (out + ((seg,) if return_segments else ())
+            + ((prep.knot_spans(td),) if return_spans else ()))
 
 
 def project_points(curve: BSplineCurve, queries, tolerance: float = 1e-4,

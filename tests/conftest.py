@@ -40,3 +40,33 @@ def gpu():
     from paper_2504_11498_b200 import _lib
     _lib.lib()
     return torch.device("cuda")
+
+
+def oracle_spans(knots, p, t):
+    """Knot span convention of core.py:108-112 on the host (numpy)."""
+    knots = np.asarray(knots)
+    return np.clip(np.searchsorted(knots, t, "right") - 1, p, len(knots) - p - 2)
+
+
+def assert_parity(t, dist, seg, o, span=None, knots=None, degree=None, dist_floor=1e-12):
+    """North-star bars against an oracle result dict o (oracle.project_block):
+    t within 1e-6; distance within 1e-9 relative (absolute floor dist_floor);
+    winning segment EXACT on every query whose segment the oracle finds
+    unambiguous (o["tie"] == 0: no other segment's candidate within
+    dmin + 2e-12); knot span exact unless a knot lies between the GPU's t and
+    the oracle's (then both spans are the correct span of their own t).
+    Returns the number of oracle-detected ties."""
+    assert np.all(np.abs(t - o["t"]) <= 1e-6), float(np.abs(t - o["t"]).max())
+    tol = np.maximum(1e-9 * o["dist"], dist_floor)
+    assert np.all(np.abs(dist - o["dist"]) <= tol), float(np.abs(dist - o["dist"]).max())
+    clear = o["tie"] == 0
+    bad = np.nonzero(clear & (seg != o["seg"]))[0]
+    assert bad.size == 0, f"{bad.size} segment mismatches outside ties, e.g. {bad[:5]}"
+    if span is not None:
+        ref = oracle_spans(knots, degree, o["t"])
+        assert np.array_equal(oracle_spans(knots, degree, t), span)
+        diff = np.nonzero(span != ref)[0]
+        for i in diff:  # only where t and t_ref straddle a knot
+            lo, hi = sorted((t[i], o["t"][i]))
+            assert np.any((knots > lo) & (knots <= hi)), (i, t[i], o["t"][i])
+    return int((~clear).sum())

@@ -276,3 +276,58 @@ class TestAcceptance:
             c3 += stats.conv3_source
             cf += stats.conv_final_source
         assert c3 / pieces >= 0.95 and cf == pieces
+
+
+class TestKnotSpans:
+    """Knot span of t* (north star: bit-exact): searchsorted(knots, t*,
+    'right') - 1 clipped to [p, n-1], the convention of core.py:108-112."""
+
+    @pytest.mark.parametrize("name", ["cfg1_random", "cfg2", "kink", "deg9", "deg5_2d"])
+    def test_spans_of_reference_t(self, gpu, name):
+        import sys
+        sys.path.insert(0, __import__("os").path.dirname(__file__))
+        from conftest import load_golden, oracle_spans
+        from paper_2504_11498_b200 import BSplineCurve, PreparedCurve, project_prepared
+        z = load_golden(f"project_{name}.npz")
+        curve = BSplineCurve(int(z["degree"]), z["knots"], z["ctrl"])
+        # the reference's own prepared arrays, so t* is comparable bit for bit
+        prep = PreparedCurve.from_arrays(curve, float(z["tolerance"]), z["seg_pts"], z["seg_ta"],
+                                         z["seg_tb"], z["seam_t"], z["seam_pt"])
+        for kw in ({}, {"with_stats": True}):
+            out = project_prepared(prep, z["queries"], return_spans=True, **kw)
+            t, span = out[0], out[-1]
+            assert span.dtype == np.int32
+            assert np.array_equal(span, oracle_spans(z["knots"], int(z["degree"]), t))
+            straddle = span != oracle_spans(z["knots"], int(z["degree"]), z["t"])
+            assert not straddle.any()
+        # the spans of the reference's own t through the device kernel
+        assert np.array_equal(prep.knot_spans(z["t"]),
+                              oracle_spans(z["knots"], int(z["degree"]), z["t"]))
+
+    def test_span_edges(self, gpu):
+        from paper_2504_11498_b200 import BSplineCurve, PreparedCurve
+        knots = np.array([0, 0, 0, 0, 0.25, 0.5, 0.5, 0.75, 1, 1, 1, 1], dtype=float)
+        curve = BSplineCurve(3, knots, np.random.default_rng(0).uniform(0, 1, (8, 3)))
+        prep = PreparedCurve(curve, 1e-4, np.zeros((1, 4, 3)), [0.0], [1.0], [0.0, 1.0],
+                             np.zeros((2, 3)))
+        t = np.array([0.0, 0.1, 0.25, 0.4999999999, 0.5, 0.74, 0.75, 0.999, 1.0])
+        want = [3, 3, 4, 4, 6, 6, 7, 7, 7]
+        assert prep.knot_spans(t).tolist() == want
+
+    def test_batch_spans(self, gpu):
+        import sys
+        sys.path.insert(0, __import__("os").path.dirname(__file__))
+        from conftest import oracle_spans
+        from paper_2504_11498_b200 import prepare_curve_set, project_batch
+        from paper_2504_11498_b200.fixtures import mixed_curve_batch
+        curves = mixed_curve_batch(12, max_control=300)
+        cs = prepare_curve_set(curves)
+        rng = np.random.default_rng(4)
+        cid = rng.integers(0, 12, 3000)
+        q = rng.uniform(0, 1, (3000, 3))
+        t, foot, dist, cand, seg, span = project_batch(cs, q, cid, return_segments=True,
+                                                       return_spans=True)
+        for c in range(12):
+            m = cid == c
+            cv = curves[c]
+            assert np.array_equal(span[m], oracle_spans(cv.knots.knots, cv.degree, t[m]))

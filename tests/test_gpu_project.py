@@ -1,16 +1,16 @@
 """Batch projection kernel (dense = reference semantics, screened = BVH) vs
 the reference's golden outputs and the pinned C oracle.
 
-Bars (north star): segment index exact except documented ties; distance
-within 1e-9 relative (absolute floor 1e-12 for on-curve queries, whose
-distance is ~0); parameter within 1e-6.  Dense mode must also reproduce the
-reference's candidate count and all six stats columns (allowing <= 0.1% of
-queries to differ where a CUDA-vs-glibc ulp in the quartic flips a sign test).
+Bars (north star): segment index exact except ties the oracle itself
+detects (another segment within dmin + 2e-12); distance within 1e-9 relative
+(absolute floor 1e-12 for on-curve queries, whose distance is ~0); parameter
+within 1e-6.  Dense mode must also reproduce the reference's candidate count
+and all six stats columns exactly.
 """
 import numpy as np
 import pytest
 
-from conftest import load_golden, project_fixture_names
+from conftest import assert_parity, load_golden, project_fixture_names
 
 pytestmark = pytest.mark.gpu
 
@@ -33,8 +33,8 @@ def test_dense_matches_reference(gpu, name):
         *_args(z), z["queries"], float(z["clip_tol"]), int(z["max_iter"]), int(z["soundness"]))
     assert_close(t, dist, z["t"], z["dist"])
     assert np.abs(foot - z["foot"]).max() <= 1e-6
-    assert np.mean(cand == z["cand"]) >= 0.999
-    assert np.mean((stats == z["stats"]).all(1)) >= 0.999
+    assert np.array_equal(cand, z["cand"])
+    assert np.array_equal(stats, z["stats"])
     if int(z["soundness"]) > 0:
         fin = np.isfinite(z["sound"])
         assert np.array_equal(np.isfinite(sound), fin)
@@ -80,11 +80,13 @@ def test_screened_equals_dense(gpu, name):
 def test_segment_ids_match_oracle(gpu, oracle_lib):
     """Winning cubic index (the north star's 'segment id') vs the oracle."""
     from paper_2504_11498_b200 import _device as D
-    for name in ("cfg1_random", "cfg2", "table_n", "deg9"):
+    for name in project_fixture_names():
         z = load_golden(f"project_{name}.npz")
         o = oracle_lib.project_block(*_args(z), z["queries"], workers=8)
-        seg = D.DeviceTable(*_args(z)).project(z["queries"])[4].cpu().numpy()
-        assert np.mean(seg == o["seg"]) >= 0.999, name
+        tab = D.DeviceTable(*_args(z))
+        for screen in (True, False):
+            r = [x.cpu().numpy() for x in tab.project(z["queries"], screen=screen)[:5]]
+            assert_parity(r[0], r[2], r[4], o)
 
 
 def test_cfg2_random_vs_oracle(gpu, oracle_lib):
@@ -97,8 +99,7 @@ def test_cfg2_random_vs_oracle(gpu, oracle_lib):
     tab = D.DeviceTable(*_args(z))
     t, foot, dist, cand, seg, _, _ = [x.cpu().numpy() if x is not None else None
                                       for x in tab.project(q)]
-    assert_close(t, dist, o["t"], o["dist"])
-    assert np.mean(seg == o["seg"]) >= 0.999
+    assert_parity(t, dist, seg, o)
     assert np.mean(t == o["t"]) >= 0.99
 
 

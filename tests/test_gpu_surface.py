@@ -146,3 +146,22 @@ def test_cell_index_matches_tree_walk(gpu, pu, pv, n, grid):
     b = [x.cpu().numpy() for x in tab.project(q, extra_flags=L.MREP_CELLS)]
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("scale", [1e-22, 1e18])
+def test_extreme_scales_use_exact_nets(gpu, oracle_lib, scale):
+    """Coordinates far outside float's comfortable range (|S|^2 ~ 1e36 or
+    ~1e-44): the Bernstein filter must switch to the double nets instead of
+    pruning real patches on an overflowed / denormal float bound."""
+    from paper_2504_11498_b200 import BSplineSurface, prepare_surface, project_surface_prepared
+    base = _surf(3, 3, 12, 21)
+    s = BSplineSurface(3, 3, base.knots_u.knots, base.knots_v.knots,
+                       base.control_points * scale)
+    prep = prepare_surface(s)
+    q = np.random.default_rng(22).uniform(0, 1, (3000, 3)) * scale
+    g = project_surface_prepared(prep, q, return_patches=True)
+    o = oracle_lib.surface_project(prep.patch_pts.reshape(-1, 4, 4, 3),
+                                   prep.patch_iv.reshape(-1, 4), 3, 3, q, workers=16)
+    u, v, foot, dist, patch = g
+    assert np.all(np.abs(dist - o["dist"]) <= np.maximum(1e-9 * o["dist"], 1e-12 * scale))
+    assert (patch == o["patch"]).mean() >= 0.999
