@@ -283,6 +283,17 @@ MREP_API int mrep_hull_cross(const double* b_dev, int64_t n, int32_t* found_dev,
 MREP_API int mrep_clip_root(const double* b_dev, int64_t n, double tol, int max_iter, double* root_dev,
                    int32_t* ok_dev, int32_t* used_dev, double* widths_dev, void* stream);
 /* _kernels._decasteljau_point (_kernels.py:344-357) */
+/* Any-degree scalar Bernstein ops (project.py NonParametricBezier for
+ * degree != 5; _kernels.py:200-341): b_dev [n][degree+1], 1 <= degree <= 31.
+ *   op 0 eval:      out[n] = value at a[i]
+ *   op 1 hull:      i0[n] = found, out[n][2] = (z1, z2)
+ *   op 2 restrict:  out[n][degree+1] = ordinates on [a[i], c[i]]
+ *   op 3 clip_root: out[n] = root, i0 = ok, i1 = iterations used,
+ *                   widths[n][max_iter] (tolerance tol) */
+MREP_API int mrep_ordinates_op(int op, const double* b_dev, int degree, int64_t n,
+                               const double* a_dev, const double* c_dev, double tol,
+                               int max_iter, double* out_dev, int32_t* i0_dev, int32_t* i1_dev,
+                               double* widths_dev, void* stream);
 MREP_API int mrep_cubic_points(const double* P_dev /*[n][4][d]*/, const double* u_dev, int64_t n, int d,
                       double* out_dev /*[n][d]*/, void* stream);
 /* project.rebase_batch (project.py:134-137): b = T5 e */

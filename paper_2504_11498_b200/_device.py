@@ -100,6 +100,33 @@ def clip_root(b, tol, max_iter):
             L.to_host(widths)[:, : int(max_iter)])
 
 
+def ordinates_op(op, b, a=None, c=None, tol=1e-6, max_iter=8):
+    """Any-degree scalar Bernstein op (mrep_ordinates_op) on rows b (n, deg+1):
+    op 0 eval at a -> (n,); 1 hull -> (found (n,), z (n, 2)); 2 restrict to
+    [a, c] -> (n, deg+1); 3 clip_root -> (root, ok, used, widths)."""
+    torch = L._torch()
+    b = _f64(b)
+    b = b.reshape(-1, b.shape[-1])
+    n, deg = b.shape[0], b.shape[1] - 1
+    bd = L.to_dev(b)
+    ad = L.to_dev(np.broadcast_to(_f64(a), (n,)).copy()) if a is not None else None
+    cd = L.to_dev(np.broadcast_to(_f64(c), (n,)).copy()) if c is not None else None
+    shape = {0: (n,), 1: (n, 2), 2: (n, deg + 1), 3: (n,)}[op]
+    out = L.empty(shape)
+    i0 = L.empty((n,), torch.int32)
+    i1 = L.empty((n,), torch.int32)
+    widths = L.empty((n, max(int(max_iter), 1))) if op == 3 else None
+    L.check(L.lib().mrep_ordinates_op(int(op), L.ptr(bd), deg, n, L.ptr(ad), L.ptr(cd),
+                                      float(tol), int(max_iter), L.ptr(out), L.ptr(i0),
+                                      L.ptr(i1), L.ptr(widths), L.stream_ptr()))
+    if op == 1:
+        return L.to_host(i0).astype(bool), L.to_host(out)
+    if op == 3:
+        return (L.to_host(out), L.to_host(i0).astype(bool), L.to_host(i1),
+                L.to_host(widths)[:, : int(max_iter)])
+    return L.to_host(out)
+
+
 def cubic_points(P, u):
     P = _f64(P)
     if P.ndim == 2:

@@ -91,6 +91,8 @@ _SIGS = {
     "mrep_eval_ordinates": ([_vp, _vp, _i64, _vp, _vp], _i32),
     "mrep_hull_cross": ([_vp, _i64, _vp, _vp, _vp], _i32),
     "mrep_clip_root": ([_vp, _i64, _dbl, _i32, _vp, _vp, _vp, _vp, _vp], _i32),
+    "mrep_ordinates_op": ([_i32, _vp, _i32, _i64, _vp, _vp, _dbl, _i32, _vp, _vp, _vp, _vp, _vp],
+                          _i32),
     "mrep_cubic_points": ([_vp, _vp, _i64, _i32, _vp, _vp], _i32),
     "mrep_rebase": ([_vp, _i64, _vp, _vp], _i32),
     "mrep_decompose_plan": ([_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp], _i32),
@@ -180,6 +182,8 @@ def to_dev(a, dtype=None):
     if isinstance(a, torch.Tensor):
         return a.to(device=device(), dtype=dtype).contiguous()
     arr = np.ascontiguousarray(a)
+    if not arr.flags.writeable:  # read-only inputs (as_readonly): torch wants a writable view
+        arr = arr.copy()
     return torch.from_numpy(arr).to(device=device(), dtype=dtype, non_blocking=False).contiguous()
 
 

@@ -2206,6 +2206,153 @@ __global__ void knot_span_batch_kernel(const double* knots, const int64_t* knot_
   span[i] = knot_span_of(knots + a, knot_ofs[c + 1] - a, degree[c], t[i]);
 }
 
+// ------------------------------------------------------------ any-degree ordinate ops
+// The reference's NonParametricBezier ops work for any degree n
+// (_kernels.py:200-341 loop over b.shape[0]); the projection only ever
+// builds quintics (the fast fixed-size kernels below), so these runtime-n
+// versions back the public per-op API for other degrees.  Same operation
+// order as the reference (abscissae i / n, de Casteljau restriction).
+constexpr int ORD_NMAX = 32;  // ordinates per polynomial (degree <= 31)
+
+__device__ void restrict_gen(double* cur, int n, double lo, double hi) {
+  double tmp[ORD_NMAX], side[ORD_NMAX];
+  if (lo > 0.0) {
+    for (int i = 0; i <= n; ++i) tmp[i] = cur[i];
+    side[n] = cur[n];
+    for (int k = 1; k <= n; ++k) {
+      for (int i = 0; i < n + 1 - k; ++i) tmp[i] = (1.0 - lo) * tmp[i] + lo * tmp[i + 1];
+      side[n - k] = tmp[n - k];
+    }
+    for (int i = 0; i <= n; ++i) cur[i] = side[i];
+    hi = (hi - lo) / (1.0 - lo);
+  }
+  if (hi < 1.0) {
+    for (int i = 0; i <= n; ++i) tmp[i] = cur[i];
+    side[0] = cur[0];
+    for (int k = 1; k <= n; ++k) {
+      for (int i = 0; i < n + 1 - k; ++i) tmp[i] = (1.0 - hi) * tmp[i] + hi * tmp[i + 1];
+      side[k] = tmp[0];
+    }
+    for (int i = 0; i <= n; ++i) cur[i] = side[i];
+  }
+}
+
+__device__ double eval_gen(const double* b, int n, double u) {
+  double tmp[ORD_NMAX];
+  for (int i = 0; i <= n; ++i) tmp[i] = b[i];
+  for (int k = 0; k < n; ++k)
+    for (int i = 0; i < n - k; ++i) tmp[i] = (1.0 - u) * tmp[i] + u * tmp[i + 1];
+  return tmp[0];
+}
+
+__device__ bool hull_cross_gen(const double* b, int n, double& z1o, double& z2o) {
+  double lox[ORD_NMAX], loy[ORD_NMAX], hix[ORD_NMAX], hiy[ORD_NMAX];
+  int nl = 0, nh = 0;
+  for (int i = 0; i <= n; ++i) {
+    const double x = (double)i / (double)n, y = b[i];
+    while (nl > 1 && ((lox[nl - 1] - lox[nl - 2]) * (y - loy[nl - 2]) -
+                      (x - lox[nl - 2]) * (loy[nl - 1] - loy[nl - 2])) <= 0.0)
+      --nl;
+    lox[nl] = x;
+    loy[nl] = y;
+    ++nl;
+    while (nh > 1 && ((hix[nh - 1] - hix[nh - 2]) * (y - hiy[nh - 2]) -
+                      (x - hix[nh - 2]) * (hiy[nh - 1] - hiy[nh - 2])) >= 0.0)
+      --nh;
+    hix[nh] = x;
+    hiy[nh] = y;
+    ++nh;
+  }
+  double z1 = 2.0, z2 = -1.0;
+  for (int chain = 0; chain < 2; ++chain) {
+    const double* cx = chain == 0 ? lox : hix;
+    const double* cy = chain == 0 ? loy : hiy;
+    const int m = chain == 0 ? nl : nh;
+    for (int i = 0; i < m - 1; ++i) {
+      const double y0 = cy[i], y1 = cy[i + 1];
+      double z;
+      if (y0 == 0.0) z = cx[i];
+      else if (y1 == 0.0) z = cx[i + 1];
+      else if ((y0 < 0.0 && 0.0 < y1) || (y1 < 0.0 && 0.0 < y0))
+        z = cx[i] + (cx[i + 1] - cx[i]) * (-y0) / (y1 - y0);
+      else continue;
+      if (z < z1) z1 = z;
+      if (z > z2) z2 = z;
+    }
+    if (m > 0 && cy[m - 1] == 0.0) {
+      const double z = cx[m - 1];
+      if (z < z1) z1 = z;
+      if (z > z2) z2 = z;
+    }
+  }
+  if (z2 < z1) {
+    z1o = z2o = 0.0;
+    return false;
+  }
+  z1o = z1;
+  z2o = z2;
+  return true;
+}
+
+// op 0: eval at a[i]; 1: hull crossings -> found, (z1, z2); 2: restrict to
+// [a[i], c[i]]; 3: clip_root (tol, max_iter) -> root, ok, used, widths
+__global__ void ordinates_gen_kernel(int op, const double* b, int n, int64_t cnt, const double* a,
+                                     const double* c, double tol, int max_iter, double* out,
+                                     int32_t* i0, int32_t* i1, double* widths) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cnt) return;
+  double cur[ORD_NMAX];
+  for (int k = 0; k <= n; ++k) cur[k] = b[i * (n + 1) + k];
+  if (op == 0) {
+    out[i] = eval_gen(cur, n, a[i]);
+  } else if (op == 1) {
+    double z1, z2;
+    i0[i] = hull_cross_gen(cur, n, z1, z2) ? 1 : 0;
+    out[2 * i] = z1;
+    out[2 * i + 1] = z2;
+  } else if (op == 2) {
+    restrict_gen(cur, n, a[i], c[i]);
+    for (int k = 0; k <= n; ++k) out[i * (n + 1) + k] = cur[k];
+  } else {  // _kernels.py:306-341
+    double* w = widths + i * max_iter;
+    double lo = 0.0, hi = 1.0;
+    int used = 0;
+    for (int it = 0; it < max_iter; ++it) {
+      double z1, z2;
+      if (!hull_cross_gen(cur, n, z1, z2)) {
+        for (int k = it; k < max_iter; ++k) w[k] = hi - lo;
+        out[i] = 0.5 * (lo + hi);
+        i0[i] = 0;
+        i1[i] = it;
+        return;
+      }
+      used = it + 1;
+      const double nlo = lo + z1 * (hi - lo), nhi = lo + z2 * (hi - lo);
+      if (z2 - z1 < 1e-15) {
+        for (int k = it; k < max_iter; ++k) w[k] = 0.0;
+        out[i] = nlo;
+        i0[i] = 1;
+        i1[i] = used;
+        return;
+      }
+      restrict_gen(cur, n, z1, z2);
+      lo = nlo;
+      hi = nhi;
+      w[it] = hi - lo;
+      if (hi - lo <= tol) {
+        for (int k = it + 1; k < max_iter; ++k) w[k] = hi - lo;
+        out[i] = 0.5 * (lo + hi);
+        i0[i] = 1;
+        i1[i] = used;
+        return;
+      }
+    }
+    out[i] = 0.5 * (lo + hi);
+    i0[i] = 1;
+    i1[i] = used;
+  }
+}
+
 // ------------------------------------------------------------ per-op kernels
 __global__ void quartic_kernel(const double* c, int64_t n, double* roots, int64_t* counts) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -3218,6 +3365,16 @@ int mrep_clip_root(const double* b, int64_t n, double tol, int max_iter, double*
     return MREP_ERR_ARG;
   }
   MREP_SIMPLE_LAUNCH(clip_kernel, n, b, n, tol, max_iter, root, ok, used, widths);
+}
+int mrep_ordinates_op(int op, const double* b, int degree, int64_t n, const double* a,
+                      const double* c, double tol, int max_iter, double* out, int32_t* i0,
+                      int32_t* i1, double* widths, void* stream) {
+  if (op < 0 || op > 3 || degree < 1 || degree >= ORD_NMAX || (op == 3 && max_iter < 1)) {
+    set_error("mrep_ordinates_op: op in 0..3, 1 <= degree <= 31, max_iter >= 1");
+    return MREP_ERR_ARG;
+  }
+  MREP_SIMPLE_LAUNCH(ordinates_gen_kernel, n, op, b, degree, n, a, c, tol, max_iter, out, i0, i1,
+                     widths);
 }
 int mrep_cubic_points(const double* P, const double* u, int64_t n, int d, double* out,
                       void* stream) {

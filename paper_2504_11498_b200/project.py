@@ -66,13 +66,19 @@ class NonParametricBezier:
         return float(self.ordinates[-1])
 
     def __call__(self, u: float) -> float:
-        _need_quintic(self)
-        return float(D.eval_ordinates(self.ordinates[None], float(u))[0])
+        if _quintic(self):
+            return float(D.eval_ordinates(self.ordinates[None], float(u))[0])
+        return float(D.ordinates_op(0, self.ordinates[None], a=float(u))[0])
 
 
-def _need_quintic(bez):
-    if len(bez.ordinates) != 6:
-        raise DomainError("device ordinate kernels handle the quintic E (6 ordinates)")
+def _quintic(bez):
+    """Quintic E (the only degree the projection builds) -> the fixed-size
+    kernels the projection itself runs; any other degree (1..31) -> the
+    runtime-degree kernels (mrep_ordinates_op)."""
+    n = len(bez.ordinates)
+    if n < 2 or n > 32:
+        raise DomainError("ordinate ops need degree 1..31")
+    return n == 6
 
 
 @dataclass(frozen=True, eq=False)
@@ -194,8 +200,8 @@ def rebase_batch(coeff_block: np.ndarray) -> np.ndarray:
 
 def hull_x_intersections(bez: NonParametricBezier):
     """Abscissa range where the convex hull meets y = 0, or None."""
-    _need_quintic(bez)
-    found, z = D.hull_cross(bez.ordinates[None])
+    found, z = (D.hull_cross if _quintic(bez) else
+                lambda b: D.ordinates_op(1, b))(bez.ordinates[None])
     return (float(z[0, 0]), float(z[0, 1])) if found[0] else None
 
 
@@ -203,20 +209,26 @@ def clip(bez: NonParametricBezier, z1: float, z2: float) -> NonParametricBezier:
     """Restrict to [z1, z2] (project.py:146-156), de Casteljau on the GPU."""
     if not 0.0 <= z1 <= z2 <= 1.0:
         raise DomainError(f"bad clip interval [{z1}, {z2}]")
-    _need_quintic(bez)
+    quintic = _quintic(bez)
     b = np.asarray(bez.ordinates)
     if z1 >= 1.0:
         return NonParametricBezier(np.full(len(b), b[-1]))
-    return NonParametricBezier(D.restrict_ordinates(b[None], z1, z2)[0])
+    if quintic:
+        return NonParametricBezier(D.restrict_ordinates(b[None], z1, z2)[0])
+    return NonParametricBezier(D.ordinates_op(2, b[None], a=z1, c=z2)[0])
 
 
 def clip_root(bez: NonParametricBezier, tol: float = 1e-6,
               max_iterations: int = 8) -> ClipResult:
     """Bezier clipping of an eliminated piece down to width tol."""
-    _need_quintic(bez)
+    quintic = _quintic(bez)
     if max_iterations < 1:
         raise DomainError("max_iterations must be >= 1")
-    root, ok, used, widths = D.clip_root(bez.ordinates[None], tol, max_iterations)
+    if quintic:
+        root, ok, used, widths = D.clip_root(bez.ordinates[None], tol, max_iterations)
+    else:
+        root, ok, used, widths = D.ordinates_op(3, bez.ordinates[None], tol=tol,
+                                                max_iter=max_iterations)
     if not ok[0]:
         raise NoRoot("convex hull never crosses the axis")
     used = int(used[0])

@@ -18,6 +18,13 @@ Files:
   batch_mixed.npz  a mixed-degree curve set (BASELINE configs[2] shape, small
                  n): prepare_curve + project_prepared per curve, queries
                  interleaved across curves
+  anydeg.npz     the public NonParametricBezier ops (__call__,
+                 hull_x_intersections, clip, clip_root) at degrees != 5
+  verify.npz     oracle.oracle_project_batch (dense grid + ternary search,
+                 oracle.py:95-128) on three curves
+  surfdec.npz    a tensor-product surface decomposed with the reference's
+                 decompose_to_bezier along v (every row), then along u (every
+                 column of the row segments) -- pins the surface patches
 """
 
 import os
@@ -359,7 +366,108 @@ def make_batch(n_curves=16, max_control=160, per_curve=48):
     print("batch_mixed", n_curves, "curves,", seg_ofs[-1], "cubics,", N, "queries")
 
 
+def make_anydeg():
+    from splinemat.project import (NonParametricBezier, clip, clip_root,
+                                   hull_x_intersections)
+    rng = np.random.default_rng(404)
+    out = {}
+    for n in (1, 2, 3, 4, 7, 9, 15):
+        m = 300
+        B = rng.normal(size=(m, n + 1))
+        B[:40] = np.abs(B[:40])                     # one-signed: no crossing
+        B[40:60, rng.integers(0, n + 1, 20)] = 0.0  # exact zeros
+        U = rng.uniform(0, 1, m)
+        lo = rng.uniform(0, 1, m)
+        hi = rng.uniform(0, 1, m)
+        lo, hi = np.minimum(lo, hi), np.maximum(lo, hi)
+        lo[:30] = 0.0
+        hi[30:60] = 1.0
+        ev = np.array([NonParametricBezier(B[i])(U[i]) for i in range(m)])
+        hf = np.zeros(m, dtype=np.int64)
+        hz = np.zeros((m, 2))
+        for i in range(m):
+            r = hull_x_intersections(NonParametricBezier(B[i]))
+            if r is not None:
+                hf[i] = 1
+                hz[i] = r
+        cl = np.array([clip(NonParametricBezier(B[i]), lo[i], hi[i]).ordinates
+                       for i in range(m)])
+        rs = np.array([_kernels._restrict_ordinates(B[i], lo[i], hi[i]) for i in range(m)])
+        # clip_root on eliminated-piece-like (increasing through zero) ordinates
+        C = np.sort(rng.normal(size=(m, n + 1)), axis=1)
+        C[:, 0] = -np.abs(C[:, 0]) - 1e-3
+        C[:, -1] = np.abs(C[:, -1]) + 1e-3
+        cr = np.zeros(m)
+        cw = np.zeros(m)
+        ci = np.zeros(m, dtype=np.int64)
+        cc = np.zeros(m, dtype=np.int64)
+        for i in range(m):
+            res = clip_root(NonParametricBezier(C[i]), 1e-6, 8)
+            cr[i], cw[i], ci[i] = res.root, res.width, res.iterations
+            cc[i] = -1 if res.converged_at is None else res.converged_at
+        for k, v in dict(b=B, u=U, lo=lo, hi=hi, ev=ev, hf=hf, hz=hz, clip=cl, restrict=rs,
+                         cb=C, croot=cr, cwidth=cw, citer=ci, cconv=cc).items():
+            out[f"d{n}_{k}"] = v
+    np.savez_compressed(os.path.join(OUT, "anydeg.npz"), degrees=np.array([1, 2, 3, 4, 7, 9, 15]),
+                        **out)
+    print("anydeg")
+
+
+def make_verify():
+    from splinemat.oracle import oracle_project_batch
+    cases = {}
+    for name, (seed, p, n, nq, grid) in dict(cfg1=(0, 3, 64, 600, 4096),
+                                              deg7=(3, 7, 96, 400, 4096),
+                                              coarse=(5, 5, 30, 300, 257)).items():
+        rng = np.random.default_rng(seed)
+        curve = random_clamped_curve(rng, p, n, 3, uniform_knots=True)
+        q = random_queries(np.random.default_rng(seed + 100), nq, 3)
+        t, dist, res = oracle_project_batch(curve, q, grid)
+        cases.update({f"{name}_degree": p, f"{name}_knots": np.array(curve.knots.knots),
+                      f"{name}_ctrl": np.array(curve.control_points), f"{name}_queries": q,
+                      f"{name}_grid": grid, f"{name}_t": t, f"{name}_dist": dist,
+                      f"{name}_res": res})
+    np.savez_compressed(os.path.join(OUT, "verify.npz"), names=np.array(["cfg1", "deg7", "coarse"]),
+                        **cases)
+    print("verify")
+
+
+def make_surfdec():
+    """Surface patches by the reference's per-direction curve decomposition."""
+    from splinemat import BSplineCurve, decompose_to_bezier
+    out = {}
+    for name, (pu, pv, nu, nv, seed) in dict(bicubic=(3, 3, 12, 10, 1),
+                                              mixed=(3, 5, 9, 11, 2),
+                                              biquintic=(5, 5, 10, 10, 3)).items():
+        rng = np.random.default_rng(seed)
+        U = np.concatenate((np.zeros(pu + 1), np.sort(rng.uniform(0.05, 0.95, nu - pu - 1)),
+                            np.ones(pu + 1)))
+        V = np.concatenate((np.zeros(pv + 1), np.linspace(0, 1, nv - pv + 1)[1:-1],
+                            np.ones(pv + 1)))
+        P = rng.uniform(0, 1, (nu, nv, 3))
+        rows = [decompose_to_bezier(BSplineCurve(pv, V, P[i])) for i in range(nu)]
+        nsv = len(rows[0])
+        cols = None
+        patches = None
+        for js in range(nsv):
+            for l in range(pv + 1):
+                segs = decompose_to_bezier(BSplineCurve(pu, U, np.array(
+                    [rows[i][js].control_points[l] for i in range(nu)])))
+                if patches is None:
+                    patches = np.zeros((len(segs), nsv, pu + 1, pv + 1, 3))
+                    ivs = np.zeros((len(segs), nsv, 4))
+                for is_, sg in enumerate(segs):
+                    patches[is_, js, :, l] = sg.control_points
+                    ivs[is_, js] = (*sg.source_interval, *rows[0][js].source_interval)
+        out.update({f"{name}_pu": pu, f"{name}_pv": pv, f"{name}_U": U, f"{name}_V": V,
+                    f"{name}_P": P, f"{name}_patches": patches, f"{name}_iv": ivs})
+    np.savez_compressed(os.path.join(OUT, "surfdec.npz"),
+                        names=np.array(["bicubic", "mixed", "biquintic"]), **out)
+    print("surfdec")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["quartic", "ops", "projection", "prep", "batch"]
+    which = sys.argv[1:] or ["quartic", "ops", "projection", "prep", "batch", "anydeg", "verify",
+                             "surfdec"]
     for w in which:
         globals()["make_" + w]()

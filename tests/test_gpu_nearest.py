@@ -83,3 +83,31 @@ def test_nearest_planar_curves(gpu):
     preps = _curves(13, m=4, dim=2)
     q = np.random.default_rng(2).uniform(-0.2, 1.2, (5000, 2))
     _check(preps, q, project_nearest(prepare_nearest_set(preps), q))
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_nearest_vs_c_oracle_per_curve_minimum(gpu, oracle_lib, dim):
+    """Against the pinned C oracle (brute force per curve, then the minimum
+    over curves): distance within 1e-9 relative; curve id exact unless
+    another curve is within 2e-12; t within 1e-6 and the cubic index exact
+    (outside the oracle's own ties) on the winning curve."""
+    from paper_2504_11498_b200 import prepare_nearest_set, project_nearest
+    preps = _curves(31 + dim, m=6, dim=dim)
+    rng = np.random.default_rng(77)
+    q = np.concatenate([rng.uniform(-0.2, 1.2, (4000, dim)),
+                        np.concatenate([p.seam_pt[[0, -1]] for p in preps])])
+    cid, t, foot, dist, seg = project_nearest(prepare_nearest_set(preps), q)
+    outs = [oracle_lib.project_block(p.seg_pts, p.seg_ta, p.seg_tb, p.seam_t, p.seam_pt, q,
+                                     workers=8) for p in preps]
+    D = np.stack([o["dist"] for o in outs])
+    best = D.min(axis=0)
+    assert np.all(np.abs(dist - best) <= np.maximum(1e-9 * best, 1e-12))
+    srt = np.sort(D, axis=0)
+    uniq = srt[1] > srt[0] + 2e-12
+    am = D.argmin(axis=0)
+    assert np.array_equal(cid[uniq], am[uniq])
+    for c, o in enumerate(outs):
+        sel = uniq & (am == c)
+        assert np.all(np.abs(t[sel] - o["t"][sel]) <= 1e-6)
+        clear = sel & (o["tie"] == 0)
+        assert np.array_equal(seg[clear], o["seg"][clear])

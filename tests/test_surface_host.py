@@ -88,3 +88,19 @@ def test_surface_fixture_shape():
     z = s.control_points[..., 2]
     assert z.min() == 0.0 and z.max() == 1.0
     assert s.domain_u == (0.0, 1.0) and s.domain_v == (0.0, 1.0)
+
+
+def test_surface_oracle_decomposition_pinned_to_reference():
+    """The surface oracle's decomposition (oracle/surface.py) equals the
+    reference's decompose_to_bezier applied along v, then u (surfdec.npz)."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(__file__))
+    from conftest import load_golden
+    from oracle import surface as OS
+    z = load_golden("surfdec.npz")
+    for name in z["names"]:
+        g = lambda k: z[f"{name}_{k}"]  # noqa: E731
+        pts, iv = OS.decompose(int(g("pu")), int(g("pv")), g("U"), g("V"), g("P"))
+        assert np.array_equal(iv, g("iv"))
+        assert np.abs(pts - g("patches")).max() <= 1e-13
