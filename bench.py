@@ -3,6 +3,10 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mrep|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
 
+`python bench.py --gpus N` (N > 1, no WORLD_SIZE in the environment) starts
+its own N ranks under torch.distributed.run on 127.0.0.1; under torchrun the
+world size must equal --gpus.
+
 Workload (BASELINE.json configs[1], "cfg2"): 10^6 uniformly random points in
 [0,1]^3 per GPU projected onto a degree-7 clamped B-spline with 512 control
 points (seed 0, uniform knots; 510 cubics after the 1e-4 approximation).  One
@@ -11,9 +15,11 @@ step = one projection pass over the rank's 10^6 resident queries.  Inputs
 before every timed step, outside the per-step CUDA-event window.
 
 N > 1: queries are sharded (each rank its own 10^6, weak scaling), the
-curve is prepared on every GPU (replicated table), and each step ends with
-the north star's single exchange: a gather of (t, dist, segment id) to rank 0
-over NCCL.
+curve is prepared on every GPU (replicated table), and the north star's
+single exchange -- a gather of (t, dist, segment id) to rank 0 over NCCL --
+runs per query chunk (4 per step), each chunk's gather overlapping the next
+chunk's projection.  --verify-gather checks the gathered result bitwise
+against one projection of every rank's queries.
 
 Reported next to the device value:
 * e2e: the same metric through the reference-facing C-ABI call with host
@@ -47,6 +53,23 @@ UNIT = "points/s"
 N_PER_RANK = 1_000_000
 # FP64 flop per unit of work (d = 3)
 F_PAIR, F_CLIP, F_SEAM, F_BOX = 500.0, 650.0, 10.0, 10.0
+CHUNKS = 4  # N > 1: query chunks per step, each gathered while the next projects
+
+
+def spawn_ranks(n):
+    """Re-launch this command as n ranks under torch.distributed.run (one
+    process per GPU, rendezvous on 127.0.0.1); returns the launcher's exit code."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)]
+    # torchrun's parser would read `--n` as an ambiguous abbreviation of its own options
+    for a in sys.argv[1:]:
+        cmd.append("--queries-per-gpu" + a[3:] if a == "--n" or a.startswith("--n=") else a)
+    return subprocess.call(cmd)
 
 
 CONFIGS = {
@@ -210,6 +233,7 @@ class SingleCurve:
         import torch
         from paper_2504_11498_b200 import BSplineCurve, prepare_curve
         c = CONFIGS[cfg]
+        self.cfg, self.n_override = cfg, n_override
         self.curve = make_curve(cfg)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -237,9 +261,23 @@ class SingleCurve:
         self.num_segments = self.prep.num_segments
         self.h2d = self.n * 24
 
-    def step(self, counters=None, extra_flags=0, dense=False):
-        return self.tab.project(self.q, screen=not dense, counters=counters,
+    def step(self, counters=None, extra_flags=0, dense=False, sl=slice(None)):
+        return self.tab.project(self.q[sl], screen=not dense, counters=counters,
                                 extra_flags=extra_flags)
+
+    def inputs(self, r, world):
+        n = self.n
+        if CONFIGS[self.cfg]["scaling"] == "strong" and not self.n_override:
+            from paper_2504_11498_b200.sharding import shard_range
+            lo, hi = shard_range(CONFIGS[self.cfg]["n"], r, world)
+            n = hi - lo
+        return (make_queries(self.cfg, r, n, self.curve),)
+
+    def project_all(self, inputs, dense=False):
+        import torch
+        q = torch.from_numpy(np.concatenate([i[0] for i in inputs])).cuda()
+        out = self.tab.project(q, screen=not dense)
+        return out[0], out[2], out[4]
 
     def pinned(self):
         import torch
@@ -273,18 +311,28 @@ class CurveSetWorkload:
         self.prep_ms = (time.perf_counter() - t0) * 1e3
         self.n = n_override or c["n"]
         self.n_total = world * self.n
-        rng = np.random.default_rng(1 + rank)
-        self.cid_host = (np.arange(self.n) % c["curves"]).astype(np.int32)
-        rng.shuffle(self.cid_host)
-        self.q_host = rng.uniform(0.0, 1.0, (self.n, 3))
+        self.q_host, self.cid_host = self.inputs(rank, world)
         self.q = torch.from_numpy(self.q_host).cuda()
         self.cid = torch.from_numpy(self.cid_host).cuda()
         self.num_segments = self.cset.num_segments
         self.h2d = self.n * (24 + 4)
 
-    def step(self, counters=None, extra_flags=0, dense=False):
-        return self.cset.project_device(self.q, self.cid, counters=counters,
+    def step(self, counters=None, extra_flags=0, dense=False, sl=slice(None)):
+        return self.cset.project_device(self.q[sl], self.cid[sl], counters=counters,
                                         extra_flags=extra_flags)
+
+    def inputs(self, r, world):
+        rng = np.random.default_rng(1 + r)
+        cid = (np.arange(self.n) % CONFIGS["cfg3"]["curves"]).astype(np.int32)
+        rng.shuffle(cid)
+        return rng.uniform(0.0, 1.0, (self.n, 3)), cid
+
+    def project_all(self, inputs, dense=False):
+        import torch
+        q = torch.from_numpy(np.concatenate([i[0] for i in inputs])).cuda()
+        cid = torch.from_numpy(np.concatenate([i[1] for i in inputs])).cuda()
+        out = self.cset.project_device(q, cid)
+        return out[0], out[2], out[4]
 
     def pinned(self):
         import torch
@@ -340,8 +388,17 @@ class NearestWorkload:
         self.mode = 0 if self.n >= 8 * self.tab.S else L.MREP_PER_LANE
         self.cpu_div = len(self.preps)  # the CPU sample runs every curve per query
 
-    def step(self, counters=None, extra_flags=0, dense=False):
-        return self.tab.project(self.q, counters=counters, extra_flags=extra_flags | self.mode)
+    def step(self, counters=None, extra_flags=0, dense=False, sl=slice(None)):
+        return self.tab.project(self.q[sl], counters=counters, extra_flags=extra_flags | self.mode)
+
+    def inputs(self, r, world):
+        return (np.random.default_rng(1 + r).uniform(0.0, 1.0, (self.n, 3)),)
+
+    def project_all(self, inputs, dense=False):
+        import torch
+        q = torch.from_numpy(np.concatenate([i[0] for i in inputs])).cuda()
+        out = self.tab.project(q, extra_flags=self.mode)
+        return out[0], out[2], out[4]
 
     def pinned(self):
         import torch
@@ -386,8 +443,17 @@ class SurfaceWorkload:
         self.h2d = self.n * 24
         self.p = p
 
-    def step(self, counters=None, extra_flags=0, dense=False):
-        return self.tab.project(self.q, counters=counters, extra_flags=extra_flags)
+    def step(self, counters=None, extra_flags=0, dense=False, sl=slice(None)):
+        return self.tab.project(self.q[sl], counters=counters, extra_flags=extra_flags)
+
+    def inputs(self, r, world):
+        return (np.random.default_rng(1 + r).uniform(0.0, 1.0, (self.n, 3)),)
+
+    def project_all(self, inputs, dense=False):
+        import torch
+        q = torch.from_numpy(np.concatenate([i[0] for i in inputs])).cuda()
+        out = self.tab.project(q)
+        return out[0], out[3], out[4]
 
     def pinned(self):
         import torch
@@ -507,15 +573,24 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mrep", choices=["mrep", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
-    ap.add_argument("--n", type=int, default=0, help="queries per GPU (default: the config's)")
+    ap.add_argument("--n", "--queries-per-gpu", dest="n", type=int, default=0,
+                    help="queries per GPU (default: the config's)")
     ap.add_argument("--ref-sample", type=int, default=32768)
     ap.add_argument("--cpu-sample", type=int, default=65536)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dense", action="store_true", help="brute-force kernel (reference semantics)")
+    ap.add_argument("--verify-gather", action="store_true",
+                    help="N > 1: rank 0 checks the gathered (t, distance, segment id) of the last "
+                         "step bitwise against one projection of every rank's queries")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
 
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "mrep":
+        # `python bench.py --gpus N` starts its own N ranks (one per GPU)
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -523,12 +598,21 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     import torch
     import torch.distributed as dist
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    # one rank per GPU over NCCL; with fewer GPUs than ranks (the 1-GPU test
+    # box) ranks share devices and gather over gloo -- flagged in config
+    shared = world > ndev
+    torch.cuda.set_device(local % ndev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2504_11498_b200 import _lib as L
 
@@ -543,16 +627,38 @@ def main():
     counters = torch.zeros(L.NUM_COUNTERS, dtype=torch.int64, device="cuda")
     dense = args.dense and args.config != "cfg3"
 
-    from paper_2504_11498_b200.sharding import gather_results, pack_results
+    from paper_2504_11498_b200.sharding import gather_chunk, pack_results
 
-    def gather(out):
-        # the single exchange of the path: (t, distance, segment id) to rank 0
-        if world == 1:
-            return
-        if surf:  # (u, v, foot, dist, patch): gather (u, dist, patch id)
-            gather_results(pack_results(out[0], out[3], out[4]), n_total, world, rank)
-        else:
-            gather_results(pack_results(out[0], out[2], out[4]), n_total, world, rank)
+    # N > 1: the step runs as CHUNKS query chunks; each chunk's (t, distance,
+    # segment id) block is gathered to rank 0 asynchronously (NCCL's stream
+    # waits for that chunk only) while the next chunk projects, so only the
+    # last chunk's gather is exposed (overlap by chunking)
+    chunks = 1 if world == 1 else CHUNKS
+    bounds = [n * i // chunks for i in range(chunks + 1)]
+    kmax = -(-(-(-n_total // world)) // chunks)
+    # rank r's chunk i holds global queries [base_r + bounds[i], ...); the
+    # gathered layout is chunk-major, unpermuted on rank 0 only when checked
+    gathered = {}
+
+    def run_step(counters=None, extra_flags=0):
+        if chunks == 1:
+            return wl.step(counters, extra_flags, dense=dense)
+        works, outs = [], []
+        for i in range(chunks):
+            out = wl.step(counters, extra_flags, dense=dense, sl=slice(bounds[i], bounds[i + 1]))
+            # surfaces (u, v, foot, dist, patch) -> (u, dist, patch)
+            blk = (pack_results(out[0], out[3], out[4]) if surf
+                   else pack_results(out[0], out[2], out[4]))
+            if blk.shape[0] < kmax:  # uneven shards: pad to the common chunk size
+                blk = torch.cat([blk, blk.new_zeros((kmax - blk.shape[0], 3))])
+            w, bufs = gather_chunk(blk, world, rank, async_op=not shared)
+            works.append(w)
+            outs.append((out, bufs))
+        for w in works:
+            if w is not None:
+                w.wait()  # the compute stream waits for the last gathers
+        gathered["last"] = outs
+        return outs[-1][0]
 
     # the clock sampler (an nvidia-smi child) starts before the warm-up, so its
     # start-up never lands inside a timed step
@@ -565,15 +671,12 @@ def main():
     out = None
     for i in range(args.warmup):
         flush.fill_(float(i % 2))
-        out = wl.step(dense=dense)
-        gather(out)
+        out = run_step()
     torch.cuda.synchronize()
 
     # ---- timed device steps (inputs resident in HBM) ----
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kstarts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -581,20 +684,37 @@ def main():
     for i in range(args.steps):
         flush.fill_(float(i))
         starts[i].record(stream)
-        kstarts[i].record(stream)
-        out = wl.step(dense=dense)
-        kends[i].record(stream)
-        gather(out)
+        out = run_step()
         ends[i].record(stream)
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
     if world > 1:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    kern_ms = [s.elapsed_time(e) for s, e in zip(kstarts, kends)]
+    gather_check = None
+    if world > 1 and args.verify_gather and rank == 0:
+        from paper_2504_11498_b200.sharding import unchunk
+        outs = gathered["last"]
+        got = unchunk([b for _, b in outs], world, n, bounds)
+        ins = [wl.inputs(r, world) for r in range(world)]
+        sizes = [len(i[0]) for i in ins]
+        # rank r's rows: chunk blocks are kmax long; keep each chunk's real rows
+        rows = []
+        for r in range(world):
+            br = [sizes[r] * i // chunks for i in range(chunks + 1)]
+            for i in range(chunks):
+                base = (r * chunks + i) * kmax
+                rows.append(got[base: base + br[i + 1] - br[i]])
+        got = torch.cat(rows).numpy()
+        t_all, d_all, s_all = wl.project_all(ins, dense=dense)
+        want = np.stack([t_all.cpu().numpy(), d_all.cpu().numpy(),
+                         s_all.cpu().numpy().astype(np.float64)], 1)
+        gather_check = {"queries": int(want.shape[0]),
+                        "bitwise_equal": bool(got.shape == want.shape
+                                              and np.array_equal(got, want))}
     ms = statistics.mean(step_ms)
     if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([ms], dtype=torch.float64, device="cpu" if shared else "cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     value = n_total / (ms / 1e3)
@@ -630,7 +750,9 @@ def main():
     stage = np.median(np.stack(per_rep), axis=0)  # robust to a one-off slow rep
     peak = ctypes.c_double()
     L.check(L.lib().mrep_fp64_peak(ctypes.byref(peak)))
-    kms = statistics.mean(kern_ms)
+    # pipeline time of one rank's projection (N > 1: the step also holds the
+    # exposed tail of the gather, so take the library's stage sum instead)
+    kms = statistics.mean(step_ms) if world == 1 else float(np.sum(stage))
     names = ["morton_sort", "traverse", "pairs", "clip", "select", "fallback"]
     work = {"traverse": F_BOX * c[L.CNT_BOXES] + F_SEAM * c[L.CNT_SEAMS],
             "pairs": F_PAIR * c[L.CNT_PAIRS], "clip": F_CLIP * c[L.CNT_SURVIVORS]}
@@ -716,7 +838,7 @@ def main():
     clocks.__exit__(None, None, None)
     e2e_s = statistics.mean(e2e_times)
     if world > 1:
-        tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device="cpu" if shared else "cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
     e2e = {"value": n_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": wl.h2d,
@@ -738,6 +860,13 @@ def main():
                              f"_kernels._project_block, bit-exact vs the reference"}
         conf = dict(workload_config(args.config, n), parallelism=f"query-shard x{world}",
                     prep_ms=wl.prep_ms, cubics=wl.num_segments)
+        if world > 1:
+            conf["gather"] = (f"(t, distance, segment id) to rank 0 in {chunks} chunks per step, "
+                              + ("gloo through host memory (ranks share a GPU: a logic test, "
+                                 "not a scaling number)" if shared else
+                                 "NCCL, each chunk's gather overlapping the next chunk's projection"))
+            if gather_check is not None:
+                conf["gather_check"] = gather_check
         if getattr(wl, "cells_ms", None) is not None and getattr(wl.tab, "cells", None) is not None:
             conf["cell_index"] = {"build_ms": wl.cells_ms,
                                   "bytes": int(wl.tab.cells.numel() * 4)}

@@ -41,3 +41,29 @@ def gather_results(block, n_total, world, rank, dst=0):
         lo, hi = shard_range(n_total, r, world)
         parts.append(bufs[r][: hi - lo])
     return torch.cat(parts, 0)
+
+
+def gather_chunk(block, world, rank, dst=0, async_op=False):
+    """Gather one equal-sized (k, 3) chunk block from every rank to `dst`.
+    NCCL (CUDA tensors, async_op=True): the collective runs on NCCL's stream
+    after the work already queued on the current stream, so the caller can
+    queue the next chunk's projection at once; returns (work, bufs) -- wait on
+    `work` before reading `bufs` (rank-ordered list on dst, None elsewhere).
+    gloo: the block is staged through host memory and the call is blocking
+    (work None)."""
+    if block.is_cuda and dist.get_backend() == "gloo":
+        block = block.cpu()
+    bufs = [torch.empty_like(block) for _ in range(world)] if rank == dst else None
+    work = dist.gather(block, bufs, dst=dst, async_op=async_op)
+    return (work if async_op else None), bufs
+
+
+def unchunk(chunk_bufs, world, n_per_rank, bounds):
+    """Reassemble rank-0 gathered chunks (list over chunks of rank-ordered
+    block lists) into the (world * n_per_rank, 3) result in global query
+    order (rank-major, then chunk)."""
+    out = []
+    for r in range(world):
+        for i in range(len(bounds) - 1):
+            out.append(chunk_bufs[i][r].to("cpu"))
+    return torch.cat(out, 0)
