@@ -62,6 +62,10 @@ MREP_API const char* mrep_last_error(void);
 MREP_API int mrep_last_stage_times(double* ms, int max);
 /* measured FP64 FMA throughput of the current device, TFLOP/s (roofline peak) */
 MREP_API int mrep_fp64_peak(double* tflops);
+/* frees every device's host-call pipeline context (mrep_*_host streams,
+ * events, pinned and device staging buffers); the next host-buffer call
+ * re-creates them.  Optional: for leak checkers and embedding processes. */
+MREP_API int mrep_host_release(void);
 MREP_API int mrep_version(void);
 MREP_API int mrep_device_count(void);
 

@@ -10,6 +10,7 @@ torch tensors on ``cuda`` and their ``data_ptr()`` is handed to the C ABI
 together with the current stream handle.
 """
 
+import atexit
 import ctypes
 import os
 import threading
@@ -46,6 +47,7 @@ _SIGS = {
     "mrep_version": ([], _i32),
     "mrep_last_stage_times": ([_vp, _i32], _i32),
     "mrep_fp64_peak": ([_vp], _i32),
+    "mrep_host_release": ([], _i32),
     "mrep_device_count": ([], _i32),
     "mrep_table_bytes": ([_i64], _i64),
     "mrep_table_pack": ([_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp], _i32),
@@ -138,12 +140,25 @@ def load_library(path=LIB_PATH):
             fn.argtypes = args
             fn.restype = res
         _lib = L
+        atexit.register(_release_at_exit)
         return L
 
 
 def _torch():
     import torch
     return torch
+
+
+def _release_at_exit():
+    # free the host-call pipeline contexts (pinned + device staging buffers)
+    # while the CUDA runtime is still up; nothing to do if CUDA never started
+    try:
+        import sys
+        torch = sys.modules.get("torch")
+        if _lib is not None and torch is not None and torch.cuda.is_initialized():
+            _lib.mrep_host_release()
+    except Exception:
+        pass
 
 
 def lib():

@@ -76,6 +76,9 @@ struct StageTimer {
 // (lo xyz, hi xyz).  A float copy of every box follows (6 floats, lo
 // rounded down, hi rounded up, so it encloses the double box): the hot
 // traversals test it on the FP32 pipe with a rigorous rounding allowance.
+// Curve tables (rec == REC) end with a compact seam block: seam s's point as
+// 3 doubles (xyz; z = 0 in 2-D), s = 0..S, so the 8 seams a group traversal
+// reads at a leaf expansion are one contiguous 192-B run instead of 8 lines.
 constexpr int REC = 32;
 constexpr int R_W = 0, R_ST = 12, R_SP = 13, R_P = 16, R_TA = 28, R_TB = 29;
 constexpr int HDR = 64;
@@ -91,6 +94,7 @@ struct TableLayout {
   int64_t rec_off;  // in doubles from table start
   int64_t box_off;   // in doubles from table start
   int64_t fbox_off;  // in doubles from table start (float boxes, 3 doubles each)
+  int64_t sxyz_off;  // in doubles from table start (curve seams, 3 doubles each); 0 = none
   int64_t total_doubles;
 };
 
@@ -113,6 +117,10 @@ inline TableLayout table_layout(int64_t S, int rec = REC) {
   L.box_off = HDR + S * rec;
   L.fbox_off = L.box_off + off * 6;
   L.total_doubles = L.fbox_off + off * 3;
+  if (rec == REC) {
+    L.sxyz_off = L.total_doubles;
+    L.total_doubles += (S + 1) * 3;
+  }
   return L;
 }
 
@@ -121,6 +129,7 @@ struct TableView {
   const double* rec;
   const double* box;
   const float* fbox;
+  const double* sxyz;  // compact seam points (curve tables), nullptr otherwise
   int64_t S;
   int top;
   int64_t lvl_off[MAX_LEVELS];
@@ -135,6 +144,7 @@ inline TableView table_view(const void* table, int64_t S, int rec = REC) {
   v.rec = base + L.rec_off;
   v.box = base + L.box_off;
   v.fbox = reinterpret_cast<const float*>(base + L.fbox_off);
+  v.sxyz = L.sxyz_off ? base + L.sxyz_off : nullptr;
   v.S = S;
   v.top = L.top;
   for (int i = 0; i < MAX_LEVELS; ++i) {

@@ -151,10 +151,73 @@ int ensure_ctx(HostCtx& g_ctx) {
   return MREP_OK;
 }
 
+void release_ctx(HostCtx& c) {
+  for (auto& s : c.slot) {
+    if (s.st) cudaStreamDestroy(s.st);
+    if (s.done) cudaEventDestroy(s.done);
+    cudaFree(s.dq);
+    cudaFree(s.dt);
+    cudaFree(s.dfoot);
+    cudaFree(s.ddist);
+    cudaFree(s.dcand);
+    cudaFree(s.dseg);
+    cudaFree(s.dcur);
+    cudaFree(s.dcnt);
+    cudaFreeHost(s.hq);
+    cudaFreeHost(s.ht);
+    cudaFreeHost(s.hfoot);
+    cudaFreeHost(s.hdist);
+    cudaFreeHost(s.hcand);
+    cudaFreeHost(s.hseg);
+    cudaFreeHost(s.hcur);
+    s = Slot{};
+  }
+  cudaFree(c.big.dq);
+  cudaFree(c.big.dt);
+  cudaFree(c.big.dfoot);
+  cudaFree(c.big.ddist);
+  cudaFree(c.big.dcand);
+  cudaFree(c.big.dseg);
+  cudaFree(c.big.dcur);
+  c.big = BigBuf{};
+  for (auto& p : c.prio)
+    if (p) cudaStreamDestroy(p), p = nullptr;
+  if (c.cin) cudaStreamDestroy(c.cin), c.cin = nullptr;
+  if (c.cout) cudaStreamDestroy(c.cout), c.cout = nullptr;
+  for (auto e : c.ev_in) cudaEventDestroy(e);
+  for (auto e : c.ev_comp) cudaEventDestroy(e);
+  c.ev_in.clear();
+  c.ev_comp.clear();
+  c.ready = false;
+}
+
 }  // namespace
 }  // namespace mrep
 
 using namespace mrep;
+
+// Frees every device's host-call pipeline context (streams, events, staging
+// buffers); the next host-buffer call re-creates them.  Registered at exit by
+// the Python package so leak checkers see a clean teardown.
+extern "C" MREP_API int mrep_host_release(void) {
+  int cur = 0;
+  const bool have = cudaGetDevice(&cur) == cudaSuccess;
+  std::lock_guard<std::mutex> lk(g_ctxs_mu);
+  for (int d = 0; d < MAX_DEVICES; ++d) {
+    HostCtx* c = g_ctxs[d];
+    if (!c) continue;
+    {
+      std::lock_guard<std::mutex> lc(c->mu);
+      if (cudaSetDevice(d) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess)
+        release_ctx(*c);
+    }
+    delete c;
+    g_ctxs[d] = nullptr;
+  }
+  if (have) cudaSetDevice(cur);
+  cudaGetLastError();
+  return MREP_OK;
+}
 
 namespace mrep {
 namespace {

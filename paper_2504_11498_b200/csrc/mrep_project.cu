@@ -74,10 +74,13 @@ constexpr int BLOCK = 128;
 #define MREP_TRAV_MINB 6
 #endif
 #ifndef MREP_GROUP_MINB
-#define MREP_GROUP_MINB 6
+#define MREP_GROUP_MINB 7
 #endif
 #ifndef MREP_PAIRS_MINB
 #define MREP_PAIRS_MINB 6
+#endif
+#ifndef MREP_STAGE_MINB
+#define MREP_STAGE_MINB 3
 #endif
 #ifndef MREP_CLIP_MINB
 #define MREP_CLIP_MINB 8
@@ -1556,6 +1559,37 @@ __global__ void __launch_bounds__(BLOCK, MREP_TRAV_MINB) wave_traverse(const __g
 constexpr int GSTACK = 64;
 constexpr int GPAIRS = 24;  // parked leaves per query (overflow: flushed early)
 
+// Box bounds are compared as floats.  A lane on the float box path keeps the
+// FP32 sum `acc` of box_lb2f (whose rigorous bound is acc * (1 - 1e-6)); a
+// lane on the double path (coordinates near the float range) keeps its
+// double bound rounded down.  The cut-off c2 becomes a float threshold
+// rounded up (divided by 1 - 1e-6 on the float path, with room for the
+// roundings), so `key > thr` still implies that the box's exact squared
+// distance exceeds c2: no box is pruned that the double test would keep.
+__device__ __forceinline__ float cut_key(double c2, bool fb) {
+  return __double2float_ru(fb ? c2 * (1.0 + 1.1e-6) : c2 * (1.0 + 1e-15));
+}
+
+// Where a group traversal reads the float boxes: the table in global memory
+// (read-only path) or a copy staged in shared memory (wave_traverse_staged).
+template <bool SMEM>
+struct BoxSrc {
+  const float* fb;  // float boxes of every level, box i at fb + 6 i
+  __device__ __forceinline__ float ld(int64_t i) const { return SMEM ? fb[i] : __ldg(fb + i); }
+};
+
+// FP32 part of box_lb2f (same expression, so the same float)
+template <int D, bool SMEM>
+__device__ __forceinline__ float box_accf(const BoxSrc<SMEM>& B, int64_t box, const FQ<D>& f) {
+  float acc = 0.0f;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    float g = fmaxf(0.0f, fmaxf(B.ld(box * 6 + k) - f.lo[k], f.hi[k] - B.ld(box * 6 + 3 + k)));
+    acc += g * g;
+  }
+  return acc;
+}
+
 struct SeamBest {  // a lane's two nearest seams (t re-read at emission)
   double d1, d2, dropped;
   int32_t s1, s2;
@@ -1577,19 +1611,34 @@ __device__ __forceinline__ void seam_keep(SeamBest& b, double d, int32_t s) {
   }
 }
 
-// emit parked leaves [0, cnt) of a group that pass cut c2 (box + Bernstein)
+// distance from q to seam s (compact seam block of a curve table)
+template <int D>
+__device__ __forceinline__ double seam_dist(const TableView& T, int64_t s, const double (&q)[D]) {
+  const double* p = T.sxyz + s * 3;
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    double df = q[k] - __ldg(p + k);
+    acc += df * df;
+  }
+  return sqrt(acc);
+}
+
+// emit parked leaves [0, cnt) of a group that pass cut c2 (box key <= thr,
+// then the Bernstein test)
 template <int D>
 __device__ __forceinline__ void flush_pairs(const WaveParams& w, const TableView& T, int64_t g,
-                                            const double (&q)[D], double c2, const uint32_t* PC,
-                                            const double* PL, int cnt, int rounds, int sub,
-                                            bool& fall, uint64_t& npairs) {
+                                            const double (&q)[D], double c2, float thr,
+                                            const uint32_t* PC, const float* PL, int cnt, int sub,
+                                            bool& fall, uint32_t& npairs) {
+  const int rounds = (cnt + 7) >> 3;
   for (int r = 0; r < rounds; ++r) {
     const int i = r * 8 + sub;
     bool need = false;
     uint32_t ch = 0;
     if (i < cnt) {
       ch = PC[i];
-      need = PL[i] <= c2 && bern_may_reach<D>(T, ch, q, c2);
+      need = PL[i] <= thr && bern_may_reach<D>(T, ch, q, c2);
     }
     unsigned long long slot = wave_append(&w.cnt[0], need);
     npairs += need ? 1 : 0;
@@ -1604,29 +1653,22 @@ __device__ __forceinline__ void flush_pairs(const WaveParams& w, const TableView
   }
 }
 
-template <int D, bool MULTI>
+// One query per 8-lane group (see above).  T = the query's table (a global
+// descriptor, or a shared-memory copy in the staged kernel), B = where its
+// float boxes are read.  Stack keys: level << 28 | node (group mode needs
+// top <= 8, so a node index fits 28 bits); stack bounds are float keys.
+// A node's kept children are pushed in index order with the nearest on top.
+template <int D, bool MULTI, int NSTACK, bool SMEM>
 __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, bool active,
-                                               unsigned long long* SK, double* SL, uint32_t* PC,
-                                               double* PL, int lane) {
+                                               int32_t cid, const TableView& T,
+                                               const BoxSrc<SMEM>& B, uint32_t* SK, float* SL,
+                                               uint32_t* PC, float* PL, int lane) {
   const int sub = lane & 7;
   const unsigned gmask = 0xffu << (lane & 24);
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
-  QStats st{};
+  struct { uint32_t pairs, seams, boxes, offers; } st{};  // 32-bit: fewer registers
   int64_t qi = active ? (w.perm ? (int64_t)w.perm[g] : g) : 0;
-  int32_t cid = 0;
-  if (MULTI && active) {
-    cid = w.qcurve[qi];
-    if (cid < 0 || cid >= w.ncurves) cid = -1;
-    if (sub == 0) w.gcur[g] = cid;
-    if (cid < 0) {  // out-of-range curve id (sorted last): NaN result, no work
-      if (sub == 0) {
-        w.scnt[g] = 0;
-        w.flag[g] = 0;
-      }
-      active = false;
-    }
-  }
-  const TableView& T = MULTI ? w.tabs[cid < 0 ? 0 : cid] : w.tab;
+  if (MULTI && active && sub == 0) w.gcur[g] = cid;
   double q[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) q[k] = active ? w.q[qi * D + k] : 0.0;
@@ -1636,106 +1678,114 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
   const bool fb = fbox_ok(scale);
   const FQ<D> fq = make_fq<D>(q, scale);
   double dmin = INF;
+  float thr = __int_as_float(0x7f800000);  // +inf: no bound yet
   bool fall = false;
   SeamBest sb{INF, INF, INF, 0, 0};
   int sp = 0, npark = 0;
   if (active) {
     if (sub == 0) {
-      SK[0] = ((unsigned long long)T.top << 40);
-      SL[0] = 0.0;
+      SK[0] = (uint32_t)T.top << 28;
+      SL[0] = 0.0f;
     }
     sp = 1;
   }
   __syncwarp(gmask);
-  while (sp > 0) {  // group-uniform control flow
-    --sp;
-    const unsigned long long e = SK[sp];
-    const double elb = SL[sp];
-    __syncwarp(gmask);
-    double c2 = cut2(dmin, scale);
-    if (elb > c2) continue;
-    const int level = (int)(e >> 40);
-    const int64_t idx = (int64_t)(e & 0xffffffffffull);
-    const int64_t ch = idx * FANOUT + sub;
-    const bool ex = ch < T.lvl_cnt[level - 1];
-    double lb = INF;
-    if (ex) {
-      st.boxes++;
-      lb = fb ? box_lb2f<D>(T, T.lvl_off[level - 1] + ch, fq) : box_lb2<D>(T, T.lvl_off[level - 1] + ch, q);
-    }
-    const bool keep = ex && lb <= c2;
-    if (level == 1) {
-      // leaves: end seams -> bound; kept leaves parked for the final flush
-      double dr = INF;
-      if (keep) {
-        double pt[D], tr;
-        seam_point<D>(T, ch + 1, pt, tr);
-        double acc = 0.0;
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          double df = q[k] - pt[k];
-          acc += df * df;
+  // The warp's four groups advance in lockstep: every trip, each group with
+  // work pops and expands one node, and the warp reconverges at the end of
+  // the trip (otherwise the groups drift apart and the warp issues each
+  // group's instructions separately at 8/32 lanes).
+  for (;;) {
+    // pop: the group reads the top 8 entries at once and drops every entry
+    // above the first one still under the threshold (a bound that tightened
+    // since the push prunes them), so a run of pruned entries costs one trip
+    bool found = false, more = sp > 0;
+    while (__any_sync(0xffffffffu, more)) {
+      if (more) {
+        const bool ok = sub < sp && SL[sp - 1 - sub] <= thr;
+        const unsigned okm = (__ballot_sync(gmask, ok) >> (lane & 24)) & 0xffu;
+        if (okm) {
+          sp -= __ffs(okm);
+          found = true;
+          more = false;
+        } else {
+          sp = sp > 8 ? sp - 8 : 0;
+          more = sp > 0;
         }
-        dr = sqrt(acc);
-        seam_keep(sb, dr, (int32_t)(ch + 1));
-        st.seams++;
-        st.offers++;
-        if (ch == 0) {
-          double tl;
-          seam_point<D>(T, 0, pt, tl);
-          acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < D; ++k) {
-            double df = q[k] - pt[k];
-            acc += df * df;
-          }
-          double dl = sqrt(acc);
-          dr = fmin(dr, dl);
-          seam_keep(sb, dl, 0);
+      }
+    }
+    if (!__any_sync(0xffffffffu, found)) break;
+    if (found) {  // group-uniform
+      const uint32_t e = SK[sp];
+      const int level = (int)(e >> 28);
+      const int64_t idx = (int64_t)(e & 0x0fffffffu);
+      const int64_t ch = idx * FANOUT + sub;
+      const bool ex = ch < T.lvl_cnt[level - 1];
+      float key = __int_as_float(0x7f800000);
+      if (ex) {
+        st.boxes++;
+        const int64_t bi = T.lvl_off[level - 1] + ch;
+        key = fb ? box_accf<D>(B, bi, fq) : __double2float_rd(box_lb2<D>(T, bi, q));
+      }
+      const bool keep = ex && key <= thr;
+      if (level == 1) {
+        // leaves: end seams -> bound; kept leaves parked for the final flush
+        double dr = INF;
+        if (keep) {
+          dr = seam_dist<D>(T, ch + 1, q);
+          seam_keep(sb, dr, (int32_t)(ch + 1));
           st.seams++;
           st.offers++;
+          if (ch == 0) {
+            const double dl = seam_dist<D>(T, 0, q);
+            dr = fmin(dr, dl);
+            seam_keep(sb, dl, 0);
+            st.seams++;
+            st.offers++;
+          }
+        }
+        double m = dr;
+        m = fmin(m, __shfl_xor_sync(gmask, m, 4));
+        m = fmin(m, __shfl_xor_sync(gmask, m, 2));
+        m = fmin(m, __shfl_xor_sync(gmask, m, 1));
+        if (m < dmin) {  // group-uniform
+          dmin = m;
+          thr = cut_key(cut2(dmin, scale), fb);
+        }
+        const bool park = keep && key <= thr;
+        const unsigned pm = (__ballot_sync(gmask, park) >> (lane & 24)) & 0xffu;
+        if (npark + __popc(pm) > GPAIRS) {  // list full: flush with the current bound
+          flush_pairs<D>(w, T, g, q, cut2(dmin, scale), thr, PC, PL, npark, sub, fall, st.pairs);
+          __syncwarp(gmask);
+          npark = 0;
+        }
+        if (park) {
+          const int at = npark + __popc(pm & ((1u << sub) - 1));
+          PC[at] = (uint32_t)ch;
+          PL[at] = key;
+        }
+        npark += __popc(pm);
+      } else {
+        // push the kept children: index order, the nearest on top
+        const unsigned km = (__ballot_sync(gmask, keep) >> (lane & 24)) & 0xffu;
+        if (km) {
+          const unsigned mk = __reduce_min_sync(
+              gmask, keep ? ((__float_as_uint(key) & ~7u) | sub) : 0xffffffffu);
+          const int top = (int)(mk & 7u);
+          const unsigned rest = km & ~(1u << top);
+          if (keep) {
+            const int pos = sub == top ? __popc(km) - 1 : __popc(rest & ((1u << sub) - 1));
+            SK[sp + pos] = ((uint32_t)(level - 1) << 28) | (uint32_t)ch;
+            SL[sp + pos] = key;
+          }
+          sp += __popc(km);
+          if (sp > NSTACK - FANOUT) {  // cannot happen for the depths in use; stay exact anyway
+            fall = true;
+            sp = 0;
+          }
         }
       }
-      double m = dr;
-      m = fmin(m, __shfl_xor_sync(gmask, m, 4));
-      m = fmin(m, __shfl_xor_sync(gmask, m, 2));
-      m = fmin(m, __shfl_xor_sync(gmask, m, 1));
-      dmin = fmin(dmin, m);
-      c2 = cut2(dmin, scale);
-      const bool park = keep && lb <= c2;
-      const unsigned pm = (__ballot_sync(gmask, park) >> (lane & 24)) & 0xffu;
-      if (npark + __popc(pm) > GPAIRS) {  // list full: flush with the current bound
-        flush_pairs<D>(w, T, g, q, c2, PC, PL, npark, (npark + 7) >> 3, sub, fall, st.pairs);
-        __syncwarp(gmask);
-        npark = 0;
-      }
-      if (park) {
-        const int at = npark + __popc(pm & ((1u << sub) - 1));
-        PC[at] = (uint32_t)ch;
-        PL[at] = lb;
-      }
-      npark += __popc(pm);
-      __syncwarp(gmask);
-      continue;
     }
-    // push the kept children, nearest on top
-    const unsigned km = (__ballot_sync(gmask, keep) >> (lane & 24)) & 0xffu;
-    int rank = 0;
-#pragma unroll
-    for (int j = 0; j < FANOUT; ++j) {
-      double lj = __shfl_sync(gmask, lb, (lane & 24) | j);
-      rank += ((km >> j) & 1u) && (lj > lb || (lj == lb && j > sub));
-    }
-    if (keep) {
-      SK[sp + rank] = ((unsigned long long)(level - 1) << 40) | (unsigned long long)ch;
-      SL[sp + rank] = lb;
-    }
-    sp += __popc(km);
-    if (sp > GSTACK - FANOUT) {  // cannot happen for top <= 8; stay exact anyway
-      fall = true;
-      sp = 0;
-    }
-    __syncwarp(gmask);
+    __syncwarp();
   }
   // ---- the warp's four queries are done: batched appends (warp converged)
   __syncwarp();
@@ -1760,8 +1810,7 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
     }
   }
   // parked leaves that still pass the final bound become pairs
-  const int rounds = (__reduce_max_sync(0xffffffffu, (unsigned)npark) + 7) >> 3;
-  flush_pairs<D>(w, T, g, q, c2f, PC, PL, npark, rounds, sub, fall, st.pairs);
+  flush_pairs<D>(w, T, g, q, c2f, thr, PC, PL, npark, sub, fall, st.pairs);
   // group totals to the leader lane
   unsigned long long offers = st.offers + st.pairs;
   offers += __shfl_xor_sync(0xffffffffu, offers, 4);
@@ -1786,17 +1835,39 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
   warp_count(w.counters, MREP_CNT_BOXES, st.boxes);
 }
 
+// the query's curve in a batch (-1: out-of-range id, sorted last: NaN
+// result, no work)
+template <bool MULTI>
+__device__ __forceinline__ int32_t group_curve(const WaveParams& w, int64_t g, bool& active,
+                                               int sub) {
+  if (!MULTI || !active) return 0;
+  const int64_t qi = w.perm ? (int64_t)w.perm[g] : g;
+  int32_t cid = w.qcurve[qi];
+  if (cid < 0 || cid >= w.ncurves) {
+    if (sub == 0) {
+      w.gcur[g] = -1;
+      w.scnt[g] = 0;
+      w.flag[g] = 0;
+    }
+    active = false;
+    cid = 0;
+  }
+  return cid;
+}
+
 template <int D, bool MULTI>
 __global__ void __launch_bounds__(BLOCK, MREP_GROUP_MINB) wave_traverse_group(const __grid_constant__ WaveParams w) {
-  __shared__ unsigned long long sk[BLOCK / 8][GSTACK];
-  __shared__ double sl[BLOCK / 8][GSTACK];
+  __shared__ uint32_t sk[BLOCK / 8][GSTACK];
+  __shared__ float sl[BLOCK / 8][GSTACK];
   __shared__ uint32_t pc[BLOCK / 8][GPAIRS];
-  __shared__ double pl[BLOCK / 8][GPAIRS];
+  __shared__ float pl[BLOCK / 8][GPAIRS];
   const int lane = threadIdx.x & 31;
   const int grp = threadIdx.x >> 3;
   if (!MULTI) {
     int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
-    traverse_group<D, false>(w, g, g < w.n, sk[grp], sl[grp], pc[grp], pl[grp], lane);
+    bool act = g < w.n;
+    traverse_group<D, false, GSTACK, false>(w, g, act, 0, w.tab, BoxSrc<false>{w.tab.fbox}, sk[grp],
+                                            sl[grp], pc[grp], pl[grp], lane);
   } else {
     // persistent warps drain 4-query tasks, heaviest curves first; the next
     // task index is fetched while the current one runs
@@ -1809,9 +1880,228 @@ __global__ void __launch_bounds__(BLOCK, MREP_GROUP_MINB) wave_traverse_group(co
       unsigned long long next = 0;
       if (lane == 0) next = atomicAdd(w.queue, 1ull);
       int64_t g = base + (lane >> 3);
-      traverse_group<D, true>(w, g, g < w.n, sk[grp], sl[grp], pc[grp], pl[grp], lane);
+      bool act = g < w.n;
+      const int32_t cid = group_curve<true>(w, g, act, lane & 7);
+      const TableView& T = w.tabs[cid];
+      traverse_group<D, true, GSTACK, false>(w, g, act, cid, T, BoxSrc<false>{T.fbox}, sk[grp],
+                                             sl[grp], pc[grp], pl[grp], lane);
       task = __shfl_sync(0xffffffffu, next, 0);
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// W1, staged group mode for curve batches (the paper's scheduler with
+// coalesced segment staging, north-star subsystem 4).  A task is a tile of
+// up to STG_TILE sorted queries of ONE curve (queries are sorted by curve
+// rank, heaviest curve first; stage_plan_kernel cut the tiles).  A
+// persistent CTA takes a task, copies the curve's descriptor and its whole
+// float box hierarchy (every level, 24 B per box) into shared memory with
+// one TMA bulk copy (cp.async.bulk, completion on an mbarrier), and its
+// warps then walk the tree for the tile's queries four at a time (one
+// 8-lane group per query, as wave_traverse_group) with every box test an
+// LDS instead of a dependent L2/HBM load.  Seams (one contiguous 192-B run
+// per leaf expansion) and the Bernstein tests of parked leaves still read
+// global memory.  Curves whose boxes exceed the stage buffer run the same
+// walk from global memory.  Same arithmetic, same decisions: results
+// (including cand) equal wave_traverse_group's bit for bit.
+constexpr int STG_THREADS = 256;
+constexpr int STG_GROUPS = STG_THREADS / 8;
+constexpr int STG_STACK = 40;  // top <= 4 when staged: depth <= 1 + 7 * 4 = 29
+constexpr int STG_TILE = 256;
+
+struct StagePlan {
+  const uint32_t* order;   // [nc] curve of scheduler rank r
+  const uint32_t* qstart;  // [nc + 1] first sorted position of rank r
+  const uint32_t* tstart;  // [nc + 1] first task of rank r
+  int64_t nc;
+  unsigned long long* queue;  // task counter
+  int64_t stage_bytes;        // float-box capacity of the stage buffer
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "MREP_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra MREP_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// counting sort of a batch's queries by curve rank (sparse batches):
+// queries per rank, then each query's sorted position = first position of
+// its rank + a warp-aggregated cursor (lanes of one rank share one atomic).
+// Invalid curve ids take rank nc (sorted after every valid query).
+__global__ void rank_count_kernel(const int32_t* qcurve, int64_t n, const uint32_t* rank, int64_t nc,
+                                  uint32_t* rcnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t c = qcurve[i];
+  const uint32_t r = (c < 0 || c >= nc) ? (uint32_t)nc : rank[c];
+  const unsigned peers = __match_any_sync(__activemask(), r);
+  if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&rcnt[r], (unsigned)__popc(peers));
+}
+
+__global__ void rank_scatter_kernel(const int32_t* qcurve, int64_t n, const uint32_t* rank,
+                                    int64_t nc, const uint32_t* qstart, uint32_t* cursor,
+                                    uint32_t* perm) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t c = qcurve[i];
+  const uint32_t r = (c < 0 || c >= nc) ? (uint32_t)nc : rank[c];
+  const unsigned peers = __match_any_sync(__activemask(), r);
+  const int leader = __ffs(peers) - 1, lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(&cursor[r], (unsigned)__popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  perm[qstart[r] + base + __popc(peers & ((1u << lane) - 1))] = (uint32_t)i;
+}
+
+// per-rank query counts -> first sorted position and first task of each
+// rank (one block: nc is the number of curves, ~1e4)
+__global__ void __launch_bounds__(1024) stage_plan_kernel(const uint32_t* cnt, int64_t nc,
+                                                          uint32_t* qstart, uint32_t* tstart) {
+  __shared__ uint32_t sq[1024], stt[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (nc + 1023) / 1024, lo = t * per, hi = lo + per < nc ? lo + per : nc;
+  uint32_t aq = 0, at = 0;
+  for (int64_t r = lo; r < hi; ++r) {
+    aq += cnt[r];
+    at += (cnt[r] + STG_TILE - 1) / STG_TILE;
+  }
+  sq[t] = aq;
+  stt[t] = at;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {  // inclusive scan
+    uint32_t vq = t >= o ? sq[t - o] : 0, vt = t >= o ? stt[t - o] : 0;
+    __syncthreads();
+    sq[t] += vq;
+    stt[t] += vt;
+    __syncthreads();
+  }
+  uint32_t bq = sq[t] - aq, bt = stt[t] - at;
+  for (int64_t r = lo; r < hi; ++r) {
+    qstart[r] = bq;
+    tstart[r] = bt;
+    bq += cnt[r];
+    bt += (cnt[r] + STG_TILE - 1) / STG_TILE;
+  }
+  if (t == 1023) {
+    qstart[nc] = sq[1023];
+    tstart[nc] = stt[1023];
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(STG_THREADS, MREP_STAGE_MINB) wave_traverse_staged(const __grid_constant__ WaveParams w,
+                                                                      const __grid_constant__ StagePlan P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint32_t sk[STG_GROUPS][STG_STACK];
+  __shared__ float sl[STG_GROUPS][STG_STACK];
+  __shared__ uint32_t pc[STG_GROUPS][GPAIRS];
+  __shared__ float pl[STG_GROUPS][GPAIRS];
+  __shared__ TableView tv;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int64_t t_lo, t_hi;
+  __shared__ int32_t t_cid;
+  __shared__ unsigned t_cursor;
+  float* fbs = reinterpret_cast<float*>(smem);
+  const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 3;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t ntask = P.tstart[P.nc];
+  unsigned phase = 0;
+  for (;;) {
+    if (tid == 0) {
+      const unsigned long long task = atomicAdd(P.queue, 1ull);
+      int64_t r = -1;
+      if (task < ntask) {  // rank of the task: last r with tstart[r] <= task
+        int64_t a = 0, b = P.nc;
+        while (b - a > 1) {
+          const int64_t m = (a + b) >> 1;
+          if (P.tstart[m] <= task) a = m;
+          else b = m;
+        }
+        r = a;
+      }
+      if (r < 0) {
+        t_lo = t_hi = 0;
+        t_cid = -1;
+      } else {
+        const int64_t q0 = P.qstart[r], q1 = P.qstart[r + 1];
+        t_lo = q0 + (int64_t)(task - P.tstart[r]) * STG_TILE;
+        t_hi = t_lo + STG_TILE < q1 ? t_lo + STG_TILE : q1;
+        t_cid = (int32_t)P.order[r];
+      }
+      t_cursor = 0;
+    }
+    __syncthreads();
+    const int32_t cid = t_cid;
+    if (cid < 0) break;
+    if (tid < (int)(sizeof(TableView) / 8))  // descriptor -> shared memory
+      reinterpret_cast<uint64_t*>(&tv)[tid] = reinterpret_cast<const uint64_t*>(&w.tabs[cid])[tid];
+    __syncthreads();
+    const int64_t nbox = tv.lvl_off[tv.top] + tv.lvl_cnt[tv.top];
+    const unsigned bytes = (unsigned)(((nbox * 24) + 15) & ~(int64_t)15);
+    const bool staged = (int64_t)bytes <= P.stage_bytes;
+    if (staged) {
+      if (tid == 0) {
+        // the previous task's generic-proxy reads of the buffer are ordered
+        // (__syncthreads) before this async-proxy overwrite
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar, bytes);
+        bulk_g2s(fbs, tv.fbox, bytes, &bar);
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+    }
+    const int64_t lo = t_lo, m = t_hi - t_lo;
+    for (;;) {  // the warp's next four queries of the tile
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(&t_cursor, 4u);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if ((int64_t)base >= m) break;
+      const int64_t g = lo + base + (lane >> 3);
+      bool act = (int64_t)(base + (lane >> 3)) < m;
+      if (staged)
+        traverse_group<D, true, STG_STACK, true>(w, g, act, cid, tv, BoxSrc<true>{fbs}, sk[grp],
+                                                 sl[grp], pc[grp], pl[grp], lane);
+      else
+        traverse_group<D, true, STG_STACK, false>(w, g, act, cid, tv, BoxSrc<false>{tv.fbox},
+                                                  sk[grp], sl[grp], pc[grp], pl[grp], lane);
+    }
+    __syncthreads();  // the stage buffer and descriptor are reused by the next task
+  }
+  // queries with an out-of-range curve id (sorted after every valid one)
+  const int64_t nvalid = P.qstart[P.nc];
+  for (int64_t g = nvalid + (int64_t)blockIdx.x * STG_THREADS + tid; g < w.n;
+       g += (int64_t)gridDim.x * STG_THREADS) {
+    w.gcur[g] = -1;
+    w.scnt[g] = 0;
+    w.flag[g] = 0;
   }
 }
 
@@ -2105,11 +2395,11 @@ __global__ void __launch_bounds__(BLOCK) wave_fallback(const __grid_constant__ W
 __global__ void pack_records_kernel(const double* seg_pts, const double* seg_ta,
                                     const double* seg_tb, const double* seam_t,
                                     const double* seam_pt, int64_t S, int d, double* hdr,
-                                    double* rec, double* box0) {
+                                    double* rec, double* box0, double* sxyz) {
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s == 0) {
     hdr[0] = seam_t[0];
-    for (int k = 0; k < 3; ++k) hdr[1 + k] = k < d ? seam_pt[k] : 0.0;
+    for (int k = 0; k < 3; ++k) hdr[1 + k] = sxyz[k] = k < d ? seam_pt[k] : 0.0;
   }
   if (s >= S) return;
   double* r = rec + s * REC;
@@ -2140,7 +2430,8 @@ __global__ void pack_records_kernel(const double* seg_pts, const double* seg_ta,
   r[R_TA] = seg_ta[s];
   r[R_TB] = seg_tb[s];
   r[R_ST] = seam_t[s + 1];
-  for (int k = 0; k < 3; ++k) r[R_SP + k] = k < d ? seam_pt[(s + 1) * d + k] : 0.0;
+  for (int k = 0; k < 3; ++k)
+    r[R_SP + k] = sxyz[(s + 1) * 3 + k] = k < d ? seam_pt[(s + 1) * d + k] : 0.0;
   r[30] = 0.0;
   r[31] = 0.0;
   // header[4]: max |coordinate| (positive doubles order like their bit patterns)
@@ -2553,7 +2844,41 @@ static int launch_project(const ProjParams& p, unsigned flags, cudaStream_t st) 
 
 enum { TRAV_PACKET = 0, TRAV_LANE = 1, TRAV_GROUP = 2, TRAV_CELLS = 3 };
 
+// staged traversal: resident CTAs per SM (MREP_STAGE_CTAS, 1..3) and the
+// float-box stage buffer each gets (the SM's shared memory split evenly,
+// minus the kernel's static arrays and the 1 KB the runtime reserves per CTA)
+static int stage_ctas_per_sm() {
+  static const int c = [] {
+    const char* e = getenv("MREP_STAGE_CTAS");
+    int v = e ? atoi(e) : MREP_STAGE_MINB;
+    return v < 1 ? 1 : (v > 3 ? 3 : v);
+  }();
+  return c;
+}
+template <int D>
+static int64_t stage_bytes_for(int ctas) {
+  int dev = 0, per_sm = 0, per_block = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&per_block, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, (const void*)wave_traverse_staged<D>);
+  int64_t b = (int64_t)per_sm / ctas - (int64_t)fa.sharedSizeBytes - 1024;
+  if (b > (int64_t)per_block - (int64_t)fa.sharedSizeBytes) b = per_block - fa.sharedSizeBytes;
+  return b < 0 ? 0 : (b & ~(int64_t)127);
+}
+
 static int trav_mode(unsigned flags, int64_t n, int64_t S, int top) {
+  // MREP_TRAV=packet|lane|group: force a traversal (A/B experiments)
+  static const unsigned forced = [] {
+    const char* e = getenv("MREP_TRAV");
+    if (!e) return 0u;
+    if (!strcmp(e, "packet")) return (unsigned)MREP_PACKET;
+    if (!strcmp(e, "lane")) return (unsigned)MREP_PER_LANE;
+    if (!strcmp(e, "group")) return (unsigned)MREP_GROUP;
+    return 0u;
+  }();
+  if (forced && !(flags & (MREP_PACKET | MREP_PER_LANE | MREP_GROUP))) flags |= forced;
   // MREP_CELLS: the caller built a cell index (mrep_cells_build) for this table
   if ((flags & MREP_CELLS) && !(flags & (MREP_PACKET | MREP_PER_LANE | MREP_GROUP)))
     return top > 7 ? TRAV_PACKET : TRAV_CELLS;
@@ -2569,7 +2894,7 @@ static int trav_mode(unsigned flags, int64_t n, int64_t S, int top) {
 template <int D, bool MULTI>
 static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tmode,
                        const TableView* tabs = nullptr, const int32_t* qcurve = nullptr,
-                       int64_t ncurves = 0) {
+                       int64_t ncurves = 0, const StagePlan* plan = nullptr) {
   const int64_t n = p.n;
   const unsigned long long pcap = (unsigned long long)std::max<int64_t>(16 * n, 1 << 16);
   const unsigned long long scap = (unsigned long long)std::max<int64_t>(2 * n, 1 << 16);
@@ -2659,7 +2984,20 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   const unsigned g_clip = persist_grid((const void*)wave_clip<D, MULTI>, BLOCK);
   StageTimer tm(timing, st);
   tm.mark();
-  if (tmode == TRAV_GROUP) {
+  if (tmode == TRAV_GROUP && MULTI && plan) {
+    // staged: persistent CTAs, one curve tile per task, boxes in shared memory
+    StagePlan P = *plan;
+    P.queue = w.cnt + 4;
+    const int ctas = stage_ctas_per_sm();
+    const int64_t stage = stage_bytes_for<D>(ctas);
+    P.stage_bytes = stage;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    MREP_CUDA_CHECK(cudaFuncSetAttribute((const void*)wave_traverse_staged<D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage));
+    wave_traverse_staged<D><<<(unsigned)(sms * ctas), STG_THREADS, (size_t)stage, st>>>(w, P);
+  } else if (tmode == TRAV_GROUP) {
     if (MULTI) {
       // persistent: one resident wave of warps drains the task queue
       unsigned need = grid_for(n * 8, BLOCK);
@@ -2719,8 +3057,20 @@ struct CurveSet {
   int64_t bytes = 0;
   TableView* desc = nullptr;  // device, [nc]
   uint32_t* rank = nullptr;   // device, [nc]: position in decreasing-cubic-count order
+  uint32_t* order = nullptr;  // device, [nc]: curve of each rank (inverse of rank)
   std::vector<int64_t> ofs;   // host, [nc + 1] cubic offsets
 };
+
+// number of AABB boxes of an S-cubic table (all levels), as table_layout
+__device__ __forceinline__ int64_t set_boxes_total(int64_t S) {
+  int64_t cnt = S, off = 0;
+  for (int lv = 0;; ++lv) {
+    off += cnt;
+    if (lv >= 1 && cnt <= 1) break;
+    cnt = (cnt + FANOUT - 1) / FANOUT;
+  }
+  return off;
+}
 
 __global__ void set_pack_kernel(const double* seg_pts, const double* seg_ta, const double* seg_tb,
                                 const int64_t* ofs, const int64_t* tab_off, int64_t nc,
@@ -2742,9 +3092,10 @@ __global__ void set_pack_kernel(const double* seg_pts, const double* seg_ta, con
   double P[4][3];
   for (int j = 0; j < 4; ++j)
     for (int k = 0; k < 3; ++k) P[j][k] = k < d ? seg_pts[(g * 4 + j) * d + k] : 0.0;
+  double* sxyz = base + HDR + S * REC + set_boxes_total(S) * 9;
   if (s == 0) {  // seam_t[0] = seg_ta[0], seam_pt[0] = seg_pts[0, 0] (project.py:234-235)
     hdr[0] = seg_ta[g];
-    for (int k = 0; k < 3; ++k) hdr[1 + k] = P[0][k];
+    for (int k = 0; k < 3; ++k) hdr[1 + k] = sxyz[k] = P[0][k];
   }
   double amax = 0.0;
   for (int k = 0; k < 3; ++k) {
@@ -2767,7 +3118,7 @@ __global__ void set_pack_kernel(const double* seg_pts, const double* seg_ta, con
   r[R_TA] = seg_ta[g];
   r[R_TB] = seg_tb[g];
   r[R_ST] = seg_tb[g];  // seam_t[s+1] = seg_tb[s], seam_pt[s+1] = seg_pts[s, 3] (project.py:236-237)
-  for (int k = 0; k < 3; ++k) r[R_SP + k] = P[3][k];
+  for (int k = 0; k < 3; ++k) r[R_SP + k] = sxyz[(s + 1) * 3 + k] = P[3][k];
   r[30] = 0.0;
   r[31] = 0.0;
   atomicMax((unsigned long long*)&hdr[4], (unsigned long long)__double_as_longlong(amax));
@@ -2819,7 +3170,7 @@ __global__ void set_boxes_kernel(const TableView* desc) {
 template <int D>
 __global__ void morton_multi_kernel(const double* q, const int32_t* qcurve, int64_t n,
                                     const TableView* desc, const uint32_t* rank, int64_t nc,
-                                    int end_bit, uint64_t* key, uint32_t* idx) {
+                                    int end_bit, uint64_t* key, uint32_t* idx, uint32_t* rcnt) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   idx[i] = (uint32_t)i;
@@ -2828,6 +3179,7 @@ __global__ void morton_multi_kernel(const double* q, const int32_t* qcurve, int6
     key[i] = (end_bit >= 64) ? ~0ull : ((1ull << end_bit) - 1ull);
     return;
   }
+  if (rcnt) atomicAdd(&rcnt[rank[c]], 1u);  // queries per rank (staged task plan)
   const TableView& T = desc[c];
   const double* box_root = T.box + T.lvl_off[T.top] * 6;
   uint64_t code = 0;
@@ -2862,7 +3214,8 @@ int set_create(const double* seg_pts, const double* seg_ta, const double* seg_tb
   // layout: [desc nc][rank nc][ofs nc+1][tab_off nc][tables...]
   auto al = [](int64_t b) { return (b + 255) & ~(int64_t)255; };
   const int64_t o_desc = 0, o_rank = al(nc * (int64_t)sizeof(TableView));
-  const int64_t o_ofs = o_rank + al(nc * 4), o_toff = o_ofs + al((nc + 1) * 8);
+  const int64_t o_order = o_rank + al(nc * 4);
+  const int64_t o_ofs = o_order + al(nc * 4), o_toff = o_ofs + al((nc + 1) * 8);
   const int64_t o_tab = o_toff + al(nc * 8);
   std::vector<int64_t> toff(nc);
   int64_t dbl = 0;
@@ -2870,7 +3223,7 @@ int set_create(const double* seg_pts, const double* seg_ta, const double* seg_tb
     toff[c] = dbl;
     dbl += (table_layout(cs->ofs[c + 1] - cs->ofs[c]).total_doubles + 31) & ~(int64_t)31;
   }
-  cs->bytes = o_tab + dbl * 8;
+  cs->bytes = o_tab + dbl * 8 + 256;  // slack: bulk copies round sizes up to 16 B
   cudaError_t e = cudaMalloc(&cs->mem, (size_t)cs->bytes);
   if (e != cudaSuccess) {
     set_error(std::string("mrep_curveset_create: cudaMalloc: ") + cudaGetErrorString(e));
@@ -2889,12 +3242,16 @@ int set_create(const double* seg_pts, const double* seg_ta, const double* seg_tb
   std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
     return cs->ofs[a + 1] - cs->ofs[a] > cs->ofs[b + 1] - cs->ofs[b];
   });
-  std::vector<uint32_t> rank(nc);
-  for (int64_t i = 0; i < nc; ++i) rank[order[i]] = (uint32_t)i;
+  std::vector<uint32_t> rank(nc), order32(nc);
+  for (int64_t i = 0; i < nc; ++i) {
+    rank[order[i]] = (uint32_t)i;
+    order32[i] = (uint32_t)order[i];
+  }
   cs->rank_bits = 1;
   while (((int64_t)1 << cs->rank_bits) < nc + 1) ++cs->rank_bits;
   cs->desc = (TableView*)(cs->mem + o_desc);
   cs->rank = (uint32_t*)(cs->mem + o_rank);
+  cs->order = (uint32_t*)(cs->mem + o_order);
   int64_t* ofs_dev = (int64_t*)(cs->mem + o_ofs);
   int64_t* toff_dev = (int64_t*)(cs->mem + o_toff);
   int rc = MREP_OK;
@@ -2904,6 +3261,7 @@ int set_create(const double* seg_pts, const double* seg_ta, const double* seg_tb
   };
   if ((e = cudaMemcpyAsync(cs->desc, desc.data(), nc * sizeof(TableView), cudaMemcpyHostToDevice, st)) != cudaSuccess) fail(e, "desc");
   if (!rc && (e = cudaMemcpyAsync(cs->rank, rank.data(), nc * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess) fail(e, "rank");
+  if (!rc && (e = cudaMemcpyAsync(cs->order, order32.data(), nc * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess) fail(e, "order");
   if (!rc && (e = cudaMemcpyAsync(ofs_dev, cs->ofs.data(), (nc + 1) * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) fail(e, "ofs");
   if (!rc && (e = cudaMemcpyAsync(toff_dev, toff.data(), nc * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) fail(e, "toff");
   if (!rc && (e = cudaMemsetAsync(tables, 0, dbl * 8, st)) != cudaSuccess) fail(e, "memset");
@@ -2943,6 +3301,16 @@ static int project_batch_chunk(const CurveSet* cs, const double* queries, const 
   p.out_cand = out_cand;
   p.out_seg = out_seg;
   p.counters = counters;
+  const int tmode0 = trav_mode(flags, n, cs->S_total, cs->max_top);
+  // Sparse batches (group walks, each query's work a function of the query
+  // alone) are ordered by a counting sort on the curve's scheduler rank:
+  // count per rank, scan, warp-aggregated scatter -- three light kernels
+  // instead of Morton keys + a 64-bit radix sort.  Dense batches (packet
+  // walks, where warp composition matters) keep the (rank, Morton) radix sort.
+  static const bool radix_env = getenv("MREP_RADIX_SORT") != nullptr;
+  const bool counting = tmode0 == TRAV_GROUP && !radix_env && n < ((int64_t)1 << 32);
+  static const bool stage_env = getenv("MREP_STAGE") != nullptr;
+  const bool staged = counting && stage_env;
   const int end_bit = 10 * d + cs->rank_bits;
   // curve rank + the top 12 Morton bits: a curve holds ~10^2 queries, so a
   // 16^3 cell grid already makes warps spatially coherent (fewer passes)
@@ -2952,12 +3320,19 @@ static int project_batch_chunk(const CurveSet* cs, const double* queries, const 
   }();
   const int begin_bit = (morton_bits > 0 && morton_bits < 10 * d) ? 10 * d - morton_bits : 0;
   size_t sort_tmp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (const uint64_t*)nullptr, (uint64_t*)nullptr,
-                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, begin_bit, end_bit,
-                                  st);
+  if (!counting)
+    cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, begin_bit,
+                                    end_bit, st);
   size_t o_k = 0, o_i = o_k + 16 * (size_t)n, o_tmp = o_i + 8 * (size_t)n + 256;
+  const size_t o_plan = (o_tmp + sort_tmp + 256 + 255) & ~(size_t)255;
+  const size_t plan_b = 4 * ((size_t)cs->nc + 1) * 4 + 256;
   char* ws = nullptr;
-  MREP_CUDA_CHECK(cudaMallocAsync((void**)&ws, o_tmp + sort_tmp + 256, st));
+  MREP_CUDA_CHECK(cudaMallocAsync((void**)&ws, o_plan + plan_b, st));
+  uint32_t* rcnt = (uint32_t*)(ws + o_plan);
+  uint32_t* cursor = rcnt + cs->nc + 1;
+  uint32_t* qstart = cursor + cs->nc + 1;
+  uint32_t* tstart = qstart + cs->nc + 1;
   uint64_t* k_in = (uint64_t*)(ws + o_k);
   uint64_t* k_out = k_in + n;
   uint32_t* i_in = (uint32_t*)(ws + o_i);
@@ -2965,21 +3340,36 @@ static int project_batch_chunk(const CurveSet* cs, const double* queries, const 
   const bool timing = (flags & MREP_TIMING) != 0;
   StageTimer sort_tm(timing, st);
   sort_tm.mark();
-  if (d == 3)
-    morton_multi_kernel<3><<<grid_for(n, 256), 256, 0, st>>>(queries, qcurve, n, cs->desc, cs->rank,
-                                                             cs->nc, end_bit, k_in, i_in);
-  else
-    morton_multi_kernel<2><<<grid_for(n, 256), 256, 0, st>>>(queries, qcurve, n, cs->desc, cs->rank,
-                                                             cs->nc, end_bit, k_in, i_in);
-  MREP_LAUNCH_CHECK();
-  MREP_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(ws + o_tmp, sort_tmp, k_in, k_out, i_in, i_out,
-                                                  (int)n, begin_bit, end_bit, st));
+  if (counting) {
+    MREP_CUDA_CHECK(cudaMemsetAsync(rcnt, 0, 2 * ((size_t)cs->nc + 1) * 4, st));
+    rank_count_kernel<<<grid_for(n, 256), 256, 0, st>>>(qcurve, n, cs->rank, cs->nc, rcnt);
+    MREP_LAUNCH_CHECK();
+    stage_plan_kernel<<<1, 1024, 0, st>>>(rcnt, cs->nc, qstart, tstart);
+    MREP_LAUNCH_CHECK();
+    rank_scatter_kernel<<<grid_for(n, 256), 256, 0, st>>>(qcurve, n, cs->rank, cs->nc, qstart,
+                                                          cursor, i_out);
+    MREP_LAUNCH_CHECK();
+  } else {
+    if (d == 3)
+      morton_multi_kernel<3><<<grid_for(n, 256), 256, 0, st>>>(queries, qcurve, n, cs->desc,
+                                                               cs->rank, cs->nc, end_bit, k_in, i_in,
+                                                               nullptr);
+    else
+      morton_multi_kernel<2><<<grid_for(n, 256), 256, 0, st>>>(queries, qcurve, n, cs->desc,
+                                                               cs->rank, cs->nc, end_bit, k_in, i_in,
+                                                               nullptr);
+    MREP_LAUNCH_CHECK();
+    MREP_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(ws + o_tmp, sort_tmp, k_in, k_out, i_in, i_out,
+                                                    (int)n, begin_bit, end_bit, st));
+  }
   sort_tm.mark();
   sort_tm.finish(0);
   p.perm = i_out;
-  const int tmode = trav_mode(flags, n, cs->S_total, cs->max_top);
-  int rc = d == 3 ? launch_wave<3, true>(p, st, timing, tmode, cs->desc, qcurve, cs->nc)
-                  : launch_wave<2, true>(p, st, timing, tmode, cs->desc, qcurve, cs->nc);
+  const int tmode = tmode0;
+  StagePlan plan{cs->order, qstart, tstart, cs->nc, nullptr, 0};
+  const StagePlan* pl = staged ? &plan : nullptr;
+  int rc = d == 3 ? launch_wave<3, true>(p, st, timing, tmode, cs->desc, qcurve, cs->nc, pl)
+                  : launch_wave<2, true>(p, st, timing, tmode, cs->desc, qcurve, cs->nc, pl);
   MREP_CUDA_CHECK(cudaFreeAsync(ws, st));
   return rc;
 }
@@ -3028,7 +3418,7 @@ int mrep_table_pack(const double* seg_pts, const double* seg_ta, const double* s
   double* box = base + L.box_off;
   pack_records_kernel<<<grid_for(S, 128), 128, 0, st>>>(seg_pts, seg_ta, seg_tb, seam_t, seam_pt,
                                                         S, d, base, base + L.rec_off,
-                                                        box + L.lvl_off[0]);
+                                                        box + L.lvl_off[0], base + L.sxyz_off);
   MREP_LAUNCH_CHECK();
   for (int lv = 1; lv <= L.top; ++lv) {
     reduce_boxes_kernel<<<grid_for(L.lvl_cnt[lv], 128), 128, 0, st>>>(

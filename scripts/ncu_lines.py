@@ -1,5 +1,7 @@
 """Aggregate an `ncu --page source --csv --print-source cuda,sass` dump by
-CUDA source line: warp-stall samples, executed instructions, top stalls."""
+CUDA source line: warp-stall samples, executed instructions, top stalls.
+
+    python scripts/ncu_lines.py dump.csv [top] [inst]   (sort by instructions)"""
 import csv
 import sys
 
@@ -40,7 +42,9 @@ for r in rows:
             if v:
                 e["stalls"][name] = e["stalls"].get(name, 0) + v
 tot = sum(e["samples"] for e in agg.values()) or 1
-for (f, ln), e in sorted(agg.items(), key=lambda kv: -kv[1]["samples"])[:top]:
+order = "inst" if len(sys.argv) > 3 and sys.argv[3] == "inst" else "samples"
+print(f"total instructions {sum(e['inst'] for e in agg.values())}")
+for (f, ln), e in sorted(agg.items(), key=lambda kv: -kv[1][order])[:top]:
     st = sorted(e["stalls"].items(), key=lambda kv: -kv[1])[:3]
     st = " ".join(f"{k[6:]}={v}" for k, v in st)
     print(f"{100 * e['samples'] / tot:5.1f}% inst={e['inst']:>10d} {f}:{ln:<5} {e['src'].strip()[:70]:70s} {st}")
