@@ -818,6 +818,34 @@ def main():
                                                + F_SEAM * (wl.num_segments + 1)) * n
                                                / (kms / 1e3) / 1e12)
 
+    # ---- the reference's brute-force candidate count (MREP_CAND_EXACT, the
+    #      Python API's default cand) on the FP64 tensor cores: one
+    #      mma.sync m8n8k4 per 8 queries x 1 cubic, 64 flop per (query, cubic)
+    #      pair; timed as its own stage (slot 6), not part of `value` ----
+    if (isinstance(wl, SingleCurve) and not dense
+            and wl.num_segments * n <= 2_000_000_000):
+        dpk = ctypes.c_double()
+        L.check(L.lib().mrep_dmma_peak(ctypes.byref(dpk)))
+        counters.zero_()
+        wl.step(counters, extra_flags=L.MREP_CAND_EXACT)
+        unc = float(counters.cpu().numpy()[L.CNT_UNCERTAIN])
+        cms = []
+        for _ in range(reps):
+            flush.fill_(3.0)
+            wl.step(extra_flags=L.MREP_CAND_EXACT | L.MREP_TIMING)
+            buf = (ctypes.c_double * 8)()
+            L.lib().mrep_last_stage_times(buf, 8)
+            cms.append(buf[6])
+        cm = float(np.median(cms))
+        ach = 64.0 * wl.num_segments * n / (cm / 1e3) / 1e12
+        roofline["cand_exact"] = {
+            "kernel": "cand_count_kernel (mma.sync.m8n8k4.f64 sign screen + exact solve of "
+                      "undecided pairs)", "bound": "tensor", "ms": cm, "achieved": ach,
+            "peak": dpk.value, "unit": "TFLOP/s", "frac": ach / dpk.value,
+            "peak_source": "DMMA m8n8k4 microbenchmark measured in this run (mrep_dmma_peak)",
+            "flop_model": "64 FP64 tensor flop per (query, cubic) pair (8x8x4 MMA per 8 queries)",
+            "uncertain_pairs_per_query": unc / n}
+
     # ---- e2e: host buffers through the C ABI (H2D + kernel + D2H per step) ----
     wl.pinned()
     outs = (torch.empty(n, dtype=torch.float64).pin_memory(),

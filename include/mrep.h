@@ -45,6 +45,9 @@ extern "C" {
 #define MREP_PER_LANE 64u /* screened traversal: force per-lane BVH walks */
 #define MREP_GROUP 128u   /* screened traversal: force one 8-lane group per query */
 #define MREP_CELLS 256u   /* screened traversal: use the table's cell index (mrep_cells_build) */
+#define MREP_CAND_EXACT 512u /* screened mode: cand = the reference's brute-force count
+                                (seams + surviving pieces of every cubic), computed on the FP64
+                                tensor cores with an exact solve of the undecided pairs */
 
 /* Work counters written (accumulated) by mrep_project when `counters_dev` != NULL. */
 #define MREP_CNT_PAIRS 0      /* (query, cubic) pairs solved: E, quartic, rebase, pieces */
@@ -54,6 +57,7 @@ extern "C" {
 #define MREP_CNT_BOXES 4      /* BVH box lower-bound tests */
 #define MREP_CNT_PASS2 5      /* queries that needed the exact tie-band second pass */
 #define MREP_CNT_HULL_MISS 6  /* surviving pieces whose hull never crossed (NoRoot, project.py:282-283) */
+#define MREP_CNT_UNCERTAIN 7  /* MREP_CAND_EXACT: (query, cubic) pairs the tensor-core sign screen left to the exact count */
 #define MREP_NUM_COUNTERS 8
 
 MREP_API const char* mrep_last_error(void);
@@ -62,6 +66,8 @@ MREP_API const char* mrep_last_error(void);
 MREP_API int mrep_last_stage_times(double* ms, int max);
 /* measured FP64 FMA throughput of the current device, TFLOP/s (roofline peak) */
 MREP_API int mrep_fp64_peak(double* tflops);
+/* measured FP64 tensor-core (mma.sync m8n8k4) throughput, TFLOP/s */
+MREP_API int mrep_dmma_peak(double* tflops);
 /* frees every device's host-call pipeline context (mrep_*_host streams,
  * events, pinned and device staging buffers); the next host-buffer call
  * re-creates them.  Optional: for leak checkers and embedding processes. */

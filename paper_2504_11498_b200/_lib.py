@@ -30,8 +30,10 @@ MREP_PACKET = 32
 MREP_PER_LANE = 64
 MREP_GROUP = 128
 MREP_CELLS = 256
+MREP_CAND_EXACT = 512
 NUM_COUNTERS = 8
-CNT_PAIRS, CNT_SURVIVORS, CNT_CLIP_ITERS, CNT_SEAMS, CNT_BOXES, CNT_PASS2, CNT_HULL_MISS = range(7)
+(CNT_PAIRS, CNT_SURVIVORS, CNT_CLIP_ITERS, CNT_SEAMS, CNT_BOXES, CNT_PASS2, CNT_HULL_MISS,
+ CNT_UNCERTAIN) = range(8)
 
 _lib = None
 _lock = threading.Lock()
@@ -47,6 +49,7 @@ _SIGS = {
     "mrep_version": ([], _i32),
     "mrep_last_stage_times": ([_vp, _i32], _i32),
     "mrep_fp64_peak": ([_vp], _i32),
+    "mrep_dmma_peak": ([_vp], _i32),
     "mrep_host_release": ([], _i32),
     "mrep_device_count": ([], _i32),
     "mrep_table_bytes": ([_i64], _i64),

@@ -1,0 +1,257 @@
+// mrep_cand.cuh -- the reference's candidate count on FP64 tensor cores.
+//
+// _kernels._project_block (_kernels.py:369-502) reports per query
+// cand = (S + 1) seams + every surviving monotone piece of EVERY cubic
+// (pieces between the roots of E' in (1e-10, 1 - 1e-10); a piece survives
+// iff its restricted ordinates have b0 < 0 and b0 * b5 <= 0,
+// _kernels.py:427-441).  That is a brute-force quantity: the screened
+// projection never looks at most cubics.  This pass reproduces it exactly
+// without solving every pair:
+//
+//  * A cubic whose six Bernstein ordinates b_i of E = D' (D = |C - q|^2) are
+//    all >= 0, or all < 0 and clear of underflow, has no survivor: every
+//    piece's restricted ordinates are positively weighted sums of them, so
+//    b0 >= 0, or b0 < 0 with b0 * b5 > 0 (the argument of prep_pair_cut).
+//  * The degree-6 Bernstein coefficients d_j of D(u) = |C(u) - q|^2 are affine
+//    in q: d_j = g_j - 2 (q - c0) . c_j + |q - c0|^2, with g_j, c_j the
+//    coefficients of |C - c0|^2 and of C - c0 elevated to degree 6 (c0 = the
+//    table's box centre), and b_i = 6 (d_{i+1} - d_i).  For 8 queries x one
+//    cubic that is ONE FP64 tensor-core MMA, mma.sync m8n8k4 (K = 4 exactly:
+//    1, qx, qy, qz; N = 8: d_0..d_6 and a pad column): A = the warp's 8
+//    queries, B = the cubic's 4 x 8 fragment stored in the table.
+//  * A cubic whose E' is strictly monotone (the five ordinates of E'' of one
+//    sign: the reference's quartic finds no interior split) with end
+//    values b_0, b_5 clear of zero holds exactly one survivor when
+//    b_0 < 0 < b_5 and none otherwise.
+//  The MMA is fed the coefficients of the ordinate differences directly
+//  (column j -> d_{j+1} - d_j = b_j / 6), so a lane's two outputs are two
+//  ordinates of E' and E'' needs one shuffle.
+//  * The MMA's values differ from the reference's FP64 b_i by rounding only;
+//    a margin of 1e-9 (scale + |q|)^2, orders of magnitude above the
+//    rounding of either computation, decides the sign.  Pairs inside the
+//    margin ("uncertain") are solved exactly as the reference does
+//    (prep_pair: E, quartic roots of E', rebase, restriction per piece) by
+//    the warp's lanes from a shared-memory queue, 32 at a time.
+//
+// Result: cand equal to the reference's, bit for bit, at a cost of one MMA
+// per 8 (query, cubic) pairs plus the few uncertain pairs.
+#pragma once
+
+namespace mrep {
+
+__device__ __forceinline__ void dmma_8x8x4(double a, double b, double& c0, double& c1) {
+  const double z = 0.0;
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};"
+               : "=d"(c0), "=d"(c1)
+               : "d"(a), "d"(b), "d"(z), "d"(z));
+}
+
+// B fragment of one cubic (control points P, centre c0).  With g_j, c_j the
+// degree-6 Bernstein coefficients of |C - c0|^2 and of C - c0, column j
+// (j = 0..5) holds the coefficients of d_{j+1} - d_j = b_j / 6:
+//   k = 0: g_{j+1} - g_j;  k = 1..3: -2 (c_{j+1} - c_j)[k-1]
+// (|q - c0|^2 cancels); columns 6, 7 are zero.  Element (k, j) is stored at
+// index 4 j + k, the lane that holds it in m8n8k4's col-major B layout
+// (lane t: k = t % 4, j = t / 4).
+__device__ __forceinline__ void bfrag_one(const double (&P)[4][3], const double (&c0)[3], int d,
+                                          double* frag) {
+  const double C3[4] = {1.0, 3.0, 3.0, 1.0};
+  const double C6[7] = {1.0, 6.0, 15.0, 20.0, 15.0, 6.0, 1.0};
+  double Q[4][3];
+  for (int i = 0; i < 4; ++i)
+    for (int k = 0; k < 3; ++k) Q[i][k] = k < d ? P[i][k] - c0[k] : 0.0;
+  // B_i,3 B_k,3 = C3[i] C3[k] / C6[i+k] B_{i+k},6: summing the product
+  // weights gives |C - c0|^2 (g) and, since sum_k B_k,3 = 1, C - c0
+  // elevated to degree 6 (c)
+  double g[7], c[7][3];
+  for (int j = 0; j < 7; ++j) {
+    g[j] = 0.0;
+    c[j][0] = c[j][1] = c[j][2] = 0.0;
+    for (int i = 0; i < 4; ++i) {
+      const int k2 = j - i;
+      if (k2 >= 0 && k2 <= 3) {
+        const double wgt = C3[i] * C3[k2] / C6[j];
+        double dot = 0.0;
+        for (int k = 0; k < 3; ++k) dot += Q[i][k] * Q[k2][k];
+        g[j] += wgt * dot;
+        for (int k = 0; k < 3; ++k) c[j][k] += wgt * Q[i][k];
+      }
+    }
+  }
+  for (int j = 0; j < 8; ++j) {
+    if (j < 6) {
+      frag[4 * j + 0] = g[j + 1] - g[j];
+      for (int k = 0; k < 3; ++k) frag[4 * j + 1 + k] = -2.0 * (c[j + 1][k] - c[j][k]);
+    } else {
+      for (int k = 0; k < 4; ++k) frag[4 * j + k] = 0.0;
+    }
+  }
+}
+
+// the centre c0 of a curve table's root box
+__device__ __forceinline__ void table_centre(const TableView& T, double (&c0)[3]) {
+  const double* rb = T.box + T.lvl_off[T.top] * 6;
+  for (int k = 0; k < 3; ++k) c0[k] = 0.5 * (rb[k] + rb[3 + k]);
+}
+
+__device__ __forceinline__ void bfrag_cubic(const TableView& T, int64_t s, int d) {
+  double P[4][3], c0[3];
+  const double* r = T.rec + s * REC + R_P;
+  for (int i = 0; i < 4; ++i)
+    for (int k = 0; k < 3; ++k) P[i][k] = r[i * 3 + k];
+  table_centre(T, c0);
+  if (s == 0) {
+    double* hdr = const_cast<double*>(T.hdr);
+    for (int k = 0; k < 3; ++k) hdr[5 + k] = c0[k];
+  }
+  bfrag_one(P, c0, d, const_cast<double*>(T.bfrag) + s * 32);
+}
+
+// single table (after its boxes are built)
+static __global__ void table_bfrag_kernel(const TableView T, int d) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < T.S) bfrag_cubic(T, s, d);
+  if (s < 64) const_cast<double*>(T.bfrag)[T.S * 32 + s] = 0.0;  // prefetch slack
+}
+
+// kept pieces of one (query, cubic) pair, exactly as _kernels.py:415-441
+template <int D>
+__device__ __forceinline__ int kept_pieces(const TableView& T, int64_t s, const double (&q)[D]) {
+  PairPrep P;
+  prep_pair<D>(T, s, q, P);
+  int kept = 0;
+  double lo = 0.0;
+  for (int k = 0; k <= P.nin; ++k) {
+    const double hi = (k == P.nin) ? 1.0 : (k == 0 ? P.b1 : (k == 1 ? P.b2 : (k == 2 ? P.b3 : P.b4)));
+    double bp[6];
+    restrict_ordinates(P.bseg, lo, hi, bp);
+    kept += (bp[0] < 0.0 && bp[0] * bp[5] <= 0.0) ? 1 : 0;
+    lo = hi;
+  }
+  return kept;
+}
+
+constexpr int CAND_WARPS = 4;
+
+// one warp = 8 queries (rows) against every cubic; out_cand in caller order.
+// TC = false computes the same two columns per lane with DFMA on the CUDA
+// cores (8 fragment loads + 8 FMAs instead of one MMA) -- the A/B baseline
+// for the tensor-core contraction (MREP_CAND_CUDA_CORES=1 selects it).
+template <int D, bool TC = true>
+__global__ void __launch_bounds__(CAND_WARPS * 32) cand_count_kernel(const TableView T, const double* qs,
+                                                                    int64_t n, int64_t* out_cand,
+                                                                    unsigned long long* n_uncertain) {
+  __shared__ uint32_t queue[CAND_WARPS][64];
+  __shared__ int kept[CAND_WARPS][8];
+  __shared__ double sq[CAND_WARPS][8][3];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31, row = lane >> 2, p = lane & 3;
+  const int64_t q0 = ((int64_t)blockIdx.x * CAND_WARPS + wi) * 8;
+  if (q0 >= n) return;  // whole warp
+  const int64_t qi = q0 + row;
+  const bool valid = qi < n;
+  double q[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) q[k] = valid ? qs[qi * D + k] : 0.0;
+  if (p == 0) {
+    kept[wi][row] = 0;
+    for (int k = 0; k < 3; ++k) sq[wi][row][k] = k < D ? q[k] : 0.0;
+  }
+  double R = T.hdr[4];
+#pragma unroll
+  for (int k = 0; k < D; ++k) R = fmax(R, fabs(q[k]));
+  // sign margins: far above the rounding of the MMA and of the reference's
+  // FP64 ordinates; end values of a monotone E' must clear a wider margin
+  // (a spurious split the reference's quartic might place within ~1e-8 of
+  // an end must not change that end's sign)
+  const double m = fmax(1e-9 * R * R, 1e-150), mneg = m, m2 = 4.0 * m,
+               mend = fmax(1e-6 * R * R, 1e-150);
+  int ones = 0;  // pairs certified to hold exactly one survivor (lanes p == 0)
+  const double a = p == 0 ? 1.0 : (p <= D ? q[p - 1] - T.hdr[4 + p] : 0.0);
+  const double* F = T.bfrag;
+  const int64_t S = T.S;
+  int qn = 0;
+  unsigned long long unc_total = 0;
+  __syncwarp();
+  auto drain = [&](int cnt) {
+    // lanes < cnt solve one queued pair each
+    if (lane < cnt) {
+      const uint32_t e = queue[wi][lane];
+      const int r = (int)(e >> 29);
+      const int64_t s = (int64_t)(e & 0x1fffffffu);
+      double qq[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) qq[k] = sq[wi][r][k];
+      const int kp = kept_pieces<D>(T, s, qq);
+      if (kp) atomicAdd(&kept[wi][r], kp);
+    }
+    __syncwarp();
+  };
+  // per-lane constant: flag bits this lane does not decide (AND-neutral)
+  //  0 all b > m  1 all b < -m  2 all E'' > m2  3 all E'' < -m2
+  //  4 b_0 < -mend  5 |b_0| > mend  (lane 0)   6 b_5 > mend  7 |b_5| > mend  (lane 2)
+  const unsigned neutral = p == 0 ? 0xc0u : (p == 1 ? 0xf0u : (p == 2 ? 0x30u : 0xffu));
+  const bool owner = valid && p == 0;
+  // the table reserves two zero fragments past the last cubic: the
+  // prefetch two cubics ahead needs no bound check
+  const double* Fp = F + lane;
+  double bn0 = __ldg(Fp), bn1 = __ldg(Fp + 32);
+#pragma unroll 1
+  for (int64_t s = 0; s < S; ++s) {
+    const double b = bn0;
+    bn0 = bn1;
+    bn1 = __ldg(Fp + 64);
+    Fp += 32;
+    double c0, c1;
+    if (TC) {
+      dmma_8x8x4(a, b, c0, c1);
+    } else {
+      // lane (row, p) owns columns 2p, 2p+1: sum_k A[row][k] B[k][col]
+      const double* Bs = Fp - 32 - lane;
+      c0 = c1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double ak = __shfl_sync(0xffffffffu, a, (lane & ~3) | k);
+        c0 = fma(ak, __ldg(Bs + 8 * p + k), c0);
+        c1 = fma(ak, __ldg(Bs + 8 * p + 4 + k), c1);
+      }
+    }
+    // lane p holds b_2p / 6, b_2p+1 / 6 of its row (lanes p = 0..2; p = 3
+    // holds the zero pad columns); b_2p+2 / 6 from lane p + 1
+    const double nx = __shfl_down_sync(0xffffffffu, c0, 1);
+    const double ea = c1 - c0, eb = nx - c1;  // E'' ordinates / 30: 2p, 2p + 1
+    const double mn = fmin(c0, c1), mx = fmax(c0, c1);
+    const double emn = p <= 1 ? fmin(ea, eb) : ea, emx = p <= 1 ? fmax(ea, eb) : ea;
+    unsigned v = (unsigned)(mn > m) | ((unsigned)(mx < -mneg) << 1) | ((unsigned)(emn > m2) << 2) |
+                 ((unsigned)(emx < -m2) << 3) | ((unsigned)(c0 < -mend) << 4) |
+                 ((unsigned)(fabs(c0) > mend) << 5) | ((unsigned)(c1 > mend) << 6) |
+                 ((unsigned)(fabs(c1) > mend) << 7);
+    v |= neutral;
+    v &= __shfl_xor_sync(0xffffffffu, v, 1);
+    v &= __shfl_xor_sync(0xffffffffu, v, 2);
+    // E' one-signed: no survivor.  E' strictly monotone (E'' one-signed, so
+    // the reference splits no piece) with robust end values: one survivor
+    // iff it rises from b_0 < 0 to b_5 > 0.
+    const bool zero = (v & 3u) != 0;
+    const bool mono = (v & 12u) && (v & 0xa0u) == 0xa0u;
+    ones += (owner && !zero && mono && (v & 0x50u) == 0x50u) ? 1 : 0;
+    const bool unc = owner && !zero && !mono;
+    const unsigned bal = __ballot_sync(0xffffffffu, unc);
+    if (bal) {
+      if (unc) queue[wi][qn + __popc(bal & ((1u << lane) - 1))] = ((uint32_t)row << 29) | (uint32_t)s;
+      qn += __popc(bal);
+      unc_total += __popc(bal);
+      __syncwarp();
+      if (qn >= 32) {
+        drain(32);
+        if (lane < qn - 32) queue[wi][lane] = queue[wi][32 + lane];
+        qn -= 32;
+        __syncwarp();
+      }
+    }
+  }
+  drain(qn);
+  if (valid && p == 0) out_cand[qi] = S + 1 + kept[wi][row] + ones;
+  if (n_uncertain && lane == 0) atomicAdd(n_uncertain, unc_total);
+}
+
+}  // namespace mrep

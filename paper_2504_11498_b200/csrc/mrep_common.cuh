@@ -76,9 +76,13 @@ struct StageTimer {
 // (lo xyz, hi xyz).  A float copy of every box follows (6 floats, lo
 // rounded down, hi rounded up, so it encloses the double box): the hot
 // traversals test it on the FP32 pipe with a rigorous rounding allowance.
+// Header [5..7] of a curve table: the centre c0 of its root box.
 // Curve tables (rec == REC) end with a compact seam block: seam s's point as
 // 3 doubles (xyz; z = 0 in 2-D), s = 0..S, so the 8 seams a group traversal
-// reads at a leaf expansion are one contiguous 192-B run instead of 8 lines.
+// reads at a leaf expansion are one contiguous 192-B run instead of 8 lines,
+// and then one 256-B block per cubic: the 4 x 8 B operand of an FP64 tensor
+// core MMA (m8n8k4) whose product with (1, q - c0) gives the degree-6
+// Bernstein coefficients of |C(u) - q|^2 - |q - c0|^2 (mrep_cand.cuh).
 constexpr int REC = 32;
 constexpr int R_W = 0, R_ST = 12, R_SP = 13, R_P = 16, R_TA = 28, R_TB = 29;
 constexpr int HDR = 64;
@@ -95,6 +99,7 @@ struct TableLayout {
   int64_t box_off;   // in doubles from table start
   int64_t fbox_off;  // in doubles from table start (float boxes, 3 doubles each)
   int64_t sxyz_off;  // in doubles from table start (curve seams, 3 doubles each); 0 = none
+  int64_t bfrag_off; // in doubles from table start (curve Bernstein fragments, 32 per cubic)
   int64_t total_doubles;
 };
 
@@ -120,6 +125,9 @@ inline TableLayout table_layout(int64_t S, int rec = REC) {
   if (rec == REC) {
     L.sxyz_off = L.total_doubles;
     L.total_doubles += (S + 1) * 3;
+    L.total_doubles = (L.total_doubles + 3) & ~(int64_t)3;  // 32-B aligned fragments
+    L.bfrag_off = L.total_doubles;
+    L.total_doubles += (S + 2) * 32;  // + two zero fragments (prefetch slack)
   }
   return L;
 }
@@ -130,6 +138,7 @@ struct TableView {
   const double* box;
   const float* fbox;
   const double* sxyz;  // compact seam points (curve tables), nullptr otherwise
+  const double* bfrag; // per-cubic DMMA B fragments of |C - c0|^2 (curve tables), see mrep_cand
   int64_t S;
   int top;
   int64_t lvl_off[MAX_LEVELS];
@@ -145,6 +154,7 @@ inline TableView table_view(const void* table, int64_t S, int rec = REC) {
   v.box = base + L.box_off;
   v.fbox = reinterpret_cast<const float*>(base + L.fbox_off);
   v.sxyz = L.sxyz_off ? base + L.sxyz_off : nullptr;
+  v.bfrag = L.bfrag_off ? base + L.bfrag_off : nullptr;
   v.S = S;
   v.top = L.top;
   for (int i = 0; i < MAX_LEVELS; ++i) {

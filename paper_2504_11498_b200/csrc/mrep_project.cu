@@ -743,6 +743,10 @@ __device__ __forceinline__ bool prep_pair_cut(const TableView& T, int64_t s, con
   return true;
 }
 
+}  // namespace mrep
+#include "mrep_cand.cuh"
+namespace mrep {
+
 // Walk the monotone pieces of the warp's current pairs in lock step
 // (piece k of every pair together), queue survivors, flush full batches.
 template <int D, bool STATS>
@@ -3163,6 +3167,20 @@ __global__ void set_boxes_kernel(const TableView* desc) {
     }
 }
 
+// Bernstein fragments of every cubic of a set (after set_boxes_kernel)
+__global__ void set_bfrag_kernel(const TableView* desc, const int64_t* ofs, int64_t nc,
+                                 int64_t S_total, int d) {
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= S_total) return;
+  int64_t lo = 0, hi = nc;
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (ofs[mid] <= g) lo = mid;
+    else hi = mid;
+  }
+  bfrag_cubic(desc[lo], g - ofs[lo], d);
+}
+
 // Scheduler key of each query: (rank of its curve, Morton code inside that
 // curve's root box).  Sorting by it groups a curve's queries, orders curves
 // by decreasing cubic count and makes the lanes of a warp spatial neighbours.
@@ -3269,6 +3287,8 @@ int set_create(const double* seg_pts, const double* seg_ta, const double* seg_tb
     set_pack_kernel<<<grid_for(cs->S_total, 128), 128, 0, st>>>(seg_pts, seg_ta, seg_tb, ofs_dev,
                                                                 toff_dev, nc, cs->S_total, d, tables);
     set_boxes_kernel<<<(unsigned)nc, 128, 0, st>>>(cs->desc);
+    set_bfrag_kernel<<<grid_for(cs->S_total, 128), 128, 0, st>>>(cs->desc, ofs_dev, nc,
+                                                                  cs->S_total, d);
     if ((e = cudaGetLastError()) != cudaSuccess) fail(e, "pack kernels");
   }
   // the host staging vectors die here: finish the copies before returning
@@ -3428,6 +3448,8 @@ int mrep_table_pack(const double* seg_pts, const double* seg_ta, const double* s
   boxes_to_float_kernel<<<grid_for(L.total_boxes, 256), 256, 0, st>>>(
       box, reinterpret_cast<float*>(base + L.fbox_off), L.total_boxes);
   MREP_LAUNCH_CHECK();
+  table_bfrag_kernel<<<grid_for(S, 128), 128, 0, st>>>(table_view(table, S), d);
+  MREP_LAUNCH_CHECK();
   return MREP_OK;
 }
 
@@ -3561,6 +3583,24 @@ static int project_chunk(const void* table, int64_t S, int d, const double* quer
     rc = d == 3 ? launch_wave<3, false>(p, st, timing, tmode)
                 : launch_wave<2, false>(p, st, timing, tmode);
   else rc = d == 3 ? launch_project<3>(p, flags, st) : launch_project<2>(p, flags, st);
+  if (rc == MREP_OK && wave && (flags & MREP_CAND_EXACT) && out_cand) {
+    // the reference's brute-force candidate count (mrep_cand.cuh), caller order
+    StageTimer cand_tm(timing, st);
+    cand_tm.mark();
+    const unsigned blocks = grid_for(n, CAND_WARPS * 8);
+    unsigned long long* unc = counters ? (unsigned long long*)&counters[MREP_CNT_UNCERTAIN] : nullptr;
+    static const bool cuda_cores = getenv("MREP_CAND_CUDA_CORES") != nullptr;
+    if (d == 3) {
+      if (cuda_cores) cand_count_kernel<3, false><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, n, out_cand, unc);
+      else cand_count_kernel<3, true><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, n, out_cand, unc);
+    } else {
+      if (cuda_cores) cand_count_kernel<2, false><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, n, out_cand, unc);
+      else cand_count_kernel<2, true><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, n, out_cand, unc);
+    }
+    MREP_LAUNCH_CHECK();
+    cand_tm.mark();
+    cand_tm.finish(6);
+  }
   MREP_CUDA_CHECK(cudaFreeAsync(ws, st));
   return rc;
 }

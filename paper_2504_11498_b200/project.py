@@ -9,11 +9,16 @@ device, runs the sm_100a projection kernel and returns host arrays, exactly
 like the reference's numba batch driver.
 
 Modes of project_prepared:
-* default (screen=True): BVH-screened exact solve.  t, foot, distance (and the
-  winning segment) are those of the brute-force reference kernel; `cand`
-  counts what the query's screened traversal examined: seams offered plus
-  cubics queued for the exact solve (the reference counts
-  every seam plus every survivor of every cubic, a brute-force quantity).
+* default (screen=True, cand="exact"): BVH-screened exact solve.  t, foot,
+  distance (and the winning segment) are those of the brute-force reference
+  kernel; `cand` is the reference's own count -- every seam plus every
+  surviving piece of every cubic -- computed by a separate pass on the FP64
+  tensor cores (one mma.sync m8n8k4 per 8 queries x 1 cubic decides the sign
+  of E' on each cubic; the few undecided pairs are solved exactly;
+  csrc/mrep_cand.cuh).
+* cand="screened": skip that pass; `cand` then counts what the query's
+  screened traversal examined (seams offered plus cubics queued for the
+  exact solve) -- the fast path the C-ABI benchmark measures.
 * screen=False, or with_stats / soundness_samples: brute force over all
   cubics with the reference's exact cand, ProjectionStats and soundness.
 `workers` is accepted and validated (plan_work) for drop-in compatibility;
@@ -321,15 +326,19 @@ def project_prepared(prep: PreparedCurve, queries, workers: int | None = None,
                      clip_tol: float = 1e-6, max_iterations: int = 8,
                      with_stats: bool = False, soundness_samples: int = 0, *,
                      screen: bool = True, return_segments: bool = False,
-                     return_spans: bool = False):
+                     return_spans: bool = False, cand: str = "exact"):
     """Project every query; returns (t, foot, distance, candidates) host arrays,
     plus (ProjectionStats, sound) when with_stats, plus the winning cubic index
     per query when return_segments, plus the knot span of t* in the original
-    B-spline (core.py:108-112) when return_spans."""
+    B-spline (core.py:108-112) when return_spans.  cand="exact" (default)
+    returns the reference's candidate count, cand="screened" the screened
+    traversal's (faster; see the module docstring)."""
     q = _as_queries(prep, queries)
     plan_work(len(q), 1 if workers is None else workers)
     if max_iterations < 1:
         raise DomainError("max_iterations must be >= 1")
+    if cand not in ("exact", "screened"):
+        raise DomainError('cand must be "exact" or "screened"')
     n = q.shape[0]
     dense = with_stats or soundness_samples > 0 or not screen
     tab = prep.table
@@ -341,11 +350,12 @@ def project_prepared(prep: PreparedCurve, queries, workers: int | None = None,
                 + ((np.empty(0, np.int32),) if return_spans else ()))
     if not dense:
         cnt = np.zeros(L.NUM_COUNTERS, dtype=np.uint64)
-        t, foot, dist, cand, seg = tab.project_host(q, clip_tol=clip_tol, max_iter=max_iterations,
-                                                    screen=True, counters=cnt)
+        t, foot, dist, cnd, seg = tab.project_host(
+            q, clip_tol=clip_tol, max_iter=max_iterations, screen=True, counters=cnt,
+            extra_flags=L.MREP_CAND_EXACT if cand == "exact" else 0)
         if int(cnt[L.CNT_HULL_MISS]) > 0:
             raise NoRoot("hull never crossed on a surviving piece; elimination bug")
-        out = (t, foot, dist, cand)
+        out = (t, foot, dist, cnd)
         return (out + ((seg,) if return_segments else ())
                 + ((prep.knot_spans(t),) if return_spans else ()))
     td, fd, dd, cd, sd, std, snd = tab.project(L.to_dev(q), clip_tol, max_iterations,
@@ -388,7 +398,7 @@ def invert_points(prep: PreparedCurve, points, tolerance: float | None = None):
     parameters of on-curve points; PointNotOnCurve if any lies beyond
     10 * tolerance."""
     tol = prep.tolerance if tolerance is None else tolerance
-    t, _, dist, _ = project_prepared(prep, points)
+    t, _, dist, _ = project_prepared(prep, points, cand="screened")
     bad = np.nonzero(dist > 10.0 * tol)[0]
     if len(bad):
         raise PointNotOnCurve(f"{len(bad)} points farther than 10 * {tol} "

@@ -1,4 +1,6 @@
-"""One screened cfg2 projection of n queries (for ncu launch lists)."""
+"""One screened cfg2 projection of n queries (for ncu launch lists).
+EXTRA_FLAGS=<int> adds mrep flags (e.g. 512 = MREP_CAND_EXACT)."""
+import os
 import sys
 
 import torch
@@ -9,7 +11,7 @@ import bench  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 125000
 warm = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 wl = bench.SingleCurve("cfg2", 0, 1, 0)
-flags = wl.tab._cell_flag(1 << 20, True)
+flags = wl.tab._cell_flag(1 << 20, True) | int(os.environ.get("EXTRA_FLAGS", "0"))
 q = wl.q[:n].contiguous()
 for _ in range(warm):
     wl.tab.project(q, extra_flags=flags)

@@ -329,3 +329,43 @@ def test_sorted_and_unsorted_agree(gpu, flags):
     b = [x.cpu().numpy() for x in tab.project(q, extra_flags=f | L.MREP_NO_SORT)[:5]]
     for k in (0, 1, 2, 4):
         assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("name", project_fixture_names())
+def test_exact_cand_matches_reference(gpu, name):
+    """MREP_CAND_EXACT (the Python default): the tensor-core sign screen plus
+    the exact solve of undecided pairs reproduces the reference's candidate
+    count bit for bit, in every traversal mode and through the host call."""
+    from paper_2504_11498_b200 import _device as D, _lib as L
+    z = load_golden(f"project_{name}.npz")
+    tab = D.DeviceTable(*_args(z))
+    for fl in (0, L.MREP_PACKET, L.MREP_GROUP):
+        r = tab.project(z["queries"], extra_flags=L.MREP_CAND_EXACT | fl)
+        assert np.array_equal(r[3].cpu().numpy(), z["cand"]), fl
+    h = tab.project_host(z["queries"], extra_flags=L.MREP_CAND_EXACT)
+    assert np.array_equal(h[3], z["cand"])
+
+
+def test_exact_cand_cfg2_and_extremes_vs_oracle(gpu, oracle_lib):
+    """cfg2's curve (510 cubics) with random, on-curve, seam, far and
+    tiny-scale queries: default project_prepared cand == the C oracle's."""
+    from paper_2504_11498_b200 import BSplineCurve, prepare_curve, project_prepared
+    from paper_2504_11498_b200.fixtures import random_clamped_curve
+    cv = random_clamped_curve(np.random.default_rng(0), 7, 512, 3, uniform_knots=True)
+    rng = np.random.default_rng(5)
+    for scale in (1.0, 1e-3, 1e3):
+        c2 = BSplineCurve(cv.degree, np.array(cv.knots.knots), np.array(cv.control_points) * scale)
+        prep = prepare_curve(c2, 1e-4 * scale)
+        q = np.concatenate([
+            rng.uniform(0, scale, (3000, 3)),                  # random
+            prep.seam_pt[::7],                                  # exactly on seams
+            prep.seg_pts[::5, 1],                               # control points
+            rng.normal(0, 1e3 * scale, (200, 3)),               # far away
+        ])
+        t, foot, dist, cand = project_prepared(prep, q)
+        o = oracle_lib.project_block(prep.seg_pts, prep.seg_ta, prep.seg_tb, prep.seam_t,
+                                     prep.seam_pt, q, workers=8)
+        assert np.array_equal(cand, o["cand"]), (scale, np.nonzero(cand != o["cand"])[0][:10])
+        ts, _, ds, cs = project_prepared(prep, q, cand="screened")
+        assert np.array_equal(ts, t) and np.array_equal(ds, dist)
+        assert np.all(cs <= cand)
