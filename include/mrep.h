@@ -334,6 +334,10 @@ MREP_API int mrep_decompose(const int32_t* degree, const int64_t* knot_ofs, cons
 MREP_API int mrep_eval_bezier(const double* pts, int degree, int d, const double* u, int64_t m,
                               double* out, void* stream);
 /* oracle.eval_de_boor_many (oracle.py:45-52): curve points at nt params */
+/* all basis values N_{i,p}(t) (oracle.py:13-42 _basis_rows): out (n, m - 1 - p),
+ * caller zero-filled; device pointers */
+MREP_API int mrep_basis_rows(int p, const double* knots, int64_t m, const double* ts, int64_t n,
+                             double* out, void* stream);
 MREP_API int mrep_eval_curve(int p, const double* knots, int64_t m, const double* ctrl,
                              int64_t ncp, int d, const double* ts, int64_t nt, double* out,
                              void* stream);

@@ -104,6 +104,7 @@ _SIGS = {
     "mrep_decompose": ([_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _vp,
                         _vp, _vp, _vp], _i32),
     "mrep_eval_bezier": ([_vp, _i32, _i32, _vp, _i64, _vp, _vp], _i32),
+    "mrep_basis_rows": ([_i32, _vp, _i64, _vp, _i64, _vp, _vp], _i32),
     "mrep_eval_curve": ([_i32, _vp, _i64, _vp, _i64, _i32, _vp, _i64, _vp, _vp], _i32),
     "mrep_approx_run": ([_vp, _vp, _vp, _vp, _i64, _i32, _dbl, _i64, _i32, _i32, _i32, _i32,
                          _vp, _vp], _i32),

@@ -65,6 +65,49 @@ __device__ void deboor_point(int p, const double* kn, int64_t m, const double* c
   }
 }
 
+// the p + 1 nonzero basis values of every t, written into its row of the
+// zero-filled (n, m - 1 - p) matrix (oracle.py:13-42's _basis_rows): same
+// span rule and two-term recursion as deboor_point
+__global__ void basis_rows_kernel(int p, const double* kn, int64_t m, const double* ts, int64_t n,
+                                  double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double t = ts[i];
+  const int64_t ncol = m - 1 - p;
+  int64_t s;
+  if (t == kn[m - 1]) {
+    s = m - 2;
+    while (s > 0 && !(kn[s] < kn[s + 1])) --s;
+  } else {
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (kn[mid] <= t) lo = mid + 1;
+      else hi = mid;
+    }
+    s = lo - 1;
+  }
+  if (s < 0 || s >= m - 1 || !(kn[s] < kn[s + 1])) return;  // outside every half-open span
+  double N[32];
+  for (int j = 0; j <= p; ++j) N[j] = 0.0;
+  N[p] = 1.0;
+  for (int lvl = 1; lvl <= p; ++lvl) {
+    for (int j = p - lvl; j <= p; ++j) {
+      int64_t b = s - p + j;
+      double acc = 0.0;
+      double d1 = kn[b + lvl] - kn[b];
+      if (d1 > 0.0) acc += (t - kn[b]) / d1 * N[j];
+      double d2 = kn[b + lvl + 1] - kn[b + 1];
+      if (d2 > 0.0 && j + 1 <= p) acc += (kn[b + lvl + 1] - t) / d2 * N[j + 1];
+      N[j] = acc;
+    }
+  }
+  for (int j = 0; j <= p; ++j) {
+    const int64_t b = s - p + j;
+    if (b >= 0 && b < ncol) out[i * ncol + b] = N[j];
+  }
+}
+
 constexpr int NB_TILE = 512;
 
 __global__ void __launch_bounds__(256) dense_nearest_kernel(const double* pts, int64_t m,
@@ -197,6 +240,18 @@ int mrep_oracle_project_batch(int p, const double* knots, int64_t m, const doubl
   ternary_final_kernel<<<grid_for(n, 256), 256, 0, st>>>(A, out_t, out_dist);
   MREP_LAUNCH_CHECK();
   MREP_CUDA_CHECK(cudaFreeAsync(ws, st));
+  return MREP_OK;
+}
+
+int mrep_basis_rows(int p, const double* knots, int64_t m, const double* ts, int64_t n,
+                    double* out, void* stream) {
+  if (p < 1 || p > 31 || m < p + 2 || n < 0) {
+    set_error("mrep_basis_rows: need 1 <= p <= 31, m >= p + 2, n >= 0");
+    return MREP_ERR_ARG;
+  }
+  if (n == 0) return MREP_OK;
+  basis_rows_kernel<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(p, knots, m, ts, n, out);
+  MREP_LAUNCH_CHECK();
   return MREP_OK;
 }
 

@@ -14,6 +14,21 @@ from . import _lib as L
 from .core import BSplineCurve, DomainError
 
 
+def _basis_rows(knots, p: int, ts) -> np.ndarray:
+    """All basis values N_{i,p}(t), one row per t (oracle.py:13-42): half-open
+    spans, the right domain end on the final nonzero span."""
+    torch = L._torch()
+    kn = np.ascontiguousarray(knots, dtype=np.float64)
+    ts = np.ascontiguousarray(np.asarray(ts, dtype=np.float64).reshape(-1))
+    ncol = len(kn) - 1 - p
+    out = torch.zeros((len(ts), max(ncol, 0)), dtype=torch.float64, device=L.device())
+    if len(ts) and ncol > 0:
+        kd, td = L.to_dev(kn), L.to_dev(ts)
+        L.check(L.lib().mrep_basis_rows(int(p), L.ptr(kd), len(kn), L.ptr(td), len(ts), L.ptr(out),
+                                        L.stream_ptr()))
+    return L.to_host(out)
+
+
 def eval_de_boor_many(curve: BSplineCurve, ts) -> np.ndarray:
     """Curve points at an array of parameters (oracle.py:45-52)."""
     ts = np.ascontiguousarray(np.asarray(ts, dtype=np.float64).reshape(-1))

@@ -56,7 +56,12 @@ def test_table_bytes():
     from paper_2504_11498_b200 import _lib
     lib = _lib.load_library()
     # header 64 + 32 doubles per cubic + 6 per box (8-ary levels incl. root)
-    # + the float copy of every box (6 floats = 3 doubles)
-    assert lib.mrep_table_bytes(1) == (64 + 32 + 9 * (1 + 1)) * 8
-    assert lib.mrep_table_bytes(510) == (64 + 32 * 510 + 9 * (510 + 64 + 8 + 1)) * 8
+    # + the float copy of every box (6 floats = 3 doubles) + the compact seam
+    # block (3 doubles per seam), rounded to 4 doubles, + the tensor-core
+    # B fragments (32 doubles per cubic, two zero fragments of slack)
+    def expect(S, boxes):
+        n = 64 + 32 * S + 9 * boxes + 3 * (S + 1)
+        return (((n + 3) // 4) * 4 + 32 * (S + 2)) * 8
+    assert lib.mrep_table_bytes(1) == expect(1, 2)
+    assert lib.mrep_table_bytes(510) == expect(510, 510 + 64 + 8 + 1)
     assert lib.mrep_table_bytes(0) < 0

@@ -111,8 +111,10 @@ def test_table_layout_levels():
                 break
             cnt = (cnt + 7) // 8
             lv += 1
-        # 6 doubles per box + its float copy (6 floats)
-        assert lib.mrep_table_bytes(S) == (64 + 32 * S + 9 * boxes) * 8
+        # 6 doubles per box + its float copy (6 floats), the compact seam
+        # block, then the tensor-core B fragments (32-B aligned, 2 of slack)
+        n = 64 + 32 * S + 9 * boxes + 3 * (S + 1)
+        assert lib.mrep_table_bytes(S) == (((n + 3) // 4) * 4 + 32 * (S + 2)) * 8
 
 
 def test_nearest_set_locate():
