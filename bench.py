@@ -309,6 +309,12 @@ class CurveSetWorkload:
         self.cset = prepare_curve_set(self.curves, 1e-4)
         torch.cuda.synchronize()
         self.prep_ms = (time.perf_counter() - t0) * 1e3
+        # per-curve cell indices (part of preparation, timed separately)
+        t0 = time.perf_counter()
+        gmax = int(os.environ.get("MREP_SET_GRID", "16"))
+        self.cells_bytes = self.cset.build_cells(gmax) if gmax > 0 else 0
+        torch.cuda.synchronize()
+        self.cells_ms = (time.perf_counter() - t0) * 1e3
         self.n = n_override or c["n"]
         self.n_total = world * self.n
         self.q_host, self.cid_host = self.inputs(rank, world)
@@ -895,9 +901,13 @@ def main():
                                  "NCCL, each chunk's gather overlapping the next chunk's projection"))
             if gather_check is not None:
                 conf["gather_check"] = gather_check
-        if getattr(wl, "cells_ms", None) is not None and getattr(wl.tab, "cells", None) is not None:
-            conf["cell_index"] = {"build_ms": wl.cells_ms,
-                                  "bytes": int(wl.tab.cells.numel() * 4)}
+        if getattr(wl, "cells_ms", None) is not None:
+            if getattr(getattr(wl, "tab", None), "cells", None) is not None:
+                conf["cell_index"] = {"build_ms": wl.cells_ms,
+                                      "bytes": int(wl.tab.cells.numel() * 4)}
+            elif getattr(wl, "cells_bytes", 0):
+                conf["cell_index"] = {"build_ms": wl.cells_ms, "bytes": int(wl.cells_bytes),
+                                      "kind": "one grid per curve (mrep_curveset_cells_build)"}
         sm_sorted = sorted(step_ms)
         conf["step_ms"] = {"median": statistics.median(step_ms), "min": sm_sorted[0],
                            "max": sm_sorted[-1], "argmax": int(np.argmax(step_ms))}

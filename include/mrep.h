@@ -162,6 +162,17 @@ MREP_API int mrep_curveset_create(const double* seg_pts_host, const double* seg_
 MREP_API int mrep_curveset_free(void* set);
 MREP_API int mrep_curveset_info(const void* set, int64_t* ncurves, int64_t* total_cubics, int* d,
                                 int64_t* device_bytes);
+/* Per-curve cell indices for dense / repeated batches (the single-table
+ * mrep_cells_build applied to every curve of the set in one batched build):
+ * curve c gets a grid of clamp(round(2.5 S_c^(1/3)), 4, grid_max) cells per
+ * axis over its root box.  Fails with MREP_ERR_ARG (and builds nothing) when
+ * the index would exceed max_bytes.  Once built, mrep_project_batch scans the
+ * query's cell list instead of walking its curve's hierarchy (same results;
+ * MREP_PACKET / MREP_PER_LANE / MREP_GROUP still force a walk).  Freed with
+ * the set.  Replaces nothing in the reference (a precomputed acceleration
+ * structure of prepare_curve's output, project.py:220-242). */
+MREP_API int mrep_curveset_cells_build(void* set, int grid_max, int64_t max_bytes,
+                                       int64_t* bytes_out, void* stream);
 /* Screened exact projection of query i onto curve curve_ids[i] (int32).
  * Per query, t / foot / dist / segment are those project_prepared returns for
  * that curve alone.  Scheduling (the paper's task scheduler): queries sorted

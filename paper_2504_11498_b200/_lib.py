@@ -67,6 +67,7 @@ _SIGS = {
     "mrep_curveset_create_dev": ([_vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp], _i32),
     "mrep_curveset_create": ([_vp, _vp, _vp, _vp, _i64, _i32, _vp], _i32),
     "mrep_curveset_free": ([_vp], _i32),
+    "mrep_curveset_cells_build": ([_vp, _i32, _i64, _vp, _vp], _i32),
     "mrep_curveset_info": ([_vp, _vp, _vp, _vp, _vp], _i32),
     "mrep_project_batch": ([_vp, _vp, _vp, _i64, _dbl, _i32, _u32, _vp, _vp, _vp, _vp, _vp, _vp,
                             _vp], _i32),

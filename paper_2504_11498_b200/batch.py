@@ -126,6 +126,23 @@ class PreparedCurveSet:
         except Exception:
             pass
 
+    CELL_MAX_BYTES = 16 << 30  # skip the index rather than spend more HBM on it
+
+    def build_cells(self, grid_max=16, max_bytes=None):
+        """Per-curve cell indices (mrep_curveset_cells_build): afterwards every
+        batch scans its query's cell list instead of walking the curve's
+        hierarchy -- same t / foot / dist / segment (cells are exact).  Returns
+        the index size in bytes, or 0 when it would exceed max_bytes (no index)."""
+        nb = ctypes.c_int64()
+        rc = L.lib().mrep_curveset_cells_build(
+            self.handle, int(grid_max), int(self.CELL_MAX_BYTES if max_bytes is None else max_bytes),
+            ctypes.byref(nb), L.stream_ptr())
+        if rc == 1 and b"budget" in L.lib().mrep_last_error():  # MREP_ERR_ARG
+            return 0
+        L.check(rc)
+        self.cells_bytes = nb.value
+        return nb.value
+
     # ------------------------------------------------------------ projection
     def project_device(self, queries, curve_ids, clip_tol=1e-6, max_iter=8, counters=None,
                        extra_flags=0):
@@ -199,6 +216,7 @@ def prepare_curve_set(curves, tolerance: float = 1e-4, batch_cap: int = 4096) ->
     res = approximate_device(dec["rows"], dec["row_ofs"], dec["iv"], dec["curve"], dec["nseg"], d,
                              tolerance, cap)
     pts, iv, err, cid = res.fetch()
+    res.free()
     counts = torch.bincount(cid.to(torch.int64), minlength=len(curves))
     ofs = np.concatenate(([0], np.cumsum(L.to_host(counts)))).astype(np.int64)
     if np.any(np.diff(ofs) < 1):

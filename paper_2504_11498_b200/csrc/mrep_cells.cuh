@@ -207,29 +207,30 @@ __device__ void cell_leaves(const TableView& T, const CellGrid& g, const double*
 }
 
 template <class LP>
-__global__ void cells_count_kernel(const __grid_constant__ TableView T, const LP lp,
-                                   const __grid_constant__ CellGrid g, int32_t* cnt) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= g.ncell) return;
+__device__ int32_t cell_count(const TableView& T, const LP& lp, const CellGrid& g, int64_t c) {
   double lo[3], hi[3];
   cell_box(g, c, lo, hi);
   const double c2 = cell_cut2(T, lp, g, lo, hi);
   int32_t n = 0;
   cell_leaves(T, g, lo, hi, c2, [&](int64_t) { ++n; });
-  cnt[c] = n;
+  return n;
 }
 
 template <class LP>
-__global__ void cells_fill_kernel(const __grid_constant__ TableView T, const LP lp,
-                                  const __grid_constant__ CellGrid g, const int32_t* off,
-                                  int32_t* ids, float* keys) {
+__global__ void cells_count_kernel(const __grid_constant__ TableView T, const LP lp,
+                                   const __grid_constant__ CellGrid g, int32_t* cnt) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= g.ncell) return;
+  cnt[c] = cell_count(T, lp, g, c);
+}
+
+// fill one cell's list (ids + sort keys) in the order the scan expects
+template <class LP>
+__device__ void cell_fill_list(const TableView& T, const LP& lp, const CellGrid& g, int64_t c,
+                               int32_t* out, float* key) {
   double lo[3], hi[3];
   cell_box(g, c, lo, hi);
   const double c2 = cell_cut2(T, lp, g, lo, hi);
-  int32_t* out = ids + off[c];
-  float* key = keys + off[c];
   int32_t n = 0;
   cell_leaves(T, g, lo, hi, c2, [&](int64_t s) { out[n++] = (int32_t)s; });
   // key = distance^2 from the (grown) cell to the leaf box, rounded down: a
@@ -266,23 +267,23 @@ __global__ void cells_fill_kernel(const __grid_constant__ TableView T, const LP 
   }
 }
 
-// grid over the table's root box (host side; reads the root box and scale)
-inline int cell_grid(const void* table, int64_t S, int d, int grid, int rec, cudaStream_t st,
-                     TableView& T, CellGrid& g) {
-  if (S < 1 || (d != 2 && d != 3) || grid < 1 || grid > 512 || !table) {
-    set_error("mrep_cells: need S >= 1, d in {2,3}, 1 <= grid <= 512");
-    return MREP_ERR_ARG;
-  }
-  T = table_view(table, S, rec);
-  double root[6], hdr5[5];
-  MREP_CUDA_CHECK(cudaMemcpyAsync(root, T.box + T.lvl_off[T.top] * 6, sizeof root,
-                                  cudaMemcpyDeviceToHost, st));
-  MREP_CUDA_CHECK(cudaMemcpyAsync(hdr5, T.hdr, sizeof hdr5, cudaMemcpyDeviceToHost, st));
-  MREP_CUDA_CHECK(cudaStreamSynchronize(st));
+template <class LP>
+__global__ void cells_fill_kernel(const __grid_constant__ TableView T, const LP lp,
+                                  const __grid_constant__ CellGrid g, const int32_t* off,
+                                  int32_t* ids, float* keys) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= g.ncell) return;
+  cell_fill_list(T, lp, g, c, ids + off[c], keys + off[c]);
+}
+
+// the grid of a table: uniform over its root box grown by 10% each side
+// (shared by the host builder below and the per-curve builder of curve sets)
+__host__ __device__ inline void grid_from_root(const double* root, double hscale, int grid, int d,
+                                               CellGrid& g) {
   g = CellGrid{};
   g.G = grid;
   g.d = d;
-  g.hscale = hdr5[4];
+  g.hscale = hscale;
   double ext_max = 0.0;
   for (int k = 0; k < 3; ++k) {
     if (k < d) {
@@ -297,6 +298,37 @@ inline int cell_grid(const void* table, int64_t S, int d, int grid, int rec, cud
   }
   g.eps = 1e-9 * (ext_max + g.hscale);
   g.ncell = (int64_t)grid * grid * (d == 3 ? grid : 1);
+}
+
+// header words of a table whose cell index starts at `cells` (cells_build
+// writes them with one copy, the curve-set builder from a kernel)
+__host__ __device__ inline void cells_header(const CellGrid& g, const void* cells, int64_t total,
+                                             double* h) {
+  uint64_t bits = (uint64_t)(uintptr_t)cells;
+  memcpy(&h[0], &bits, 8);
+  h[1] = g.G;
+  for (int k = 0; k < 3; ++k) {
+    h[2 + k] = g.glo[k];
+    h[5 + k] = 1.0 / g.h[k];
+    h[8 + k] = g.glo[k] + g.h[k] * g.G;
+  }
+  h[11] = (double)total;
+}
+
+// grid over the table's root box (host side; reads the root box and scale)
+inline int cell_grid(const void* table, int64_t S, int d, int grid, int rec, cudaStream_t st,
+                     TableView& T, CellGrid& g) {
+  if (S < 1 || (d != 2 && d != 3) || grid < 1 || grid > 512 || !table) {
+    set_error("mrep_cells: need S >= 1, d in {2,3}, 1 <= grid <= 512");
+    return MREP_ERR_ARG;
+  }
+  T = table_view(table, S, rec);
+  double root[6], hdr5[5];
+  MREP_CUDA_CHECK(cudaMemcpyAsync(root, T.box + T.lvl_off[T.top] * 6, sizeof root,
+                                  cudaMemcpyDeviceToHost, st));
+  MREP_CUDA_CHECK(cudaMemcpyAsync(hdr5, T.hdr, sizeof hdr5, cudaMemcpyDeviceToHost, st));
+  MREP_CUDA_CHECK(cudaStreamSynchronize(st));
+  grid_from_root(root, hdr5[4], grid, d, g);
   return MREP_OK;
 }
 
@@ -369,15 +401,7 @@ int cells_build(void* table, int64_t S, int d, int grid, int rec, const LP& lp, 
   // header: cell index pointer, grid, lower corner, inverse cell size, upper
   // corner, number of list entries
   double h[12];
-  uint64_t bits = (uint64_t)(uintptr_t)cells;
-  memcpy(&h[0], &bits, 8);
-  h[1] = grid;
-  for (int k = 0; k < 3; ++k) {
-    h[2 + k] = g.glo[k];
-    h[5 + k] = 1.0 / g.h[k];
-    h[8 + k] = g.glo[k] + g.h[k] * grid;
-  }
-  h[11] = (double)total;
+  cells_header(g, cells, total, h);
   MREP_CUDA_CHECK(cudaMemcpyAsync((double*)table + H_CELLS, h, sizeof h, cudaMemcpyHostToDevice, st));
   MREP_CUDA_CHECK(cudaStreamSynchronize(st));  // h dies here
   return MREP_OK;

@@ -290,6 +290,18 @@ int host_pipeline(HostCtx& g_ctx, int d, const double* queries, const int32_t* c
         }
       }
       if (last > 0) cl.push_back({n - last, last});
+    } else if (getenv("MREP_E2E_FIRST") && !getenv("MREP_E2E_CHUNK")) {
+      // geometric schedule: first chunk MREP_E2E_FIRST queries, each next
+      // one MREP_E2E_GEOM times larger (the last takes the remainder)
+      const double r = getenv("MREP_E2E_GEOM") ? atof(getenv("MREP_E2E_GEOM")) : 2.0;
+      double sz = (double)std::max<int64_t>(4096, atoll(getenv("MREP_E2E_FIRST")));
+      for (int64_t lo2 = 0; lo2 < n;) {
+        int64_t c2 = std::min<int64_t>(n - lo2, ((int64_t)sz + 4095) & ~(int64_t)4095);
+        if (n - lo2 - c2 < c2 / 4) c2 = n - lo2;  // no sliver at the end
+        cl.push_back({lo2, c2});
+        lo2 += c2;
+        sz *= r;
+      }
     } else {
       const int64_t CHU = getenv("MREP_E2E_CHUNK")
                               ? CH
@@ -306,6 +318,7 @@ int host_pipeline(HostCtx& g_ctx, int d, const double* queries, const int32_t* c
       g_ctx.ev_in.push_back(a);
       g_ctx.ev_comp.push_back(b);
     }
+    static const int conc = getenv("MREP_E2E_CONC") ? atoi(getenv("MREP_E2E_CONC")) : 0;
     static const bool dtrace = getenv("MREP_E2E_TRACE") != nullptr;
     std::vector<cudaEvent_t> te;  // per chunk: upload end, kernels end, download end
     cudaEvent_t te0 = nullptr;
@@ -345,6 +358,9 @@ int host_pipeline(HostCtx& g_ctx, int d, const double* queries, const int32_t* c
       MREP_CUDA_CHECK(cudaEventRecord(g_ctx.ev_in[c], ci));
       tmark(ci);
       MREP_CUDA_CHECK(cudaStreamWaitEvent(v.st, g_ctx.ev_in[c], 0));
+      // at most `conc` chunks' kernels in flight (MREP_E2E_CONC; default all)
+      if (conc > 0 && c >= conc)
+        MREP_CUDA_CHECK(cudaStreamWaitEvent(v.st, g_ctx.ev_comp[c - conc], 0));
       const auto t_l0 = std::chrono::steady_clock::now();
       if ((rc = launch(v)) != MREP_OK) return rc;
       if (dtrace)
@@ -381,7 +397,8 @@ int host_pipeline(HostCtx& g_ctx, int d, const double* queries, const int32_t* c
         cudaEventElapsedTime(&a, te0, te[k]);
         cudaEventElapsedTime(&b, te0, te[k + 1]);
         cudaEventElapsedTime(&e, te0, te[k + 2]);
-        fprintf(stderr, "chunk %zu: h2d_end %.3f  kern_end %.3f  d2h_end %.3f\n", k / 3, a, b, e);
+        fprintf(stderr, "chunk %zu n=%lld: h2d_end %.3f  kern_end %.3f  d2h_end %.3f\n", k / 3,
+                (long long)cl[k / 3].second, a, b, e);
       }
       for (auto ev : te) cudaEventDestroy(ev);
       cudaEventDestroy(te0);

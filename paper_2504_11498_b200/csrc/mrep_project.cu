@@ -3012,7 +3012,10 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
     }
   } else if (MULTI) {
     unsigned need = grid_for(n, BLOCK);
-    if (tmode == TRAV_PACKET) {
+    if (tmode == TRAV_CELLS) {
+      unsigned g = persist_grid((const void*)wave_traverse<D, true, TM_CELLS>, BLOCK);
+      wave_traverse<D, true, TM_CELLS><<<g < need ? g : need, BLOCK, 0, st>>>(w);
+    } else if (tmode == TRAV_PACKET) {
       unsigned g = persist_grid((const void*)wave_traverse<D, true, TM_PACKET>, BLOCK);
       wave_traverse<D, true, TM_PACKET><<<g < need ? g : need, BLOCK, 0, st>>>(w);
     } else {
@@ -3063,6 +3066,10 @@ struct CurveSet {
   uint32_t* rank = nullptr;   // device, [nc]: position in decreasing-cubic-count order
   uint32_t* order = nullptr;  // device, [nc]: curve of each rank (inverse of rank)
   std::vector<int64_t> ofs;   // host, [nc + 1] cubic offsets
+  // per-curve cell indices (mrep_curveset_cells_build): one allocation, each
+  // curve's index referenced from its own table header
+  char* cells = nullptr;
+  int64_t cells_bytes = 0;
 };
 
 // number of AABB boxes of an S-cubic table (all levels), as table_layout
@@ -3302,6 +3309,163 @@ int set_create(const double* seg_pts, const double* seg_ta, const double* seg_tb
   return MREP_OK;
 }
 
+// ------------------------------------------------------------ curve-set cell indices
+// Every curve of a set gets the single-table cell index (mrep_cells.cuh):
+// a uniform grid over its root box, each cell listing the cubics that can
+// hold a tie-band candidate for any query of the cell, nearest first.  The
+// grid of curve c has G_c = clamp(round(2.5 S_c^(1/3)), 4, gmax) cells per
+// axis.  All curves are built together: one thread per (curve, cell) counts
+// and fills, one scan sizes every list, and a kernel writes each curve's
+// header words, so the build costs a handful of launches for 10^4 curves.
+// Layout (int32 words): curve c's index starts at cstart_c + c + 2 E_c
+// (E = exclusive scan of the counts over all cells of all curves):
+// offsets [ncell_c + 1], leaf ids [tot_c], float keys [tot_c] -- exactly
+// what cell_list / cell_keys read for a single table.
+__device__ __forceinline__ int64_t set_cell_owner(const int64_t* cstart, int64_t nc, int64_t i) {
+  int64_t lo = 0, hi = nc;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (cstart[mid] <= i) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void set_grid_kernel(const TableView* desc, const int32_t* G, int64_t nc, int d,
+                                CellGrid* grids) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  const TableView& T = desc[c];
+  grid_from_root(T.box + T.lvl_off[T.top] * 6, T.hdr[4], G[c], d, grids[c]);
+}
+
+__global__ void set_cells_count_kernel(const TableView* desc, const CellGrid* grids,
+                                       const int64_t* cstart, int64_t nc, int64_t ncell,
+                                       int32_t* cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ncell) return;
+  const int64_t c = set_cell_owner(cstart, nc, i);
+  cnt[i] = cell_count(desc[c], CurveLeaves{}, grids[c], i - cstart[c]);
+}
+
+__global__ void set_cells_header_kernel(const TableView* desc, const CellGrid* grids,
+                                        const int64_t* cstart, const int64_t* E, int64_t nc,
+                                        int32_t* mem) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  const int64_t e0 = E[cstart[c]], tot = E[cstart[c + 1]] - e0;
+  int32_t* off = mem + cstart[c] + c + 2 * e0;
+  off[cstart[c + 1] - cstart[c]] = (int32_t)tot;
+  cells_header(grids[c], off, tot, const_cast<double*>(desc[c].hdr) + H_CELLS);
+}
+
+__global__ void set_cells_fill_kernel(const TableView* desc, const CellGrid* grids,
+                                      const int64_t* cstart, const int64_t* E, int64_t nc,
+                                      int64_t ncell, int32_t* mem) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ncell) return;
+  const int64_t c = set_cell_owner(cstart, nc, i);
+  const int64_t e0 = E[cstart[c]], tot = E[cstart[c + 1]] - e0, nloc = cstart[c + 1] - cstart[c];
+  int32_t* off = mem + cstart[c] + c + 2 * e0;
+  const int32_t at = (int32_t)(E[i] - e0);
+  off[i - cstart[c]] = at;
+  int32_t* ids = off + nloc + 1;
+  cell_fill_list(desc[c], CurveLeaves{}, grids[c], i - cstart[c], ids + at,
+                 reinterpret_cast<float*>(ids + tot) + at);
+}
+
+static int set_cells_build(CurveSet* cs, int gmax, int64_t max_bytes, cudaStream_t st) {
+  if (gmax < 1 || gmax > 64) {
+    set_error("mrep_curveset_cells_build: grid_max in [1, 64]");
+    return MREP_ERR_ARG;
+  }
+  if (cs->max_top > 7) {
+    set_error("mrep_curveset_cells_build: a curve's hierarchy is too deep (> 8^7 cubics)");
+    return MREP_ERR_ARG;
+  }
+  const int64_t nc = cs->nc;
+  const int d = cs->d;
+  std::vector<int32_t> G(nc);
+  std::vector<int64_t> cstart(nc + 1, 0);
+  for (int64_t c = 0; c < nc; ++c) {
+    const double S = (double)(cs->ofs[c + 1] - cs->ofs[c]);
+    int g = (int)std::lround(2.5 * std::cbrt(S));
+    g = std::max(4, std::min(gmax, g));
+    G[c] = g;
+    cstart[c + 1] = cstart[c] + (int64_t)g * g * (d == 3 ? g : 1);
+  }
+  const int64_t ncell = cstart[nc];
+  if (ncell + nc + 1 > INT32_MAX) {
+    set_error("mrep_curveset_cells_build: too many cells; lower grid_max");
+    return MREP_ERR_ARG;
+  }
+  // scratch: grids, G, cstart, counts (int32) and their scan (int64, ncell + 1)
+  auto al = [](int64_t b) { return (b + 255) & ~(int64_t)255; };
+  const int64_t o_grid = 0, o_G = al(nc * (int64_t)sizeof(CellGrid)), o_cs = o_G + al(nc * 4);
+  const int64_t o_cnt = o_cs + al((nc + 1) * 8), o_E = o_cnt + al((ncell + 1) * 4);
+  size_t scan_tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (const int32_t*)nullptr, (int64_t*)nullptr,
+                                (int)(ncell + 1), st);
+  const int64_t o_tmp = o_E + al((ncell + 1) * 8), scratch = o_tmp + al((int64_t)scan_tmp + 16);
+  char* ws = nullptr;
+  MREP_CUDA_CHECK(cudaMallocAsync((void**)&ws, scratch, st));
+  CellGrid* grids = (CellGrid*)(ws + o_grid);
+  int32_t* Gd = (int32_t*)(ws + o_G);
+  int64_t* csd = (int64_t*)(ws + o_cs);
+  int32_t* cnt = (int32_t*)(ws + o_cnt);
+  int64_t* E = (int64_t*)(ws + o_E);
+  int rc = MREP_OK;
+  auto fail = [&](int code) {
+    cudaFreeAsync(ws, st);
+    cudaStreamSynchronize(st);
+    return code;
+  };
+  MREP_CUDA_CHECK(cudaMemcpyAsync(Gd, G.data(), nc * 4, cudaMemcpyHostToDevice, st));
+  MREP_CUDA_CHECK(cudaMemcpyAsync(csd, cstart.data(), (nc + 1) * 8, cudaMemcpyHostToDevice, st));
+  MREP_CUDA_CHECK(cudaMemsetAsync(cnt + ncell, 0, 4, st));
+  set_grid_kernel<<<grid_for(nc, 128), 128, 0, st>>>(cs->desc, Gd, nc, d, grids);
+  set_cells_count_kernel<<<grid_for(ncell, 128), 128, 0, st>>>(cs->desc, grids, csd, nc, ncell, cnt);
+  MREP_LAUNCH_CHECK();
+  MREP_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ws + o_tmp, scan_tmp, cnt, E, (int)(ncell + 1), st));
+  int64_t total = 0;
+  MREP_CUDA_CHECK(cudaMemcpyAsync(&total, E + ncell, 8, cudaMemcpyDeviceToHost, st));
+  MREP_CUDA_CHECK(cudaStreamSynchronize(st));
+  const int64_t words = ncell + nc + 2 * total;
+  if (words > INT32_MAX || 4 * words > max_bytes) {
+    set_error("mrep_curveset_cells_build: the index needs " + std::to_string(4 * words) +
+              " bytes (budget " + std::to_string(max_bytes) + ", int32 offsets)");
+    return fail(MREP_ERR_ARG);
+  }
+  char* mem = nullptr;
+  cudaError_t e = cudaMalloc(&mem, (size_t)(4 * words + 256));
+  if (e != cudaSuccess) {
+    set_error(std::string("mrep_curveset_cells_build: cudaMalloc: ") + cudaGetErrorString(e));
+    return fail(MREP_ERR_CUDA);
+  }
+  set_cells_fill_kernel<<<grid_for(ncell, 128), 128, 0, st>>>(cs->desc, grids, csd, E, nc, ncell,
+                                                             (int32_t*)mem);
+  set_cells_header_kernel<<<grid_for(nc, 128), 128, 0, st>>>(cs->desc, grids, csd, E, nc,
+                                                            (int32_t*)mem);
+  if ((e = cudaGetLastError()) != cudaSuccess) {
+    set_error(std::string("mrep_curveset_cells_build: launch: ") + cudaGetErrorString(e));
+    rc = MREP_ERR_CUDA;
+  }
+  cudaFreeAsync(ws, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess && !rc) {
+    set_error(std::string("mrep_curveset_cells_build: ") + cudaGetErrorString(e));
+    rc = MREP_ERR_CUDA;
+  }
+  if (rc) {
+    cudaFree(mem);
+    return rc;
+  }
+  // the headers now point at the new index: the old one (if any) can go
+  if (cs->cells) cudaFree(cs->cells);
+  cs->cells = mem;
+  cs->cells_bytes = 4 * words;
+  return MREP_OK;
+}
+
 static int project_batch_chunk(const CurveSet* cs, const double* queries, const int32_t* qcurve,
                                int64_t n, double clip_tol, int max_iter, unsigned flags,
                                double* out_t, double* out_foot, double* out_dist,
@@ -3321,6 +3485,10 @@ static int project_batch_chunk(const CurveSet* cs, const double* queries, const 
   p.out_cand = out_cand;
   p.out_seg = out_seg;
   p.counters = counters;
+  // a set with per-curve cell indices scans them (unless a walk is forced)
+  static const bool no_set_cells = getenv("MREP_SET_NO_CELLS") != nullptr;
+  if (cs->cells && !no_set_cells && !(flags & (MREP_PACKET | MREP_PER_LANE | MREP_GROUP)))
+    flags |= MREP_CELLS;
   const int tmode0 = trav_mode(flags, n, cs->S_total, cs->max_top);
   // Sparse batches (group walks, each query's work a function of the query
   // alone) are ordered by a counting sort on the curve's scheduler rank:
@@ -3328,9 +3496,10 @@ static int project_batch_chunk(const CurveSet* cs, const double* queries, const 
   // instead of Morton keys + a 64-bit radix sort.  Dense batches (packet
   // walks, where warp composition matters) keep the (rank, Morton) radix sort.
   static const bool radix_env = getenv("MREP_RADIX_SORT") != nullptr;
-  const bool counting = tmode0 == TRAV_GROUP && !radix_env && n < ((int64_t)1 << 32);
+  const bool counting = (tmode0 == TRAV_GROUP || tmode0 == TRAV_CELLS) && !radix_env &&
+                        n < ((int64_t)1 << 32);
   static const bool stage_env = getenv("MREP_STAGE") != nullptr;
-  const bool staged = counting && stage_env;
+  const bool staged = counting && stage_env && tmode0 == TRAV_GROUP;
   const int end_bit = 10 * d + cs->rank_bits;
   // curve rank + the top 12 Morton bits: a curve holds ~10^2 queries, so a
   // 16^3 cell grid already makes warps spatially coherent (fewer passes)
@@ -3674,12 +3843,28 @@ int mrep_curveset_free(void* set) {
   CurveSet* cs = (CurveSet*)set;
   if (!cs) return MREP_OK;
   cudaError_t e = cudaFree(cs->mem);
+  if (cs->cells) {
+    cudaError_t e2 = cudaFree(cs->cells);
+    if (e == cudaSuccess) e = e2;
+  }
   delete cs;
   if (e != cudaSuccess) {
     set_error(std::string("mrep_curveset_free: ") + cudaGetErrorString(e));
     return MREP_ERR_CUDA;
   }
   return MREP_OK;
+}
+
+int mrep_curveset_cells_build(void* set, int grid_max, int64_t max_bytes, int64_t* bytes_out,
+                              void* stream) {
+  CurveSet* cs = (CurveSet*)set;
+  if (!cs) {
+    set_error("mrep_curveset_cells_build: null set");
+    return MREP_ERR_ARG;
+  }
+  int rc = set_cells_build(cs, grid_max, max_bytes, (cudaStream_t)stream);
+  if (bytes_out) *bytes_out = cs->cells_bytes;
+  return rc;
 }
 
 int mrep_curveset_info(const void* set, int64_t* ncurves, int64_t* total_cubics, int* d,

@@ -300,6 +300,7 @@ def prepare_curves(curves, tolerance: float = 1e-4, batch_cap: int = 4096):
         res = approximate_device(dec["rows"], dec["row_ofs"], dec["iv"], dec["curve"],
                                  dec["nseg"], d, tolerance, batch_cap)
         pts, iv, err, cid = res.fetch()
+        res.free()
         cid_h = L.to_host(cid)
         bounds = np.searchsorted(cid_h, np.arange(len(batch) + 1))
         for j, i in enumerate(idx):

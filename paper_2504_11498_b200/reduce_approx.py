@@ -173,11 +173,16 @@ class ApproxResult:
             out.append(SubdivisionLevel(recs, prefix, keys[:F]))
         return out
 
+    def free(self):
+        """Release the device buffers now (prepare paths call this right
+        after fetch() instead of waiting for garbage collection)."""
+        if self.handle:
+            L.load_library().mrep_approx_free(self.handle)
+            self.handle = None
+
     def __del__(self):
         try:
-            if self.handle:
-                L.load_library().mrep_approx_free(self.handle)
-                self.handle = None
+            self.free()
         except Exception:
             pass
 
@@ -222,6 +227,6 @@ def approximate_error_controlled(segments, tol: float, batch_cap: int = 4096,
     pts, ivs, err = L.to_host(pts), L.to_host(ivs), L.to_host(err)
     cubics = [CubicApproxSegment(pts[i], (ivs[i, 0], ivs[i, 1]), float(err[i]))
               for i in range(res.count)]
-    if collect_levels:
-        return cubics, res.levels()
-    return cubics
+    levels = res.levels() if collect_levels else None
+    res.free()
+    return (cubics, levels) if collect_levels else cubics

@@ -66,12 +66,16 @@ def stage_batch():
     for mode in (L.MREP_PACKET, L.MREP_PER_LANE, L.MREP_GROUP):
         cs.project_device(L.to_dev(q), L.to_dev(cid, torch.int32), extra_flags=mode)
     cs.project_host(q, cid)
+    cs.build_cells(8)
+    cs.project_device(L.to_dev(q), L.to_dev(cid, torch.int32))
+    cs.free()
 
 
 def stage_nearest():
     cs = prepare_curve_set(mixed_curve_batch(6, max_control=64))
     ns = prepare_nearest_set([cs[i] for i in range(6)])
     project_nearest(ns, np.random.default_rng(4).uniform(0, 1, (N, 3)))
+    cs.free()
 
 
 def stage_surface():

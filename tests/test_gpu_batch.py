@@ -161,3 +161,41 @@ def test_batch_edge_cases(gpu):
     assert r[2][1] == 0.0
     with pytest.raises(DomainError):
         prepare_curve_set([single_span_cubic(2), single_span_cubic(3)])
+
+
+def test_curve_set_cells_bitwise_equal_to_walks(gpu):
+    """Per-curve cell indices (mrep_curveset_cells_build) are exact: the cell
+    scan returns the walks' t / foot / dist / segment bit for bit, including
+    queries outside their curve's grid (they walk the tree) and bad ids."""
+    import torch
+    from paper_2504_11498_b200 import _lib as L, prepare_curve_set
+    from paper_2504_11498_b200.fixtures import mixed_curve_batch, single_span_cubic
+    curves = mixed_curve_batch(80, first_seed=700, max_control=700)
+    cs = prepare_curve_set(curves)
+    rng = np.random.default_rng(11)
+    cid = rng.integers(0, len(curves), 20000).astype(np.int32)
+    q = rng.uniform(0, 1, (len(cid), 3))
+    q[::7] = rng.uniform(-1.0, 2.0, (len(q[::7]), 3))  # many outside the grids
+    cid[5] = 999
+    qd, cd = torch.from_numpy(q).cuda(), torch.from_numpy(cid).cuda()
+    ref = [x.cpu().numpy() for x in cs.project_device(qd, cd, extra_flags=L.MREP_GROUP)]
+    for gmax in (4, 16):
+        nb = cs.build_cells(gmax)
+        assert nb > 0
+        got = [x.cpu().numpy() for x in cs.project_device(qd, cd)]
+        for k in (0, 1, 2, 4):
+            assert np.array_equal(got[k], ref[k], equal_nan=True), (gmax, k)
+        # forced walks still walk (and agree)
+        lane = [x.cpu().numpy() for x in cs.project_device(qd, cd, extra_flags=L.MREP_PER_LANE)]
+        assert np.array_equal(lane[2], ref[2], equal_nan=True)
+    # a budget too small builds nothing and keeps the old index usable
+    assert cs.build_cells(16, max_bytes=1024) == 0
+    # host pipeline over an indexed set
+    out = cs.project_host(q, np.where(cid == 999, 0, cid))
+    assert np.all(np.isfinite(out[0]))
+    # 2-D set
+    cs2 = prepare_curve_set([single_span_cubic(2), single_span_cubic(2)])
+    assert cs2.build_cells(8) > 0
+    r = cs2.project_device(torch.tensor([[0.5, 0.5], [0.0, 0.0]], dtype=torch.float64).cuda(),
+                           torch.tensor([0, 1], dtype=torch.int32).cuda())
+    assert r[2].cpu().numpy()[1] == 0.0
