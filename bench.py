@@ -222,6 +222,66 @@ def cpu_time(jobs, workers):
     return nq, time.perf_counter() - t0
 
 
+def _prep_one(args):
+    """oracle/prep.py prepare() of one curve (the reference's numpy
+    decomposition + error-controlled approximation, restated): cubic count."""
+    from oracle import prep as P
+    p, knots, ctrl = args
+    return len(P.prepare(p, knots, ctrl, 1e-4)["cubics"])
+
+
+def prep_measure(wl, cfg, cpu_sample_s=8.0):
+    """Subsystem 1 (decomposition + approximation + packing) on the GPU vs the
+    oracle's numpy restatement of the reference preprocessing on host cores."""
+    import torch
+    from concurrent.futures import ProcessPoolExecutor
+    from paper_2504_11498_b200 import BSplineCurve, prepare_curve, prepare_curve_set
+    if cfg == "cfg3":
+        curves = [(c.degree, np.asarray(c.knots.knots), np.asarray(c.control_points))
+                  for c in wl.curves]
+        reps, S = 2, wl.num_segments
+        run = lambda: prepare_curve_set(wl.curves, 1e-4).free()  # noqa: E731
+    else:
+        curves = [wl.curve]
+        reps, S = 5, wl.num_segments
+        run = lambda: prepare_curve(BSplineCurve(*wl.curve), 1e-4)  # noqa: E731
+    run()
+    ts = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        run()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    gpu_s = statistics.median(ts)
+    # CPU: a stratified sample of the same curves, one process per core
+    cores = len(os.sched_getaffinity(0))
+    if len(curves) == 1:
+        sample, desc = curves, "the same curve, single-threaded (one curve has one serial level loop)"
+        cores_used = 1
+    else:
+        k = max(cores * 3, 16)
+        idx = np.linspace(0, len(curves) - 1, k).astype(int)
+        sample = [curves[i] for i in idx]
+        desc = f"{k} of the {len(curves)} curves (evenly spaced), one process per core"
+        cores_used = cores
+    t0 = time.perf_counter()
+    if cores_used == 1:
+        nc = sum(_prep_one(c) for c in sample)
+    else:
+        with ProcessPoolExecutor(cores_used) as ex:
+            nc = sum(ex.map(_prep_one, sample))
+    cpu_s = time.perf_counter() - t0
+    return {"what": "prepare_curve / prepare_curve_set: knot-insertion decomposition, G1 "
+                    "reduction + error-controlled subdivision, packing (north-star subsystem 1)",
+            "gpu_ms": gpu_s * 1e3, "cubics": int(S), "cubics_per_s": S / gpu_s,
+            "cpu": {"cubics_per_s": nc / cpu_s, "cores": cores_used, "kind": "port",
+                    "sample": f"{desc}: {nc} cubics in {cpu_s:.1f} s; oracle/prep.py, the "
+                              f"reference's numpy preprocessing restated (bit-exact goldens)"},
+            "kernels": "approx_eval_kernel / approx_child_kernel / decompose_kernel "
+                       "(profiles/r02_prep_launch_shares.txt)"}
+
+
 def _seg(prep):
     return (prep.seg_pts, prep.seg_ta, prep.seg_tb, prep.seam_t, prep.seam_pt)
 
@@ -311,7 +371,7 @@ class CurveSetWorkload:
         self.prep_ms = (time.perf_counter() - t0) * 1e3
         # per-curve cell indices (part of preparation, timed separately)
         t0 = time.perf_counter()
-        gmax = int(os.environ.get("MREP_SET_GRID", "16"))
+        gmax = int(os.environ.get("MREP_SET_GRID", "12"))
         self.cells_bytes = self.cset.build_cells(gmax) if gmax > 0 else 0
         torch.cuda.synchronize()
         self.cells_ms = (time.perf_counter() - t0) * 1e3
@@ -894,6 +954,10 @@ def main():
                              f"_kernels._project_block, bit-exact vs the reference"}
         conf = dict(workload_config(args.config, n), parallelism=f"query-shard x{world}",
                     prep_ms=wl.prep_ms, cubics=wl.num_segments)
+        prep_line = None
+        if (world == 1 and not args.no_cpu_baseline and not surf
+                and args.config in ("cfg2", "cfg3")):
+            prep_line = prep_measure(wl, args.config)
         if world > 1:
             conf["gather"] = (f"(t, distance, segment id) to rank 0 in {chunks} chunks per step, "
                               + ("gloo through host memory (ranks share a GPU: a logic test, "
@@ -917,6 +981,8 @@ def main():
                 "dtype": "f64", "data": "synthetic", "config": conf,
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks.summary()}
+        if prep_line is not None:
+            line["preparation"] = prep_line
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

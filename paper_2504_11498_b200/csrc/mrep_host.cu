@@ -290,6 +290,18 @@ int host_pipeline(HostCtx& g_ctx, int d, const double* queries, const int32_t* c
         }
       }
       if (last > 0) cl.push_back({n - last, last});
+    } else if (getenv("MREP_E2E_SIZES") && !getenv("MREP_E2E_CHUNK")) {
+      // explicit chunk sizes, comma separated; the remainder is one more chunk
+      const char* e = getenv("MREP_E2E_SIZES");
+      int64_t lo2 = 0;
+      while (*e && lo2 < n) {
+        const int64_t c2 = std::min<int64_t>(n - lo2, std::max<int64_t>(1024, atoll(e)));
+        cl.push_back({lo2, c2});
+        lo2 += c2;
+        while (*e && *e != ',') ++e;
+        if (*e == ',') ++e;
+      }
+      if (lo2 < n) cl.push_back({lo2, n - lo2});
     } else if (getenv("MREP_E2E_FIRST") && !getenv("MREP_E2E_CHUNK")) {
       // geometric schedule: first chunk MREP_E2E_FIRST queries, each next
       // one MREP_E2E_GEOM times larger (the last takes the remainder)

@@ -1102,8 +1102,10 @@ struct WaveParams {
   uint32_t* sq;
   uint32_t* ssk;  // cubic << 3 | piece
   unsigned long long scap;
-  uint32_t* chead;  // per sorted query: last candidate appended (linked list), ~0 = none
-  Cand* cand;       // candidate records (one 32-B sector each)
+  uint32_t* ccnt;   // per sorted query: candidates appended so far
+  Cand* cin;        // per sorted query: the first CIN candidates, inline ([n][CIN])
+  uint32_t* chead;  // per sorted query: last overflow candidate (linked list), ~0 = none
+  Cand* cand;       // overflow candidate records (one 32-B sector each)
   unsigned long long ccap;
   int64_t* fb;
   // multi-curve batch (mrep_project_batch): per-curve table descriptors, the
@@ -1118,6 +1120,25 @@ struct WaveParams {
   int32_t* gcur;
   unsigned long long* queue;
 };
+
+// A query's first CIN candidates live inline in its own [CIN] row of `cin`
+// (sorted order: the emit pass reads them as one coalesced 64-B run per
+// query instead of chasing a linked list through a shared append buffer);
+// later ones (rare: a tie band with many members) go to the overflow buffer,
+// linked from chead.  Any thread may append for any query.
+constexpr int CIN = 2;
+__device__ __forceinline__ bool add_cand(const WaveParams& w, int64_t g, double t, double d,
+                                         double v, uint32_t ord) {
+  const uint32_t k = atomicAdd(&w.ccnt[g], 1u);
+  if (k < CIN) {
+    put_cand(w.cin + g * CIN + k, t, d, v, ord, ~0u);
+    return true;
+  }
+  const unsigned long long slot = atomicAdd(&w.cnt[2], 1ull);
+  if (slot >= w.ccap) return false;
+  put_cand(w.cand + slot, t, d, v, ord, atomicExch(&w.chead[g], (uint32_t)slot));
+  return true;
+}
 
 // table of sorted position g: the single curve, or its curve in a batch
 template <bool MULTI>
@@ -1495,16 +1516,9 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
   // the seam members of the seam tie band become candidates
 #pragma unroll
   for (int j = 0; j < BAND_K; ++j) {
-    bool want = active && ((B.valid >> j) & 1u);
-    unsigned long long slot = wave_append(&w.cnt[2], want);
-    if (want) {
-      if (slot < w.ccap) {
-        put_cand(w.cand + slot, B.t[j], B.d[j], -1.0, (uint32_t)B.ord[j],
-                 atomicExch(&w.chead[gi], (uint32_t)slot));
-      } else {
-        fall = true;
-      }
-    }
+    if (active && ((B.valid >> j) & 1u) &&
+        !add_cand(w, gi, B.t[j], B.d[j], -1.0, (uint32_t)B.ord[j]))
+      fall = true;
   }
   if (active) {
     // cand (screened): seams offered + cubics queued for the exact solve by
@@ -1800,17 +1814,10 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     const double d = j == 0 ? sb.d1 : sb.d2;
-    const bool want = active && d <= lim;
-    unsigned long long slot = wave_append(&w.cnt[2], want);
-    if (want) {
-      if (slot < w.ccap) {
-        double pt[D], ts;
-        seam_point<D>(T, j == 0 ? sb.s1 : sb.s2, pt, ts);
-        put_cand(w.cand + slot, ts, d, -1.0, (uint32_t)(j == 0 ? sb.s1 : sb.s2),
-                 atomicExch(&w.chead[g], (uint32_t)slot));
-      } else {
-        fall = true;
-      }
+    if (active && d <= lim) {
+      double pt[D], ts;
+      seam_point<D>(T, j == 0 ? sb.s1 : sb.s2, pt, ts);
+      if (!add_cand(w, g, ts, d, -1.0, (uint32_t)(j == 0 ? sb.s1 : sb.s2))) fall = true;
     }
   }
   // parked leaves that still pass the final bound become pairs
@@ -2269,13 +2276,10 @@ __global__ void __launch_bounds__(BLOCK, MREP_CLIP_MINB) wave_clip(const __grid_
     double t = ta + v * (tb - ta);
     double cur = dmin_of(w, qi);
     bool keep = d <= cur + 1e-12;
-    unsigned long long slot = wave_append(&w.cnt[2], keep);
     if (keep) {
       atomicMin(dmin_ptr(w, qi), (unsigned long long)__double_as_longlong(d));
-      if (slot < w.ccap) {
-        put_cand(w.cand + slot, t, d, v, CAND_SURV | (uint32_t)sk,
-                 atomicExch(&w.chead[qi], (uint32_t)slot));
-      } else if (atomicExch(&w.flag[qi], 1) == 0) {
+      if (!add_cand(w, qi, t, d, v, CAND_SURV | (uint32_t)sk) &&
+          atomicExch(&w.flag[qi], 1) == 0) {
         unsigned long long fs = atomicAdd(&w.cnt[3], 1ull);
         w.fb[fs] = qi;
       }
@@ -2303,13 +2307,10 @@ __global__ void __launch_bounds__(256) wave_emit(const __grid_constant__ WavePar
   uint32_t bo = ~0u;
   bool found = false;
   double best_t = 0.0, best_d = 0.0, best_v = 0.0;
-  for (uint32_t c = w.chead[g]; c != ~0u;) {
-    const double4 r = *reinterpret_cast<const double4*>(w.cand + c);
-    const uint64_t on = (uint64_t)__double_as_longlong(r.w);
-    c = (uint32_t)(on >> 32);
-    if (!(r.y <= lim)) continue;
+  auto consider = [&](const double4 r) {
+    if (!(r.y <= lim)) return;
     const unsigned long long tk = tkey_of(r.x);
-    const uint32_t ok = (uint32_t)on;
+    const uint32_t ok = (uint32_t)(uint64_t)__double_as_longlong(r.w);
     if (tk < bt || (tk == bt && ok < bo)) {
       bt = tk;
       bo = ok;
@@ -2317,6 +2318,18 @@ __global__ void __launch_bounds__(256) wave_emit(const __grid_constant__ WavePar
       best_d = r.y;
       best_v = r.z;
       found = true;
+    }
+  };
+  const uint32_t nc = w.ccnt[g];
+  const double4* row = reinterpret_cast<const double4*>(w.cin + g * CIN);
+#pragma unroll
+  for (int k = 0; k < CIN; ++k)
+    if ((uint32_t)k < nc) consider(row[k]);
+  if (nc > (uint32_t)CIN) {
+    for (uint32_t c = w.chead[g]; c != ~0u;) {
+      const double4 r = *reinterpret_cast<const double4*>(w.cand + c);
+      c = (uint32_t)((uint64_t)__double_as_longlong(r.w) >> 32);
+      consider(r);
     }
   }
   if (!found) {
@@ -2902,7 +2915,7 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   const int64_t n = p.n;
   const unsigned long long pcap = (unsigned long long)std::max<int64_t>(16 * n, 1 << 16);
   const unsigned long long scap = (unsigned long long)std::max<int64_t>(2 * n, 1 << 16);
-  const unsigned long long ccap = (unsigned long long)std::max<int64_t>(4 * n, 1 << 16);
+  const unsigned long long ccap = (unsigned long long)std::max<int64_t>(n, 1 << 16);
   size_t bytes = 0;
   auto take = [&](size_t b) {
     size_t o = bytes;
@@ -2915,6 +2928,7 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
          o_ps2 = take(pcap * 4);
   size_t o_sb = take(scap * 64), o_sq = take(scap * 4), o_ssk = take(scap * 4);
   size_t o_cand = take(ccap * sizeof(Cand)), o_chead = take(n * 4);
+  size_t o_ccnt = take(n * 4), o_cin = take(n * CIN * sizeof(Cand));
   size_t o_fb = take(n * 8);
   size_t o_qs = take(n * 4 * 8), o_wt = take(n * 8), o_wd = take(n * 8), o_wv = take(n * 8),
          o_sc = take(n * 8);
@@ -2949,6 +2963,9 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   w.cand = (Cand*)(base + o_cand);
   w.chead = (uint32_t*)(base + o_chead);
   MREP_CUDA_CHECK(cudaMemsetAsync(w.chead, 0xff, n * 4, st));
+  w.ccnt = (uint32_t*)(base + o_ccnt);
+  w.cin = (Cand*)(base + o_cin);
+  MREP_CUDA_CHECK(cudaMemsetAsync(w.ccnt, 0, n * 4, st));
   w.ccap = ccap;
   w.fb = (int64_t*)(base + o_fb);
   w.qs = (double*)(base + o_qs);
