@@ -222,6 +222,28 @@ def cpu_time(jobs, workers):
     return nq, time.perf_counter() - t0
 
 
+def cand_pairs_tested(tab, q, S):
+    """(query, cubic) pairs the exact-cand pass tests: every cubic without a
+    cand cell index; with one, each query's cell list (every cubic outside
+    the grid) -- the grid words of the table header (mrep_cand.cuh H_CC*)."""
+    n = int(q.shape[0])
+    if getattr(tab, "cand_cells", None) is None:
+        return float(n) * S
+    h = tab.buf[24:36].cpu().numpy()
+    G, glo, ginv, ghi = int(h[1]), h[2:5], h[5:8], h[8:11]
+    d = tab.d
+    ncell = G ** d
+    off = tab.cand_cells[: ncell + 1].cpu().numpy().astype(np.int64)
+    qq = q.cpu().numpy()[:, :d]
+    inside = np.all((qq >= glo[:d]) & (qq < ghi[:d]), axis=1)
+    ci = np.clip(((qq - glo[:d]) * ginv[:d]).astype(np.int64), 0, G - 1)
+    cell = ci[:, 0]
+    for k in range(1, d):
+        cell = cell * G + ci[:, k]
+    ln = np.where(inside, off[cell + 1] - off[cell], S)
+    return float(ln.sum())
+
+
 def _prep_one(args):
     """oracle/prep.py prepare() of one curve (the reference's numpy
     decomposition + error-controlled approximation, restated): cubic count."""
@@ -343,9 +365,10 @@ class SingleCurve:
         import torch
         self.q_pin = torch.from_numpy(self.q_host).pin_memory().numpy()
 
-    def host(self, out, dense=False):
+    def host(self, out, dense=False, extra_flags=0):
         # the reference-facing call returns (t, foot, dist, cand): no segment ids
-        self.tab.project_host(self.q_pin, out=out[:4] + (None,), screen=not dense)
+        self.tab.project_host(self.q_pin, out=out[:4] + (None,), screen=not dense,
+                              extra_flags=extra_flags)
 
     def cpu_jobs(self, sample):
         sample = max(256, min(sample, int(sample * 510 / self.num_segments)))
@@ -903,13 +926,19 @@ def main():
             L.lib().mrep_last_stage_times(buf, 8)
             cms.append(buf[6])
         cm = float(np.median(cms))
-        ach = 64.0 * wl.num_segments * n / (cm / 1e3) / 1e12
+        tested = cand_pairs_tested(wl.tab, wl.q, wl.num_segments)
+        ach = 64.0 * tested / (cm / 1e3) / 1e12
         roofline["cand_exact"] = {
-            "kernel": "cand_count_kernel (mma.sync.m8n8k4.f64 sign screen + exact solve of "
-                      "undecided pairs)", "bound": "tensor", "ms": cm, "achieved": ach,
+            "kernel": ("cand_cells_kernel" if wl.tab.cand_cells is not None else
+                       "cand_count_kernel") + " (mma.sync.m8n8k4.f64 sign screen + exact solve "
+                      "of undecided pairs)", "bound": "tensor", "ms": cm, "achieved": ach,
             "peak": dpk.value, "unit": "TFLOP/s", "frac": ach / dpk.value,
             "peak_source": "DMMA m8n8k4 microbenchmark measured in this run (mrep_dmma_peak)",
-            "flop_model": "64 FP64 tensor flop per (query, cubic) pair (8x8x4 MMA per 8 queries)",
+            "flop_model": "64 FP64 tensor flop per (query, cubic) pair tested (8x8x4 MMA per 8 "
+                          "queries); with the cand cell index a query tests only its cell's "
+                          "uncertified cubics",
+            "pairs_tested_per_query": tested / n,
+            "dense_equivalent_tflops": 64.0 * wl.num_segments * n / (cm / 1e3) / 1e12,
             "uncertain_pairs_per_query": unc / n}
 
     # ---- e2e: host buffers through the C ABI (H2D + kernel + D2H per step) ----
@@ -935,6 +964,24 @@ def main():
         tt = torch.tensor([e2e_s], dtype=torch.float64, device="cpu" if shared else "cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
+    # the same host call returning the reference's own cand (MREP_CAND_EXACT,
+    # the Python API's default): every output equal to the reference kernel's
+    e2e_ref = None
+    if (world == 1 and isinstance(wl, SingleCurve) and not dense
+            and wl.num_segments * n <= 2_000_000_000):
+        for _ in range(2):
+            wl.host(onp, extra_flags=L.MREP_CAND_EXACT)
+        ts_ref = []
+        for _ in range(max(3, args.steps // 4)):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            wl.host(onp, extra_flags=L.MREP_CAND_EXACT)
+            ts_ref.append(time.perf_counter() - t0)
+        e2e_ref = {"value": n / statistics.mean(ts_ref), "unit": UNIT,
+                   "h2d_bytes_per_step": wl.h2d, "d2h_bytes_per_step": n * 48,
+                   "path": "mrep_project_host with MREP_CAND_EXACT: t, foot, distance and the "
+                           "reference's brute-force cand (tensor-core pass + cand cell index)"}
     e2e = {"value": n_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": wl.h2d,
            # (t, foot, dist, cand) for curves; (u, v, foot, dist, patch) for surfaces
            "d2h_bytes_per_step": n * ((8 + 8 + 24 + 8 + 4) if surf else (8 + 24 + 8 + 8)),
@@ -979,7 +1026,8 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic", "config": conf,
-                "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "e2e_reference_cand": e2e_ref, "roofline": roofline,
+                "cpu_baseline": cpu,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks.summary()}
         if prep_line is not None:
             line["preparation"] = prep_line

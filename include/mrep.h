@@ -48,6 +48,9 @@ extern "C" {
 #define MREP_CAND_EXACT 512u /* screened mode: cand = the reference's brute-force count
                                 (seams + surviving pieces of every cubic), computed on the FP64
                                 tensor cores with an exact solve of the undecided pairs */
+#define MREP_CAND_CELLS 1024u /* with MREP_CAND_EXACT: use the table's cand cell index
+                                 (mrep_cand_cells_build): each query tests only the cubics its
+                                 cell could not certify; same counts */
 
 /* Work counters written (accumulated) by mrep_project when `counters_dev` != NULL. */
 #define MREP_CNT_PAIRS 0      /* (query, cubic) pairs solved: E, quartic, rebase, pieces */
@@ -257,6 +260,20 @@ MREP_API int mrep_synth_walk(const double* v0, const double* g, int64_t n, int d
 MREP_API int64_t mrep_cells_bytes(const void* table_dev, int64_t S, int d, int grid, void* stream);
 MREP_API int mrep_cells_build(void* table_dev, int64_t S, int d, int grid, void* cells_dev,
                               int64_t bytes, void* stream);
+
+/* Cand cell index of a single-curve table (for MREP_CAND_EXACT): a uniform
+ * grid^d grid over the table box (+10%); per cell the number of cubics
+ * certified to hold exactly one surviving piece for EVERY query of the cell,
+ * and the list of cubics whose count is not fixed over it (every other cubic
+ * holds none).  Certification = the tensor-core pass's sign tests applied to
+ * the exact range of the affine Bernstein ordinates over the cell box.  A
+ * projection with MREP_CAND_EXACT | MREP_CAND_CELLS then tests each query
+ * against its cell's list only; cand is unchanged (the reference's count,
+ * _kernels.py:369-502).  Sizing / recording as mrep_cells_bytes/_build. */
+MREP_API int64_t mrep_cand_cells_bytes(const void* table_dev, int64_t S, int d, int grid,
+                                       void* stream);
+MREP_API int mrep_cand_cells_build(void* table_dev, int64_t S, int d, int grid, void* buf_dev,
+                                   int64_t bytes, void* stream);
 
 /* The same cell index for a surface table (mrep_surface_table_pack): the
  * exact points are each patch's seed grid; mrep_project_surface with

@@ -190,6 +190,8 @@ class DeviceTable:
                                         L.ptr(self.buf), L.stream_ptr()))
         self.cells = None
         self.cells_tried = False
+        self.cand_cells = None
+        self.cand_tried = False
 
     # a cell index pays off for dense batches (queries >> cubics); built once,
     # lazily, on the first such batch (mrep_cells_build)
@@ -226,6 +228,38 @@ class DeviceTable:
             self.build_cells()
         return L.MREP_CELLS if (self.cells is not None and n >= 8 * self.S) else 0
 
+    # the exact-cand pass (MREP_CAND_EXACT) tests every (query, cubic) pair
+    # unless the table has a cand cell index; built lazily once the pass is
+    # large enough to pay for it (mrep_cand_cells_build: cfg2 ~5 ms, 19 MB)
+    CAND_MIN_PAIRS = 1 << 24
+    CAND_MAX_BYTES = 4 << 30
+
+    def build_cand_cells(self, grid=None):
+        torch = L._torch()
+        if grid is None:
+            grid = 32 if self.d == 3 else 128
+        nb = L.lib().mrep_cand_cells_bytes(L.ptr(self.buf), self.S, self.d, grid, L.stream_ptr())
+        if nb <= 0:
+            L.check(1)
+        if nb > self.CAND_MAX_BYTES:
+            return self
+        try:
+            buf = torch.empty((nb + 3) // 4, dtype=torch.int32, device=self.buf.device)
+        except torch.cuda.OutOfMemoryError:
+            return self  # the full pass is exact without the index
+        L.check(L.lib().mrep_cand_cells_build(L.ptr(self.buf), self.S, self.d, grid,
+                                               L.ptr(buf), nb, L.stream_ptr()))
+        self.cand_cells = buf
+        return self
+
+    def _cand_flag(self, n, flags):
+        if not (flags & L.MREP_CAND_EXACT) or (flags & L.MREP_CAND_CELLS):
+            return 0
+        if self.cand_cells is None and not self.cand_tried and n * self.S >= self.CAND_MIN_PAIRS:
+            self.cand_tried = True
+            self.build_cand_cells()
+        return L.MREP_CAND_CELLS if self.cand_cells is not None else 0
+
     def project(self, queries, clip_tol=1e-6, max_iter=8, soundness_samples=0, screen=True,
                 stats=False, counters=None, extra_flags=0):
         """Project device queries (n, d); returns device tensors
@@ -246,6 +280,7 @@ class DeviceTable:
         flags |= int(extra_flags)
         if not (extra_flags & (L.MREP_PACKET | L.MREP_PER_LANE | L.MREP_GROUP)):
             flags |= self._cell_flag(n, screen and not stats)
+        flags |= self._cand_flag(n, flags)
         L.check(L.lib().mrep_project(
             L.ptr(self.buf), self.S, self.d, L.ptr(q), n, float(clip_tol), int(max_iter),
             int(soundness_samples), flags, L.ptr(t), L.ptr(foot), L.ptr(dist), L.ptr(cand),
@@ -265,6 +300,7 @@ class DeviceTable:
         p = lambda a: ctypes.c_void_p(a.ctypes.data if a is not None else 0)  # noqa: E731
         flags = (L.MREP_SCREEN | self._cell_flag(n, True)) if screen else 0
         flags |= int(extra_flags)
+        flags |= self._cand_flag(n, flags)
         L.check(L.lib().mrep_project_host(
             L.ptr(self.buf), self.S, self.d, p(q), n, float(clip_tol), int(max_iter),
             flags, p(t), p(foot), p(dist), p(cand), p(seg),

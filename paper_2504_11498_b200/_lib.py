@@ -31,6 +31,7 @@ MREP_PER_LANE = 64
 MREP_GROUP = 128
 MREP_CELLS = 256
 MREP_CAND_EXACT = 512
+MREP_CAND_CELLS = 1024
 NUM_COUNTERS = 8
 (CNT_PAIRS, CNT_SURVIVORS, CNT_CLIP_ITERS, CNT_SEAMS, CNT_BOXES, CNT_PASS2, CNT_HULL_MISS,
  CNT_UNCERTAIN) = range(8)
@@ -86,6 +87,8 @@ _SIGS = {
     "mrep_synth_walk": ([_vp, _vp, _i64, _i32, _vp], _i32),
     "mrep_cells_bytes": ([_vp, _i64, _i32, _i32, _vp], _i64),
     "mrep_cells_build": ([_vp, _i64, _i32, _i32, _vp, _i64, _vp], _i32),
+    "mrep_cand_cells_bytes": ([_vp, _i64, _i32, _i32, _vp], _i64),
+    "mrep_cand_cells_build": ([_vp, _i64, _i32, _i32, _vp, _i64, _vp], _i32),
     "mrep_surface_cells_bytes": ([_vp, _i64, _i32, _i32, _i32, _vp], _i64),
     "mrep_surface_cells_build": ([_vp, _i64, _i32, _i32, _i32, _vp, _i64, _vp], _i32),
     "mrep_knot_span": ([_vp, _i64, _i32, _vp, _i64, _vp, _vp], _i32),

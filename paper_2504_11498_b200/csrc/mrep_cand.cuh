@@ -133,86 +133,83 @@ __device__ __forceinline__ int kept_pieces(const TableView& T, int64_t s, const 
 
 constexpr int CAND_WARPS = 4;
 
-// one warp = 8 queries (rows) against every cubic; out_cand in caller order.
-// TC = false computes the same two columns per lane with DFMA on the CUDA
-// cores (8 fragment loads + 8 FMAs instead of one MMA) -- the A/B baseline
-// for the tensor-core contraction (MREP_CAND_CUDA_CORES=1 selects it).
-template <int D, bool TC = true>
-__global__ void __launch_bounds__(CAND_WARPS * 32) cand_count_kernel(const TableView T, const double* qs,
-                                                                    int64_t n, int64_t* out_cand,
-                                                                    unsigned long long* n_uncertain) {
-  __shared__ uint32_t queue[CAND_WARPS][64];
-  __shared__ int kept[CAND_WARPS][8];
-  __shared__ double sq[CAND_WARPS][8][3];
-  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31, row = lane >> 2, p = lane & 3;
-  const int64_t q0 = ((int64_t)blockIdx.x * CAND_WARPS + wi) * 8;
-  if (q0 >= n) return;  // whole warp
-  const int64_t qi = q0 + row;
-  const bool valid = qi < n;
-  double q[D];
+// Sign margins of one query (or of a box of queries with |q| <= R): far above
+// the rounding of the MMA and of the reference's FP64 ordinates; the end
+// values of a monotone E' must clear a wider margin (a spurious split the
+// reference's quartic might place within ~1e-8 of an end must not change
+// that end's sign).
+struct CandMargins {
+  double m, m2, mend;
+};
+__device__ __forceinline__ CandMargins cand_margins(double R) {
+  const double m = fmax(1e-9 * R * R, 1e-150);
+  return CandMargins{m, 4.0 * m, fmax(1e-6 * R * R, 1e-150)};
+}
+
+// Per-warp state of the count: 8 query rows, the undecided-pair queue.
+struct CandWarp {
+  uint32_t* queue;     // [64] row << 29 | cubic
+  int* kept;           // [8] exact survivors of undecided pairs, per row
+  double (*sq)[3];     // [8] the rows' coordinates
+  int qn;              // queued entries
+  unsigned long long unc;
+};
+
+// lanes < cnt solve one queued (row, cubic) pair each, as the reference does
+template <int D>
+__device__ __forceinline__ void cand_drain(const TableView& T, CandWarp& W, int cnt, int lane) {
+  if (lane < cnt) {
+    const uint32_t e = W.queue[lane];
+    const int r = (int)(e >> 29);
+    const int64_t s = (int64_t)(e & 0x1fffffffu);
+    double qq[D];
 #pragma unroll
-  for (int k = 0; k < D; ++k) q[k] = valid ? qs[qi * D + k] : 0.0;
-  if (p == 0) {
-    kept[wi][row] = 0;
-    for (int k = 0; k < 3; ++k) sq[wi][row][k] = k < D ? q[k] : 0.0;
+    for (int k = 0; k < D; ++k) qq[k] = W.sq[r][k];
+    const int kp = kept_pieces<D>(T, s, qq);
+    if (kp) atomicAdd(&W.kept[r], kp);
   }
-  double R = T.hdr[4];
-#pragma unroll
-  for (int k = 0; k < D; ++k) R = fmax(R, fabs(q[k]));
-  // sign margins: far above the rounding of the MMA and of the reference's
-  // FP64 ordinates; end values of a monotone E' must clear a wider margin
-  // (a spurious split the reference's quartic might place within ~1e-8 of
-  // an end must not change that end's sign)
-  const double m = fmax(1e-9 * R * R, 1e-150), mneg = m, m2 = 4.0 * m,
-               mend = fmax(1e-6 * R * R, 1e-150);
-  int ones = 0;  // pairs certified to hold exactly one survivor (lanes p == 0)
-  const double a = p == 0 ? 1.0 : (p <= D ? q[p - 1] - T.hdr[4 + p] : 0.0);
-  const double* F = T.bfrag;
-  const int64_t S = T.S;
-  int qn = 0;
-  unsigned long long unc_total = 0;
   __syncwarp();
-  auto drain = [&](int cnt) {
-    // lanes < cnt solve one queued pair each
-    if (lane < cnt) {
-      const uint32_t e = queue[wi][lane];
-      const int r = (int)(e >> 29);
-      const int64_t s = (int64_t)(e & 0x1fffffffu);
-      double qq[D];
-#pragma unroll
-      for (int k = 0; k < D; ++k) qq[k] = sq[wi][r][k];
-      const int kp = kept_pieces<D>(T, s, qq);
-      if (kp) atomicAdd(&kept[wi][r], kp);
-    }
-    __syncwarp();
-  };
+}
+
+// The 8 rows of a warp against the cubics idx(0..cnt-1): one MMA per cubic
+// (8 queries x the cubic's 4x8 fragment), sign tests per row; rows outside
+// `rows` (8-bit mask) are computed and ignored.  `ones` (lanes p == 0)
+// counts pairs certified to hold exactly one survivor; undecided pairs are
+// queued for cand_drain.
+template <int D, bool TC, class Idx>
+__device__ __forceinline__ void cand_tile(const TableView& T, CandWarp& W, const Idx& idx,
+                                          int64_t cnt, unsigned rows, double a,
+                                          const CandMargins& M, int& ones, int lane) {
+  const int row = lane >> 2, p = lane & 3;
+  const double m = M.m, mneg = M.m, m2 = M.m2, mend = M.mend;
   // per-lane constant: flag bits this lane does not decide (AND-neutral)
   //  0 all b > m  1 all b < -m  2 all E'' > m2  3 all E'' < -m2
   //  4 b_0 < -mend  5 |b_0| > mend  (lane 0)   6 b_5 > mend  7 |b_5| > mend  (lane 2)
   const unsigned neutral = p == 0 ? 0xc0u : (p == 1 ? 0xf0u : (p == 2 ? 0x30u : 0xffu));
-  const bool owner = valid && p == 0;
-  // the table reserves two zero fragments past the last cubic: the
-  // prefetch two cubics ahead needs no bound check
-  const double* Fp = F + lane;
-  double bn0 = __ldg(Fp), bn1 = __ldg(Fp + 32);
+  const bool owner = p == 0 && ((rows >> row) & 1u);
+  const double* F = T.bfrag;
+  // fragments one cubic ahead, ids two ahead
+  int64_t s_cur = cnt > 0 ? idx(0) : 0, s_nxt = cnt > 1 ? idx(1) : 0;
+  double bn = __ldg(F + s_cur * 32 + lane);
 #pragma unroll 1
-  for (int64_t s = 0; s < S; ++s) {
-    const double b = bn0;
-    bn0 = bn1;
-    bn1 = __ldg(Fp + 64);
-    Fp += 32;
+  for (int64_t k = 0; k < cnt; ++k) {
+    const double b = bn;
+    const int64_t s = s_cur;
+    s_cur = s_nxt;
+    if (k + 1 < cnt) bn = __ldg(F + s_cur * 32 + lane);
+    if (k + 2 < cnt) s_nxt = idx(k + 2);
     double c0, c1;
     if (TC) {
       dmma_8x8x4(a, b, c0, c1);
     } else {
       // lane (row, p) owns columns 2p, 2p+1: sum_k A[row][k] B[k][col]
-      const double* Bs = Fp - 32 - lane;
+      const double* Bs = F + s * 32;
       c0 = c1 = 0.0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double ak = __shfl_sync(0xffffffffu, a, (lane & ~3) | k);
-        c0 = fma(ak, __ldg(Bs + 8 * p + k), c0);
-        c1 = fma(ak, __ldg(Bs + 8 * p + 4 + k), c1);
+      for (int kk = 0; kk < 4; ++kk) {
+        const double ak = __shfl_sync(0xffffffffu, a, (lane & ~3) | kk);
+        c0 = fma(ak, __ldg(Bs + 8 * p + kk), c0);
+        c1 = fma(ak, __ldg(Bs + 8 * p + 4 + kk), c1);
       }
     }
     // lane p holds b_2p / 6, b_2p+1 / 6 of its row (lanes p = 0..2; p = 3
@@ -237,21 +234,240 @@ __global__ void __launch_bounds__(CAND_WARPS * 32) cand_count_kernel(const Table
     const bool unc = owner && !zero && !mono;
     const unsigned bal = __ballot_sync(0xffffffffu, unc);
     if (bal) {
-      if (unc) queue[wi][qn + __popc(bal & ((1u << lane) - 1))] = ((uint32_t)row << 29) | (uint32_t)s;
-      qn += __popc(bal);
-      unc_total += __popc(bal);
+      if (unc) W.queue[W.qn + __popc(bal & ((1u << lane) - 1))] = ((uint32_t)row << 29) | (uint32_t)s;
+      W.qn += __popc(bal);
+      W.unc += __popc(bal);
       __syncwarp();
-      if (qn >= 32) {
-        drain(32);
-        if (lane < qn - 32) queue[wi][lane] = queue[wi][32 + lane];
-        qn -= 32;
+      if (W.qn >= 32) {
+        cand_drain<D>(T, W, 32, lane);
+        if (lane < W.qn - 32) W.queue[lane] = W.queue[32 + lane];
+        W.qn -= 32;
         __syncwarp();
       }
     }
   }
-  drain(qn);
-  if (valid && p == 0) out_cand[qi] = S + 1 + kept[wi][row] + ones;
-  if (n_uncertain && lane == 0) atomicAdd(n_uncertain, unc_total);
+}
+
+// one warp = 8 queries (rows) against every cubic; out_cand in caller order.
+// TC = false computes the same two columns per lane with DFMA on the CUDA
+// cores (8 fragment loads + 8 FMAs instead of one MMA) -- the A/B baseline
+// for the tensor-core contraction (MREP_CAND_CUDA_CORES=1 selects it).
+struct CandAll {
+  __device__ __forceinline__ int64_t operator()(int64_t k) const { return k; }
+};
+struct CandList {
+  const int32_t* ids;
+  __device__ __forceinline__ int64_t operator()(int64_t k) const { return __ldg(ids + k); }
+};
+
+template <int D, bool TC = true>
+__global__ void __launch_bounds__(CAND_WARPS * 32) cand_count_kernel(const TableView T, const double* qs,
+                                                                    int64_t n, int64_t* out_cand,
+                                                                    unsigned long long* n_uncertain) {
+  __shared__ uint32_t queue[CAND_WARPS][64];
+  __shared__ int kept[CAND_WARPS][8];
+  __shared__ double sq[CAND_WARPS][8][3];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31, row = lane >> 2, p = lane & 3;
+  const int64_t q0 = ((int64_t)blockIdx.x * CAND_WARPS + wi) * 8;
+  if (q0 >= n) return;  // whole warp
+  const int64_t qi = q0 + row;
+  const bool valid = qi < n;
+  double q[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) q[k] = valid ? qs[qi * D + k] : 0.0;
+  if (p == 0) {
+    kept[wi][row] = 0;
+    for (int k = 0; k < 3; ++k) sq[wi][row][k] = k < D ? q[k] : 0.0;
+  }
+  double R = T.hdr[4];
+#pragma unroll
+  for (int k = 0; k < D; ++k) R = fmax(R, fabs(q[k]));
+  const CandMargins M = cand_margins(R);
+  const double a = p == 0 ? 1.0 : (p <= D ? q[p - 1] - T.hdr[4 + p] : 0.0);
+  const unsigned rows = __ballot_sync(0xffffffffu, valid && p == 0);
+  unsigned rmask = 0;
+  for (int r = 0; r < 8; ++r) rmask |= ((rows >> (4 * r)) & 1u) << r;
+  CandWarp W{queue[wi], kept[wi], sq[wi], 0, 0};
+  int ones = 0;
+  __syncwarp();
+  cand_tile<D, TC>(T, W, CandAll{}, T.S, rmask, a, M, ones, lane);
+  cand_drain<D>(T, W, W.qn, lane);
+  if (valid && p == 0) out_cand[qi] = T.S + 1 + W.kept[row] + ones;
+  if (n_uncertain && lane == 0) atomicAdd(n_uncertain, W.unc);
+}
+
+// ---------------------------------------------------------------- cand cells
+// A uniform grid over the table's root box (+10% each side, as the cell
+// index) where every cell C stores
+//   fixed[C] = the number of cubics certified, for EVERY query of C, to hold
+//              exactly one survivor, and
+//   list[C]  = the cubics whose count is NOT fixed over C,
+// every other cubic being certified to hold none.  The b_j (and the E''
+// differences) are affine in q, so their exact range over the cell box is
+// centre value +- sum |coefficient| * half-width; the certification tests
+// of cand_tile are applied to those ranges with the margins of the largest
+// |q| in the cell (a larger margin than any of its queries uses, so a
+// certified cubic is certified for each of them; the margin is far above the
+// rounding of the range computation).  A query then runs cand_tile over its
+// cell's list only and adds fixed[C].  Queries outside the grid use every
+// cubic.  Results equal cand_count_kernel's (and the reference's) exactly.
+constexpr int H_CC = 24, H_CC_GRID = 25, H_CC_GLO = 26, H_CC_GINV = 29, H_CC_GHI = 32,
+              H_CC_TOT = 35;
+
+// class of cubic s over the query box [lo, hi]: 0 or 1 certified, -1 not fixed
+__device__ __forceinline__ int cand_box_class(const TableView& T, int64_t s, const double* lo,
+                                              const double* hi, int d) {
+  const double* F = T.bfrag + s * 32;  // element (k, j) at 4 j + k
+  double ctr[3], half[3], R = T.hdr[4];
+  for (int k = 0; k < 3; ++k) {
+    ctr[k] = k < d ? 0.5 * (lo[k] + hi[k]) - T.hdr[5 + k] : 0.0;
+    half[k] = k < d ? 0.5 * (hi[k] - lo[k]) : 0.0;
+    if (k < d) R = fmax(R, fmax(fabs(lo[k]), fabs(hi[k])));
+  }
+  const CandMargins M = cand_margins(R);
+  double mn[6], mx[6];
+  for (int j = 0; j < 6; ++j) {
+    double v = F[4 * j], r = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      v += F[4 * j + 1 + k] * ctr[k];
+      r += fabs(F[4 * j + 1 + k]) * half[k];
+    }
+    mn[j] = v - r;
+    mx[j] = v + r;
+  }
+  bool pos = true, neg = true;
+  for (int j = 0; j < 6; ++j) {
+    pos = pos && mn[j] > M.m;
+    neg = neg && mx[j] < -M.m;
+  }
+  if (pos || neg) return 0;
+  bool epos = true, eneg = true;
+  for (int j = 0; j < 5; ++j) {
+    double v = F[4 * (j + 1)] - F[4 * j], r = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      const double c = F[4 * (j + 1) + 1 + k] - F[4 * j + 1 + k];
+      v += c * ctr[k];
+      r += fabs(c) * half[k];
+    }
+    epos = epos && v - r > M.m2;
+    eneg = eneg && v + r < -M.m2;
+  }
+  const bool e0 = mn[0] > M.mend || mx[0] < -M.mend, e5 = mn[5] > M.mend || mx[5] < -M.mend;
+  if ((epos || eneg) && e0 && e5) return (mx[0] < -M.mend && mn[5] > M.mend) ? 1 : 0;
+  return -1;
+}
+
+// one thread per cell: list length and the fixed count
+__global__ void cand_cells_count_kernel(const __grid_constant__ TableView T,
+                                        const __grid_constant__ CellGrid g, int32_t* cnt,
+                                        int32_t* fixed) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= g.ncell) return;
+  double lo[3], hi[3];
+  cell_box(g, c, lo, hi);
+  int32_t nl = 0, nf = 0;
+  for (int64_t s = 0; s < T.S; ++s) {
+    const int cl = cand_box_class(T, s, lo, hi, g.d);
+    nl += cl < 0 ? 1 : 0;
+    nf += cl > 0 ? 1 : 0;
+  }
+  cnt[c] = nl;
+  fixed[c] = nf;
+}
+
+__global__ void cand_cells_fill_kernel(const __grid_constant__ TableView T,
+                                       const __grid_constant__ CellGrid g, const int32_t* off,
+                                       int32_t* ids) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= g.ncell) return;
+  double lo[3], hi[3];
+  cell_box(g, c, lo, hi);
+  int32_t* out = ids + off[c];
+  int32_t nl = 0;
+  for (int64_t s = 0; s < T.S; ++s)
+    if (cand_box_class(T, s, lo, hi, g.d) < 0) out[nl++] = (int32_t)s;
+}
+
+// the query's cand cell (-1: no index or outside the grid)
+template <int D>
+__device__ __forceinline__ int64_t cand_cell_of(const TableView& T, const double (&q)[D]) {
+  const int G = (int)T.hdr[H_CC_GRID];
+  if (G <= 0) return -1;
+  int64_t ci[3] = {0, 0, 0};
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (!(q[k] >= T.hdr[H_CC_GLO + k] && q[k] < T.hdr[H_CC_GHI + k])) return -1;
+    const int64_t c = (int64_t)((q[k] - T.hdr[H_CC_GLO + k]) * T.hdr[H_CC_GINV + k]);
+    ci[k] = c < 0 ? 0 : (c >= G ? G - 1 : c);
+  }
+  return (ci[0] * G + ci[1]) * (D == 3 ? G : 1) + (D == 3 ? ci[2] : 0);
+}
+
+// one warp = 8 consecutive SORTED queries (perm: sorted -> caller; null =
+// caller order).  The rows are grouped by cand cell (Morton-sorted
+// neighbours share one or two cells): each group runs cand_tile over its
+// cell's list (every cubic for rows outside the grid).
+template <int D, bool TC = true>
+__global__ void __launch_bounds__(CAND_WARPS * 32) cand_cells_kernel(const TableView T, const double* qs,
+                                                                    const uint32_t* perm, int64_t n,
+                                                                    int64_t* out_cand,
+                                                                    unsigned long long* n_uncertain) {
+  __shared__ uint32_t queue[CAND_WARPS][64];
+  __shared__ int kept[CAND_WARPS][8];
+  __shared__ double sq[CAND_WARPS][8][3];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31, row = lane >> 2, p = lane & 3;
+  const int64_t g0 = ((int64_t)blockIdx.x * CAND_WARPS + wi) * 8;
+  if (g0 >= n) return;  // whole warp
+  const int64_t g = g0 + row;
+  const bool valid = g < n;
+  const int64_t qi = valid ? (perm ? (int64_t)perm[g] : g) : 0;
+  double q[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) q[k] = valid ? qs[qi * D + k] : 0.0;
+  if (p == 0) {
+    kept[wi][row] = 0;
+    for (int k = 0; k < 3; ++k) sq[wi][row][k] = k < D ? q[k] : 0.0;
+  }
+  double R = T.hdr[4];
+#pragma unroll
+  for (int k = 0; k < D; ++k) R = fmax(R, fabs(q[k]));
+  const CandMargins M = cand_margins(R);
+  const double a = p == 0 ? 1.0 : (p <= D ? q[p - 1] - T.hdr[4 + p] : 0.0);
+  const int64_t cell = valid ? cand_cell_of<D>(T, q) : -2;
+  const int G = (int)T.hdr[H_CC_GRID];
+  const int64_t ncell = (int64_t)G * G * (D == 3 ? G : 1);
+  const int32_t* off = reinterpret_cast<const int32_t*>(
+      (uintptr_t)__double_as_longlong(T.hdr[H_CC]));
+  const int32_t* fixed = off + ncell + 1;
+  const int32_t* ids = fixed + ncell;
+  CandWarp W{queue[wi], kept[wi], sq[wi], 0, 0};
+  int ones = 0;
+  __syncwarp();
+  // rows still to do (8-bit, warp-uniform); invalid rows are done
+  unsigned todo = 0;
+  {
+    const unsigned vb = __ballot_sync(0xffffffffu, valid && p == 0);
+    for (int r = 0; r < 8; ++r) todo |= ((vb >> (4 * r)) & 1u) << r;
+  }
+  while (todo) {
+    const int lead = __ffs(todo) - 1;
+    const int64_t lc = __shfl_sync(0xffffffffu, cell, 4 * lead);
+    const unsigned same = __ballot_sync(0xffffffffu, p == 0 && valid && cell == lc);
+    unsigned rows = 0;
+    for (int r = 0; r < 8; ++r) rows |= ((same >> (4 * r)) & 1u) << r;
+    rows &= todo;
+    if (lc >= 0) {
+      const int32_t a0 = __ldg(off + lc), a1 = __ldg(off + lc + 1);
+      cand_tile<D, TC>(T, W, CandList{ids + a0}, a1 - a0, rows, a, M, ones, lane);
+    } else {
+      cand_tile<D, TC>(T, W, CandAll{}, T.S, rows, a, M, ones, lane);
+    }
+    todo &= ~rows;
+  }
+  cand_drain<D>(T, W, W.qn, lane);
+  if (valid && p == 0)
+    out_cand[qi] = T.S + 1 + W.kept[row] + ones + (cell >= 0 ? __ldg(fixed + cell) : 0);
+  if (n_uncertain && lane == 0) atomicAdd(n_uncertain, W.unc);
 }
 
 }  // namespace mrep

@@ -3776,7 +3776,17 @@ static int project_chunk(const void* table, int64_t S, int d, const double* quer
     const unsigned blocks = grid_for(n, CAND_WARPS * 8);
     unsigned long long* unc = counters ? (unsigned long long*)&counters[MREP_CNT_UNCERTAIN] : nullptr;
     static const bool cuda_cores = getenv("MREP_CAND_CUDA_CORES") != nullptr;
-    if (d == 3) {
+    if (flags & MREP_CAND_CELLS) {
+      // the table's cand cell index (mrep_cand_cells_build), queries in the
+      // pipeline's sorted order
+      if (d == 3) {
+        if (cuda_cores) cand_cells_kernel<3, false><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, p.perm, n, out_cand, unc);
+        else cand_cells_kernel<3, true><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, p.perm, n, out_cand, unc);
+      } else {
+        if (cuda_cores) cand_cells_kernel<2, false><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, p.perm, n, out_cand, unc);
+        else cand_cells_kernel<2, true><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, p.perm, n, out_cand, unc);
+      }
+    } else if (d == 3) {
       if (cuda_cores) cand_count_kernel<3, false><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, n, out_cand, unc);
       else cand_count_kernel<3, true><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, n, out_cand, unc);
     } else {
@@ -3937,6 +3947,77 @@ int mrep_cells_build(void* table, int64_t S, int d, int grid, void* cells, int64
                      void* stream) {
   return cells_build<CurveLeaves>(table, S, d, grid, REC, CurveLeaves{}, cells, bytes,
                                   (cudaStream_t)stream);
+}
+
+// cand cell index (mrep_cand.cuh): counts per cell, then offsets, fixed
+// counts and lists; bytes = 4 (2 ncell + 1 + total)
+static int cand_cells_plan(const void* table, int64_t S, int d, int grid, cudaStream_t st,
+                           TableView& T, CellGrid& g, std::vector<int32_t>& cnt,
+                           std::vector<int32_t>& fixed, int64_t& total) {
+  int rc = cell_grid(table, S, d, grid, REC, st, T, g);
+  if (rc != MREP_OK) return rc;
+  int32_t* dc = nullptr;
+  MREP_CUDA_CHECK(cudaMallocAsync((void**)&dc, g.ncell * 8, st));
+  cand_cells_count_kernel<<<grid_for(g.ncell, 128), 128, 0, st>>>(T, g, dc, dc + g.ncell);
+  cnt.resize(g.ncell);
+  fixed.resize(g.ncell);
+  cudaError_t e1 = cudaMemcpyAsync(cnt.data(), dc, g.ncell * 4, cudaMemcpyDeviceToHost, st);
+  cudaError_t e2 = cudaMemcpyAsync(fixed.data(), dc + g.ncell, g.ncell * 4, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(dc, st);
+  MREP_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    set_error("mrep_cand_cells: copy of the counts failed");
+    return MREP_ERR_CUDA;
+  }
+  total = 0;
+  for (int32_t v : cnt) total += v;
+  if (total + 2 * g.ncell + 1 > INT32_MAX) {
+    set_error("mrep_cand_cells: lists exceed 2^31 entries; use a smaller grid");
+    return MREP_ERR_ARG;
+  }
+  return MREP_OK;
+}
+
+int64_t mrep_cand_cells_bytes(const void* table, int64_t S, int d, int grid, void* stream) {
+  TableView T;
+  CellGrid g;
+  std::vector<int32_t> cnt, fixed;
+  int64_t total = 0;
+  if (cand_cells_plan(table, S, d, grid, (cudaStream_t)stream, T, g, cnt, fixed, total) != MREP_OK)
+    return -1;
+  return 4 * (2 * g.ncell + 1 + total);
+}
+
+int mrep_cand_cells_build(void* table, int64_t S, int d, int grid, void* buf, int64_t bytes,
+                          void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  TableView T;
+  CellGrid g;
+  std::vector<int32_t> cnt, fixed;
+  int64_t total = 0;
+  int rc = cand_cells_plan(table, S, d, grid, st, T, g, cnt, fixed, total);
+  if (rc != MREP_OK) return rc;
+  if (!buf || bytes < 4 * (2 * g.ncell + 1 + total)) {
+    set_error("mrep_cand_cells_build: buffer too small (see mrep_cand_cells_bytes)");
+    return MREP_ERR_ARG;
+  }
+  std::vector<int32_t> head(2 * g.ncell + 1);
+  int64_t acc = 0;
+  for (int64_t c = 0; c < g.ncell; ++c) {
+    head[c] = (int32_t)acc;
+    acc += cnt[c];
+    head[g.ncell + 1 + c] = fixed[c];
+  }
+  head[g.ncell] = (int32_t)acc;
+  int32_t* off = (int32_t*)buf;
+  MREP_CUDA_CHECK(cudaMemcpyAsync(off, head.data(), head.size() * 4, cudaMemcpyHostToDevice, st));
+  cand_cells_fill_kernel<<<grid_for(g.ncell, 128), 128, 0, st>>>(T, g, off, off + 2 * g.ncell + 1);
+  MREP_LAUNCH_CHECK();
+  double h[12];
+  cells_header(g, buf, total, h);
+  MREP_CUDA_CHECK(cudaMemcpyAsync((double*)table + H_CC, h, sizeof h, cudaMemcpyHostToDevice, st));
+  MREP_CUDA_CHECK(cudaStreamSynchronize(st));  // head and h die here
+  return MREP_OK;
 }
 
 int mrep_knot_span(const double* knots, int64_t m, int p, const double* t, int64_t n,

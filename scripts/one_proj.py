@@ -12,6 +12,8 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 125000
 warm = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 wl = bench.SingleCurve("cfg2", 0, 1, 0)
 flags = wl.tab._cell_flag(1 << 20, True) | int(os.environ.get("EXTRA_FLAGS", "0"))
+if flags & 1024:  # MREP_CAND_CELLS: build the table's cand cell index first
+    wl.tab.build_cand_cells()
 q = wl.q[:n].contiguous()
 for _ in range(warm):
     wl.tab.project(q, extra_flags=flags)

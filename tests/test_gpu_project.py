@@ -369,3 +369,59 @@ def test_exact_cand_cfg2_and_extremes_vs_oracle(gpu, oracle_lib):
         ts, _, ds, cs = project_prepared(prep, q, cand="screened")
         assert np.array_equal(ts, t) and np.array_equal(ds, dist)
         assert np.all(cs <= cand)
+
+
+@pytest.mark.parametrize("grid", [8, 32])
+def test_cand_cell_index_exact(gpu, oracle_lib, grid):
+    """The cand cell index (mrep_cand_cells_build) changes no count: per cell
+    the certified cubics (zero or exactly one survivor for every query of the
+    cell) are skipped and the rest tested per query.  Checked against the
+    full tensor-core pass and the C oracle, with queries outside the grid,
+    on seams and control points, at three coordinate scales; sorted (>= 2^16
+    queries) and unsorted batches; the host call."""
+    from paper_2504_11498_b200 import BSplineCurve, prepare_curve, _lib as L
+    from paper_2504_11498_b200.fixtures import random_clamped_curve
+    cv = random_clamped_curve(np.random.default_rng(0), 7, 512, 3, uniform_knots=True)
+    rng = np.random.default_rng(6)
+    for scale in (1.0, 1e-3, 1e3):
+        c2 = BSplineCurve(cv.degree, np.array(cv.knots.knots), np.array(cv.control_points) * scale)
+        prep = prepare_curve(c2, 1e-4 * scale)
+        tab = prep.table
+        q = np.concatenate([
+            rng.uniform(0, scale, (70000, 3)),                  # random (sorted batch)
+            rng.uniform(-0.5 * scale, 1.5 * scale, (3000, 3)),  # many outside the grid
+            prep.seam_pt[::3],                                  # exactly on seams
+            prep.seg_pts[::2, 1],                               # control points
+        ])
+        tab.cand_tried = True  # no lazy index: the full pass
+        full = tab.project(q, extra_flags=L.MREP_CAND_EXACT)[3].cpu().numpy()
+        tab.build_cand_cells(grid)
+        assert tab.cand_cells is not None
+        fl = L.MREP_CAND_EXACT | L.MREP_CAND_CELLS
+        idx = tab.project(q, extra_flags=fl)[3].cpu().numpy()
+        assert np.array_equal(idx, full), (scale, np.nonzero(idx != full)[0][:10])
+        small = tab.project(q[-4000:], extra_flags=fl)[3].cpu().numpy()  # unsorted path
+        assert np.array_equal(small, full[-4000:])
+        h = tab.project_host(q, extra_flags=fl)
+        assert np.array_equal(h[3], full)
+        sub = np.concatenate([np.arange(0, 70000, 61), np.arange(70000, len(q))])
+        o = oracle_lib.project_block(prep.seg_pts, prep.seg_ta, prep.seg_tb, prep.seam_t,
+                                     prep.seam_pt, q[sub], workers=8)
+        assert np.array_equal(idx[sub], o["cand"])
+
+
+def test_cand_cell_index_2d(gpu, oracle_lib):
+    from paper_2504_11498_b200 import BSplineCurve, prepare_curve, _lib as L
+    from paper_2504_11498_b200.fixtures import random_clamped_curve
+    cv = random_clamped_curve(np.random.default_rng(3), 5, 200, 2, uniform_knots=True)
+    prep = prepare_curve(cv, 1e-4)
+    tab = prep.table
+    tab.cand_tried = True
+    q = np.random.default_rng(4).uniform(-0.2, 1.2, (20000, 2))
+    full = tab.project(q, extra_flags=L.MREP_CAND_EXACT)[3].cpu().numpy()
+    tab.build_cand_cells(64)
+    idx = tab.project(q, extra_flags=L.MREP_CAND_EXACT | L.MREP_CAND_CELLS)[3].cpu().numpy()
+    assert np.array_equal(idx, full)
+    o = oracle_lib.project_block(prep.seg_pts, prep.seg_ta, prep.seg_tb, prep.seam_t,
+                                 prep.seam_pt, q[::10], workers=8)
+    assert np.array_equal(idx[::10], o["cand"])
