@@ -664,8 +664,8 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--n", "--queries-per-gpu", dest="n", type=int, default=0,
                     help="queries per GPU (default: the config's)")
-    ap.add_argument("--ref-sample", type=int, default=32768)
-    ap.add_argument("--cpu-sample", type=int, default=65536)
+    ap.add_argument("--ref-sample", type=int, default=131072)
+    ap.add_argument("--cpu-sample", type=int, default=131072)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dense", action="store_true", help="brute-force kernel (reference semantics)")
     ap.add_argument("--verify-gather", action="store_true",

@@ -153,6 +153,13 @@ struct CandWarp {
   double (*sq)[3];     // [8] the rows' coordinates
   int qn;              // queued entries
   unsigned long long unc;
+  // undecided pairs go to a global list solved by cand_solve_kernel (when
+  // given; the local queue takes what does not fit)
+  uint2* glist;                // (caller index, cubic)
+  unsigned long long* gcount;
+  unsigned long long gcap;
+  const int64_t* rowq;         // [8] caller index of each row (shared)
+  unsigned* redo_rows;         // (shared) rows with a pair that did not fit
 };
 
 // lanes < cnt solve one queued (row, cubic) pair each, as the reference does
@@ -171,12 +178,28 @@ __device__ __forceinline__ void cand_drain(const TableView& T, CandWarp& W, int 
   __syncwarp();
 }
 
+// the first cnt entries of the warp's queue -> the global list (one atomic);
+// a row whose pair does not fit is recounted from scratch afterwards (redo)
+__device__ __forceinline__ void cand_flush(CandWarp& W, int cnt, int lane) {
+  if (cnt <= 0) return;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(W.gcount, (unsigned long long)cnt);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (lane < cnt) {
+    const uint32_t e = W.queue[lane];
+    const int r = (int)(e >> 29);
+    if (base + lane < W.gcap) W.glist[base + lane] = make_uint2((uint32_t)W.rowq[r], e & 0x1fffffffu);
+    else atomicOr(W.redo_rows, 1u << r);
+  }
+  __syncwarp();
+}
+
 // The 8 rows of a warp against the cubics idx(0..cnt-1): one MMA per cubic
 // (8 queries x the cubic's 4x8 fragment), sign tests per row; rows outside
 // `rows` (8-bit mask) are computed and ignored.  `ones` (lanes p == 0)
 // counts pairs certified to hold exactly one survivor; undecided pairs are
 // queued for cand_drain.
-template <int D, bool TC, class Idx>
+template <int D, bool TC, bool GLOBAL, class Idx>
 __device__ __forceinline__ void cand_tile(const TableView& T, CandWarp& W, const Idx& idx,
                                           int64_t cnt, unsigned rows, double a,
                                           const CandMargins& M, int& ones, int lane) {
@@ -213,7 +236,16 @@ __device__ __forceinline__ void cand_tile(const TableView& T, CandWarp& W, const
       }
     }
     // lane p holds b_2p / 6, b_2p+1 / 6 of its row (lanes p = 0..2; p = 3
-    // holds the zero pad columns); b_2p+2 / 6 from lane p + 1
+    // holds the zero pad columns); b_2p+2 / 6 from lane p + 1.
+    // Fast path: most tested pairs are one-signed for every row of the tile
+    // (no survivor) -- two compares per column, an AND over the row's lanes.
+    {
+      unsigned z = p == 3 ? 3u
+                          : ((unsigned)(c0 > m && c1 > m) | ((unsigned)(c0 < -mneg && c1 < -mneg) << 1));
+      z &= __shfl_xor_sync(0xffffffffu, z, 1);
+      z &= __shfl_xor_sync(0xffffffffu, z, 2);
+      if (__all_sync(0xffffffffu, z != 0 || !((rows >> row) & 1u))) continue;
+    }
     const double nx = __shfl_down_sync(0xffffffffu, c0, 1);
     const double ea = c1 - c0, eb = nx - c1;  // E'' ordinates / 30: 2p, 2p + 1
     const double mn = fmin(c0, c1), mx = fmax(c0, c1);
@@ -233,6 +265,23 @@ __device__ __forceinline__ void cand_tile(const TableView& T, CandWarp& W, const
     ones += (owner && !zero && mono && (v & 0x50u) == 0x50u) ? 1 : 0;
     const bool unc = owner && !zero && !mono;
     const unsigned bal = __ballot_sync(0xffffffffu, unc);
+    if (GLOBAL) {
+      // to the global list (cand_solve_kernel) in batches of 32 through the
+      // warp's shared queue: one atomic per batch on the list counter
+      if (bal) {
+        if (unc) W.queue[W.qn + __popc(bal & ((1u << lane) - 1))] = ((uint32_t)row << 29) | (uint32_t)s;
+        W.qn += __popc(bal);
+        W.unc += __popc(bal);
+        __syncwarp();
+        if (W.qn >= 32) {
+          cand_flush(W, 32, lane);
+          if (lane < W.qn - 32) W.queue[lane] = W.queue[32 + lane];
+          W.qn -= 32;
+          __syncwarp();
+        }
+      }
+      continue;
+    }
     if (bal) {
       if (unc) W.queue[W.qn + __popc(bal & ((1u << lane) - 1))] = ((uint32_t)row << 29) | (uint32_t)s;
       W.qn += __popc(bal);
@@ -260,18 +309,24 @@ struct CandList {
   __device__ __forceinline__ int64_t operator()(int64_t k) const { return __ldg(ids + k); }
 };
 
+// list / list_n (device count): the redo pass of cand_cells_kernel -- the
+// warp's rows are list entries (grid-stride over tiles of 8), not 0..n-1
 template <int D, bool TC = true>
 __global__ void __launch_bounds__(CAND_WARPS * 32) cand_count_kernel(const TableView T, const double* qs,
                                                                     int64_t n, int64_t* out_cand,
-                                                                    unsigned long long* n_uncertain) {
+                                                                    unsigned long long* n_uncertain,
+                                                                    const int64_t* list = nullptr,
+                                                                    const unsigned long long* list_n = nullptr) {
   __shared__ uint32_t queue[CAND_WARPS][64];
   __shared__ int kept[CAND_WARPS][8];
   __shared__ double sq[CAND_WARPS][8][3];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31, row = lane >> 2, p = lane & 3;
-  const int64_t q0 = ((int64_t)blockIdx.x * CAND_WARPS + wi) * 8;
-  if (q0 >= n) return;  // whole warp
-  const int64_t qi = q0 + row;
-  const bool valid = qi < n;
+  if (list) n = (int64_t)*list_n;
+  for (int64_t q0 = ((int64_t)blockIdx.x * CAND_WARPS + wi) * 8; q0 < n;
+       q0 += (int64_t)gridDim.x * CAND_WARPS * 8) {
+  const int64_t qi0 = q0 + row;
+  const bool valid = qi0 < n;
+  const int64_t qi = valid && list ? list[qi0] : qi0;
   double q[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) q[k] = valid ? qs[qi * D + k] : 0.0;
@@ -287,13 +342,15 @@ __global__ void __launch_bounds__(CAND_WARPS * 32) cand_count_kernel(const Table
   const unsigned rows = __ballot_sync(0xffffffffu, valid && p == 0);
   unsigned rmask = 0;
   for (int r = 0; r < 8; ++r) rmask |= ((rows >> (4 * r)) & 1u) << r;
-  CandWarp W{queue[wi], kept[wi], sq[wi], 0, 0};
+  CandWarp W{queue[wi], kept[wi], sq[wi], 0, 0, nullptr, nullptr, 0, nullptr, nullptr};
   int ones = 0;
   __syncwarp();
-  cand_tile<D, TC>(T, W, CandAll{}, T.S, rmask, a, M, ones, lane);
+  cand_tile<D, TC, false>(T, W, CandAll{}, T.S, rmask, a, M, ones, lane);
   cand_drain<D>(T, W, W.qn, lane);
   if (valid && p == 0) out_cand[qi] = T.S + 1 + W.kept[row] + ones;
   if (n_uncertain && lane == 0) atomicAdd(n_uncertain, W.unc);
+  __syncwarp();
+  }
 }
 
 // ---------------------------------------------------------------- cand cells
@@ -411,10 +468,15 @@ template <int D, bool TC = true>
 __global__ void __launch_bounds__(CAND_WARPS * 32) cand_cells_kernel(const TableView T, const double* qs,
                                                                     const uint32_t* perm, int64_t n,
                                                                     int64_t* out_cand,
-                                                                    unsigned long long* n_uncertain) {
+                                                                    unsigned long long* n_uncertain,
+                                                                    uint2* glist,
+                                                                    unsigned long long* gcount,
+                                                                    unsigned long long gcap,
+                                                                    int64_t* redo_list,
+                                                                    unsigned long long* redo_n) {
+  __shared__ int64_t rowq[CAND_WARPS][8];
   __shared__ uint32_t queue[CAND_WARPS][64];
-  __shared__ int kept[CAND_WARPS][8];
-  __shared__ double sq[CAND_WARPS][8][3];
+  __shared__ unsigned redo_rows[CAND_WARPS];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31, row = lane >> 2, p = lane & 3;
   const int64_t g0 = ((int64_t)blockIdx.x * CAND_WARPS + wi) * 8;
   if (g0 >= n) return;  // whole warp
@@ -424,10 +486,8 @@ __global__ void __launch_bounds__(CAND_WARPS * 32) cand_cells_kernel(const Table
   double q[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) q[k] = valid ? qs[qi * D + k] : 0.0;
-  if (p == 0) {
-    kept[wi][row] = 0;
-    for (int k = 0; k < 3; ++k) sq[wi][row][k] = k < D ? q[k] : 0.0;
-  }
+  if (p == 0) rowq[wi][row] = qi;
+  if (lane == 0) redo_rows[wi] = 0u;
   double R = T.hdr[4];
 #pragma unroll
   for (int k = 0; k < D; ++k) R = fmax(R, fabs(q[k]));
@@ -440,7 +500,7 @@ __global__ void __launch_bounds__(CAND_WARPS * 32) cand_cells_kernel(const Table
       (uintptr_t)__double_as_longlong(T.hdr[H_CC]));
   const int32_t* fixed = off + ncell + 1;
   const int32_t* ids = fixed + ncell;
-  CandWarp W{queue[wi], kept[wi], sq[wi], 0, 0};
+  CandWarp W{queue[wi], nullptr, nullptr, 0, 0, glist, gcount, gcap, rowq[wi], &redo_rows[wi]};
   int ones = 0;
   __syncwarp();
   // rows still to do (8-bit, warp-uniform); invalid rows are done
@@ -458,16 +518,39 @@ __global__ void __launch_bounds__(CAND_WARPS * 32) cand_cells_kernel(const Table
     rows &= todo;
     if (lc >= 0) {
       const int32_t a0 = __ldg(off + lc), a1 = __ldg(off + lc + 1);
-      cand_tile<D, TC>(T, W, CandList{ids + a0}, a1 - a0, rows, a, M, ones, lane);
+      cand_tile<D, TC, true>(T, W, CandList{ids + a0}, a1 - a0, rows, a, M, ones, lane);
     } else {
-      cand_tile<D, TC>(T, W, CandAll{}, T.S, rows, a, M, ones, lane);
+      cand_tile<D, TC, true>(T, W, CandAll{}, T.S, rows, a, M, ones, lane);
     }
     todo &= ~rows;
   }
-  cand_drain<D>(T, W, W.qn, lane);
-  if (valid && p == 0)
-    out_cand[qi] = T.S + 1 + W.kept[row] + ones + (cell >= 0 ? __ldg(fixed + cell) : 0);
+  cand_flush(W, W.qn, lane);
+  // cand_solve_kernel adds the undecided pairs' survivors afterwards
+  if (valid && p == 0) {
+    out_cand[qi] = T.S + 1 + ones + (cell >= 0 ? __ldg(fixed + cell) : 0);
+    if ((redo_rows[wi] >> row) & 1u) redo_list[atomicAdd(redo_n, 1ull)] = qi;
+  }
   if (n_uncertain && lane == 0) atomicAdd(n_uncertain, W.unc);
+}
+
+// the undecided pairs of cand_cells_kernel, one thread each, solved as the
+// reference does (kept_pieces); adds to the query's count in caller order
+template <int D>
+__global__ void __launch_bounds__(128) cand_solve_kernel(const TableView T, const double* qs,
+                                                         const uint2* glist,
+                                                         const unsigned long long* gcount,
+                                                         unsigned long long gcap, int64_t* out_cand) {
+  unsigned long long total = *gcount;
+  if (total > gcap) total = gcap;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint2 e = glist[i];
+    double q[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) q[k] = qs[(int64_t)e.x * D + k];
+    const int kp = kept_pieces<D>(T, (int64_t)e.y, q);
+    if (kp) atomicAdd((unsigned long long*)&out_cand[e.x], (unsigned long long)kp);
+  }
 }
 
 }  // namespace mrep

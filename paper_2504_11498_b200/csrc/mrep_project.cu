@@ -3778,14 +3778,34 @@ static int project_chunk(const void* table, int64_t S, int d, const double* quer
     static const bool cuda_cores = getenv("MREP_CAND_CUDA_CORES") != nullptr;
     if (flags & MREP_CAND_CELLS) {
       // the table's cand cell index (mrep_cand_cells_build), queries in the
-      // pipeline's sorted order
+      // pipeline's sorted order; undecided pairs solved by a second kernel
+      unsigned long long gcap = (unsigned long long)std::max<int64_t>(16 * n, 1 << 16);
+      if (const char* e = getenv("MREP_CAND_GCAP"))  // tests: force the redo pass
+        gcap = std::min<unsigned long long>(gcap, (unsigned long long)std::max(1LL, atoll(e)));
+      char* gws = nullptr;
+      MREP_CUDA_CHECK(cudaMallocAsync((void**)&gws, 256 + gcap * sizeof(uint2) + n * 8, st));
+      unsigned long long* gcount = (unsigned long long*)gws;
+      unsigned long long* redo_n = gcount + 1;
+      uint2* glist = (uint2*)(gws + 256);
+      int64_t* redo = (int64_t*)(gws + 256 + gcap * sizeof(uint2));
+      MREP_CUDA_CHECK(cudaMemsetAsync(gcount, 0, 16, st));
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       if (d == 3) {
-        if (cuda_cores) cand_cells_kernel<3, false><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, p.perm, n, out_cand, unc);
-        else cand_cells_kernel<3, true><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, p.perm, n, out_cand, unc);
+        if (cuda_cores) cand_cells_kernel<3, false><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, p.perm, n, out_cand, unc, glist, gcount, gcap, redo, redo_n);
+        else cand_cells_kernel<3, true><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, p.perm, n, out_cand, unc, glist, gcount, gcap, redo, redo_n);
+        cand_solve_kernel<3><<<(unsigned)sms * 16u, 128, 0, st>>>(p.tab, queries, glist, gcount, gcap, out_cand);
+        // rows whose undecided pairs overflowed the list: recounted whole
+        cand_count_kernel<3, true><<<(unsigned)sms * 4u, CAND_WARPS * 32, 0, st>>>(p.tab, queries, 0, out_cand, nullptr, redo, redo_n);
       } else {
-        if (cuda_cores) cand_cells_kernel<2, false><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, p.perm, n, out_cand, unc);
-        else cand_cells_kernel<2, true><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, p.perm, n, out_cand, unc);
+        if (cuda_cores) cand_cells_kernel<2, false><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, p.perm, n, out_cand, unc, glist, gcount, gcap, redo, redo_n);
+        else cand_cells_kernel<2, true><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, p.perm, n, out_cand, unc, glist, gcount, gcap, redo, redo_n);
+        cand_solve_kernel<2><<<(unsigned)sms * 16u, 128, 0, st>>>(p.tab, queries, glist, gcount, gcap, out_cand);
+        cand_count_kernel<2, true><<<(unsigned)sms * 4u, CAND_WARPS * 32, 0, st>>>(p.tab, queries, 0, out_cand, nullptr, redo, redo_n);
       }
+      MREP_LAUNCH_CHECK();
+      MREP_CUDA_CHECK(cudaFreeAsync(gws, st));
     } else if (d == 3) {
       if (cuda_cores) cand_count_kernel<3, false><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, n, out_cand, unc);
       else cand_count_kernel<3, true><<<blocks, CAND_WARPS * 32, 0, st>>>(p.tab, queries, n, out_cand, unc);

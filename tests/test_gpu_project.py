@@ -425,3 +425,30 @@ def test_cand_cell_index_2d(gpu, oracle_lib):
     o = oracle_lib.project_block(prep.seg_pts, prep.seg_ta, prep.seg_tb, prep.seam_t,
                                  prep.seam_pt, q[::10], workers=8)
     assert np.array_equal(idx[::10], o["cand"])
+
+
+def test_cand_cell_index_list_overflow_redo(gpu):
+    """Undecided pairs that overflow the global list (forced tiny with
+    MREP_CAND_GCAP) send their rows to the whole-row recount: same counts."""
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, sys
+sys.path.insert(0, '.')
+from paper_2504_11498_b200 import prepare_curve, _lib as L
+from paper_2504_11498_b200.fixtures import random_clamped_curve
+cv = random_clamped_curve(np.random.default_rng(0), 7, 300, 3, uniform_knots=True)
+tab = prepare_curve(cv, 1e-4).table
+tab.cand_tried = True
+q = np.random.default_rng(8).uniform(-0.2, 1.2, (70000, 3))
+full = tab.project(q, extra_flags=L.MREP_CAND_EXACT)[3].cpu().numpy()
+tab.build_cand_cells(32)
+idx = tab.project(q, extra_flags=L.MREP_CAND_EXACT | L.MREP_CAND_CELLS)[3].cpu().numpy()
+assert np.array_equal(idx, full), np.nonzero(idx != full)[0][:10]
+print("ok")
+"""
+    import os
+    env = dict(os.environ, MREP_CAND_GCAP="5000")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
