@@ -1558,6 +1558,186 @@ __global__ void __launch_bounds__(BLOCK, MREP_TRAV_MINB) wave_traverse(const __g
   }
 }
 
+// W1, tensor-core cell screen (MREP_TRAV_DMMA; single table with a cell
+// index).  One warp = 8 consecutive sorted queries (rows of an m8n8k4 FP64
+// MMA).  Rows of one cell scan its list together; per listed cubic ONE
+// mma.sync with the cubic's tensor-core fragment (the same B operand as the
+// exact-cand pass: the differences d_{j+1} - d_j of the degree-6 Bernstein
+// coefficients of |C(u) - q|^2, affine in q) gives all 8 rows' coefficient
+// differences; with d_0 = |P_0 - q|^2 a prefix over the row's lanes yields
+// d_0..d_6, whose minimum (less a 1e-9 relative margin, as bern_may_reach)
+// is a rigorous lower bound of |C(u) - q|^2 on the cubic -- tighter than the
+// control-point box, and computed on the tensor pipe instead of per lane.
+// A row stops at the first list key past its cut (keys ascend); the rest
+// is traverse_task's cell mode: seams of kept cubics into the row's band,
+// pairs buffered and appended once.  Rows outside the grid run
+// traverse_task's per-lane walk.  Same exactness argument as the box test
+// (any pruned cubic's candidates lie beyond dmin + 1e-12), so t / foot /
+// distance / segment are unchanged; the screened `cand` counts this walk.
+template <int D>
+__global__ void __launch_bounds__(BLOCK, MREP_TRAV_MINB) wave_traverse_dmma(const __grid_constant__ WaveParams w) {
+  const int lane = threadIdx.x & 31, row = lane >> 2, p = lane & 3;
+  const int64_t g0 = (((int64_t)blockIdx.x * BLOCK + threadIdx.x) >> 5) * 8;
+  const int64_t gi = g0 + row;
+  const bool active = gi < w.n;
+  const TableView& T = w.tab;
+  const int64_t qi = active ? (w.perm ? (int64_t)w.perm[gi] : gi) : 0;
+  double q[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) q[k] = active ? w.q[qi * D + k] : 0.0;
+  double scale = T.hdr[4];
+#pragma unroll
+  for (int k = 0; k < D; ++k) scale = fmax(scale, fabs(q[k]));
+  int64_t cell = -1;
+  const bool incell = active && cell_of<D>(T, q, cell);
+  // rows outside the grid: the per-lane walk of traverse_task (lane p == 0)
+  if (active && !incell && p == 0) traverse_task<D, false, TM_LANE>(w, gi, nullptr, lane);
+  const unsigned vin = __ballot_sync(0xffffffffu, incell && p == 0);
+  unsigned todo = 0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) todo |= ((vin >> (4 * r)) & 1u) << r;
+  if (!todo) return;  // warp-uniform
+  const double a = p == 0 ? 1.0 : (p <= D ? q[p - 1] - T.hdr[4 + p] : 0.0);
+  const bool owner = incell && p == 0;
+  bool fall = false;
+  Band B;
+  band_init(B, false, 0.0);
+  QStats st{};
+  constexpr int PEND = 8;
+  uint32_t pend[PEND];
+  int np = 0;
+  const double* F = T.bfrag;
+  while (todo) {
+    const int lead = __ffs(todo) - 1;
+    const int64_t lc = __shfl_sync(0xffffffffu, cell, 4 * lead);
+    const unsigned same = __ballot_sync(0xffffffffu, p == 0 && incell && cell == lc);
+    unsigned rows = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) rows |= ((same >> (4 * r)) & 1u) << r;
+    rows &= todo;
+    todo &= ~rows;
+    int32_t a0, a1;
+    const int32_t* ids = cell_list(T, D, lc, a0, a1);
+    const float* keys = cell_keys(T, ids);
+    bool mine = ((rows >> row) & 1u) != 0;  // this row still scans (all 4 lanes)
+    int32_t s_nxt = a0 < a1 ? __ldg(ids + a0) : 0;
+#pragma unroll 1
+    for (int32_t k = a0; k < a1; ++k) {
+      const int64_t s = s_nxt;
+      if (k + 1 < a1) s_nxt = __ldg(ids + k + 1);
+      // keys ascend: past a row's cut no later cubic can hold a band candidate
+      bool go = false;
+      if (owner && mine) go = !((double)__ldg(keys + k) > cut2(B.dmin, scale));
+      const unsigned gb = __ballot_sync(0xffffffffu, go);
+      mine = ((gb >> (lane & ~3)) & 1u) != 0;
+      if (!gb) break;
+      const double b = __ldg(F + s * 32 + lane);
+      double c0, c1;
+      dmma_8x8x4(a, b, c0, c1);
+      // d_0 = |P_0 - q|^2 (lane p == 0), then d_{j+1} = d_j + (d_{j+1} - d_j)
+      double d0 = 0.0;
+      if (p == 0) {
+        const double* r0 = T.rec + s * REC + R_P;
+#pragma unroll
+        for (int k2 = 0; k2 < D; ++k2) {
+          const double df = __ldg(r0 + k2) - q[k2];
+          d0 += df * df;
+        }
+      }
+      const bool col = p <= 2;  // lanes p = 0..2 hold the six differences
+      const double x = col ? c0 : 0.0, y = col ? c1 : 0.0;
+      const double xy = x + y;
+      double pre = __shfl_up_sync(0xffffffffu, xy, 1);
+      if (p == 0) pre = 0.0;
+      const double pre2 = __shfl_up_sync(0xffffffffu, pre, 1);
+      pre += (p >= 2) ? pre2 : 0.0;
+      d0 = __shfl_sync(0xffffffffu, d0, lane & ~3);
+      double mn = fmin(d0 + pre + x, d0 + pre + xy);
+      if (!col) mn = d0;
+      double mag = fabs(x) + fabs(y);
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, 2));
+      mag += __shfl_xor_sync(0xffffffffu, mag, 1);
+      mag += __shfl_xor_sync(0xffffffffu, mag, 2);
+      mn = fmin(mn, d0);
+      if (go) {
+        st.boxes++;
+        // as bern_may_reach: prune iff min_j d_j - 1e-9 mag > cut^2
+        // (mag = |d_0| + sum |b_j|, b_j = 6 (d_{j+1} - d_j))
+        const double magb = fabs(d0) + 6.0 * mag;
+        const bool need = !(mn - 1e-9 * magb > cut2(B.dmin, scale));
+        if (need) {
+#pragma unroll 1
+          for (int e = 0; e < 2; ++e) offer_seam<D>(T, s + e, q, B, st);
+          st.pairs++;
+          if (np == PEND) {  // buffer full (rare): this lane appends alone
+            const unsigned long long base = atomicAdd(&w.cnt[0], (unsigned long long)PEND);
+#pragma unroll
+            for (int e = 0; e < PEND; ++e) {
+              if (base + e < w.pcap) {
+                w.pq[base + e] = (uint32_t)gi;
+                w.ps[base + e] = pend[e];
+              } else {
+                fall = true;
+              }
+            }
+            np = 0;
+          }
+#pragma unroll
+          for (int e = 0; e < PEND; ++e)
+            if (e == np) pend[e] = (uint32_t)s;
+          ++np;
+        }
+      }
+    }
+  }
+  // buffered pairs: one warp-wide reservation
+  int incl = np;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total) {
+    unsigned long long base = 0;
+    if (lane == 31) base = atomicAdd(&w.cnt[0], (unsigned long long)total);
+    base = __shfl_sync(0xffffffffu, base, 31) + (unsigned long long)(incl - np);
+#pragma unroll
+    for (int e = 0; e < PEND; ++e) {
+      if (e < np) {
+        if (base + e < w.pcap) {
+          w.pq[base + e] = (uint32_t)gi;
+          w.ps[base + e] = pend[e];
+        } else {
+          fall = true;
+        }
+      }
+    }
+  }
+  if (owner) {
+    if (B.overflow) fall = true;
+    double4 rec;
+    rec.x = q[0];
+    rec.y = q[1];
+    rec.z = D == 3 ? q[D - 1] : 0.0;
+    rec.w = B.dmin;
+    *(double4*)(w.qs + gi * 4) = rec;
+#pragma unroll
+    for (int j = 0; j < BAND_K; ++j)
+      if (((B.valid >> j) & 1u) && !add_cand(w, gi, B.t[j], B.d[j], -1.0, (uint32_t)B.ord[j]))
+        fall = true;
+    w.scnt[gi] = (int64_t)(st.offers + st.pairs);
+    w.flag[gi] = fall ? 1 : 0;
+    if (fall) {
+      unsigned long long slot = atomicAdd(&w.cnt[3], 1ull);
+      w.fb[slot] = gi;
+    }
+  }
+  warp_count(w.counters, MREP_CNT_SEAMS, owner ? st.seams : 0);
+  warp_count(w.counters, MREP_CNT_BOXES, owner ? st.boxes : 0);
+}
+
 // W1, group mode: one 8-lane group per query, lane c tests child c of the
 // node being expanded (the 8-ary hierarchy maps onto the group: one
 // coalesced 384-B box load per expansion instead of 8 dependent loads).
@@ -3042,7 +3222,11 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   } else if (tmode == TRAV_PACKET) {
     wave_traverse<D, false, TM_PACKET><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
   } else if (tmode == TRAV_CELLS) {
-    wave_traverse<D, false, TM_CELLS><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
+    static const bool dmma = getenv("MREP_TRAV_DMMA") != nullptr;
+    if (dmma && D == 3)
+      wave_traverse_dmma<D><<<grid_for((n + 7) / 8 * 32, BLOCK), BLOCK, 0, st>>>(w);
+    else
+      wave_traverse<D, false, TM_CELLS><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
   } else {
     wave_traverse<D, false, TM_LANE><<<grid_for(n, BLOCK), BLOCK, 0, st>>>(w);
   }
