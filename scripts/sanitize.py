@@ -48,6 +48,11 @@ def stage_curve():
     tab.project(qd)
     project_prepared(prep, q, return_segments=True, return_spans=True)
     project_prepared(prep, q[:256], with_stats=True, soundness_samples=4)
+    # exact cand: full tensor-core pass, then with the cand cell index
+    tab.cand_tried = True
+    tab.project(qd, extra_flags=L.MREP_CAND_EXACT)
+    tab.build_cand_cells(8)
+    tab.project(qd, extra_flags=L.MREP_CAND_EXACT | L.MREP_CAND_CELLS)
 
 
 def stage_host():
