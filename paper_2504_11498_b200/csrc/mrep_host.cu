@@ -237,9 +237,11 @@ int host_pipeline(HostCtx& g_ctx, int d, const double* queries, const int32_t* c
 
   const int NS = num_slots();
   const bool fast = pin_in && pin_out && !getenv("MREP_E2E_SLOTTED");
-  for (auto& s : g_ctx.slot)
-    MREP_CUDA_CHECK(cudaMemsetAsync(s.dcnt, 0, MREP_NUM_COUNTERS * sizeof(uint64_t),
-                                    fast ? g_ctx.cin : s.st));
+  // work counters only when the caller asked for them (4 memsets saved per call)
+  if (counters_host)
+    for (auto& s : g_ctx.slot)
+      MREP_CUDA_CHECK(cudaMemsetAsync(s.dcnt, 0, MREP_NUM_COUNTERS * sizeof(uint64_t),
+                                      fast ? g_ctx.cin : s.st));
   if (fast) {
     static const bool use_prio = !getenv("MREP_E2E_PRIO") || atoi(getenv("MREP_E2E_PRIO")) != 0;
     const int NS = getenv("MREP_E2E_SLOTS") ? num_slots() : 2;
@@ -561,7 +563,8 @@ extern "C" int mrep_project_host(const void* table, int64_t S, int d, const doub
                        counters_host, [&](Slot& s) {
                          return mrep_project(table, S, d, s.dq, s.cnt, clip_tol, max_iter, 0,
                                              flags, s.dt, s.dfoot, s.ddist, s.dcand, s.dseg,
-                                             nullptr, nullptr, s.dcnt, s.st);
+                                             nullptr, nullptr, counters_host ? s.dcnt : nullptr,
+                                             s.st);
                        });
 }
 
@@ -583,7 +586,7 @@ extern "C" int mrep_project_batch_host(const void* set, const double* queries,
                        counters_host, [&](Slot& s) {
                          return mrep_project_batch(set, s.dq, s.dcur, s.cnt, clip_tol, max_iter,
                                                    flags, s.dt, s.dfoot, s.ddist, s.dcand, s.dseg,
-                                                   s.dcnt, s.st);
+                                                   counters_host ? s.dcnt : nullptr, s.st);
                        });
 }
 
@@ -606,7 +609,8 @@ extern "C" int mrep_project_surface_host(const void* table, int64_t npatch, int 
                        out_patch, counters_host, [&](Slot& s) {
                          return mrep_project_surface(table, npatch, pu, pv, s.dq, s.cnt, flags,
                                                      s.dt, (double*)s.dcand, s.dfoot, s.ddist,
-                                                     s.dseg, s.dcnt, s.st);
+                                                     s.dseg, counters_host ? s.dcnt : nullptr,
+                                                     s.st);
                        });
 }
 

@@ -3088,6 +3088,28 @@ static int trav_mode(unsigned flags, int64_t n, int64_t S, int top) {
   return TRAV_GROUP;
 }
 
+// resident blocks x SMs of a kernel on the current device (cached: the
+// occupancy query costs microseconds of host time per launch otherwise)
+static unsigned persistent_grid(const void* fn, int block) {
+  struct Key {
+    const void* fn;
+    int block, dev;
+  };
+  static std::mutex mu;
+  static std::vector<std::pair<Key, unsigned>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto& e : cache)
+    if (e.first.fn == fn && e.first.block == block && e.first.dev == dev) return e.second;
+  int sms = 148, per = 1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, block, 0);
+  const unsigned g = (unsigned)(sms * (per > 0 ? per : 1));
+  cache.push_back({Key{fn, block, dev}, g});
+  return g;
+}
+
 template <int D, bool MULTI>
 static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tmode,
                        const TableView* tabs = nullptr, const int32_t* qcurve = nullptr,
@@ -3174,13 +3196,7 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   w.trav_bern = trav_bern;
   w.trav_sort = trav_sort;
   MREP_CUDA_CHECK(cudaMemsetAsync(w.cnt, 0, 8 * sizeof(unsigned long long), st));
-  auto persist_grid = [](const void* fn, int block) {
-    int dev = 0, sms = 148, per = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, block, 0);
-    return (unsigned)(sms * (per > 0 ? per : 1));
-  };
+  auto persist_grid = [](const void* fn, int block) { return persistent_grid(fn, block); };
   const unsigned g_pairs = persist_grid((const void*)wave_pairs<D, MULTI>, BLOCK);
   const unsigned g_clip = persist_grid((const void*)wave_clip<D, MULTI>, BLOCK);
   StageTimer tm(timing, st);
