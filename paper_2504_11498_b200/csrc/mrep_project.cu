@@ -3853,7 +3853,11 @@ int mrep_project(const void* table, int64_t S, int d, const double* queries, int
                  double* out_t, double* out_foot, double* out_dist, int64_t* out_cand,
                  int32_t* out_seg, int64_t* out_stats, double* out_sound, uint64_t* counters,
                  void* stream) {
-  const int64_t CHUNK_Q = (int64_t)1 << 23;
+  static const int64_t CHUNK_Q = [] {
+    const char* e = getenv("MREP_CHUNK_Q");  // A/B: queries per internal chunk
+    const int64_t v = e ? atoll(e) : ((int64_t)1 << 23);
+    return v < 4096 ? (int64_t)4096 : v;
+  }();
   if (flags & MREP_TIMING)
     for (double& v : g_stage_ms) v = 0.0;
   if (n <= CHUNK_Q)

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include <cub/cub.cuh>
 
@@ -23,7 +24,12 @@ inline int bucket_bits(int64_t n, int D) {
   int lg = 0;
   while (lg < 40 && ((int64_t)1 << (lg + 1)) <= n) ++lg;  // floor(log2 n)
   int b = (lg - 1 + D / 2) / D;
-  const int lo = D == 3 ? 4 : 6, hi = D == 3 ? 6 : 9;
+  static const int hi3 = [] {
+    const char* e = getenv("MREP_BUCKET_MAX");  // A/B: finest bits per axis (3-D)
+    const int v = e ? atoi(e) : 6;
+    return v < 4 ? 4 : (v > 9 ? 9 : v);
+  }();
+  const int lo = D == 3 ? 4 : 6, hi = D == 3 ? hi3 : 9;
   return b < lo ? lo : (b > hi ? hi : b);
 }
 

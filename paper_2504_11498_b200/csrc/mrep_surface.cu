@@ -707,7 +707,10 @@ __global__ void __launch_bounds__(256) surf_filter(const __grid_constant__ SurfP
 // do not leave lanes idle.  PASS 0: each query's greedy-descent patch
 // (its minimum is a tight bound); PASS 1: the compacted survivors.
 template <int PU, int PV, int PASS>
-__global__ void __launch_bounds__(128, (PU + PV <= 6) ? 3 : 1) surf_solve(const __grid_constant__ SurfParams w) {
+#ifndef MREP_SURF_SOLVE_MINB
+#define MREP_SURF_SOLVE_MINB 3
+#endif
+__global__ void __launch_bounds__(128, (PU + PV <= 6) ? MREP_SURF_SOLVE_MINB : 1) surf_solve(const __grid_constant__ SurfParams w) {
   // each lane's current control net, staged column-wise in shared memory
   // (element k of lane t at [k][t]: conflict-free), so the ~20 surface
   // evaluations of a solve read shared memory instead of 3(p+1)^2 scattered
