@@ -452,3 +452,35 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_dmma_cell_screen_bitwise_equal(gpu):
+    """MREP_TRAV_DMMA (tensor-core Bernstein screen of the cell lists, an A/B
+    variant) returns the default pipeline's t / foot / distance / segment
+    bit for bit, including queries outside the cell grid."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, sys, torch
+sys.path.insert(0, '.')
+from paper_2504_11498_b200 import prepare_curve
+from paper_2504_11498_b200.fixtures import random_clamped_curve
+cv = random_clamped_curve(np.random.default_rng(0), 7, 400, 3, uniform_knots=True)
+tab = prepare_curve(cv, 1e-4).table
+tab.CELL_MIN_QUERIES = 0
+q = np.random.default_rng(9).uniform(-0.3, 1.3, (90000, 3))
+r = tab.project(q)
+np.savez(sys.argv[1], t=r[0].cpu().numpy(), f=r[1].cpu().numpy(), d=r[2].cpu().numpy(),
+         s=r[4].cpu().numpy())
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for k, env in enumerate((dict(os.environ), dict(os.environ, MREP_TRAV_DMMA="1"))):
+        path = os.path.join(root, "build", f"dmma_{k}.npz")
+        r = subprocess.run([sys.executable, "-c", code, path], env=env, cwd=root,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    for key in ("t", "f", "d", "s"):
+        assert np.array_equal(outs[0][key], outs[1][key], equal_nan=True), key
