@@ -274,6 +274,10 @@ MREP_API int64_t mrep_cand_cells_bytes(const void* table_dev, int64_t S, int d, 
                                        void* stream);
 MREP_API int mrep_cand_cells_build(void* table_dev, int64_t S, int d, int grid, void* buf_dev,
                                    int64_t bytes, void* stream);
+/* host-side convenience (no GPU framework on the caller's side): allocates,
+ * builds and records the index; free *buf_out with mrep_table_free once the
+ * table is no longer projected with MREP_CAND_CELLS */
+MREP_API int mrep_cand_cells_create(void* table_dev, int64_t S, int d, int grid, void** buf_out);
 
 /* The same cell index for a surface table (mrep_surface_table_pack): the
  * exact points are each patch's seed grid; mrep_project_surface with

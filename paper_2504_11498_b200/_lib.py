@@ -89,6 +89,7 @@ _SIGS = {
     "mrep_cells_build": ([_vp, _i64, _i32, _i32, _vp, _i64, _vp], _i32),
     "mrep_cand_cells_bytes": ([_vp, _i64, _i32, _i32, _vp], _i64),
     "mrep_cand_cells_build": ([_vp, _i64, _i32, _i32, _vp, _i64, _vp], _i32),
+    "mrep_cand_cells_create": ([_vp, _i64, _i32, _i32, _vp], _i32),
     "mrep_surface_cells_bytes": ([_vp, _i64, _i32, _i32, _i32, _vp], _i64),
     "mrep_surface_cells_build": ([_vp, _i64, _i32, _i32, _i32, _vp, _i64, _vp], _i32),
     "mrep_knot_span": ([_vp, _i64, _i32, _vp, _i64, _vp, _vp], _i32),

@@ -4244,6 +4244,25 @@ int mrep_cand_cells_build(void* table, int64_t S, int d, int grid, void* buf, in
   return MREP_OK;
 }
 
+int mrep_cand_cells_create(void* table, int64_t S, int d, int grid, void** buf_out) {
+  if (!buf_out) {
+    set_error("mrep_cand_cells_create: null output pointer");
+    return MREP_ERR_ARG;
+  }
+  *buf_out = nullptr;
+  const int64_t nb = mrep_cand_cells_bytes(table, S, d, grid, nullptr);
+  if (nb <= 0) return MREP_ERR_ARG;
+  void* buf = nullptr;
+  MREP_CUDA_CHECK(cudaMalloc(&buf, (size_t)nb));
+  const int rc = mrep_cand_cells_build(table, S, d, grid, buf, nb, nullptr);
+  if (rc != MREP_OK) {
+    cudaFree(buf);
+    return rc;
+  }
+  *buf_out = buf;
+  return MREP_OK;
+}
+
 int mrep_knot_span(const double* knots, int64_t m, int p, const double* t, int64_t n,
                    int32_t* span, void* stream) {
   if (n <= 0) return MREP_OK;

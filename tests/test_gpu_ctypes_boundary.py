@@ -69,3 +69,31 @@ def test_table_handle_and_host_projection(lib):
     assert np.all(np.abs(t - z["t"]) <= 1e-6)
     assert np.all(np.abs(dist - z["dist"]) <= 1e-9 * z["dist"])
     assert cnt[0] > 0 and cnt[6] == 0  # pairs solved, no hull misses
+
+
+@pytest.mark.parametrize("name", ["cfg1_random", "cfg2", "deg5_2d"])
+def test_host_call_reference_cand_with_cand_index(lib, name):
+    """flags MREP_SCREEN | MREP_CAND_EXACT return the
+    reference's own cand; with mrep_cand_cells_create + MREP_CAND_CELLS too."""
+    z = load_golden(f"project_{name}.npz")
+    S, _, d = z["seg_pts"].shape
+    n = len(z["queries"])
+    arrs = [np.ascontiguousarray(z[k]) for k in ("seg_pts", "seg_ta", "seg_tb", "seam_t", "seam_pt")]
+    h = ctypes.c_void_p()
+    assert lib.mrep_table_create(*[_p(a) for a in arrs], S, d, ctypes.byref(h)) == 0
+    lib.mrep_cand_cells_create.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                           ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
+    q = np.ascontiguousarray(z["queries"])
+    for flags, with_index in ((1 | 512, False), (1 | 512 | 1024, True)):
+        cc = ctypes.c_void_p()
+        if with_index:
+            assert lib.mrep_cand_cells_create(h, S, d, 16, ctypes.byref(cc)) == 0
+        out = (np.empty(n), np.empty((n, d)), np.empty(n), np.empty(n, np.int64),
+               np.empty(n, np.int32))
+        assert lib.mrep_project_host(h, S, d, _p(q), n, float(z["clip_tol"]), int(z["max_iter"]),
+                                     flags, *[_p(o) for o in out], None) == 0
+        assert np.array_equal(out[3], z["cand"]), (name, flags)
+        assert np.all(np.abs(out[0] - z["t"]) <= 1e-6)
+        if with_index:
+            lib.mrep_table_free(cc)
+    lib.mrep_table_free(h)
