@@ -132,6 +132,40 @@ __device__ __noinline__ Cubic3 cubic_roots3(double c0, double c1, double c2, dou
   return o;
 }
 
+// The largest real root of the resolvent cubic, as the reference computes it
+// (_kernels.py:141-145: every root of _cubic_roots, then the strict max).
+// In the three-real-roots branch th = acos(.)/3 lies in [0, pi/3], so
+// cos(th) >= 1/2 >= cos(th - 2pi/3) and cos(th - 4pi/3) <= -1/2: with m > 0
+// the k = 2 root is below the k = 0 root by m (1 - 2 eps) and can only equal
+// it when both round to `off` -- it never changes the maximum, and its
+// cosine is skipped.  Same operations otherwise, so the same bits.
+__device__ __noinline__ bool resolvent_max_root(double c0, double c1, double c2, double c3,
+                                               double& mmax) {
+  // c3 = 8 here (never zero)
+  double b = c2 / c3, c = c1 / c3, d = c0 / c3;
+  double p = c - b * b / 3.0;
+  double q = 2.0 * pow3(b) / 27.0 - b * c / 3.0 + d;
+  double off = -b / 3.0;
+  double disc = -4.0 * pow3(p) - 27.0 * q * q;
+  if (disc >= 0.0 && p < 0.0) {
+    double m = 2.0 * sqrt(-p / 3.0);
+    double arg = 3.0 * q / (p * m);
+    if (arg > 1.0) arg = 1.0;
+    else if (arg < -1.0) arg = -1.0;
+    double th = acos(arg) / 3.0;
+    const double r0 = m * cos(th - 2.0943951023931953 * 0.0) + off;
+    const double r1 = m * cos(th - 2.0943951023931953 * 1.0) + off;
+    mmax = r1 > r0 ? r1 : r0;
+    return true;
+  }
+  double rr = q * q / 4.0 + pow3(p) / 27.0;
+  double srt = sqrt((0.0 > rr) ? 0.0 : rr);  // Python max(rr, 0.0)
+  double u = -q / 2.0 + srt;
+  double v = -q / 2.0 - srt;
+  mmax = np_cbrt(u) + np_cbrt(v) + off;
+  return true;
+}
+
 // Root set of E' on [0,1]: up to 4 sorted slots, `valid` bitmask (bit i = slot i).
 struct Roots4 {
   double r[4];
@@ -217,11 +251,9 @@ __device__ __forceinline__ Roots4 quartic_roots_01(const double c[5]) {
       }
     } else {
       // resolvent cubic 8m^3 + 8p m^2 + (2p^2 - 8r) m - q^2 = 0
-      Cubic3 cr = cubic_roots3(-q * q, 2.0 * p * p - 8.0 * r, 8.0 * p, 8.0);
-      double m = cr.r0;
-      if (cr.n > 1 && cr.r1 > m) m = cr.r1;
-      if (cr.n > 2 && cr.r2 > m) m = cr.r2;
-      if (cr.n > 0 && m > 0.0) {
+      double m = 0.0;
+      const bool have = resolvent_max_root(-q * q, 2.0 * p * p - 8.0 * r, 8.0 * p, 8.0, m);
+      if (have && m > 0.0) {
         double s = sqrt(2.0 * m);
 #pragma unroll 1
         for (int j = 0; j < 2; ++j) {
