@@ -70,7 +70,7 @@ def lib():
                                             ctypes.POINTER(ctypes.c_int)]
         L.oracle_surface_project.argtypes = [_dp, _dp, ctypes.c_int64, ctypes.c_int,
                                              ctypes.c_int, _dp, ctypes.c_int64, ctypes.c_int,
-                                             _dp, _dp, _dp, _dp, _i32p]
+                                             _dp, _dp, _dp, _dp, _i32p, _i32p]
         _lib = L
     return _lib
 
@@ -180,17 +180,19 @@ def project_block(seg_pts, seg_ta, seg_tb, seam_t, seam_pt, queries, clip_tol=1e
 def surface_project(patch_pts, patch_iv, pu, pv, queries, workers=1):
     """Brute-force surface projection (mrep_surface_oracle.c): patch_pts
     [np][pu+1][pv+1][3] and patch_iv [np][4] in patch-id order.
-    Returns dict(u, v, foot, dist, patch)."""
+    Returns dict(u, v, foot, dist, patch, tie); tie = another patch's
+    minimum within dmin (1 + 1e-9) + 1e-12 (the winner then rests on
+    rounding-level differences)."""
     P = _f64(patch_pts).reshape(-1)
     I = _f64(patch_iv).reshape(-1)
     q = _f64(np.atleast_2d(queries))
     npat = P.size // ((pu + 1) * (pv + 1) * 3)
     n = q.shape[0]
     out = dict(u=np.empty(n), v=np.empty(n), foot=np.empty((n, 3)), dist=np.empty(n),
-               patch=np.empty(n, dtype=np.int32))
+               patch=np.empty(n, dtype=np.int32), tie=np.empty(n, dtype=np.int32))
     lib().oracle_surface_project(_p(P), _p(I), npat, pu, pv, _p(q), n, int(workers),
                                  _p(out["u"]), _p(out["v"]), _p(out["foot"]), _p(out["dist"]),
-                                 _p(out["patch"], _i32p))
+                                 _p(out["patch"], _i32p), _p(out["tie"], _i32p))
     return out
 
 

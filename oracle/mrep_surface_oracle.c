@@ -206,6 +206,7 @@ typedef struct {
   int pu, pv;
   double *ou, *ov, *ofoot, *odist;
   int32_t* opatch;
+  int32_t* otie; /* 1: another patch's minimum lies within dmin (1 + 1e-9) + 1e-12 */
 } Job;
 
 static void* run(void* arg) {
@@ -238,6 +239,15 @@ static void* run(void* arg) {
     J->odist[i] = cu[w * 3 + 2];
     for (int k = 0; k < 3; ++k) J->ofoot[i * 3 + k] = S[k];
     J->opatch[i] = (int32_t)w;
+    if (J->otie) {
+      /* a tie: the winner is decided by rounding-level distance differences
+       * (feet on shared patch edges), so another solver may pick the other */
+      int tie = 0;
+      const double band = dmin * (1.0 + 1e-9) + 1e-12;
+      for (int64_t s = 0; s < J->np && !tie; ++s)
+        if (s != w && cu[s * 3 + 2] <= band) tie = 1;
+      J->otie[i] = tie;
+    }
   }
   free(cu);
   return NULL;
@@ -246,7 +256,8 @@ static void* run(void* arg) {
 /* patch_pts [np][pu+1][pv+1][3] and patch_iv [np][4] in patch-id order */
 void oracle_surface_project(const double* patch_pts, const double* patch_iv, int64_t np, int pu,
                             int pv, const double* q, int64_t n, int threads, double* ou,
-                            double* ov, double* ofoot, double* odist, int32_t* opatch) {
+                            double* ov, double* ofoot, double* odist, int32_t* opatch,
+                            int32_t* otie) {
   if (threads < 1) threads = 1;
   if (n < threads) threads = n > 0 ? (int)n : 1;
   Job* jobs = (Job*)calloc((size_t)threads, sizeof(Job));
@@ -254,7 +265,7 @@ void oracle_surface_project(const double* patch_pts, const double* patch_iv, int
   int64_t k = (n + threads - 1) / threads;
   for (int t = 0; t < threads; ++t) {
     Job j = {patch_pts, patch_iv, q, np, t * k, (t + 1) * k < n ? (t + 1) * k : n, pu, pv,
-             ou, ov, ofoot, odist, opatch};
+             ou, ov, ofoot, odist, opatch, otie};
     jobs[t] = j;
     pthread_create(&th[t], NULL, run, &jobs[t]);
   }

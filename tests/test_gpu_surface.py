@@ -48,7 +48,10 @@ def _check(gpu_out, o):
     assert np.all(np.abs(dist - o["dist"]) <= np.maximum(1e-9 * o["dist"], 1e-12)), \
         np.abs(dist - o["dist"]).max()
     same = patch == o["patch"]
-    assert same.mean() >= 0.999
+    # the patch id EXACT except oracle-detected ties (another patch's minimum
+    # within dmin (1 + 1e-9) + 1e-12: a foot on a shared edge)
+    bad = np.nonzero(~same & (o["tie"] == 0))[0]
+    assert bad.size == 0, f"{bad.size} patch mismatches outside ties, e.g. {bad[:5]}"
     assert np.abs(u[same] - o["u"][same]).max() <= 1e-6
     assert np.abs(v[same] - o["v"][same]).max() <= 1e-6
     assert np.abs(foot[same] - o["foot"][same]).max() <= 1e-6
@@ -164,4 +167,4 @@ def test_extreme_scales_use_exact_nets(gpu, oracle_lib, scale):
                                    prep.patch_iv.reshape(-1, 4), 3, 3, q, workers=16)
     u, v, foot, dist, patch = g
     assert np.all(np.abs(dist - o["dist"]) <= np.maximum(1e-9 * o["dist"], 1e-12 * scale))
-    assert (patch == o["patch"]).mean() >= 0.999
+    assert np.all((patch == o["patch"]) | (o["tie"] != 0))
