@@ -104,6 +104,7 @@ struct ProjParams {
   unsigned long long* pass2_count;
   int64_t* pass2_list;
   const uint32_t* perm;  // Morton order of the queries (nullptr = identity)
+  const uint32_t* inv;   // its inverse (large batches: emit through a sorted staging pass)
 };
 
 // ------------------------------------------------------------ tie band
@@ -1102,6 +1103,8 @@ struct WaveParams {
   uint32_t* sq;
   uint32_t* ssk;  // cubic << 3 | piece
   unsigned long long scap;
+  const uint32_t* inv;  // caller -> sorted position (large batches; null otherwise)
+  double* orec;         // with inv: each sorted query's outputs, 8 doubles (unpermuted after)
   uint32_t* ccnt;   // per sorted query: candidates appended so far
   Cand* cin;        // per sorted query: the first CIN candidates, inline ([n][CIN])
   uint32_t* chead;  // per sorted query: last overflow candidate (linked list), ~0 = none
@@ -2155,7 +2158,7 @@ __global__ void rank_count_kernel(const int32_t* qcurve, int64_t n, const uint32
 
 __global__ void rank_scatter_kernel(const int32_t* qcurve, int64_t n, const uint32_t* rank,
                                     int64_t nc, const uint32_t* qstart, uint32_t* cursor,
-                                    uint32_t* perm) {
+                                    uint32_t* perm, uint32_t* inv) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int32_t c = qcurve[i];
@@ -2165,7 +2168,9 @@ __global__ void rank_scatter_kernel(const int32_t* qcurve, int64_t n, const uint
   uint32_t base = 0;
   if (lane == leader) base = atomicAdd(&cursor[r], (unsigned)__popc(peers));
   base = __shfl_sync(peers, base, leader);
-  perm[qstart[r] + base + __popc(peers & ((1u << lane) - 1))] = (uint32_t)i;
+  const uint32_t pos = qstart[r] + base + __popc(peers & ((1u << lane) - 1));
+  perm[pos] = (uint32_t)i;
+  if (inv) inv[i] = pos;  // caller -> sorted position (coalesced)
 }
 
 // per-rank query counts -> first sorted position and first task of each
@@ -2481,7 +2486,7 @@ __global__ void __launch_bounds__(256) wave_emit(const __grid_constant__ WavePar
   if (g >= w.n) return;
   if (w.flag[g]) return;  // written by the fallback kernel
   int64_t qi = w.perm ? (int64_t)w.perm[g] : g;
-  if (w.out_cand) w.out_cand[qi] = w.scnt[g];
+  if (w.out_cand && !w.orec) w.out_cand[qi] = w.scnt[g];
   const double lim = dmin_of(w, g) + 1e-12;
   unsigned long long bt = ~0ull;
   uint32_t bo = ~0u;
@@ -2514,6 +2519,16 @@ __global__ void __launch_bounds__(256) wave_emit(const __grid_constant__ WavePar
   }
   if (!found) {
     const double NaN = __longlong_as_double(0x7ff8000000000000LL);
+    if (w.orec) {
+      double* o = w.orec + g * 8;
+      o[0] = NaN;
+      o[1] = NaN;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) o[2 + k] = NaN;
+      o[5] = __longlong_as_double((long long)w.scnt[g]);
+      o[6] = __longlong_as_double(-1LL);
+      return;
+    }
     w.out_t[qi] = NaN;
     w.out_dist[qi] = NaN;
 #pragma unroll
@@ -2538,11 +2553,42 @@ __global__ void __launch_bounds__(256) wave_emit(const __grid_constant__ WavePar
     seam_point<D>(T, s, foot, stt);
     seg = (int32_t)(s > 0 ? s - 1 : 0);
   }
+  if (w.orec) {
+    // sorted-order staging record (two full 32-B sectors per query); the
+    // unpermute pass writes the caller-order outputs coalesced
+    double4* o = reinterpret_cast<double4*>(w.orec + g * 8);
+    o[0] = make_double4(best_t, best_d, foot[0], foot[1]);
+    o[1] = make_double4(D == 3 ? foot[D - 1] : 0.0, __longlong_as_double((long long)w.scnt[g]),
+                        __longlong_as_double((long long)seg), 0.0);
+    return;
+  }
   w.out_t[qi] = best_t;
   w.out_dist[qi] = best_d;
 #pragma unroll
   for (int k = 0; k < D; ++k) w.out_foot[qi * D + k] = foot[k];
   if (w.out_seg) w.out_seg[qi] = seg;
+}
+
+// Large batches: caller-order outputs from the sorted staging records, one
+// thread per CALLER index -- every output array written coalesced (the
+// scattered 8-B writes of wave_emit would cost partial-sector DRAM
+// read-modify-writes once the outputs exceed L2).  Fallback queries were
+// written directly by wave_fallback and are skipped.
+template <int D>
+__global__ void __launch_bounds__(256) wave_unpermute(const __grid_constant__ WaveParams w) {
+  const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (qi >= w.n) return;
+  const int64_t g = w.inv[qi];
+  if (w.flag[g]) return;
+  const double4* o = reinterpret_cast<const double4*>(w.orec + g * 8);
+  const double4 a = o[0], b = o[1];
+  w.out_t[qi] = a.x;
+  w.out_dist[qi] = a.y;
+  w.out_foot[qi * D] = a.z;
+  w.out_foot[qi * D + 1] = a.w;
+  if (D == 3) w.out_foot[qi * D + D - 1] = b.x;
+  if (w.out_cand) w.out_cand[qi] = (int64_t)__double_as_longlong(b.y);
+  if (w.out_seg) w.out_seg[qi] = (int32_t)__double_as_longlong(b.z);
 }
 
 // diagnostics: emitted pairs / survivors / candidates into counters[7] (packed 21 bits each)
@@ -3131,6 +3177,7 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   size_t o_sb = take(scap * 64), o_sq = take(scap * 4), o_ssk = take(scap * 4);
   size_t o_cand = take(ccap * sizeof(Cand)), o_chead = take(n * 4);
   size_t o_ccnt = take(n * 4), o_cin = take(n * CIN * sizeof(Cand));
+  size_t o_orec = p.inv ? take(n * 64) : 0;
   size_t o_fb = take(n * 8);
   size_t o_qs = take(n * 4 * 8), o_wt = take(n * 8), o_wd = take(n * 8), o_wv = take(n * 8),
          o_sc = take(n * 8);
@@ -3165,6 +3212,8 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   w.cand = (Cand*)(base + o_cand);
   w.chead = (uint32_t*)(base + o_chead);
   MREP_CUDA_CHECK(cudaMemsetAsync(w.chead, 0xff, n * 4, st));
+  w.inv = p.inv;
+  w.orec = w.inv ? (double*)(base + o_orec) : nullptr;
   w.ccnt = (uint32_t*)(base + o_ccnt);
   w.cin = (Cand*)(base + o_cin);
   MREP_CUDA_CHECK(cudaMemsetAsync(w.ccnt, 0, n * 4, st));
@@ -3257,6 +3306,10 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   tm.mark();
   wave_emit<D, MULTI><<<grid_for(n, 256), 256, 0, st>>>(w);
   MREP_LAUNCH_CHECK();
+  if (w.inv) {  // flagged queries are skipped: the fallback writes them
+    wave_unpermute<D><<<grid_for(n, 256), 256, 0, st>>>(w);
+    MREP_LAUNCH_CHECK();
+  }
   tm.mark();
   wave_fallback<D, MULTI><<<148u, BLOCK, 0, st>>>(w, p);
   MREP_LAUNCH_CHECK();
@@ -3752,8 +3805,10 @@ static int project_batch_chunk(const CurveSet* cs, const double* queries, const 
     MREP_LAUNCH_CHECK();
     stage_plan_kernel<<<1, 1024, 0, st>>>(rcnt, cs->nc, qstart, tstart);
     MREP_LAUNCH_CHECK();
+    // k_in is unused on this path: the inverse permutation for the unpermute pass
     rank_scatter_kernel<<<grid_for(n, 256), 256, 0, st>>>(qcurve, n, cs->rank, cs->nc, qstart,
-                                                          cursor, i_out);
+                                                          cursor, i_out, (uint32_t*)k_in);
+    p.inv = (const uint32_t*)k_in;
     MREP_LAUNCH_CHECK();
   } else {
     if (d == 3)
@@ -3930,6 +3985,14 @@ static int project_chunk(const void* table, int64_t S, int d, const double* quer
   p.pass2_list = (int64_t*)(wc + off_list);
   MREP_CUDA_CHECK(cudaMemsetAsync(ws, 0, 16, st));
   p.perm = nullptr;
+  p.inv = nullptr;
+  // sorted batches emit through sorted staging records and an unpermute
+  // pass (MREP_UNPERM_MIN queries; default 2^16, i.e. whenever sorted):
+  // cfg2 emit 0.094 -> 0.073 ms, cfg5 4.1 -> 1.4 ms per 2*10^7 queries
+  static const int64_t unperm_min = [] {
+    const char* e = getenv("MREP_UNPERM_MIN");
+    return e ? (int64_t)atoll(e) : ((int64_t)1 << 16);
+  }();
   const bool timing = (flags & MREP_TIMING) != 0;
   StageTimer sort_tm(timing, st);
   sort_tm.mark();
@@ -3943,11 +4006,13 @@ static int project_chunk(const void* table, int64_t S, int d, const double* quer
     uint32_t* i_out = i_in + n;
     const double* root = p.tab.box + p.tab.lvl_off[p.tab.top] * 6;
     if (!radix) {
-      const int rc = bucket_sort(queries, n, d, root, wc + off_tmp, sort_tmp, i_out, st);
+      uint32_t* inv = n >= unperm_min ? k_in : nullptr;  // k_in is free on this path
+      const int rc = bucket_sort(queries, n, d, root, wc + off_tmp, sort_tmp, i_out, st, inv);
       if (rc != MREP_OK) {
         cudaFreeAsync(ws, st);
         return rc;
       }
+      p.inv = inv;
     } else {
     if (d == 3) morton_kernel<3><<<grid_for(n, 256), 256, 0, st>>>(queries, n, root, k_in, i_in);
     else morton_kernel<2><<<grid_for(n, 256), 256, 0, st>>>(queries, n, root, k_in, i_in);

@@ -55,10 +55,13 @@ __global__ void bucket_key_kernel(const double* __restrict__ q, int64_t n,
 }
 
 static __global__ void bucket_scatter_kernel(const uint32_t* __restrict__ key, int64_t n,
-                                      int32_t* __restrict__ off, uint32_t* __restrict__ perm) {
+                                      int32_t* __restrict__ off, uint32_t* __restrict__ perm,
+                                      uint32_t* __restrict__ inv) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  perm[atomicAdd(off + key[i], 1)] = (uint32_t)i;
+  const int32_t pos = atomicAdd(off + key[i], 1);
+  perm[pos] = (uint32_t)i;
+  if (inv) inv[i] = (uint32_t)pos;  // caller -> sorted position (coalesced)
 }
 
 // workspace bytes of bucket_sort for n queries in D dimensions
@@ -71,7 +74,8 @@ inline size_t bucket_sort_bytes(int64_t n, int D) {
 
 // perm[j] = the query at sorted position j (device, n entries)
 inline int bucket_sort(const double* q, int64_t n, int D, const double* root, void* ws,
-                       size_t ws_bytes, uint32_t* perm, cudaStream_t st) {
+                       size_t ws_bytes, uint32_t* perm, cudaStream_t st,
+                       uint32_t* inv = nullptr) {
   const int bits = bucket_bits(n, D);
   const int64_t B = (int64_t)1 << (bits * D);
   char* p = (char*)ws;
@@ -97,7 +101,7 @@ inline int bucket_sort(const double* q, int64_t n, int D, const double* root, vo
     bucket_key_kernel<2><<<grid_for(n, 256), 256, 0, st>>>(q, n, root, bits, key, cnt);
   MREP_LAUNCH_CHECK();
   MREP_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp, scan, cnt, off, (int)B, st));
-  bucket_scatter_kernel<<<grid_for(n, 256), 256, 0, st>>>(key, n, off, perm);
+  bucket_scatter_kernel<<<grid_for(n, 256), 256, 0, st>>>(key, n, off, perm, inv);
   MREP_LAUNCH_CHECK();
   return MREP_OK;
 }
