@@ -224,21 +224,31 @@ __global__ void cells_count_kernel(const __grid_constant__ TableView T, const LP
   cnt[c] = cell_count(T, lp, g, c);
 }
 
-// fill one cell's list (ids + sort keys) in the order the scan expects
+// A list entry: the sort key and the leaf id side by side (one 8-B load
+// gives a scan both, and a list is one contiguous stream).
+struct alignas(8) CellEntry {
+  float key;
+  int32_t id;
+};
+// int32 words before the entries: the ncell + 1 offsets, padded to even so
+// the entries are 8-B aligned
+__host__ __device__ inline int64_t cell_head_words(int64_t ncell) { return (ncell + 2) & ~(int64_t)1; }
+
+// fill one cell's list (keys + ids) in the order the scan expects
 template <class LP>
 __device__ void cell_fill_list(const TableView& T, const LP& lp, const CellGrid& g, int64_t c,
-                               int32_t* out, float* key) {
+                               CellEntry* E) {
   double lo[3], hi[3];
   cell_box(g, c, lo, hi);
   const double c2 = cell_cut2(T, lp, g, lo, hi);
   int32_t n = 0;
-  cell_leaves(T, g, lo, hi, c2, [&](int64_t s) { out[n++] = (int32_t)s; });
+  cell_leaves(T, g, lo, hi, c2, [&](int64_t s) { E[n++].id = (int32_t)s; });
   // key = distance^2 from the (grown) cell to the leaf box, rounded down: a
   // lower bound of box_lb2(q, box) for every query q of the cell.  Sorted
   // ascending (ties by leaf id), the scan of a query can stop at the first
   // key above its cut: every later leaf fails the box test too.
   for (int32_t i = 0; i < n; ++i)
-    key[i] = __double2float_rd(cellbox_lb2(T, g.d, T.lvl_off[0] + out[i], lo, hi));
+    E[i].key = __double2float_rd(cellbox_lb2(T, g.d, T.lvl_off[0] + E[i].id, lo, hi));
   // equal keys (typically 0: boxes meeting the cell) go nearest to the cell
   // centre first, so the running bound tightens early; then by leaf id
   double ctr[3];
@@ -253,16 +263,13 @@ __device__ void cell_fill_list(const TableView& T, const LP& lp, const CellGrid&
   while (gap < n / 3) gap = 3 * gap + 1;
   for (; gap > 0; gap /= 3) {  // shell sort
     for (int32_t i = gap; i < n; ++i) {
-      const float kv = key[i];
-      const int32_t v = out[i];
+      const CellEntry ev = E[i];
       int32_t j = i;
-      while (j >= gap && after(key[j - gap], out[j - gap], kv, v)) {
-        key[j] = key[j - gap];
-        out[j] = out[j - gap];
+      while (j >= gap && after(E[j - gap].key, E[j - gap].id, ev.key, ev.id)) {
+        E[j] = E[j - gap];
         j -= gap;
       }
-      key[j] = kv;
-      out[j] = v;
+      E[j] = ev;
     }
   }
 }
@@ -270,10 +277,10 @@ __device__ void cell_fill_list(const TableView& T, const LP& lp, const CellGrid&
 template <class LP>
 __global__ void cells_fill_kernel(const __grid_constant__ TableView T, const LP lp,
                                   const __grid_constant__ CellGrid g, const int32_t* off,
-                                  int32_t* ids, float* keys) {
+                                  CellEntry* E) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= g.ncell) return;
-  cell_fill_list(T, lp, g, c, ids + off[c], keys + off[c]);
+  cell_fill_list(T, lp, g, c, E + off[c]);
 }
 
 // the grid of a table: uniform over its root box grown by 10% each side
@@ -352,7 +359,7 @@ int64_t cells_bytes(const void* table, int64_t S, int d, int grid, int rec, cons
     set_error("mrep_cells_bytes: cell lists exceed 2^31 entries; use a smaller grid");
     return -1;
   }
-  return (g.ncell + 1 + 2 * total) * 4;  // offsets, leaf ids, keys
+  return (cell_head_words(g.ncell) + 2 * total) * 4;  // offsets (padded), (key, id) entries
 }
 
 template <class LP>
@@ -391,12 +398,12 @@ int cells_build(void* table, int64_t S, int d, int grid, int rec, const LP& lp, 
   int32_t total = 0;
   MREP_CUDA_CHECK(cudaMemcpyAsync(&total, off + g.ncell, 4, cudaMemcpyDeviceToHost, st));
   MREP_CUDA_CHECK(cudaStreamSynchronize(st));
-  if ((g.ncell + 1 + 2 * (int64_t)total) * 4 > bytes) {
+  if ((cell_head_words(g.ncell) + 2 * (int64_t)total) * 4 > bytes) {
     set_error("mrep_cells_build: cells buffer too small (see mrep_cells_bytes)");
     return MREP_ERR_ARG;
   }
   cells_fill_kernel<LP><<<grid_for(g.ncell, 128), 128, 0, st>>>(
-      T, lp, g, off, off + g.ncell + 1, reinterpret_cast<float*>(off + g.ncell + 1 + total));
+      T, lp, g, off, reinterpret_cast<CellEntry*>(off + cell_head_words(g.ncell)));
   MREP_LAUNCH_CHECK();
   // header: cell index pointer, grid, lower corner, inverse cell size, upper
   // corner, number of list entries
@@ -424,20 +431,17 @@ __device__ __forceinline__ bool cell_of(const TableView& T, const double (&q)[D]
   return in;
 }
 
-__device__ __forceinline__ const int32_t* cell_list(const TableView& T, int d, int64_t cell,
-                                                    int32_t& a, int32_t& b) {
+// the entries of every list (entry k: x = key bits, y = leaf id); cell's
+// list is [a, b)
+__device__ __forceinline__ const uint2* cell_list(const TableView& T, int d, int64_t cell,
+                                                  int32_t& a, int32_t& b) {
   const int G = (int)T.hdr[H_GRID];
   const int64_t ncell = (int64_t)G * G * (d == 3 ? G : 1);
   const int32_t* off = reinterpret_cast<const int32_t*>(
       (uintptr_t)__double_as_longlong(T.hdr[H_CELLS]));
   a = __ldg(off + cell);
   b = __ldg(off + cell + 1);
-  return off + ncell + 1;
-}
-
-// the lists' sort keys (parallel to the ids cell_list returns)
-__device__ __forceinline__ const float* cell_keys(const TableView& T, const int32_t* ids) {
-  return reinterpret_cast<const float*>(ids + (int64_t)T.hdr[H_CTOT]);
+  return reinterpret_cast<const uint2*>(off + cell_head_words(ncell));
 }
 
 }  // namespace mrep

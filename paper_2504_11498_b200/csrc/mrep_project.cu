@@ -1263,16 +1263,16 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
   int np = 0;
   if (TM == TM_CELLS && incell) {
     int32_t a, b;
-    const int32_t* ids = cell_list(T, D, cell, a, b);
-    const float* keys = cell_keys(T, ids);
-    int32_t nxt = a < b ? __ldg(ids + a) : 0;
+    const uint2* E = cell_list(T, D, cell, a, b);
+    uint2 nxt = a < b ? __ldg(E + a) : make_uint2(0u, 0u);
 #pragma unroll 1
     for (int32_t k = a; k < b; ++k) {
       // keys ascend and bound the box distance of every query of the cell:
       // past the cut, no later cubic can hold a band candidate
-      if ((double)__ldg(keys + k) > cut2(B.dmin, scale)) break;
-      const int64_t ch = nxt;
-      if (k + 1 < b) nxt = __ldg(ids + k + 1);  // next id in flight during this entry
+      const uint2 cur = nxt;
+      if ((double)__uint_as_float(cur.x) > cut2(B.dmin, scale)) break;
+      const int64_t ch = (int32_t)cur.y;
+      if (k + 1 < b) nxt = __ldg(E + k + 1);  // next entry in flight during this one
       st.boxes++;
       bool need = (fb ? box_lb2f<D>(T, T.lvl_off[0] + ch, fq) : box_lb2<D>(T, T.lvl_off[0] + ch, q)) <=
                   cut2(B.dmin, scale);
@@ -1620,17 +1620,17 @@ __global__ void __launch_bounds__(BLOCK, MREP_TRAV_MINB) wave_traverse_dmma(cons
     rows &= todo;
     todo &= ~rows;
     int32_t a0, a1;
-    const int32_t* ids = cell_list(T, D, lc, a0, a1);
-    const float* keys = cell_keys(T, ids);
+    const uint2* EL = cell_list(T, D, lc, a0, a1);
     bool mine = ((rows >> row) & 1u) != 0;  // this row still scans (all 4 lanes)
-    int32_t s_nxt = a0 < a1 ? __ldg(ids + a0) : 0;
+    uint2 e_nxt = a0 < a1 ? __ldg(EL + a0) : make_uint2(0u, 0u);
 #pragma unroll 1
     for (int32_t k = a0; k < a1; ++k) {
-      const int64_t s = s_nxt;
-      if (k + 1 < a1) s_nxt = __ldg(ids + k + 1);
+      const uint2 e_cur = e_nxt;
+      const int64_t s = (int32_t)e_cur.y;
+      if (k + 1 < a1) e_nxt = __ldg(EL + k + 1);
       // keys ascend: past a row's cut no later cubic can hold a band candidate
       bool go = false;
-      if (owner && mine) go = !((double)__ldg(keys + k) > cut2(B.dmin, scale));
+      if (owner && mine) go = !((double)__uint_as_float(e_cur.x) > cut2(B.dmin, scale));
       const unsigned gb = __ballot_sync(0xffffffffu, go);
       mine = ((gb >> (lane & ~3)) & 1u) != 0;
       if (!gb) break;
@@ -3587,10 +3587,11 @@ int set_create(const double* seg_pts, const double* seg_ta, const double* seg_tb
 // axis.  All curves are built together: one thread per (curve, cell) counts
 // and fills, one scan sizes every list, and a kernel writes each curve's
 // header words, so the build costs a handful of launches for 10^4 curves.
-// Layout (int32 words): curve c's index starts at cstart_c + c + 2 E_c
-// (E = exclusive scan of the counts over all cells of all curves):
-// offsets [ncell_c + 1], leaf ids [tot_c], float keys [tot_c] -- exactly
-// what cell_list / cell_keys read for a single table.
+// Layout (int32 words): curve c's index starts at hstart_c + 2 E_c
+// (E = exclusive scan of the counts over all cells of all curves, hstart =
+// prefix of the padded offset-block sizes cell_head_words(ncell_c)):
+// offsets [ncell_c + 1] (padded to even), (key, id) entries [tot_c] --
+// exactly what cell_list reads for a single table.
 __device__ __forceinline__ int64_t set_cell_owner(const int64_t* cstart, int64_t nc, int64_t i) {
   int64_t lo = 0, hi = nc;
   while (hi - lo > 1) {
@@ -3619,29 +3620,28 @@ __global__ void set_cells_count_kernel(const TableView* desc, const CellGrid* gr
 }
 
 __global__ void set_cells_header_kernel(const TableView* desc, const CellGrid* grids,
-                                        const int64_t* cstart, const int64_t* E, int64_t nc,
-                                        int32_t* mem) {
+                                        const int64_t* cstart, const int64_t* hstart,
+                                        const int64_t* E, int64_t nc, int32_t* mem) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nc) return;
   const int64_t e0 = E[cstart[c]], tot = E[cstart[c + 1]] - e0;
-  int32_t* off = mem + cstart[c] + c + 2 * e0;
+  int32_t* off = mem + hstart[c] + 2 * e0;
   off[cstart[c + 1] - cstart[c]] = (int32_t)tot;
   cells_header(grids[c], off, tot, const_cast<double*>(desc[c].hdr) + H_CELLS);
 }
 
 __global__ void set_cells_fill_kernel(const TableView* desc, const CellGrid* grids,
-                                      const int64_t* cstart, const int64_t* E, int64_t nc,
-                                      int64_t ncell, int32_t* mem) {
+                                      const int64_t* cstart, const int64_t* hstart,
+                                      const int64_t* E, int64_t nc, int64_t ncell, int32_t* mem) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ncell) return;
   const int64_t c = set_cell_owner(cstart, nc, i);
-  const int64_t e0 = E[cstart[c]], tot = E[cstart[c + 1]] - e0, nloc = cstart[c + 1] - cstart[c];
-  int32_t* off = mem + cstart[c] + c + 2 * e0;
+  const int64_t e0 = E[cstart[c]], nloc = cstart[c + 1] - cstart[c];
+  int32_t* off = mem + hstart[c] + 2 * e0;
   const int32_t at = (int32_t)(E[i] - e0);
   off[i - cstart[c]] = at;
-  int32_t* ids = off + nloc + 1;
-  cell_fill_list(desc[c], CurveLeaves{}, grids[c], i - cstart[c], ids + at,
-                 reinterpret_cast<float*>(ids + tot) + at);
+  CellEntry* entries = reinterpret_cast<CellEntry*>(off + cell_head_words(nloc));
+  cell_fill_list(desc[c], CurveLeaves{}, grids[c], i - cstart[c], entries + at);
 }
 
 static int set_cells_build(CurveSet* cs, int gmax, int64_t max_bytes, cudaStream_t st) {
@@ -3656,13 +3656,15 @@ static int set_cells_build(CurveSet* cs, int gmax, int64_t max_bytes, cudaStream
   const int64_t nc = cs->nc;
   const int d = cs->d;
   std::vector<int32_t> G(nc);
-  std::vector<int64_t> cstart(nc + 1, 0);
+  std::vector<int64_t> cstart(nc + 1, 0), hstart(nc + 1, 0);
   for (int64_t c = 0; c < nc; ++c) {
     const double S = (double)(cs->ofs[c + 1] - cs->ofs[c]);
     int g = (int)std::lround(2.5 * std::cbrt(S));
     g = std::max(4, std::min(gmax, g));
     G[c] = g;
-    cstart[c + 1] = cstart[c] + (int64_t)g * g * (d == 3 ? g : 1);
+    const int64_t nl = (int64_t)g * g * (d == 3 ? g : 1);
+    cstart[c + 1] = cstart[c] + nl;
+    hstart[c + 1] = hstart[c] + cell_head_words(nl);
   }
   const int64_t ncell = cstart[nc];
   if (ncell + nc + 1 > INT32_MAX) {
@@ -3672,7 +3674,8 @@ static int set_cells_build(CurveSet* cs, int gmax, int64_t max_bytes, cudaStream
   // scratch: grids, G, cstart, counts (int32) and their scan (int64, ncell + 1)
   auto al = [](int64_t b) { return (b + 255) & ~(int64_t)255; };
   const int64_t o_grid = 0, o_G = al(nc * (int64_t)sizeof(CellGrid)), o_cs = o_G + al(nc * 4);
-  const int64_t o_cnt = o_cs + al((nc + 1) * 8), o_E = o_cnt + al((ncell + 1) * 4);
+  const int64_t o_hs = o_cs + al((nc + 1) * 8);
+  const int64_t o_cnt = o_hs + al((nc + 1) * 8), o_E = o_cnt + al((ncell + 1) * 4);
   size_t scan_tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (const int32_t*)nullptr, (int64_t*)nullptr,
                                 (int)(ncell + 1), st);
@@ -3682,6 +3685,7 @@ static int set_cells_build(CurveSet* cs, int gmax, int64_t max_bytes, cudaStream
   CellGrid* grids = (CellGrid*)(ws + o_grid);
   int32_t* Gd = (int32_t*)(ws + o_G);
   int64_t* csd = (int64_t*)(ws + o_cs);
+  int64_t* hsd = (int64_t*)(ws + o_hs);
   int32_t* cnt = (int32_t*)(ws + o_cnt);
   int64_t* E = (int64_t*)(ws + o_E);
   int rc = MREP_OK;
@@ -3692,6 +3696,7 @@ static int set_cells_build(CurveSet* cs, int gmax, int64_t max_bytes, cudaStream
   };
   MREP_CUDA_CHECK(cudaMemcpyAsync(Gd, G.data(), nc * 4, cudaMemcpyHostToDevice, st));
   MREP_CUDA_CHECK(cudaMemcpyAsync(csd, cstart.data(), (nc + 1) * 8, cudaMemcpyHostToDevice, st));
+  MREP_CUDA_CHECK(cudaMemcpyAsync(hsd, hstart.data(), (nc + 1) * 8, cudaMemcpyHostToDevice, st));
   MREP_CUDA_CHECK(cudaMemsetAsync(cnt + ncell, 0, 4, st));
   set_grid_kernel<<<grid_for(nc, 128), 128, 0, st>>>(cs->desc, Gd, nc, d, grids);
   set_cells_count_kernel<<<grid_for(ncell, 128), 128, 0, st>>>(cs->desc, grids, csd, nc, ncell, cnt);
@@ -3700,7 +3705,7 @@ static int set_cells_build(CurveSet* cs, int gmax, int64_t max_bytes, cudaStream
   int64_t total = 0;
   MREP_CUDA_CHECK(cudaMemcpyAsync(&total, E + ncell, 8, cudaMemcpyDeviceToHost, st));
   MREP_CUDA_CHECK(cudaStreamSynchronize(st));
-  const int64_t words = ncell + nc + 2 * total;
+  const int64_t words = hstart[nc] + 2 * total;
   if (words > INT32_MAX || 4 * words > max_bytes) {
     set_error("mrep_curveset_cells_build: the index needs " + std::to_string(4 * words) +
               " bytes (budget " + std::to_string(max_bytes) + ", int32 offsets)");
@@ -3712,9 +3717,9 @@ static int set_cells_build(CurveSet* cs, int gmax, int64_t max_bytes, cudaStream
     set_error(std::string("mrep_curveset_cells_build: cudaMalloc: ") + cudaGetErrorString(e));
     return fail(MREP_ERR_CUDA);
   }
-  set_cells_fill_kernel<<<grid_for(ncell, 128), 128, 0, st>>>(cs->desc, grids, csd, E, nc, ncell,
-                                                             (int32_t*)mem);
-  set_cells_header_kernel<<<grid_for(nc, 128), 128, 0, st>>>(cs->desc, grids, csd, E, nc,
+  set_cells_fill_kernel<<<grid_for(ncell, 128), 128, 0, st>>>(cs->desc, grids, csd, hsd, E, nc,
+                                                             ncell, (int32_t*)mem);
+  set_cells_header_kernel<<<grid_for(nc, 128), 128, 0, st>>>(cs->desc, grids, csd, hsd, E, nc,
                                                             (int32_t*)mem);
   if ((e = cudaGetLastError()) != cudaSuccess) {
     set_error(std::string("mrep_curveset_cells_build: launch: ") + cudaGetErrorString(e));

@@ -491,16 +491,16 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
     // cell index: the list holds every patch that can come within the cut of
     // any query in the cell, nearest first; the first one seeds the bound
     int32_t a, b;
-    const int32_t* ids = cell_list(T, 3, cell, a, b);
-    const float* keys = cell_keys(T, ids);
-    const int64_t p0 = __ldg(ids + a);
+    const uint2* E = cell_list(T, 3, cell, a, b);
+    const int64_t p0 = (int32_t)__ldg(E + a).y;
     offer_points<PU, PV>(w, p0, q, ub, st);
     int64_t prim = p0;  // the patch holding the nearest seed point: solved first
 #pragma unroll 1
     for (int32_t i = a; i < b; ++i) {
       const double c2 = cut2(ub, scale);
-      if ((double)__ldg(keys + i) > c2) break;  // keys ascend: the rest lie beyond the cut
-      const int64_t s = __ldg(ids + i);
+      const uint2 e = __ldg(E + i);
+      if ((double)__uint_as_float(e.x) > c2) break;  // keys ascend: the rest lie beyond the cut
+      const int64_t s = (int32_t)e.y;
       st.boxes++;
       if (box_lb2<3>(T, T.lvl_off[0] + s, q) <= c2 &&
           obb_lb2(T.rec + s * w.rec + surf_obb(PU, PV), q) <= c2) {
