@@ -394,8 +394,9 @@ class CurveSetWorkload:
         self.prep_ms = (time.perf_counter() - t0) * 1e3
         # per-curve cell indices (part of preparation, timed separately)
         t0 = time.perf_counter()
-        gmax = int(os.environ.get("MREP_SET_GRID", "12"))
-        self.cells_bytes = self.cset.build_cells(gmax) if gmax > 0 else 0
+        gmax = int(os.environ.get("MREP_SET_GRID", "20"))
+        budget = int(float(os.environ.get("MREP_SET_BUDGET_GB", "16")) * (1 << 30))
+        self.cells_bytes = self.cset.build_cells(gmax, budget) if gmax > 0 else 0
         torch.cuda.synchronize()
         self.cells_ms = (time.perf_counter() - t0) * 1e3
         self.n = n_override or c["n"]

@@ -3677,6 +3677,11 @@ static int set_cells_build(CurveSet* cs, int gmax, int64_t max_bytes, cudaStream
     hstart[c + 1] = hstart[c] + cell_head_words(nl);
   }
   const int64_t ncell = cstart[nc];
+  for (int64_t c = 0; c < nc; ++c)
+    if ((cstart[c + 1] - cstart[c]) * (cs->ofs[c + 1] - cs->ofs[c]) >= INT32_MAX) {
+      set_error("mrep_curveset_cells_build: a curve's lists could exceed int32 offsets; lower grid_max");
+      return MREP_ERR_ARG;
+    }
   if (ncell + nc + 1 > INT32_MAX) {
     set_error("mrep_curveset_cells_build: too many cells; lower grid_max");
     return MREP_ERR_ARG;
@@ -3715,10 +3720,13 @@ static int set_cells_build(CurveSet* cs, int gmax, int64_t max_bytes, cudaStream
   int64_t total = 0;
   MREP_CUDA_CHECK(cudaMemcpyAsync(&total, E + ncell, 8, cudaMemcpyDeviceToHost, st));
   MREP_CUDA_CHECK(cudaStreamSynchronize(st));
+  // offsets are int32 but local to each curve's region (checked above: a
+  // curve lists at most ncell_c * S_c entries), and the regions are
+  // addressed with 64-bit word offsets: beyond that only the budget limits
   const int64_t words = hstart[nc] + 2 * total;
-  if (words > INT32_MAX || 4 * words > max_bytes) {
+  if (4 * words > max_bytes) {
     set_error("mrep_curveset_cells_build: the index needs " + std::to_string(4 * words) +
-              " bytes (budget " + std::to_string(max_bytes) + ", int32 offsets)");
+              " bytes (budget " + std::to_string(max_bytes) + ")");
     return fail(MREP_ERR_ARG);
   }
   char* mem = nullptr;
