@@ -809,16 +809,18 @@ def main():
         ms = float(tt.item())
     value = n_total / (ms / 1e3)
     # own kernels per projection call (the timed steps' ncu launch lists,
-    # profiles/r01_<cfg>_launch_shares.txt): ordering -- bucket sort (keys,
-    # scan init, scan, scatter) from 2^16 queries, none below; cfg3: Morton
-    # keys + 6 radix kernels -- then the wavefront: traverse, pairs filter,
-    # pairs, clip, emit, fallback (surfaces: traverse, solve x2, filter,
-    # select x2, fallback); dense mode: 2.  Per 2^23-query chunk.
+    # profiles/r02_<cfg>_launch_shares.txt): ordering -- bucket sort (keys,
+    # scan init, scan, scatter) from 2^16 queries, none below; cfg3: the
+    # curve-rank counting sort (count, plan, scatter) -- then the wavefront:
+    # traverse, pairs filter, pairs, clip, emit, unpermute (sorted batches),
+    # fallback (surfaces: traverse, solve x2, filter, select x2, fallback);
+    # dense mode: 2.  Per 2^23-query chunk.
     if args.config == "cfg3":
-        sort_k = 7
+        sort_k = 3
     else:
         sort_k = 4 if min(n, 1 << 23) >= (1 << 16) else 0
-    launches_per_step = sort_k + (7 if surf else (6 if not dense else 2))
+    unperm = 1 if (sort_k and not surf and not dense) else 0
+    launches_per_step = sort_k + (7 if surf else (6 + unperm if not dense else 2))
     launches_per_step *= max(1, -(-n // (1 << 23)))
 
     # ---- roofline: per-stage device times (CUDA events between the pipeline's

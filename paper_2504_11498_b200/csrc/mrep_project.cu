@@ -1283,6 +1283,11 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
       } else if (k + 1 < b) {
         nxt = __ldg(E + k + 1);  // next entry in flight during this one
       }
+#ifdef MREP_LIST_PREFETCH
+      // the list's sector two ahead toward L2, once per sector (4 entries)
+      if (((k - a) & 3) == 0 && k + 8 < b)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(E + k + 8));
+#endif
       st.boxes++;
       bool need = (fb ? box_lb2f<D>(T, T.lvl_off[0] + ch, fq) : box_lb2<D>(T, T.lvl_off[0] + ch, q)) <=
                   cut2(B.dmin, scale);
