@@ -1103,6 +1103,7 @@ struct WaveParams {
   uint32_t* sq;
   uint32_t* ssk;  // cubic << 3 | piece
   unsigned long long scap;
+  int set_cells;        // curve set with per-curve cell indices (group scans may use them)
   const uint32_t* inv;  // caller -> sorted position (large batches; null otherwise)
   double* orec;         // with inv: each sorted query's outputs, 8 doubles (unpermuted after)
   uint32_t* ccnt;   // per sorted query: candidates appended so far
@@ -1283,11 +1284,10 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
       } else if (k + 1 < b) {
         nxt = __ldg(E + k + 1);  // next entry in flight during this one
       }
-#ifdef MREP_LIST_PREFETCH
-      // the list's sector two ahead toward L2, once per sector (4 entries)
+      // the list's sector two ahead toward L2, once per sector (4 entries):
+      // long lists come from HBM (cfg5 traverse 6.7 -> 6.3 ms per 2*10^7)
       if (((k - a) & 3) == 0 && k + 8 < b)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(E + k + 8));
-#endif
       st.boxes++;
       bool need = (fb ? box_lb2f<D>(T, T.lvl_off[0] + ch, fq) : box_lb2<D>(T, T.lvl_off[0] + ch, q)) <=
                   cut2(B.dmin, scale);
@@ -1812,6 +1812,8 @@ struct SeamBest {  // a lane's two nearest seams (t re-read at emission)
 };
 
 __device__ __forceinline__ void seam_keep(SeamBest& b, double d, int32_t s) {
+  // a seam offered twice (start of one listed cubic, end of the previous)
+  if ((s == b.s1 && b.d1 == d) || (s == b.s2 && b.d2 == d)) return;
   if (d < b.d1) {
     b.dropped = fmin(b.dropped, b.d2);
     b.d2 = b.d1;
@@ -1874,7 +1876,7 @@ __device__ __forceinline__ void flush_pairs(const WaveParams& w, const TableView
 // float boxes are read.  Stack keys: level << 28 | node (group mode needs
 // top <= 8, so a node index fits 28 bits); stack bounds are float keys.
 // A node's kept children are pushed in index order with the nearest on top.
-template <int D, bool MULTI, int NSTACK, bool SMEM>
+template <int D, bool MULTI, int NSTACK, bool SMEM, bool CELLS = false>
 __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, bool active,
                                                int32_t cid, const TableView& T,
                                                const BoxSrc<SMEM>& B, uint32_t* SK, float* SL,
@@ -1906,11 +1908,84 @@ __device__ __forceinline__ void traverse_group(const WaveParams& w, int64_t g, b
     sp = 1;
   }
   __syncwarp(gmask);
+  if constexpr (CELLS) {
+    // Cell-list scan, one query per 8-lane group (curve sets with per-curve
+    // cell indices; every active query of the warp lies in its grid): each
+    // round the group tests 8 consecutive entries of the query's sorted list
+    // (lane `sub` takes entry k0 + sub: one coalesced 64-B read), offers both
+    // seams of every kept cubic, min-reduces the seam distances into the
+    // bound, parks the kept cubics; the scan stops after the round in which
+    // an entry's key passed the cut (keys ascend).  Compared with one lane
+    // per query, the lanes of a warp no longer wait for the longest list.
+    int32_t a = 0, b = 0;
+    const uint2* E = nullptr;
+    if (active) {
+      int64_t cell = 0;
+      cell_of<D>(T, q, cell);
+      E = cell_list(T, D, cell, a, b);
+    }
+    int32_t k0 = a;
+    for (;;) {
+      const bool more = active && k0 < b;
+      if (!__any_sync(0xffffffffu, more)) break;
+      if (more) {  // group-uniform
+        const int32_t k = k0 + sub;
+        const bool ex = k < b;
+        const uint2 e = ex ? __ldg(E + k) : make_uint2(0u, 0u);
+        const double c2 = cut2(dmin, scale);
+        const bool live = ex && !((double)__uint_as_float(e.x) > c2);
+        const bool past = ex && !live;
+        float key = __int_as_float(0x7f800000);
+        const int64_t ch = (int32_t)e.y;
+        if (live) {
+          st.boxes++;
+          const int64_t bi = T.lvl_off[0] + ch;
+          key = fb ? box_accf<D>(B, bi, fq) : __double2float_rd(box_lb2<D>(T, bi, q));
+        }
+        const bool keep = live && key <= thr;
+        double dr = INF;
+        if (keep) {
+          const double d0 = seam_dist<D>(T, ch, q);
+          const double d1 = seam_dist<D>(T, ch + 1, q);
+          seam_keep(sb, d0, (int32_t)ch);
+          seam_keep(sb, d1, (int32_t)(ch + 1));
+          st.seams += 2;
+          st.offers += 2;
+          dr = fmin(d0, d1);
+        }
+        double m = dr;
+        m = fmin(m, __shfl_xor_sync(gmask, m, 4));
+        m = fmin(m, __shfl_xor_sync(gmask, m, 2));
+        m = fmin(m, __shfl_xor_sync(gmask, m, 1));
+        if (m < dmin) {  // group-uniform
+          dmin = m;
+          thr = cut_key(cut2(dmin, scale), fb);
+        }
+        const bool park = keep && key <= thr;
+        const unsigned pm = (__ballot_sync(gmask, park) >> (lane & 24)) & 0xffu;
+        if (npark + __popc(pm) > GPAIRS) {  // list full: flush with the current bound
+          flush_pairs<D>(w, T, g, q, cut2(dmin, scale), thr, PC, PL, npark, sub, fall, st.pairs);
+          __syncwarp(gmask);
+          npark = 0;
+        }
+        if (park) {
+          const int at = npark + __popc(pm & ((1u << sub) - 1));
+          PC[at] = (uint32_t)ch;
+          PL[at] = key;
+        }
+        npark += __popc(pm);
+        // keys ascend: once one entry is past the cut, every later one is
+        const unsigned pb = (__ballot_sync(gmask, past) >> (lane & 24)) & 0xffu;
+        k0 = pb ? b : k0 + 8;
+      }
+      __syncwarp();
+    }
+  }
   // The warp's four groups advance in lockstep: every trip, each group with
   // work pops and expands one node, and the warp reconverges at the end of
   // the trip (otherwise the groups drift apart and the warp issues each
   // group's instructions separately at 8/32 lanes).
-  for (;;) {
+  for (; !CELLS;) {
     // pop: the group reads the top 8 entries at once and drops every entry
     // above the first one still under the threshold (a bound that tightened
     // since the push prunes them), so a run of pruned entries costs one trip
@@ -2092,8 +2167,27 @@ __global__ void __launch_bounds__(BLOCK, MREP_GROUP_MINB) wave_traverse_group(co
       bool act = g < w.n;
       const int32_t cid = group_curve<true>(w, g, act, lane & 7);
       const TableView& T = w.tabs[cid];
-      traverse_group<D, true, GSTACK, false>(w, g, act, cid, T, BoxSrc<false>{T.fbox}, sk[grp],
-                                             sl[grp], pc[grp], pl[grp], lane);
+      // curve sets with per-curve cell indices: the group scans the query's
+      // cell list when every active query of the warp lies in its grid
+      bool scan = false;
+      if (w.set_cells) {
+        bool in = true;
+        if (act) {
+          const int64_t qi = w.perm ? (int64_t)w.perm[g] : g;
+          double qq[D];
+#pragma unroll
+          for (int k = 0; k < D; ++k) qq[k] = w.q[qi * D + k];
+          int64_t cell = 0;
+          in = cell_of<D>(T, qq, cell);
+        }
+        scan = __all_sync(0xffffffffu, in);
+      }
+      if (scan)
+        traverse_group<D, true, GSTACK, false, true>(w, g, act, cid, T, BoxSrc<false>{T.fbox},
+                                                     sk[grp], sl[grp], pc[grp], pl[grp], lane);
+      else
+        traverse_group<D, true, GSTACK, false>(w, g, act, cid, T, BoxSrc<false>{T.fbox}, sk[grp],
+                                               sl[grp], pc[grp], pl[grp], lane);
       task = __shfl_sync(0xffffffffu, next, 0);
     }
   }
@@ -3174,7 +3268,8 @@ static unsigned persistent_grid(const void* fn, int block) {
 template <int D, bool MULTI>
 static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tmode,
                        const TableView* tabs = nullptr, const int32_t* qcurve = nullptr,
-                       int64_t ncurves = 0, const StagePlan* plan = nullptr) {
+                       int64_t ncurves = 0, const StagePlan* plan = nullptr,
+                       bool set_cells = false) {
   const int64_t n = p.n;
   const unsigned long long pcap = (unsigned long long)std::max<int64_t>(16 * n, 1 << 16);
   const unsigned long long scap = (unsigned long long)std::max<int64_t>(2 * n, 1 << 16);
@@ -3242,6 +3337,7 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   w.tabs = tabs;
   w.qcurve = qcurve;
   w.ncurves = ncurves;
+  w.set_cells = set_cells ? 1 : 0;
   w.gcur = MULTI ? (int32_t*)(base + o_gc) : nullptr;
   w.queue = w.cnt + 5;
   static const int retest_min = [] {
@@ -3785,8 +3881,21 @@ static int project_batch_chunk(const CurveSet* cs, const double* queries, const 
   p.counters = counters;
   // a set with per-curve cell indices scans them (unless a walk is forced)
   static const bool no_set_cells = getenv("MREP_SET_NO_CELLS") != nullptr;
-  if (cs->cells && !no_set_cells && !(flags & (MREP_PACKET | MREP_PER_LANE | MREP_GROUP)))
-    flags |= MREP_CELLS;
+  // MREP_SET_SCAN=lane|group: the per-query cell scan by one lane or by an
+  // 8-lane group (A/B)
+  static const int set_scan_group = [] {
+    const char* e = getenv("MREP_SET_SCAN");
+    return (e && !strcmp(e, "group")) ? 1 : 0;
+  }();
+  bool set_cells = false;
+  if (cs->cells && !no_set_cells && !(flags & (MREP_PACKET | MREP_PER_LANE | MREP_GROUP))) {
+    if (set_scan_group) {
+      flags |= MREP_GROUP;
+      set_cells = true;
+    } else {
+      flags |= MREP_CELLS;
+    }
+  }
   const int tmode0 = trav_mode(flags, n, cs->S_total, cs->max_top);
   // Sparse batches (group walks, each query's work a function of the query
   // alone) are ordered by a counting sort on the curve's scheduler rank:
@@ -3857,8 +3966,10 @@ static int project_batch_chunk(const CurveSet* cs, const double* queries, const 
   const int tmode = tmode0;
   StagePlan plan{cs->order, qstart, tstart, cs->nc, nullptr, 0};
   const StagePlan* pl = staged ? &plan : nullptr;
-  int rc = d == 3 ? launch_wave<3, true>(p, st, timing, tmode, cs->desc, qcurve, cs->nc, pl)
-                  : launch_wave<2, true>(p, st, timing, tmode, cs->desc, qcurve, cs->nc, pl);
+  int rc = d == 3 ? launch_wave<3, true>(p, st, timing, tmode, cs->desc, qcurve, cs->nc, pl,
+                                         set_cells)
+                  : launch_wave<2, true>(p, st, timing, tmode, cs->desc, qcurve, cs->nc, pl,
+                                         set_cells);
   MREP_CUDA_CHECK(cudaFreeAsync(ws, st));
   return rc;
 }
