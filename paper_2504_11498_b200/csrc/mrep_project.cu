@@ -236,6 +236,40 @@ __device__ __forceinline__ void offer_seam(const TableView& T, int64_t s, const 
   band_offer(B, stt, sqrt(acc), -1.0, (uint64_t)s);
 }
 
+// The roots of E' on [0, 1] that _quartic_roots_01 reports (_kernels.py
+// :91-176), skipping the solve when there can be none: E'(u) lies between
+// 5 min_j (b_{j+1} - b_j) and 5 max_j (b_{j+1} - b_j) (b = the Bernstein
+// ordinates of E).  The reference keeps a candidate x only if its residual
+// |E'(x)| <= 1e-9 max_k |c_k| <= 5e-9 sum_k |e_k| (c_k = (k+1) e_{k+1}), so
+// when the differences are of one sign and clear 2e-9 sum |e| (far above the
+// rounding of b and of the residual, and of E' on the 1e-12 slack outside
+// [0, 1]) no candidate can pass: the reference returns no root, and so does
+// this.  Typical near the foot point (E' = |C'|^2 + (C - q).C'' > 0), where
+// most solved pairs are.
+__device__ __forceinline__ Roots4 eprime_roots(const double (&e)[6], const double (&b)[6]) {
+  double S = 0.0;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) S += fabs(e[k]);
+  const double m = fmax(2e-9 * S, 1e-290);
+  bool pos = true, neg = true;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    const double beta = b[j + 1] - b[j];
+    pos = pos && beta > m;
+    neg = neg && beta < -m;
+  }
+  if (pos || neg) {
+    Roots4 none;
+    none.count = 0;
+    none.r[0] = none.r[1] = none.r[2] = none.r[3] = 0.0;
+    return none;
+  }
+  double ep[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) ep[k] = (double)(k + 1) * e[k + 1];
+  return quartic_roots_01(ep);
+}
+
 // _kernels.py:421-479 for one cubic s: E, E' roots, monotone pieces,
 // elimination, clipping, foot points; survivors are offered to the band.
 template <int D, bool STATS>
@@ -250,10 +284,9 @@ __device__ __forceinline__ void solve_segment(const TableView& T, int64_t s, con
     for (int dim = 0; dim < D; ++dim) w[k][dim] = __ldg(r + k * 3 + dim);
   double e[6];
   distance_poly_w<D>(w, q, e);
-  double ep[5];
-#pragma unroll
-  for (int k = 0; k < 5; ++k) ep[k] = (double)(k + 1) * e[k + 1];
-  Roots4 rt = quartic_roots_01(ep);
+  double bseg[6];
+  rebase5(e, bseg);
+  Roots4 rt = eprime_roots(e, bseg);
   // interior split points (1e-10 < r < 1 - 1e-10), compacted in order
   double b1 = 1.0, b2 = 1.0, b3 = 1.0, b4 = 1.0;
   int nin = 0;
@@ -268,8 +301,6 @@ __device__ __forceinline__ void solve_segment(const TableView& T, int64_t s, con
       ++nin;
     }
   }
-  double bseg[6];
-  rebase5(e, bseg);
   st.pairs++;
   double lo = 0.0;
   for (int k = 0; k <= nin; ++k) {
@@ -595,10 +626,8 @@ __device__ __forceinline__ void prep_pair(const TableView& T, int64_t s, const d
     for (int dim = 0; dim < D; ++dim) w[k][dim] = __ldg(r + k * 3 + dim);
   double e[6];
   distance_poly_w<D>(w, q, e);
-  double ep[5];
-#pragma unroll
-  for (int k = 0; k < 5; ++k) ep[k] = (double)(k + 1) * e[k + 1];
-  Roots4 rt = quartic_roots_01(ep);
+  rebase5(e, P.bseg);
+  Roots4 rt = eprime_roots(e, P.bseg);
   P.b1 = P.b2 = P.b3 = P.b4 = 1.0;
   P.nin = 0;
 #pragma unroll
@@ -612,7 +641,6 @@ __device__ __forceinline__ void prep_pair(const TableView& T, int64_t s, const d
       ++P.nin;
     }
   }
-  rebase5(e, P.bseg);
 }
 
 // Rigorous lower bound on min_u |C_s(u) - q|^2 from the Bernstein
@@ -724,10 +752,7 @@ __device__ __forceinline__ bool prep_pair_cut(const TableView& T, int64_t s, con
     }
     if (pos || neg) return false;
   }
-  double ep[5];
-#pragma unroll
-  for (int k = 0; k < 5; ++k) ep[k] = (double)(k + 1) * e[k + 1];
-  Roots4 rt = quartic_roots_01(ep);
+  Roots4 rt = eprime_roots(e, P.bseg);
   P.b1 = P.b2 = P.b3 = P.b4 = 1.0;
   P.nin = 0;
 #pragma unroll
