@@ -484,3 +484,29 @@ np.savez(sys.argv[1], t=r[0].cpu().numpy(), f=r[1].cpu().numpy(), d=r[2].cpu().n
         outs.append(np.load(path))
     for key in ("t", "f", "d", "s"):
         assert np.array_equal(outs[0][key], outs[1][key], equal_nan=True), key
+
+
+def test_fallback_queries_in_sorted_batches(gpu, oracle_lib):
+    """Batches of >= 2^16 queries take the sorted path whose outputs go
+    through staging records + the unpermute pass; queries finished by the
+    exact fallback (tie-band overflow at the star's centre) must keep the
+    fallback's outputs, every other query the staged ones."""
+    from paper_2504_11498_b200 import _lib as L, prepare_curve
+    curve = _star_polyline(12, 3)
+    prep = prepare_curve(curve, 1e-4)
+    rng = np.random.default_rng(12)
+    q = rng.uniform(-12, 12, (70000, 3))
+    q[::997] = 0.0  # the tie point, scattered through the caller order
+    tab = prep.table
+    cnt = np.zeros(L.NUM_COUNTERS, dtype=np.uint64)
+    import torch
+    ct = torch.from_numpy(cnt.astype(np.int64)).cuda()
+    t, foot, dist, cand, seg, _, _ = tab.project(q, counters=ct)
+    t, foot, dist = t.cpu().numpy(), foot.cpu().numpy(), dist.cpu().numpy()
+    assert ct.cpu().numpy()[L.CNT_PASS2] > 0  # the fallback ran
+    o = oracle_lib.project_block(prep.seg_pts, prep.seg_ta, prep.seg_tb, prep.seam_t,
+                                 prep.seam_pt, q, workers=8)
+    assert np.abs(dist - o["dist"]).max() <= 1e-12
+    assert np.abs(t - o["t"]).max() <= 1e-12
+    z = np.nonzero(np.all(q == 0.0, axis=1))[0]
+    assert np.all(t[z] == 0.0) and np.all(dist[z] == 5.0)
