@@ -6,6 +6,8 @@ returns host arrays.  They back the public single-pair ops of the reference
 projection itself keeps its data on the device (see project.py).
 """
 
+import os
+
 import numpy as np
 
 from . import _lib as L
@@ -201,11 +203,15 @@ class DeviceTable:
 
     def build_cells(self, grid=None):
         torch = L._torch()
+        if grid is None and os.environ.get("MREP_CELL_GRID"):  # A/B override
+            grid = int(os.environ["MREP_CELL_GRID"])
         if grid is None:
             big = self.S > (1 << 14)
-            # big tables: 256^3 (cfg5, 10^5 cubics: 5.7 GB, built in 1.5 s;
-            # 22% faster projection than 128^3, 384^3 only 8% more)
-            grid = (256 if big else 64) if self.d == 3 else (512 if big else 256)
+            # big tables: 256^3; from 2^16 cubics 384^3 (cfg5, 10^5 cubics:
+            # 11.7 GB built in 4.2 s, projection 8% faster than 256^3 with
+            # 5.7 GB / 2.0 s; cfg6's 41k cubics gain 1% for 3x the build)
+            huge = self.S >= (1 << 16)
+            grid = ((384 if huge else 256) if big else 64) if self.d == 3 else (512 if big else 256)
         nb = L.lib().mrep_cells_bytes(L.ptr(self.buf), self.S, self.d, grid, L.stream_ptr())
         if nb <= 0:
             L.check(1)

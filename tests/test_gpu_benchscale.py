@@ -1,7 +1,7 @@
 """Parity at the bench's own scale: the exact inputs bench.py times.
 
 * cfg5 (BASELINE configs[4]): random_clamped_curve(default_rng(0), 3, 100003)
-  -> 10^5 cubics, the default 256^3 cell index, the rank-0 shard of 10^8
+  -> 10^5 cubics, the default cell index (384^3 from 2^16 cubics), the rank-0 shard of 10^8
   uniform queries (default_rng(1)), all projected on the GPU;
 * cfg3 (BASELINE configs[2]): mixed_curve_batch(10_000) prepared as one
   device set (3.96 M cubics), 10^6 queries, 100 per curve, one batched call.
