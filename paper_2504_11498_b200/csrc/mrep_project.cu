@@ -1296,12 +1296,13 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
     constexpr bool AHEAD2 = MULTI;
     uint2 nxt = a < b ? __ldg(E + a) : make_uint2(0u, 0u);
     uint2 nxt2 = (AHEAD2 && a + 1 < b) ? __ldg(E + a + 1) : make_uint2(0u, 0u);
+    double c2 = cut2(B.dmin, scale);  // refreshed only when the bound moves
 #pragma unroll 1
     for (int32_t k = a; k < b; ++k) {
       // keys ascend and bound the box distance of every query of the cell:
       // past the cut, no later cubic can hold a band candidate
       const uint2 cur = nxt;
-      if ((double)__uint_as_float(cur.x) > cut2(B.dmin, scale)) break;
+      if ((double)__uint_as_float(cur.x) > c2) break;
       const int64_t ch = (int32_t)cur.y;
       if (AHEAD2) {
         nxt = nxt2;
@@ -1315,10 +1316,11 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
         asm volatile("prefetch.global.L2 [%0];" ::"l"(E + k + 8));
       st.boxes++;
       bool need = (fb ? box_lb2f<D>(T, T.lvl_off[0] + ch, fq) : box_lb2<D>(T, T.lvl_off[0] + ch, q)) <=
-                  cut2(B.dmin, scale);
+                  c2;
       if (need) {
 #pragma unroll 1
         for (int e = 0; e < 2; ++e) offer_seam<D>(T, ch + e, q, B, st);
+        c2 = cut2(B.dmin, scale);
         st.pairs++;
         if (np == PEND) {  // buffer full (rare): this lane appends alone
           const unsigned long long base = atomicAdd(&w.cnt[0], (unsigned long long)PEND);
