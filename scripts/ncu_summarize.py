@@ -56,9 +56,11 @@ def launches(path):
 def main():
     rep, ll, tag = sys.argv[1], sys.argv[2], sys.argv[3]
     config = sys.argv[4] if len(sys.argv) > 4 else "cfg2"
-    kern = full(rep)
     lst = launches(ll) if ll != "-" else []
     prof = os.path.join(ROOT, "profiles")
+    if rep == "-":  # launch shares only
+        return write_shares(prof, tag, lst)
+    kern = full(rep)
     per = {}
     for k in kern:
         name = k["kernel"].split("(")[0].replace("void ", "").split("<")[0].split("::")[-1]
@@ -84,6 +86,10 @@ def main():
             for m in METRICS:
                 if m in k:
                     f.write(f"    {m:62s} {k[m]} {k.get(m + '.unit', '')}\n")
+    write_shares(prof, tag, lst)
+
+
+def write_shares(prof, tag, lst):
     if not lst:
         return
     # launch list: share of device time per kernel name over the whole command
