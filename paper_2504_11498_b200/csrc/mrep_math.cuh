@@ -367,6 +367,10 @@ __device__ __forceinline__ double eval_ordinates(const double (&b)[6], double u)
   return tmp[0];
 }
 
+#ifndef MREP_HULL_CARRY
+#define MREP_HULL_CARRY 1
+#endif
+
 // _kernels.py:239-303.  Monotone chains over (i/5, b_i); the stacks hold point
 // indices, 3 bits per entry, so the chains stay in registers.
 __device__ __forceinline__ bool hull_cross(const double (&b)[6], double& z1o, double& z2o) {
@@ -426,10 +430,20 @@ __device__ __forceinline__ bool hull_cross(const double (&b)[6], double& z1o, do
   for (int chain = 0; chain < 2; ++chain) {
     uint32_t st = chain == 0 ? lo_st : hi_st;
     int m = chain == 0 ? nl : nh;
+#if MREP_HULL_CARRY
+    // the chain starts at point 0; each edge's end is the next edge's start
+    double x1 = 0.0, y1 = b[0];
+    for (int i = 0; i < m - 1; ++i) {
+      const int ib = (st >> (3 * (i + 1))) & 7;
+      const double x0 = x1, y0 = y1;
+      x1 = xs5(ib);
+      y1 = sel6(b, ib);
+#else
     for (int i = 0; i < m - 1; ++i) {
       int ia = (st >> (3 * i)) & 7, ib = (st >> (3 * (i + 1))) & 7;
       double x0 = xs5(ia), x1 = xs5(ib);
       double y0 = sel6(b, ia), y1 = sel6(b, ib);
+#endif
       double z;
       bool hit = true;
       if (y0 == 0.0) z = x0;
