@@ -481,6 +481,15 @@ __global__ void __launch_bounds__(128) surf_traverse(const __grid_constant__ Sur
   double q[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) q[k] = active ? w.q[qi * 3 + k] : 0.0;
+  if (active && (isnan(q[0]) || isnan(q[1]) || isnan(q[2]))) {
+    // a NaN coordinate: every candidate distance is NaN and no later stage
+    // writes this query, so its answer (NaN, patch -1) is written here
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
+    w.out_u[qi] = w.out_v[qi] = w.out_dist[qi] = nan;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) w.out_foot[qi * 3 + k] = nan;
+    if (w.out_patch) w.out_patch[qi] = -1;
+  }
   double scale = T.hdr[4];
 #pragma unroll
   for (int k = 0; k < 3; ++k) scale = fmax(scale, fabs(q[k]));

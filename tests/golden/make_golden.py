@@ -22,6 +22,9 @@ Files:
                  hull_x_intersections, clip, clip_root) at degrees != 5
   verify.npz     oracle.oracle_project_batch (dense grid + ternary search,
                  oracle.py:95-128) on three curves
+  edge.npz       non-finite and huge queries (+-inf, 1e150..1e300) mixed
+                 with ordinary ones through project_prepared (NaN is left out:
+                 the reference returns uninitialised memory for it)
   surfdec.npz    a tensor-product surface decomposed with the reference's
                  decompose_to_bezier along v (every row), then along u (every
                  column of the row segments) -- pins the surface patches
@@ -466,8 +469,24 @@ def make_surfdec():
     print("surfdec")
 
 
+def make_edge():
+    c = random_clamped_curve(np.random.default_rng(5), 3, 12, 3, uniform_knots=True)
+    rng = np.random.default_rng(6)
+    big = [[np.inf, 0, 0], [-np.inf, 1, 0], [0, 0, np.inf], [np.inf, -np.inf, 0],
+           [1e300, 0, 0], [1e200, 0, 0], [1e150, 1e150, 0], [-1e154, 0, 1e154],
+           [1e100, 1e100, 1e100], [1e30, 0, 0]]
+    q = rng.random((40, 3))
+    q[::4] = np.array(big, dtype=np.float64)
+    prep = splinemat.prepare_curve(c, 1e-4)
+    t, foot, dist, cand = splinemat.project_prepared(prep, q, workers=1)
+    np.savez_compressed(os.path.join(OUT, "edge.npz"), degree=c.degree,
+                        knots=np.array(c.knots.knots), ctrl=np.array(c.control_points),
+                        queries=q, t=t, foot=foot, dist=dist, cand=cand)
+    print("edge", t[::4], dist[::4], cand[::4])
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["quartic", "ops", "projection", "prep", "batch", "anydeg", "verify",
-                             "surfdec"]
+                             "surfdec", "edge"]
     for w in which:
         globals()["make_" + w]()
