@@ -372,9 +372,15 @@ class SingleCurve:
 
     def cpu_jobs(self, sample):
         sample = max(256, min(sample, int(sample * 510 / self.num_segments)))
-        desc = (f"first {sample} of the {self.n} queries, brute force over all "
-                f"{self.num_segments} cubics")
-        return [(_seg(self.prep), self.q_host[:sample])], desc
+        if sample <= len(self.q_host):
+            qs = self.q_host[:sample]
+            desc = f"first {sample} of the {self.n} queries"
+        else:  # small batch (cfg1): the whole batch, repeated to a timeable sample
+            reps = -(-sample // len(self.q_host))
+            qs = np.concatenate([self.q_host] * reps)
+            desc = f"the {len(self.q_host)} queries x {reps}"
+        desc += f", brute force over all {self.num_segments} cubics"
+        return [(_seg(self.prep), qs)], desc
 
 
 class CurveSetWorkload:
