@@ -1143,6 +1143,7 @@ struct WaveParams {
   int retest_min;  // re-test popped packet nodes at levels >= this (MREP_RETEST_LEVEL)
   int trav_bern;   // Bernstein distance test at packet leaves (MREP_TRAV_BERN)
   int trav_sort;   // full best-first child order in packets (MREP_TRAV_SORT)
+  int fuse_filter;  // cell scans run W2a themselves (MREP_TRAV_FILTER)
   const TableView* tabs;
   const int32_t* qcurve;
   int64_t ncurves;
@@ -1350,7 +1351,66 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
       if (lane >= o) incl += y;
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
-    if (total) {
+    if (w.fuse_filter) {
+      // W2a fused (MREP_TRAV_FILTER): the query's bound is final here (only its
+      // own seams move it), so the warp re-tests its buffered pairs now, with
+      // the pairs dealt round-robin over the lanes (converged, one pair per
+      // lane per round), and appends the ones that pass straight to the
+      // compacted list W2b reads -- wave_pairs_filter's tests on the same
+      // operands, without the pair list's round trip through memory (the
+      // records are still in L1 from the scan).
+      int maxnp = __reduce_max_sync(0xffffffffu, np);
+      const double dmin_l = B.dmin;
+#pragma unroll 1
+      for (int r = 0; r < total; r += 32) {
+        const int p = r + lane;
+        int lo = 0, hi = 31;  // owner: the first lane whose inclusive count exceeds p
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const int mid = (lo + hi) >> 1;
+          const int v = __shfl_sync(0xffffffffu, incl, mid);
+          if (v > p) hi = mid;
+          else lo = mid + 1;
+        }
+        const int owner = lo > 31 ? 31 : lo;
+        const int e = p - (__shfl_sync(0xffffffffu, incl, owner) - __shfl_sync(0xffffffffu, np, owner));
+        uint32_t s = 0;
+#pragma unroll
+        for (int j = 0; j < PEND; ++j) {
+          if (j < maxnp) {
+            const uint32_t v = __shfl_sync(0xffffffffu, pend[j], owner);
+            s = (j == e) ? v : s;
+          }
+        }
+        double qo[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) qo[k] = __shfl_sync(0xffffffffu, q[k], owner);
+        const double so = __shfl_sync(0xffffffffu, scale, owner);
+        const double c2o = cut2(__shfl_sync(0xffffffffu, dmin_l, owner), so);
+        const int64_t go = __shfl_sync(0xffffffffu, gi, owner);
+        const int32_t co = MULTI ? __shfl_sync(0xffffffffu, cid, owner) : 0;
+        bool keep = p < total;
+        if (keep) {
+          const TableView& TO = MULTI ? w.tabs[co] : w.tab;
+          st.boxes++;
+          keep = (fbox_ok(so) ? box_lb2f<D>(TO, TO.lvl_off[0] + s, make_fq<D>(qo, so))
+                              : box_lb2<D>(TO, TO.lvl_off[0] + s, qo)) <= c2o;
+          if (keep) keep = pair_may_survive<D>(TO, s, qo, c2o);
+        }
+        const unsigned long long slot = wave_append(&w.cnt[7], keep);
+        bool ovf = false;
+        if (keep) {
+          if (slot < w.pcap) {
+            w.pq2[slot] = (uint32_t)go;
+            w.ps2[slot] = s;
+          } else {
+            ovf = true;
+          }
+        }
+        const unsigned om = __reduce_or_sync(0xffffffffu, ovf ? 1u << owner : 0u);
+        if ((om >> lane) & 1u) fall = true;
+      }
+    } else if (total) {
       unsigned long long base = 0;
       if (lane == 31) base = atomicAdd(&w.cnt[0], (unsigned long long)total);
       base = __shfl_sync(0xffffffffu, base, 31) + (unsigned long long)(incl - np);
@@ -2465,9 +2525,14 @@ __global__ void __launch_bounds__(BLOCK) wave_pairs_filter(const __grid_constant
                                 : box_lb2<D>(T, T.lvl_off[0] + s, q)) <= c2;
     if (keep) keep = pair_may_survive<D>(T, s, q, c2);
     unsigned long long slot = wave_append(&w.cnt[7], keep);
-    if (keep) {  // slot < pcap: never longer than the input list
-      w.pq2[slot] = (uint32_t)qi;
-      w.ps2[slot] = (uint32_t)s;
+    if (keep) {  // the fused cell-scan pairs share the list: check the capacity
+      if (slot < w.pcap) {
+        w.pq2[slot] = (uint32_t)qi;
+        w.ps2[slot] = (uint32_t)s;
+      } else if (atomicExch(&w.flag[qi], 1) == 0) {  // finished by the fallback kernel
+        unsigned long long fs = atomicAdd(&w.cnt[3], 1ull);
+        w.fb[fs] = qi;
+      }
     }
   }
   warp_count(w.counters, MREP_CNT_BOXES, nboxes);
@@ -3382,6 +3447,14 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
   }();
   w.trav_bern = trav_bern;
   w.trav_sort = trav_sort;
+  // fused W2a: cfg2 0.650 -> 0.638 ms, cfg5 69.9 -> 67.7 ms per 10^8, cfg3 /
+  // cfg6 neutral; small batches (cfg1, 10^4) lose 2.5% (the longer traversal
+  // kernel is on their latency chain), so it is on from 2^16 queries
+  static const int fuse_filter = [] {
+    const char* e = getenv("MREP_TRAV_FILTER");
+    return e ? atoi(e) : -1;
+  }();
+  w.fuse_filter = fuse_filter >= 0 ? fuse_filter : (n >= (int64_t(1) << 16) ? 1 : 0);
   MREP_CUDA_CHECK(cudaMemsetAsync(w.cnt, 0, 8 * sizeof(unsigned long long), st));
   auto persist_grid = [](const void* fn, int block) { return persistent_grid(fn, block); };
   const unsigned g_pairs = persist_grid((const void*)wave_pairs<D, MULTI>, BLOCK);
