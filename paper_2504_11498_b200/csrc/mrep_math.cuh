@@ -370,11 +370,35 @@ __device__ __forceinline__ double eval_ordinates(const double (&b)[6], double u)
 #ifndef MREP_HULL_CARRY
 #define MREP_HULL_CARRY 1
 #endif
+#ifndef MREP_HULL_MASK
+#define MREP_HULL_MASK 1
+#endif
+
+// one chain edge (x0, y0) -> (x1, y1) of _kernels.py:285-297: its crossing of
+// y = 0 (a zero end point, or the interpolated root), folded into [z1, z2]
+__device__ __forceinline__ void hull_edge(double x0, double y0, double x1, double y1, double& z1,
+                                          double& z2) {
+  double z;
+  bool hit = true;
+  if (y0 == 0.0) z = x0;
+  else if (y1 == 0.0) z = x1;
+  else if ((y0 < 0.0 && 0.0 < y1) || (y1 < 0.0 && 0.0 < y0))
+    z = x0 + (x1 - x0) * (-y0) / (y1 - y0);
+  else {
+    z = 0.0;
+    hit = false;
+  }
+  if (hit) {
+    if (z < z1) z1 = z;
+    if (z > z2) z2 = z;
+  }
+}
 
 // _kernels.py:239-303.  Monotone chains over (i/5, b_i); the stacks hold point
 // indices, 3 bits per entry, so the chains stay in registers.
 __device__ __forceinline__ bool hull_cross(const double (&b)[6], double& z1o, double& z2o) {
   uint32_t lo_st = 0, hi_st = 0;
+  uint32_t lo_m = 0, hi_m = 0;  // chain members as bit sets (x-ordered: bit i = point i)
   int nl = 0, nh = 0;
   // the top two points of each chain are kept as values (a = top, c = the
   // one below); a pop fetches only the new second point.  Same tests on the
@@ -386,6 +410,7 @@ __device__ __forceinline__ bool hull_cross(const double (&b)[6], double& z1o, do
     const double x = xs5(i), y = b[i];
     while (nl > 1) {
       if (((lax - lcx) * (y - lcy) - (x - lcx) * (lay - lcy)) <= 0.0) {
+        lo_m &= ~(1u << ((lo_st >> (3 * (nl - 1))) & 7));
         --nl;
         lax = lcx;
         lay = lcy;
@@ -399,6 +424,7 @@ __device__ __forceinline__ bool hull_cross(const double (&b)[6], double& z1o, do
       }
     }
     lo_st = (lo_st & ~(7u << (3 * nl))) | ((uint32_t)i << (3 * nl));
+    lo_m |= 1u << i;
     ++nl;
     lcx = lax;
     lcy = lay;
@@ -406,6 +432,7 @@ __device__ __forceinline__ bool hull_cross(const double (&b)[6], double& z1o, do
     lay = y;
     while (nh > 1) {
       if (((hax - hcx) * (y - hcy) - (x - hcx) * (hay - hcy)) >= 0.0) {
+        hi_m &= ~(1u << ((hi_st >> (3 * (nh - 1))) & 7));
         --nh;
         hax = hcx;
         hay = hcy;
@@ -419,6 +446,7 @@ __device__ __forceinline__ bool hull_cross(const double (&b)[6], double& z1o, do
       }
     }
     hi_st = (hi_st & ~(7u << (3 * nh))) | ((uint32_t)i << (3 * nh));
+    hi_m |= 1u << i;
     ++nh;
     hcx = hax;
     hcy = hay;
@@ -426,6 +454,30 @@ __device__ __forceinline__ bool hull_cross(const double (&b)[6], double& z1o, do
     hay = y;
   }
   double z1 = 2.0, z2 = -1.0;
+#if MREP_HULL_MASK
+  // the chains' edges walked with compile-time point indices: each chain runs
+  // from point 0 to point 5 through its member bits, so an edge's end points
+  // are registers (no stack decode, no select chain); the edges and their
+  // operands are the reference's, and min / max do not depend on the order
+#pragma unroll
+  for (int chain = 0; chain < 2; ++chain) {
+    const uint32_t mk = chain == 0 ? lo_m : hi_m;
+    double px = 0.0, py = b[0];
+#pragma unroll
+    for (int i = 1; i < 6; ++i) {
+      if ((mk >> i) & 1u) {
+        hull_edge(px, py, xs5(i), b[i], z1, z2);
+        px = xs5(i);
+        py = b[i];
+      }
+    }
+    // the last chain vertex is always point 5 (x = 1)
+    if (b[5] == 0.0) {
+      if (1.0 < z1) z1 = 1.0;
+      if (1.0 > z2) z2 = 1.0;
+    }
+  }
+#else
 #pragma unroll 1
   for (int chain = 0; chain < 2; ++chain) {
     uint32_t st = chain == 0 ? lo_st : hi_st;
@@ -465,6 +517,7 @@ __device__ __forceinline__ bool hull_cross(const double (&b)[6], double& z1o, do
       if (1.0 > z2) z2 = 1.0;
     }
   }
+#endif
   if (z2 < z1) {
     z1o = 0.0;
     z2o = 0.0;
