@@ -1361,6 +1361,32 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
       // records are still in L1 from the scan).
       int maxnp = __reduce_max_sync(0xffffffffu, np);
       const double dmin_l = B.dmin;
+      int nk = 0;  // staged kept pairs (warp-uniform)
+      auto stage_flush = [&](int cnt) {
+        __syncwarp();
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&w.cnt[7], (unsigned long long)cnt);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        unsigned om = 0;
+#pragma unroll 1
+        for (int j0 = 0; j0 < cnt; j0 += 32) {
+          const int j = j0 + lane;
+          const unsigned long long e = j < cnt ? S[j] : 0ull;
+          const int o = (int)(e >> 32) & 31;
+          const int64_t go = __shfl_sync(0xffffffffu, gi, o);
+          if (j < cnt) {
+            if (base + j < w.pcap) {
+              w.pq2[base + j] = (uint32_t)go;
+              w.ps2[base + j] = (uint32_t)e;
+            } else {
+              om |= 1u << o;
+            }
+          }
+        }
+        om = __reduce_or_sync(0xffffffffu, om);
+        if ((om >> lane) & 1u) fall = true;
+        __syncwarp();
+      };
 #pragma unroll 1
       for (int r = 0; r < total; r += 32) {
         const int p = r + lane;
@@ -1397,19 +1423,18 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
                               : box_lb2<D>(TO, TO.lvl_off[0] + s, qo)) <= c2o;
           if (keep) keep = pair_may_survive<D>(TO, s, qo, c2o);
         }
-        const unsigned long long slot = wave_append(&w.cnt[7], keep);
-        bool ovf = false;
-        if (keep) {
-          if (slot < w.pcap) {
-            w.pq2[slot] = (uint32_t)go;
-            w.ps2[slot] = s;
-          } else {
-            ovf = true;
-          }
+        // kept pairs are staged in the warp's (here unused) packet stack and
+        // reserved with one atomic per warp, not one per round
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (nk + __popc(bal) > PSTACK) {
+          stage_flush(nk);
+          nk = 0;
         }
-        const unsigned om = __reduce_or_sync(0xffffffffu, ovf ? 1u << owner : 0u);
-        if ((om >> lane) & 1u) fall = true;
+        if (keep) S[nk + __popc(bal & ((1u << lane) - 1u))] = ((unsigned long long)owner << 32) | s;
+        nk += __popc(bal);
+        (void)go;
       }
+      if (nk) stage_flush(nk);
     } else if (total) {
       unsigned long long base = 0;
       if (lane == 31) base = atomicAdd(&w.cnt[0], (unsigned long long)total);
@@ -1618,13 +1643,27 @@ __device__ __forceinline__ void traverse_task(const WaveParams& w, int64_t gi,
     rec.w = B.dmin;
     *(double4*)(w.qs + gi * 4) = rec;
   }
-  // the seam members of the seam tie band become candidates
+  // the seam members of the seam tie band become candidates; this thread is
+  // the only writer of its query's candidate row during the traversal (the
+  // solve kernels append later), so the row fills without atomics
+  uint32_t ncand = 0;
 #pragma unroll
   for (int j = 0; j < BAND_K; ++j) {
-    if (active && ((B.valid >> j) & 1u) &&
-        !add_cand(w, gi, B.t[j], B.d[j], -1.0, (uint32_t)B.ord[j]))
-      fall = true;
+    if (active && ((B.valid >> j) & 1u)) {
+      if (ncand < CIN) {
+        put_cand(w.cin + gi * CIN + ncand, B.t[j], B.d[j], -1.0, (uint32_t)B.ord[j], ~0u);
+      } else {
+        const unsigned long long slot = atomicAdd(&w.cnt[2], 1ull);
+        if (slot < w.ccap)
+          put_cand(w.cand + slot, B.t[j], B.d[j], -1.0, (uint32_t)B.ord[j],
+                   atomicExch(&w.chead[gi], (uint32_t)slot));
+        else
+          fall = true;
+      }
+      ++ncand;
+    }
   }
+  if (ncand) w.ccnt[gi] = ncand;
   if (active) {
     // cand (screened): seams offered + cubics queued for the exact solve by
     // this query's traversal -- independent of the other queries' timing
