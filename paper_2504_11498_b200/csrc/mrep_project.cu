@@ -2628,6 +2628,12 @@ __global__ void __launch_bounds__(BLOCK, MREP_PAIRS_MINB) wave_pairs(const __gri
   warp_count(w.counters, MREP_CNT_PAIRS, npairs);
 }
 
+// W3's survivor queue is split into CLIP_QP partitions with one claim counter
+// each (its own 128-B line, after the 8 pipeline counters): a single counter
+// was every warp's refill atomic on one L2 address (the kernel's top stall)
+constexpr int CLIP_QP = 32, CLIP_QS = 16;
+constexpr int CNT_WORDS = 8 + CLIP_QP * CLIP_QS;
+
 // W3 with lane refill: each lane runs one clipping iteration of its current
 // survivor per loop trip and takes the next survivor from the queue as soon
 // as its own is finished (1..8 iterations per survivor no longer leave
@@ -2636,27 +2642,27 @@ template <int D, bool MULTI>
 __global__ void __launch_bounds__(BLOCK, MREP_CLIP_MINB) wave_clip(const __grid_constant__ WaveParams w) {
   const unsigned long long total0 = *(volatile unsigned long long*)&w.cnt[1];
   const unsigned long long total = total0 > w.scap ? w.scap : total0;
-  unsigned long long* queue = &w.cnt[6];
+  unsigned long long* qctr = w.cnt + 8;  // partition p's claims at qctr[p * CLIP_QS]
   const int lane = threadIdx.x & 31;
   uint64_t nsurv = 0, nit = 0, nmiss = 0;
-  bool have = false, done = false;
+  bool have = false, drained = false;  // drained: warp-uniform, every partition claimed
+  int part = (int)(((blockIdx.x * blockDim.x + threadIdx.x) >> 5) % CLIP_QP);
   int64_t qi = 0;
   uint32_t sk = 0;
   double plo = 0.0, phi = 0.0;
   ClipState S;
   for (;;) {
-    const bool want = !have && !done;
+    const bool want = !have && !drained;
     const unsigned wm = __ballot_sync(0xffffffffu, want);
     if (wm) {
       const int leader = __ffs(wm) - 1;
+      const unsigned long long lo = total * part / CLIP_QP, hi = total * (part + 1) / CLIP_QP;
       unsigned long long base = 0;
-      if (lane == leader) base = atomicAdd(queue, (unsigned long long)__popc(wm));
+      if (lane == leader) base = atomicAdd(qctr + part * CLIP_QS, (unsigned long long)__popc(wm));
       base = __shfl_sync(0xffffffffu, base, leader);
       if (want) {
-        const unsigned long long i = base + __popc(wm & ((1u << lane) - 1));
-        if (i >= total) {
-          done = true;
-        } else {
+        const unsigned long long i = lo + base + __popc(wm & ((1u << lane) - 1));
+        if (i < hi) {
           // no flag test here: a survivor of a query already handed to the
           // fallback is clipped anyway (harmless: emit skips the query and the
           // fallback recomputes it), which keeps the refill's loads independent
@@ -2672,8 +2678,18 @@ __global__ void __launch_bounds__(BLOCK, MREP_CLIP_MINB) wave_clip(const __grid_
           have = true;
         }
       }
+      if (lo + base + __popc(wm) >= hi) {
+        // this partition is used up: one load per lane reads the claim
+        // counters of all partitions, the warp moves to the first with work
+        const int pp = (part + 1 + lane) % CLIP_QP;
+        const unsigned long long c = *(volatile unsigned long long*)(qctr + pp * CLIP_QS);
+        const bool avail = total * pp / CLIP_QP + c < total * (pp + 1) / CLIP_QP;
+        const unsigned am = __ballot_sync(0xffffffffu, avail);
+        if (am) part = __shfl_sync(0xffffffffu, pp, __ffs(am) - 1);
+        else drained = true;
+      }
     }
-    if (__all_sync(0xffffffffu, done)) break;
+    if (drained && __all_sync(0xffffffffu, !have)) break;
     if (!have) continue;
     if (!clip_step(S, w.clip_tol, w.max_iter)) continue;
     have = false;
@@ -3411,7 +3427,7 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
     bytes += (b + 255) & ~(size_t)255;
     return o;
   };
-  size_t o_cnt = take(8 * sizeof(unsigned long long));
+  size_t o_cnt = take(CNT_WORDS * sizeof(unsigned long long));
   size_t o_dmin = take(n * 8), o_flag = take(n * 4);
   size_t o_pq = take(pcap * 4), o_ps = take(pcap * 4), o_pq2 = take(pcap * 4),
          o_ps2 = take(pcap * 4);
@@ -3494,7 +3510,7 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
     return e ? atoi(e) : -1;
   }();
   w.fuse_filter = fuse_filter >= 0 ? fuse_filter : (n >= (int64_t(1) << 16) ? 1 : 0);
-  MREP_CUDA_CHECK(cudaMemsetAsync(w.cnt, 0, 8 * sizeof(unsigned long long), st));
+  MREP_CUDA_CHECK(cudaMemsetAsync(w.cnt, 0, CNT_WORDS * sizeof(unsigned long long), st));
   auto persist_grid = [](const void* fn, int block) { return persistent_grid(fn, block); };
   const unsigned g_pairs = persist_grid((const void*)wave_pairs<D, MULTI>, BLOCK);
   const unsigned g_clip = persist_grid((const void*)wave_clip<D, MULTI>, BLOCK);
