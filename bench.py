@@ -906,6 +906,26 @@ def main():
                              "frac": flops / (kms / 1e3) / 1e12 / peak.value},
                 "per_query": {"pairs": c[L.CNT_PAIRS] / n, "survivors": c[L.CNT_SURVIVORS] / n,
                               "seams": c[L.CNT_SEAMS] / n, "box_tests": c[L.CNT_BOXES] / n}}
+    if dom == "traverse" and not surf:
+        # the scan does little arithmetic: its roofline is the bytes it must
+        # touch: 24 per query + 32 per box test (8-B list
+        # entry + 24-B float box) + 24 per offered seam, against measured HBM
+        # copy bandwidth (most of these bytes are L1/L2 hits; `traffic` is the
+        # DRAM share from ncu)
+        hbm = None
+        try:
+            hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+            hsrc = "MEASURED_PEAKS.json hbm_gbs (burst copy)"
+        except Exception:
+            hbm, hsrc = 7700.0, "B200_PROFILING.md fallback"
+        tb = 24.0 * n + 32.0 * c[L.CNT_BOXES] + 24.0 * c[L.CNT_SEAMS]
+        ach_gbs = tb / (stages["traverse"]["ms"] / 1e3) / 1e9
+        roofline.update({"bound": "hbm", "achieved": ach_gbs, "peak": hbm, "unit": "GB/s",
+                         "frac": ach_gbs / hbm, "peak_source": hsrc,
+                         "bytes_model": "24/query + 32/box test + 24/offered seam "
+                                        f"({tb / n:.0f} B per query)",
+                         "fp64_view": {"achieved": achieved, "peak": peak.value,
+                                       "unit": "TFLOP/s", "frac": achieved / peak.value}})
     if surf:
         roofline["per_query"] = {"patch_solves": c[L.CNT_PAIRS] / n,
                                  "newton_iters": c[L.CNT_CLIP_ITERS] / n,
