@@ -3418,8 +3418,20 @@ static int launch_wave(const ProjParams& p, cudaStream_t st, bool timing, int tm
                        int64_t ncurves = 0, const StagePlan* plan = nullptr,
                        bool set_cells = false) {
   const int64_t n = p.n;
-  const unsigned long long pcap = (unsigned long long)std::max<int64_t>(16 * n, 1 << 16);
-  const unsigned long long scap = (unsigned long long)std::max<int64_t>(2 * n, 1 << 16);
+  // MREP_WAVE_PCAP / MREP_WAVE_SCAP (tests): tiny pair / survivor buffers, so
+  // the overflow -> fallback paths of every stage run
+  static const int64_t pcap_env = [] {
+    const char* e = getenv("MREP_WAVE_PCAP");
+    return e ? (int64_t)atoll(e) : (int64_t)0;
+  }();
+  static const int64_t scap_env = [] {
+    const char* e = getenv("MREP_WAVE_SCAP");
+    return e ? (int64_t)atoll(e) : (int64_t)0;
+  }();
+  const unsigned long long pcap =
+      (unsigned long long)(pcap_env > 0 ? pcap_env : std::max<int64_t>(16 * n, 1 << 16));
+  const unsigned long long scap =
+      (unsigned long long)(scap_env > 0 ? scap_env : std::max<int64_t>(2 * n, 1 << 16));
   const unsigned long long ccap = (unsigned long long)std::max<int64_t>(n, 1 << 16);
   size_t bytes = 0;
   auto take = [&](size_t b) {

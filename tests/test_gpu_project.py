@@ -510,3 +510,35 @@ def test_fallback_queries_in_sorted_batches(gpu, oracle_lib):
     assert np.abs(t - o["t"]).max() <= 1e-12
     z = np.nonzero(np.all(q == 0.0, axis=1))[0]
     assert np.all(t[z] == 0.0) and np.all(dist[z] == 5.0)
+
+
+def test_wave_buffer_overflow_falls_back_exactly(gpu):
+    """Pair and survivor buffers forced far below the batch's needs
+    (MREP_WAVE_PCAP / MREP_WAVE_SCAP): the fused cell-scan filter's staged
+    appends, the filter kernel, the pairs kernel and the partitioned clip
+    queue all overflow, their queries finish in the fallback kernel, and
+    t / foot / distance / segment still equal the dense kernel bit for bit."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, sys
+sys.path.insert(0, '.')
+from paper_2504_11498_b200 import prepare_curve
+from paper_2504_11498_b200.fixtures import random_clamped_curve
+cv = random_clamped_curve(np.random.default_rng(0), 7, 400, 3, uniform_knots=True)
+tab = prepare_curve(cv, 1e-4).table
+q = np.random.default_rng(11).uniform(-0.1, 1.1, (70000, 3))
+ra, rb = tab.project(q), tab.project(q, screen=False)
+for k in (0, 1, 2, 4):
+    a, b = ra[k].cpu().numpy(), rb[k].cpu().numpy()
+    assert np.array_equal(a, b), (k, np.nonzero(a != b)[0][:10])
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for caps in ({"MREP_WAVE_PCAP": "20000"}, {"MREP_WAVE_SCAP": "15000"},
+                 {"MREP_WAVE_PCAP": "40000", "MREP_WAVE_SCAP": "30000", "MREP_TRAV_FILTER": "1"}):
+        env = dict(os.environ, **caps)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           cwd=root, timeout=600)
+        assert r.returncode == 0 and "ok" in r.stdout, (caps, r.stderr[-2000:])
