@@ -2741,9 +2741,29 @@ __global__ void __launch_bounds__(256) wave_emit(const __grid_constant__ WavePar
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= w.n) return;
   if (w.flag[g]) return;  // written by the fallback kernel
-  int64_t qi = w.perm ? (int64_t)w.perm[g] : g;
+  const int64_t qi = (w.perm && !w.orec) ? (int64_t)w.perm[g] : g;
   if (w.out_cand && !w.orec) w.out_cand[qi] = w.scnt[g];
-  const double lim = dmin_of(w, g) + 1e-12;
+  const uint32_t nc = w.ccnt[g];
+  const double4* row = reinterpret_cast<const double4*>(w.cin + g * CIN);
+  // the running minimum is the smallest candidate distance: the seam that
+  // set the traversal's bound is in its band and every survivor that lowered
+  // it was appended (an overflow of either sends the query to the fallback),
+  // so the row gives it without reading the query's state record
+  double4 rr[CIN];
+  double dm = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll
+  for (int k = 0; k < CIN; ++k) {
+    rr[k] = (uint32_t)k < nc ? row[k] : make_double4(0.0, dm, 0.0, 0.0);
+    dm = fmin(dm, rr[k].y);
+  }
+  if (nc > (uint32_t)CIN) {
+    for (uint32_t c = w.chead[g]; c != ~0u;) {
+      const double4 r = *reinterpret_cast<const double4*>(w.cand + c);
+      c = (uint32_t)((uint64_t)__double_as_longlong(r.w) >> 32);
+      dm = fmin(dm, r.y);
+    }
+  }
+  const double lim = dm + 1e-12;
   unsigned long long bt = ~0ull;
   uint32_t bo = ~0u;
   bool found = false;
@@ -2761,11 +2781,9 @@ __global__ void __launch_bounds__(256) wave_emit(const __grid_constant__ WavePar
       found = true;
     }
   };
-  const uint32_t nc = w.ccnt[g];
-  const double4* row = reinterpret_cast<const double4*>(w.cin + g * CIN);
 #pragma unroll
   for (int k = 0; k < CIN; ++k)
-    if ((uint32_t)k < nc) consider(row[k]);
+    if ((uint32_t)k < nc) consider(rr[k]);
   if (nc > (uint32_t)CIN) {
     for (uint32_t c = w.chead[g]; c != ~0u;) {
       const double4 r = *reinterpret_cast<const double4*>(w.cand + c);
