@@ -2577,12 +2577,27 @@ __global__ void __launch_bounds__(BLOCK) wave_pairs_filter(const __grid_constant
   warp_count(w.counters, MREP_CNT_BOXES, nboxes);
 }
 
+// The survivor buffer is split into CLIP_QP partitions: W2b's warps append
+// to partition (warp % CLIP_QP) through its own counter and W3 claims from
+// each partition through another (every counter on its own 128-B line after
+// the 8 pipeline counters).  One counter for all of them was both kernels'
+// top stall: every warp's append / refill atomic hit a single L2 address.
+constexpr int CLIP_QP = 32, CLIP_QS = 16;
+constexpr int CNT_WORDS = 8 + 2 * CLIP_QP * CLIP_QS;
+__device__ __forceinline__ unsigned long long* clip_claims(const WaveParams& w) { return w.cnt + 8; }
+__device__ __forceinline__ unsigned long long* surv_appends(const WaveParams& w) {
+  return w.cnt + 8 + CLIP_QP * CLIP_QS;
+}
+
 // W2b: E' roots, monotone pieces, elimination for the filtered pairs
 template <int D, bool MULTI>
 __global__ void __launch_bounds__(BLOCK, MREP_PAIRS_MINB) wave_pairs(const __grid_constant__ WaveParams w) {
   unsigned long long total = *(volatile unsigned long long*)&w.cnt[7];
   if (total > w.pcap) total = w.pcap;
   uint64_t npairs = 0;
+  const int part = (int)(((blockIdx.x * blockDim.x + threadIdx.x) >> 5) % CLIP_QP);
+  unsigned long long* const acnt = surv_appends(w) + part * CLIP_QS;
+  const unsigned long long pcap = w.scap / CLIP_QP, pbase = (unsigned long long)part * pcap;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     int64_t qi = w.pq2[i];  // sorted position
@@ -2607,9 +2622,10 @@ __global__ void __launch_bounds__(BLOCK, MREP_PAIRS_MINB) wave_pairs(const __gri
       double bp[6];
       restrict_ordinates(P.bseg, lo, hi, bp);
       bool surv = bp[0] < 0.0 && bp[0] * bp[5] <= 0.0;
-      unsigned long long slot = wave_append(&w.cnt[1], surv);
+      unsigned long long slot = wave_append(acnt, surv);
       if (surv) {
-        if (slot < w.scap) {
+        if (slot < pcap) {
+          slot += pbase;
           double* o = w.sb + slot * 8;
 #pragma unroll
           for (int j = 0; j < 6; ++j) o[j] = bp[j];
@@ -2628,11 +2644,6 @@ __global__ void __launch_bounds__(BLOCK, MREP_PAIRS_MINB) wave_pairs(const __gri
   warp_count(w.counters, MREP_CNT_PAIRS, npairs);
 }
 
-// W3's survivor queue is split into CLIP_QP partitions with one claim counter
-// each (its own 128-B line, after the 8 pipeline counters): a single counter
-// was every warp's refill atomic on one L2 address (the kernel's top stall)
-constexpr int CLIP_QP = 32, CLIP_QS = 16;
-constexpr int CNT_WORDS = 8 + CLIP_QP * CLIP_QS;
 
 // W3 with lane refill: each lane runs one clipping iteration of its current
 // survivor per loop trip and takes the next survivor from the queue as soon
@@ -2640,13 +2651,18 @@ constexpr int CNT_WORDS = 8 + CLIP_QP * CLIP_QS;
 // lanes idle).  Same arithmetic as clip_root (clip_init + clip_step).
 template <int D, bool MULTI>
 __global__ void __launch_bounds__(BLOCK, MREP_CLIP_MINB) wave_clip(const __grid_constant__ WaveParams w) {
-  const unsigned long long total0 = *(volatile unsigned long long*)&w.cnt[1];
-  const unsigned long long total = total0 > w.scap ? w.scap : total0;
-  unsigned long long* qctr = w.cnt + 8;  // partition p's claims at qctr[p * CLIP_QS]
+  unsigned long long* qctr = clip_claims(w);           // partition p's claims at qctr[p * CLIP_QS]
+  const unsigned long long* actr = surv_appends(w);   // and its survivors at actr[p * CLIP_QS]
+  const unsigned long long pcap = w.scap / CLIP_QP;
+  auto part_end = [&](int p) {  // survivors stored in partition p
+    const unsigned long long c = *(volatile const unsigned long long*)(actr + p * CLIP_QS);
+    return c < pcap ? c : pcap;
+  };
   const int lane = threadIdx.x & 31;
   uint64_t nsurv = 0, nit = 0, nmiss = 0;
   bool have = false, drained = false;  // drained: warp-uniform, every partition claimed
   int part = (int)(((blockIdx.x * blockDim.x + threadIdx.x) >> 5) % CLIP_QP);
+  unsigned long long pend_n = part_end(part);  // warp-uniform
   int64_t qi = 0;
   uint32_t sk = 0;
   double plo = 0.0, phi = 0.0;
@@ -2656,7 +2672,7 @@ __global__ void __launch_bounds__(BLOCK, MREP_CLIP_MINB) wave_clip(const __grid_
     const unsigned wm = __ballot_sync(0xffffffffu, want);
     if (wm) {
       const int leader = __ffs(wm) - 1;
-      const unsigned long long lo = total * part / CLIP_QP, hi = total * (part + 1) / CLIP_QP;
+      const unsigned long long lo = (unsigned long long)part * pcap, hi = lo + pend_n;
       unsigned long long base = 0;
       if (lane == leader) base = atomicAdd(qctr + part * CLIP_QS, (unsigned long long)__popc(wm));
       base = __shfl_sync(0xffffffffu, base, leader);
@@ -2683,10 +2699,16 @@ __global__ void __launch_bounds__(BLOCK, MREP_CLIP_MINB) wave_clip(const __grid_
         // counters of all partitions, the warp moves to the first with work
         const int pp = (part + 1 + lane) % CLIP_QP;
         const unsigned long long c = *(volatile unsigned long long*)(qctr + pp * CLIP_QS);
-        const bool avail = total * pp / CLIP_QP + c < total * (pp + 1) / CLIP_QP;
+        const unsigned long long e = part_end(pp);
+        const bool avail = c < e;
         const unsigned am = __ballot_sync(0xffffffffu, avail);
-        if (am) part = __shfl_sync(0xffffffffu, pp, __ffs(am) - 1);
-        else drained = true;
+        if (am) {
+          const int src = __ffs(am) - 1;
+          part = __shfl_sync(0xffffffffu, pp, src);
+          pend_n = __shfl_sync(0xffffffffu, e, src);
+        } else {
+          drained = true;
+        }
       }
     }
     if (drained && __all_sync(0xffffffffu, !have)) break;
@@ -2868,7 +2890,9 @@ __global__ void __launch_bounds__(256) wave_unpermute(const __grid_constant__ Wa
 // diagnostics: emitted pairs / survivors / candidates into counters[7] (packed 21 bits each)
 __global__ void wave_diag(const __grid_constant__ WaveParams w) {
   if (w.counters && threadIdx.x == 0 && blockIdx.x == 0) {
-    unsigned long long a = w.cnt[0] >> 10, b = w.cnt[1] >> 10, c = w.cnt[2] >> 10;
+    unsigned long long sv = 0;
+    for (int p = 0; p < CLIP_QP; ++p) sv += surv_appends(w)[p * CLIP_QS];
+    unsigned long long a = w.cnt[0] >> 10, b = sv >> 10, c = w.cnt[2] >> 10;
     atomicAdd((unsigned long long*)&w.counters[7], (a & 0x1fffff) | ((b & 0x1fffff) << 21) |
                                                        ((c & 0x1fffff) << 42));
   }
