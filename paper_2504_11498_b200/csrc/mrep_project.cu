@@ -2582,7 +2582,10 @@ __global__ void __launch_bounds__(BLOCK) wave_pairs_filter(const __grid_constant
 // each partition through another (every counter on its own 128-B line after
 // the 8 pipeline counters).  One counter for all of them was both kernels'
 // top stall: every warp's append / refill atomic hit a single L2 address.
-constexpr int CLIP_QP = 32, CLIP_QS = 16;
+#ifndef MREP_CLIP_QP
+#define MREP_CLIP_QP 32
+#endif
+constexpr int CLIP_QP = MREP_CLIP_QP, CLIP_QS = 16;
 constexpr int CNT_WORDS = 8 + 2 * CLIP_QP * CLIP_QS;
 __device__ __forceinline__ unsigned long long* clip_claims(const WaveParams& w) { return w.cnt + 8; }
 __device__ __forceinline__ unsigned long long* surv_appends(const WaveParams& w) {
